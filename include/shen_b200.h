@@ -1,0 +1,110 @@
+/*
+ * shen_b200.h -- C ABI of the B200 (sm_100a) Shen-Galerkin wall-normal
+ * solvers and transforms (the data-parallel core of arXiv 1701.03787).
+ *
+ * Plain C: device pointers, sizes and an opaque CUDA stream handle
+ * (cudaStream_t passed as void*, NULL = legacy default stream).  Every call
+ * is stream-ordered and asynchronous unless stated; no call allocates
+ * device memory behind the caller's back.  Return value: SHEN_OK or an
+ * error code; shen_last_error() gives a message (thread-local).
+ *
+ * Layouts follow the reference package chebchan (reference paths relative
+ * to /root/reference/pkg/src/chebchan):
+ *   right-hand sides / solutions: C-contiguous (n_modes, batch) arrays,
+ *     complex128 (interleaved re,im) or float64, one column per
+ *     wavenumber pair -- the flattened (n_modes,) + z2.shape of
+ *     HelmholtzLU.solve / BiharmonicLU.solve (solvers.py:100-109,162-170);
+ *   parity p rows are p, p+2, ... (the stride-2 split, solvers.py:107-108);
+ *   factor arrays: per parity, (rows, batch) float64 (solvers.py:78-94,
+ *     129-152).
+ *
+ * The reference exposes no native interface; these entry points are what
+ * its Python modules bind (see INTEGRATION.md for the ctypes stub).
+ */
+#ifndef SHEN_B200_H
+#define SHEN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum shen_status {
+  SHEN_OK = 0,
+  SHEN_ERR_ARG = 1,   /* invalid argument / unsupported size */
+  SHEN_ERR_CUDA = 2,  /* CUDA runtime error (message via shen_last_error) */
+};
+
+/* number of biharmonic row constants per mode in the table passed to the
+ * biharmonic entry points (see shen_rows.cuh: BihCol) */
+#define SHEN_BIH_NCOL 17
+
+const char* shen_version(void);
+const char* shen_last_error(void);
+/* visible CUDA devices (0 on a machine without a GPU; never aborts) */
+int shen_device_count(void);
+/* set pivot[0] = pivot[1] = INT32_MAX on the device (stream-ordered) */
+int shen_pivot_reset(int* pivot_dev, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Helmholtz  H = ca*K + cb*B  (Shen-Dirichlet, n_dir = n_x - 1 modes)
+ * replaces build_helmholtz (solvers.py:201-241) and HelmholtzLU.solve
+ * (solvers.py:100-126).
+ *   cb[batch]          : 1 + nu*dt*z2/2 per system (helmholtz_coefficients,
+ *                        solvers.py:67-69); ca = nu*dt/2.
+ *   sd, st, md [n_dir] : stiff_dir diagonal, stiff_dir tail, mass_dir
+ *                        diagonal (MatrixSet, matrices.py:264-337).
+ * shen_helm_factor: sequential unpivoted elimination per (system, parity).
+ *   exact != 0 -> reference evaluation order and IEEE division (bit-equal
+ *   factors); exact == 0 -> reciprocal/FMA arithmetic shared with the
+ *   chunked solve.  Outputs are optional (NULL to skip):
+ *     factors[8] = {low_p0, low_p1, d_p0, d_p1, e_p0, e_p1, tail_p0, tail_p1}
+ *                  device arrays (rows_p - 1 or rows_p, batch);
+ *     ckpt       = [C][2][3][batch] factor state entering each chunk of
+ *                  chunk_rows rows (C = ceil(rows_p0 / chunk_rows));
+ *     pivot_dev  = int[2]; atomic-min of the first row (within parity) whose
+ *                  pivot has |d| < 1e-300 (reset it first).
+ * shen_helm_solve_chunked: fused factor+solve from the checkpoints
+ *   (requires 32 * chunk_rows >= rows_p0; ckpt made with exact == 0).
+ * shen_helm_solve_stored: solve with full stored factors (reference order).
+ * rhs and out may alias only for the stored variant.
+ * ------------------------------------------------------------------- */
+int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
+                     const double* md, int chunk_rows, double* ckpt, double* const* factors, int exact,
+                     int* pivot_dev, void* stream);
+int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                            const double* st, const double* md, int chunk_rows, const double* ckpt,
+                            const void* rhs, void* out, int is_complex, void* stream);
+int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
+                           int is_complex, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Biharmonic  H = xi0*Q + xi1*A + xi2*B  (n_bih = n_x - 3 modes)
+ * replaces build_biharmonic (solvers.py:244-355) and BiharmonicLU.solve
+ * (solvers.py:162-198).
+ *   xi1[batch], xi2[batch] : biharmonic_coefficients (solvers.py:72-75).
+ *   tab[n_bih][17]         : per-mode row constants
+ *      {q0, -A0, B0, tail2, -A+2, B+2, tail4, B+4, -A-2(k-2), B+2(k-2),
+ *       B+4(k-4), p, r, q(k+2), s(k+2), q(k+4), s(k+4)}
+ *      with entries outside the band set to 0 (solvers.py:244-268).
+ *   q, s [n_bih]           : tail factors (matrices.py:163-170).
+ *   factors[14] = {low2_p0, low2_p1, low4_p0, low4_p1, d_p0, d_p1, e_p0,
+ *                  e_p1, f_p0, f_p1, a_p0, a_p1, b_p0, b_p1}
+ *   ckpt = [C][2][10][batch] (rows s-1 and s-2 of U entering each chunk).
+ * ------------------------------------------------------------------- */
+int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                    const double* tab, int chunk_rows, double* ckpt, double* const* factors, int exact,
+                    int* pivot_dev, void* stream);
+int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                           int is_complex, void* stream);
+int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
+                          const double* const* factors, const void* rhs, void* out, int is_complex,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHEN_B200_H */

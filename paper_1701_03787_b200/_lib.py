@@ -1,0 +1,96 @@
+"""ctypes binding of the in-tree C-ABI library ``libshen_b200.so``.
+
+There is no CPU fallback: if the library is missing, or no CUDA device is
+visible, every solver/transform entry point raises ``ShenBackendError``.
+Loading the library itself does not need a GPU (cudart is linked
+statically), so the symbol table can be checked on a CPU-only machine.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+__all__ = ["ShenBackendError", "lib", "lib_path", "require_device", "check", "declared_symbols"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libshen_b200.so")
+
+
+class ShenBackendError(RuntimeError):
+    """The B200 backend (CUDA library or device) is unavailable."""
+
+
+_c_int64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_pp = ctypes.POINTER(ctypes.c_void_p)
+
+# name -> (restype, argtypes); mirrors include/shen_b200.h
+_SIGS = {
+    "shen_version": (ctypes.c_char_p, []),
+    "shen_last_error": (ctypes.c_char_p, []),
+    "shen_device_count": (ctypes.c_int, []),
+    "shen_pivot_reset": (ctypes.c_int, [_vp, _vp]),
+    "shen_helm_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
+                                        ctypes.c_int, _vp, _pp, ctypes.c_int, _vp, _vp]),
+    "shen_helm_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
+                                               ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
+    "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
+    "shen_bih_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp, ctypes.c_int,
+                                       _vp, _pp, ctypes.c_int, _vp, _vp]),
+    "shen_bih_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
+                                              ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
+    "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
+                                             ctypes.c_int, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def declared_symbols():
+    return tuple(_SIGS)
+
+
+def lib():
+    """The loaded library (raises ShenBackendError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(lib_path):
+                raise ShenBackendError(
+                    f"{lib_path} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "or `make -C paper_1701_03787_b200/csrc` (no CPU fallback exists)")
+            handle = ctypes.CDLL(lib_path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def require_device():
+    """Fail loudly unless a CUDA device is usable from both torch and the library."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise ShenBackendError("paper_1701_03787_b200 needs a CUDA (B200) device; there is no CPU fallback")
+    handle = lib()
+    if handle.shen_device_count() < 1:
+        raise ShenBackendError("libshen_b200.so sees no CUDA device")
+    return handle
+
+
+def check(status: int, what: str):
+    if status != 0:
+        msg = lib().shen_last_error().decode(errors="replace")
+        raise ShenBackendError(f"{what} failed (status {status}): {msg}")
+
+
+def ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(p) for p in ptrs])
+    return ctypes.cast(arr, _pp), arr

@@ -1,0 +1,143 @@
+// extern "C" boundary: argument validation, stream plumbing, error text.
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/shen_b200.h"
+#include "shen_kernels.h"
+#include "shen_rows.cuh"
+
+static_assert(SHEN_BIH_NCOL == shen::B_NCOL, "table width mismatch");
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+int cuda_check(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return SHEN_OK;
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return SHEN_ERR_CUDA;
+}
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__global__ void fill_int_kernel(int* p, int n, int v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+}  // namespace
+
+extern "C" {
+
+const char* shen_version(void) { return "shen_b200 0.1 (sm_100a)"; }
+
+const char* shen_last_error(void) { return g_err.c_str(); }
+
+int shen_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int shen_pivot_reset(int* pivot_dev, void* stream) {
+  if (!pivot_dev) return fail(SHEN_ERR_ARG, "pivot_dev is NULL");
+  fill_int_kernel<<<1, 32, 0, S(stream)>>>(pivot_dev, 2, INT_MAX);
+  return cuda_check(cudaGetLastError(), "shen_pivot_reset");
+}
+
+int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
+                     const double* md, int chunk_rows, double* ckpt, double* const* factors, int exact,
+                     int* pivot_dev, void* stream) {
+  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md) return fail(SHEN_ERR_ARG, "shen_helm_factor: bad args");
+  if (ckpt && chunk_rows <= 0) return fail(SHEN_ERR_ARG, "shen_helm_factor: ckpt needs chunk_rows > 0");
+  shen::HelmFactorArgs a{};
+  a.n_dir = n_dir; a.ca = ca; a.cb = cb; a.batch = batch; a.sd = sd; a.st = st; a.md = md;
+  a.chunk_rows = chunk_rows; a.ckpt = ckpt; a.pivot = pivot_dev;
+  for (int p = 0; p < 2; ++p) {
+    a.low[p] = factors ? factors[0 + p] : nullptr;
+    a.d[p] = factors ? factors[2 + p] : nullptr;
+    a.e[p] = factors ? factors[4 + p] : nullptr;
+    a.t[p] = factors ? factors[6 + p] : nullptr;
+    if (factors && (!a.d[p] || !a.e[p] || !a.t[p])) return fail(SHEN_ERR_ARG, "shen_helm_factor: null factor");
+  }
+  return cuda_check(shen::launch_helm_factor(a, exact != 0, S(stream)), "shen_helm_factor");
+}
+
+int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                            const double* st, const double* md, int chunk_rows, const double* ckpt,
+                            const void* rhs, void* out, int is_complex, void* stream) {
+  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: bad args");
+  const int rows0 = (n_dir + 1) / 2;
+  if (chunk_rows <= 0 || 32LL * chunk_rows < rows0) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: chunk_rows");
+  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: ckpt required");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: rhs must not alias out");
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
+  return cuda_check(shen::launch_helm_chunk(a, is_complex != 0, S(stream)), "shen_helm_solve_chunked");
+}
+
+int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
+                           int is_complex, void* stream) {
+  if (n_dir < 2 || batch < 0 || !factors || !rhs || !out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stored: bad args");
+  shen::HelmSeqArgs a{};
+  a.n_dir = n_dir; a.batch = batch; a.rhs = rhs; a.out = out;
+  for (int p = 0; p < 2; ++p) {
+    a.low[p] = factors[0 + p]; a.d[p] = factors[2 + p]; a.e[p] = factors[4 + p]; a.t[p] = factors[6 + p];
+  }
+  return cuda_check(shen::launch_helm_seq(a, is_complex != 0, S(stream)), "shen_helm_solve_stored");
+}
+
+int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                    const double* tab, int chunk_rows, double* ckpt, double* const* factors, int exact,
+                    int* pivot_dev, void* stream) {
+  if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab) return fail(SHEN_ERR_ARG, "shen_bih_factor: bad args");
+  if (ckpt && chunk_rows <= 0) return fail(SHEN_ERR_ARG, "shen_bih_factor: ckpt needs chunk_rows > 0");
+  shen::BihFactorArgs a{};
+  a.n_bih = n_bih; a.xi0 = xi0; a.xi1 = xi1; a.xi2 = xi2; a.batch = batch; a.tab = tab;
+  a.chunk_rows = chunk_rows; a.ckpt = ckpt; a.pivot = pivot_dev;
+  for (int p = 0; p < 2; ++p) {
+    a.low2[p] = factors ? factors[0 + p] : nullptr;
+    a.low4[p] = factors ? factors[2 + p] : nullptr;
+    a.d[p] = factors ? factors[4 + p] : nullptr;
+    a.e[p] = factors ? factors[6 + p] : nullptr;
+    a.f[p] = factors ? factors[8 + p] : nullptr;
+    a.a[p] = factors ? factors[10 + p] : nullptr;
+    a.b[p] = factors ? factors[12 + p] : nullptr;
+  }
+  return cuda_check(shen::launch_bih_factor(a, exact != 0, S(stream)), "shen_bih_factor");
+}
+
+int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                           int is_complex, void* stream) {
+  if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: bad args");
+  const int rows0 = (n_bih + 1) / 2;
+  if (chunk_rows <= 0 || 32LL * chunk_rows < rows0) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: chunk_rows");
+  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: ckpt required");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: rhs must not alias out");
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
+  return cuda_check(shen::launch_bih_chunk(a, is_complex != 0, S(stream)), "shen_bih_solve_chunked");
+}
+
+int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
+                          const double* const* factors, const void* rhs, void* out, int is_complex,
+                          void* stream) {
+  if (n_bih < 2 || batch < 0 || !q || !s || !factors || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stored: bad args");
+  shen::BihSeqArgs a{};
+  a.n_bih = n_bih; a.batch = batch; a.xi0 = xi0; a.q = q; a.s = s; a.rhs = rhs; a.out = out;
+  for (int p = 0; p < 2; ++p) {
+    a.low2[p] = factors[0 + p]; a.low4[p] = factors[2 + p]; a.d[p] = factors[4 + p]; a.e[p] = factors[6 + p];
+    a.f[p] = factors[8 + p]; a.a[p] = factors[10 + p]; a.b[p] = factors[12 + p];
+  }
+  return cuda_check(shen::launch_bih_seq(a, is_complex != 0, S(stream)), "shen_bih_solve_stored");
+}
+
+}  // extern "C"

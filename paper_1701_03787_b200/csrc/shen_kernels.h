@@ -1,0 +1,109 @@
+// Internal launch interface between the C-ABI layer (shen_capi.cu) and the
+// kernels.  Not part of the public header (include/shen_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace shen {
+
+struct HelmFactorArgs {
+  int n_dir;
+  double ca;
+  const double* cb;  // [batch]
+  int64_t batch;
+  const double* sd;  // stiff_dir diag  [n_dir]
+  const double* st;  // stiff_dir tail  [n_dir]
+  const double* md;  // mass_dir diag   [n_dir]
+  int chunk_rows;    // R for checkpoints (0: none)
+  double* ckpt;      // [C][2][3][batch] or null
+  double* low[2];    // full factors per parity (null: not wanted)
+  double* d[2];
+  double* e[2];
+  double* t[2];
+  int* pivot;        // [2] min failing row per parity (INT_MAX = none), or null
+};
+
+struct BihFactorArgs {
+  int n_bih;
+  double xi0;
+  const double* xi1;  // [batch]
+  const double* xi2;  // [batch]
+  int64_t batch;
+  const double* tab;  // [n_bih][B_NCOL] row constants
+  int chunk_rows;
+  double* ckpt;       // [C][2][10][batch] or null
+  double* low2[2];
+  double* low4[2];
+  double* d[2];
+  double* e[2];
+  double* f[2];
+  double* a[2];
+  double* b[2];
+  int* pivot;
+};
+
+// Stored-factor (reference-exact) solve: one thread per (system, parity).
+struct HelmSeqArgs {
+  int n_dir;
+  int64_t batch;
+  const double* low[2];
+  const double* d[2];
+  const double* e[2];
+  const double* t[2];
+  const void* rhs;  // (n_dir, batch) complex128 or float64
+  void* out;
+};
+
+struct BihSeqArgs {
+  int n_bih;
+  int64_t batch;
+  double xi0;
+  const double* q;  // [n_bih]
+  const double* s;  // [n_bih]
+  const double* low2[2];
+  const double* low4[2];
+  const double* d[2];
+  const double* e[2];
+  const double* f[2];
+  const double* a[2];
+  const double* b[2];
+  const void* rhs;
+  void* out;
+};
+
+// Chunk-parallel fused solve: factors recomputed from checkpoints.
+struct HelmChunkArgs {
+  int n_dir;
+  double ca;
+  const double* cb;
+  int64_t batch;
+  const double* sd;
+  const double* st;
+  const double* md;
+  int chunk_rows;
+  const double* ckpt;
+  const void* rhs;
+  void* out;
+};
+
+struct BihChunkArgs {
+  int n_bih;
+  double xi0;
+  const double* xi1;
+  const double* xi2;
+  int64_t batch;
+  const double* tab;
+  int chunk_rows;
+  const double* ckpt;
+  const void* rhs;
+  void* out;
+};
+
+cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);
+cudaError_t launch_bih_factor(const BihFactorArgs& a, bool exact, cudaStream_t st);
+cudaError_t launch_helm_seq(const HelmSeqArgs& a, bool complex_rhs, cudaStream_t st);
+cudaError_t launch_bih_seq(const BihSeqArgs& a, bool complex_rhs, cudaStream_t st);
+cudaError_t launch_helm_chunk(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
+cudaError_t launch_bih_chunk(const BihChunkArgs& a, bool complex_rhs, cudaStream_t st);
+
+}  // namespace shen

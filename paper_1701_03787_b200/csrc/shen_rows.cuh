@@ -1,0 +1,160 @@
+// Row recurrences of the compressed unpivoted LU (reference solvers.py),
+// written once and shared by the factor kernel and the chunked solve so the
+// factors a chunk recomputes from its checkpoint are bit-identical to the
+// ones the build kernel walked through.
+//
+// Two arithmetic modes:
+//   EXACT = true : the reference's numpy evaluation order, IEEE division,
+//                  no contraction  -> bit-equal to chebchan's factors.
+//   EXACT = false: reciprocal-multiply and fused multiply-add (fast path).
+#pragma once
+#include "shen_common.cuh"
+
+namespace shen {
+
+// ------------------------------------------------------------ Helmholtz
+// Per-system coefficients: ca (scalar), cb = 1 + nu*dt*z2/2.
+// Row constants by full mode k: sd = stiff_dir diag, st = stiff_dir tail,
+// md = mass_dir diag (solvers.py:209-223).
+struct HelmRow {
+  double diag, sup, tail;
+};
+
+__device__ __forceinline__ HelmRow helm_row(double ca, double cb, double sub, double sd, double st, double md,
+                                            bool has_sup) {
+  HelmRow h;
+  h.diag = __dadd_rn(__dmul_rn(ca, sd), __dmul_rn(cb, md));
+  h.tail = __dadd_rn(__dmul_rn(ca, st), 0.0);
+  h.sup = has_sup ? __dadd_rn(h.tail, sub) : h.tail;
+  return h;
+}
+
+// Factor state after row i: d, e, t (+ reciprocal of d for the fast mode).
+struct HelmState {
+  double d, e, t, rd;
+};
+
+// One elimination step (solvers.py:231-236).  Returns low (0 for row 0).
+template <bool EXACT>
+__device__ __forceinline__ double helm_step(HelmState& s, const HelmRow& h, double sub, bool first) {
+  if (first) {
+    s.d = h.diag;
+    s.e = h.sup;
+    s.t = h.tail;
+    s.rd = EXACT ? 0.0 : __drcp_rn(s.d);
+    return 0.0;
+  }
+  double low;
+  if (EXACT) {
+    low = __ddiv_rn(sub, s.d);
+    s.d = __dsub_rn(h.diag, __dmul_rn(low, s.e));
+    s.e = __dsub_rn(h.sup, __dmul_rn(low, s.t));
+    s.t = __dsub_rn(h.tail, __dmul_rn(low, s.t));
+  } else {
+    low = __dmul_rn(sub, s.rd);
+    s.d = __fma_rn(-low, s.e, h.diag);
+    s.e = __fma_rn(-low, s.t, h.sup);
+    s.t = __fma_rn(-low, s.t, h.tail);
+    s.rd = __drcp_rn(s.d);
+  }
+  return low;
+}
+
+// ------------------------------------------------------------ biharmonic
+// Row-constant table, one record per full biharmonic mode k (host built
+// from MatrixSet + tail_factors, solvers.py:244-268); entries that the
+// reference's band() leaves at zero are stored as 0.
+enum BihCol {
+  B_Q0 = 0, B_AR0, B_BB0,          // d0 band
+  B_T2, B_AR2, B_BB2,              // p2 band (row k, col k+2)
+  B_T4, B_BB4,                     // p4 band
+  B_ARM2, B_BB2M,                  // m2 band (values at k-2)
+  B_BB4M,                          // m4 band (value at k-4)
+  B_P, B_R,                        // tail row factors p_k, r_k
+  B_Q2, B_S2, B_Q4, B_S4,          // q, s at k+2 and k+4 (0 past the end)
+  B_NCOL
+};
+
+struct BihBands {
+  double hd, hp2, hp4, hm2, hm4;
+};
+
+__device__ __forceinline__ BihBands bih_bands(double xi0, double xi1, double xi2, const double* c) {
+  BihBands b;
+  b.hd = __dadd_rn(__dadd_rn(__dmul_rn(xi0, c[B_Q0]), __dmul_rn(xi1, c[B_AR0])), __dmul_rn(xi2, c[B_BB0]));
+  b.hp2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(xi0, c[B_T2]), 0.0), __dmul_rn(xi1, c[B_AR2])),
+                    __dmul_rn(xi2, c[B_BB2]));
+  b.hp4 = __dadd_rn(__dadd_rn(__dmul_rn(xi0, c[B_T4]), 0.0), __dmul_rn(xi2, c[B_BB4]));
+  b.hm2 = __dadd_rn(__dmul_rn(xi1, c[B_ARM2]), __dmul_rn(xi2, c[B_BB2M]));
+  b.hm4 = __dmul_rn(xi2, c[B_BB4M]);
+  return b;
+}
+
+// U-row record (d, e, f, a, b) of one eliminated row (+ 1/d in fast mode).
+struct BihU {
+  double d, e, f, a, b, rd;
+};
+
+// One elimination step, rows i-1 (u1) and i-2 (u2) already eliminated
+// (solvers.py:314-346).  i is the row within the parity.  Returns l2, l4.
+template <bool EXACT>
+__device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2, const BihBands& h, const double* c,
+                                         double xi0, int i, double& l2, double& l4) {
+  if (i == 0) {
+    u.d = h.hd;
+    u.e = h.hp2;
+    u.f = h.hp4;
+    u.a = c[B_P];
+    u.b = c[B_R];
+    l2 = 0.0;
+    l4 = 0.0;
+  } else if (i == 1) {
+    l4 = 0.0;
+    if (EXACT) {
+      l2 = __ddiv_rn(h.hm2, u1.d);
+      double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
+      u.d = __dsub_rn(h.hd, __dmul_rn(l2, u1.e));
+      u.e = __dsub_rn(h.hp2, __dmul_rn(l2, u1.f));
+      u.f = __dsub_rn(h.hp4, __dmul_rn(l2, u24));
+      u.a = __dsub_rn(c[B_P], __dmul_rn(l2, u1.a));
+      u.b = __dsub_rn(c[B_R], __dmul_rn(l2, u1.b));
+    } else {
+      l2 = __dmul_rn(h.hm2, u1.rd);
+      double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
+      u.d = __fma_rn(-l2, u1.e, h.hd);
+      u.e = __fma_rn(-l2, u1.f, h.hp2);
+      u.f = __fma_rn(-l2, u24, h.hp4);
+      u.a = __fma_rn(-l2, u1.a, c[B_P]);
+      u.b = __fma_rn(-l2, u1.b, c[B_R]);
+    }
+  } else {
+    if (EXACT) {
+      l4 = __ddiv_rn(h.hm4, u2.d);
+      double tmp = __dsub_rn(h.hm2, __dmul_rn(l4, u2.e));
+      l2 = __ddiv_rn(tmp, u1.d);
+      double u42 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q2]), __dmul_rn(u2.b, c[B_S2])));
+      double u44 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q4]), __dmul_rn(u2.b, c[B_S4])));
+      double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
+      u.d = __dsub_rn(__dsub_rn(h.hd, __dmul_rn(l4, u2.f)), __dmul_rn(l2, u1.e));
+      u.e = __dsub_rn(__dsub_rn(h.hp2, __dmul_rn(l4, u42)), __dmul_rn(l2, u1.f));
+      u.f = __dsub_rn(__dsub_rn(h.hp4, __dmul_rn(l4, u44)), __dmul_rn(l2, u24));
+      u.a = __dsub_rn(__dsub_rn(c[B_P], __dmul_rn(l2, u1.a)), __dmul_rn(l4, u2.a));
+      u.b = __dsub_rn(__dsub_rn(c[B_R], __dmul_rn(l2, u1.b)), __dmul_rn(l4, u2.b));
+    } else {
+      l4 = __dmul_rn(h.hm4, u2.rd);
+      double tmp = __fma_rn(-l4, u2.e, h.hm2);
+      l2 = __dmul_rn(tmp, u1.rd);
+      double u42 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2])));
+      double u44 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4])));
+      double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
+      u.d = __fma_rn(-l2, u1.e, __fma_rn(-l4, u2.f, h.hd));
+      u.e = __fma_rn(-l2, u1.f, __fma_rn(-l4, u42, h.hp2));
+      u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
+      u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
+      u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
+    }
+  }
+  u.rd = EXACT ? 0.0 : __drcp_rn(u.d);
+}
+
+}  // namespace shen

@@ -1,0 +1,463 @@
+// Chunk-parallel fused factor+solve for the wall-normal systems.
+//
+// One warp owns one (wavenumber system, parity); its 32 lanes own 32
+// consecutive chunks of R rows.  Per lane, in registers + shared memory:
+//
+//  pass 1  (rows forward)  recompute the compressed-LU rows from the
+//          chunk's checkpoint (same recurrence as the build kernel, so the
+//          factors are bit-identical), form the forward particular
+//          solution y0 with zero entry and its homogeneous responses, and
+//          accumulate the chunk's backward transfer  sigma_s = P sigma_{s+R}
+//          + tau  (sigma = back-substitution state), all in one sweep;
+//  scan F  warp shuffle scan (Hillis-Steele) of the forward affine maps ->
+//          the y entering every chunk;
+//  scan B  warp shuffle suffix scan of the backward maps -> estimated
+//          back-substitution state entering every chunk;
+//  pass 3  (rows backward) the reference back-substitution, row by row;
+//  fix     the estimate and what the right-hand neighbour actually
+//          produced differ by a few ulps; that inconsistency is pushed
+//          through two truncated neighbour steps and removed with a
+//          homogeneous correction sweep (keeps the residual at the
+//          reference's level; without it the biharmonic residual at
+//          BASELINE config 4 corners is ~10x the reference's).
+//
+// Global traffic: the RHS once in, the solution once out (32 B per complex
+// unknown) plus the chunk checkpoints (3 or 10 doubles per chunk).
+#include "shen_rows.cuh"
+#include "shen_kernels.h"
+
+namespace shen {
+
+template <typename V> struct SlotsH { static constexpr int n = VOps<V>::ndouble + 4; };   // y, h, rd, e, t
+template <typename V> struct SlotsB { static constexpr int n = VOps<V>::ndouble + 7; };   // y, g1, g2, rd, e, f, a, b
+
+// per-warp row store: [row][slot][lane]
+struct RowStore {
+  double* base;
+  int lane;
+  __device__ __forceinline__ double& at(int r, int slot, int nslot) { return base[(r * nslot + slot) * 32 + lane]; }
+};
+
+template <typename V>
+__device__ __forceinline__ void put_v(RowStore& s, int r, int slot, int nslot, V v);
+template <>
+__device__ __forceinline__ void put_v<double>(RowStore& s, int r, int slot, int nslot, double v) {
+  s.at(r, slot, nslot) = v;
+}
+template <>
+__device__ __forceinline__ void put_v<cplx>(RowStore& s, int r, int slot, int nslot, cplx v) {
+  s.at(r, slot, nslot) = v.re;
+  s.at(r, slot + 1, nslot) = v.im;
+}
+template <typename V>
+__device__ __forceinline__ V get_v(RowStore& s, int r, int slot, int nslot);
+template <>
+__device__ __forceinline__ double get_v<double>(RowStore& s, int r, int slot, int nslot) {
+  return s.at(r, slot, nslot);
+}
+template <>
+__device__ __forceinline__ cplx get_v<cplx>(RowStore& s, int r, int slot, int nslot) {
+  return {s.at(r, slot, nslot), s.at(r, slot + 1, nslot)};
+}
+
+__device__ __forceinline__ cplx vfma(double s, cplx b, cplx a) { return {__fma_rn(s, b.re, a.re), __fma_rn(s, b.im, a.im)}; }
+__device__ __forceinline__ double vfma(double s, double b, double a) { return __fma_rn(s, b, a); }
+__device__ __forceinline__ cplx vmul(double s, cplx b) { return {s * b.re, s * b.im}; }
+__device__ __forceinline__ double vmul(double s, double b) { return s * b; }
+__device__ __forceinline__ cplx vadd(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ double vadd(double a, double b) { return a + b; }
+__device__ __forceinline__ cplx vsub(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ double vsub(double a, double b) { return a - b; }
+template <typename V> __device__ __forceinline__ V vzero();
+template <> __device__ __forceinline__ double vzero<double>() { return 0.0; }
+template <> __device__ __forceinline__ cplx vzero<cplx>() { return {0.0, 0.0}; }
+
+// ======================================================================= Helmholtz
+template <typename V>
+__global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
+  using O = VOps<V>;
+  constexpr int NS = SlotsH<V>::n;
+  constexpr int SY = 0, SH = O::ndouble, SRD = SH + 1, SE = SH + 2, ST = SH + 3;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int par = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * nwarp + warp;
+  if (j >= a.batch) return;
+  const int64_t B = a.batch;
+  const int R = a.chunk_rows;
+  const int n = (a.n_dir - par + 1) / 2;
+  const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
+  const int s0 = lane * R;
+  const int nr = max(0, min(R, n - s0));
+  RowStore rs{smem + (size_t)warp * R * NS * 32, lane};
+  const V* rhs = static_cast<const V*>(a.rhs);
+  V* out = static_cast<V*>(a.out);
+  const double cb = __ldg(a.cb + j);
+  const double sub = __dmul_rn(cb, -1.5707963267948966);
+
+  // ---- pass 1
+  HelmState st{0, 0, 0, 0};
+  if (s0 > 0 && nr > 0) {
+    const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + j;
+    st.d = ck[0];
+    st.e = ck[B];
+    st.t = ck[2 * B];
+    st.rd = __drcp_rn(st.d);
+  }
+  V y = vzero<V>();
+  double h = 1.0;
+  double p00 = 1.0, p01 = 0.0, p10 = 0.0, p11 = 1.0;
+  V t0a = vzero<V>(), t0b = vzero<V>();
+  double t1a = 0.0, t1b = 0.0;
+  // issue the chunk's RHS loads up front (independent of the recurrence)
+  for (int r = 0; r < nr; ++r) {
+    const int i = s0 + r;
+    const int k = par + 2 * i;
+    HelmRow row = helm_row(a.ca, cb, sub, __ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsup);
+    const double low = helm_step<false>(st, row, sub, i == 0);
+    const V b = O::ld_cs(rhs + (int64_t)k * B + j);
+    if (i == 0) {
+      y = b;
+      h = 0.0;
+    } else {
+      y = vfma(-low, y, b);
+      h = -low * h;
+    }
+    put_v<V>(rs, r, SY, NS, y);
+    rs.at(r, SH, NS) = h;
+    rs.at(r, SRD, NS) = st.rd;
+    rs.at(r, SE, NS) = st.e;
+    rs.at(r, ST, NS) = st.t;
+    const double al = -st.rd * st.e, be = -st.rd * st.t;
+    const V cy = vmul(st.rd, y);
+    const double ch = st.rd * h;
+    t0a = vfma(p00, cy, t0a);
+    t0b = vfma(p10, cy, t0b);
+    t1a = fma(p00, ch, t1a);
+    t1b = fma(p10, ch, t1b);
+    const double n00 = fma(p00, al, p01), n01 = fma(p00, be, p01);
+    const double n10 = fma(p10, al, p11), n11 = fma(p10, be, p11);
+    p00 = n00; p01 = n01; p10 = n10; p11 = n11;
+  }
+
+  // ---- scan F: exit_c = Y_c + m_c * exit_{c-1}
+  double m = h;
+  V Y = y;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const double mb = shfl_up_d(m, dd);
+    const V Yb = shfl_up_v(Y, dd);
+    if (lane >= dd) {
+      Y = vfma(m, Yb, Y);
+      m = m * mb;
+    }
+  }
+  V E = shfl_up_v(Y, 1);
+  if (lane == 0) E = vzero<V>();
+
+  // ---- scan B: sigma_s = P sigma_{s+R} + tau, suffix over lanes
+  V ta = vfma(t1a, E, t0a), tb = vfma(t1b, E, t0b);
+  // tau is complex, t1 real: vfma(real, V, V) with real multiplier t1 times E
+  const double o00 = p00, o01 = p01, o10 = p10, o11 = p11;
+  {
+    double q00 = p00, q01 = p01, q10 = p10, q11 = p11;
+    V ua = ta, ub = tb;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const double r00 = shfl_down_d(q00, dd), r01 = shfl_down_d(q01, dd);
+      const double r10 = shfl_down_d(q10, dd), r11 = shfl_down_d(q11, dd);
+      const V va = shfl_down_v(ua, dd), vb = shfl_down_v(ub, dd);
+      if (lane + dd < 32) {
+        ua = vfma(q00, va, vfma(q01, vb, ua));
+        ub = vfma(q10, va, vfma(q11, vb, ub));
+        const double n00 = fma(q00, r00, q01 * r10), n01 = fma(q00, r01, q01 * r11);
+        const double n10 = fma(q10, r00, q11 * r10), n11 = fma(q10, r01, q11 * r11);
+        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+      }
+    }
+    ta = ua;
+    tb = ub;
+  }
+  // ta/tb: estimated state entering this chunk from the left view = sigma_est(c)
+  V x1 = shfl_down_v(ta, 1), S = shfl_down_v(tb, 1);
+  if (lane == 31) { x1 = vzero<V>(); S = vzero<V>(); }
+
+  // ---- pass 3: reference back-substitution
+  for (int r = nr - 1; r >= 0; --r) {
+    const V y0 = get_v<V>(rs, r, SY, NS);
+    const double hh = rs.at(r, SH, NS);
+    const V yy = vfma(hh, E, y0);
+    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), t = rs.at(r, ST, NS);
+    const V acc = vsub(vsub(yy, vmul(e, x1)), vmul(t, S));
+    const V x = vmul(rd, acc);
+    S = vadd(x1, S);
+    x1 = x;
+    put_v<V>(rs, r, SY, NS, x);
+  }
+  // ---- fix: delta = actual - estimated entering state, 2 truncated neighbour steps
+  const V da = vsub(x1, ta), db = vsub(S, tb);
+  V wa = shfl_down_v(da, 1), wb = shfl_down_v(db, 1);
+  if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
+  V w1a = vfma(o00, wa, vfma(o01, wb, da)), w1b = vfma(o10, wa, vfma(o11, wb, db));
+  wa = shfl_down_v(w1a, 1); wb = shfl_down_v(w1b, 1);
+  if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
+  V w2a = vfma(o00, wa, vfma(o01, wb, da)), w2b = vfma(o10, wa, vfma(o11, wb, db));
+  V xc1 = shfl_down_v(w2a, 1), Sc = shfl_down_v(w2b, 1);
+  if (lane == 31) { xc1 = vzero<V>(); Sc = vzero<V>(); }
+  for (int r = nr - 1; r >= 0; --r) {
+    const int k = par + 2 * (s0 + r);
+    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), t = rs.at(r, ST, NS);
+    const V xc = vmul(-rd, vfma(e, xc1, vmul(t, Sc)));
+    Sc = vadd(xc1, Sc);
+    xc1 = xc;
+    const V x = vadd(get_v<V>(rs, r, SY, NS), xc);
+    O::st_cs(out + (int64_t)k * B + j, x);
+  }
+}
+
+// ======================================================================= biharmonic
+template <typename V>
+__global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
+  using O = VOps<V>;
+  constexpr int NS = SlotsB<V>::n;
+  constexpr int SY = 0, SG1 = O::ndouble, SG2 = SG1 + 1, SRD = SG1 + 2, SE = SG1 + 3, SF = SG1 + 4, SA = SG1 + 5,
+                SB = SG1 + 6;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int par = blockIdx.y;
+  const int64_t j = (int64_t)blockIdx.x * nwarp + warp;
+  if (j >= a.batch) return;
+  const int64_t B = a.batch;
+  const int R = a.chunk_rows;
+  const int n = (a.n_bih - par + 1) / 2;
+  const int s0 = lane * R;
+  const int nr = max(0, min(R, n - s0));
+  double* wbase = smem + (size_t)warp * (R * NS * 32 + 16 * 32);
+  RowStore rs{wbase, lane};
+  double* pown = wbase + R * NS * 32;  // [16][32] own transfer matrix
+  const V* rhs = static_cast<const V*>(a.rhs);
+  V* out = static_cast<V*>(a.out);
+  const double xi0 = a.xi0, xi1 = __ldg(a.xi1 + j), xi2 = __ldg(a.xi2 + j);
+
+  BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
+  if (s0 > 0 && nr > 0) {
+    const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 10) * B + j;
+    u1.d = ck[0]; u1.e = ck[B]; u1.f = ck[2 * B]; u1.a = ck[3 * B]; u1.b = ck[4 * B];
+    u2.d = ck[5 * B]; u2.e = ck[6 * B]; u2.f = ck[7 * B]; u2.a = ck[8 * B]; u2.b = ck[9 * B];
+    u1.rd = __drcp_rn(u1.d);
+    u2.rd = s0 >= 2 ? __drcp_rn(u2.d) : 0.0;
+  }
+  V yp1 = vzero<V>(), yp2 = vzero<V>();
+  double h11 = 1.0, h12 = 0.0, h21 = 0.0, h22 = 1.0;
+  double P[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) P[r][c] = (r == c) ? 1.0 : 0.0;
+  V t0[4];
+  double t1[4], t2[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) { t0[r] = vzero<V>(); t1[r] = 0.0; t2[r] = 0.0; }
+
+  for (int r = 0; r < nr; ++r) {
+    const int i = s0 + r;
+    const int k = par + 2 * i;
+    double c[B_NCOL];
+#pragma unroll
+    for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+    const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+    double l2, l4;
+    bih_step<false>(u, u1, u2, hb, c, xi0, i, l2, l4);
+    u2 = u1;
+    u1 = u;
+    const V b = O::ld_cs(rhs + (int64_t)k * B + j);
+    const V y = vfma(-l4, yp2, vfma(-l2, yp1, b));
+    const double g1 = -fma(l2, h11, l4 * h21), g2 = -fma(l2, h12, l4 * h22);
+    yp2 = yp1; yp1 = y;
+    h21 = h11; h22 = h12; h11 = g1; h12 = g2;
+    put_v<V>(rs, r, SY, NS, y);
+    rs.at(r, SG1, NS) = g1;
+    rs.at(r, SG2, NS) = g2;
+    rs.at(r, SRD, NS) = u.rd;
+    rs.at(r, SE, NS) = u.e;
+    rs.at(r, SF, NS) = u.f;
+    rs.at(r, SA, NS) = u.a;
+    rs.at(r, SB, NS) = u.b;
+    // backward transfer of this row, accumulated left to right
+    const double al = -u.rd * u.e, be = -u.rd * u.f;
+    const double ga = -u.rd * (xi0 * u.a), de = -u.rd * (xi0 * u.b);
+    const double qn = c[B_Q4], sn = c[B_S4];
+    const V cy = vmul(u.rd, y);
+    const double cg1 = u.rd * g1, cg2 = u.rd * g2;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      t0[q] = vfma(P[q][0], cy, t0[q]);
+      t1[q] = fma(P[q][0], cg1, t1[q]);
+      t2[q] = fma(P[q][0], cg2, t2[q]);
+      const double p0 = P[q][0], p1 = P[q][1], p2 = P[q][2], p3 = P[q][3];
+      P[q][0] = fma(p0, al, p1);
+      P[q][1] = fma(p0, be, fma(p2, qn, p3 * sn));
+      P[q][2] = fma(p0, ga, p2);
+      P[q][3] = fma(p0, de, p3);
+    }
+  }
+
+  // ---- scan F: (y_last, y_last-1) = Y + H (E1, E2)
+  double H0 = h11, H1 = h12, H2 = h21, H3 = h22;
+  V Ya = yp1, Yb = yp2;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const double g0 = shfl_up_d(H0, dd), g1 = shfl_up_d(H1, dd), g2 = shfl_up_d(H2, dd), g3 = shfl_up_d(H3, dd);
+    const V wa = shfl_up_v(Ya, dd), wb = shfl_up_v(Yb, dd);
+    if (lane >= dd) {
+      Ya = vfma(H0, wa, vfma(H1, wb, Ya));
+      Yb = vfma(H2, wa, vfma(H3, wb, Yb));
+      const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
+      const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
+      H0 = n0; H1 = n1; H2 = n2; H3 = n3;
+    }
+  }
+  V E1 = shfl_up_v(Ya, 1), E2 = shfl_up_v(Yb, 1);
+  if (lane == 0) { E1 = vzero<V>(); E2 = vzero<V>(); }
+
+  // ---- scan B
+  V tau[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tau[q] = vfma(t1[q], E1, vfma(t2[q], E2, t0[q]));
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) pown[(q * 4 + c) * 32 + lane] = P[q][c];
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    double Q[4][4];
+    V ub[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ub[q] = shfl_down_v(tau[q], dd);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) Q[q][c] = shfl_down_d(P[q][c], dd);
+    }
+    if (lane + dd < 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tau[q] = vfma(P[q][0], ub[0], vfma(P[q][1], ub[1], vfma(P[q][2], ub[2], vfma(P[q][3], ub[3], tau[q]))));
+      }
+      double N[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          N[q][c] = fma(P[q][0], Q[0][c], fma(P[q][1], Q[1][c], fma(P[q][2], Q[2][c], P[q][3] * Q[3][c])));
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) P[q][c] = N[q][c];
+    }
+  }
+  V sg[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    sg[q] = shfl_down_v(tau[q], 1);
+    if (lane == 31) sg[q] = vzero<V>();
+  }
+
+  // ---- pass 3: reference back-substitution (Alg. 4 order)
+  V x1 = sg[0], x2 = sg[1], sq = sg[2], sv = sg[3];
+  for (int r = nr - 1; r >= 0; --r) {
+    const int k = par + 2 * (s0 + r);
+    const V y0 = get_v<V>(rs, r, SY, NS);
+    const V yy = vfma(rs.at(r, SG1, NS), E1, vfma(rs.at(r, SG2, NS), E2, y0));
+    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), f = rs.at(r, SF, NS);
+    const double av = rs.at(r, SA, NS), bv = rs.at(r, SB, NS);
+    V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
+    acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
+    const V x = vmul(rd, acc);
+    const double qn = __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4), sn = __ldg(a.tab + (int64_t)k * B_NCOL + B_S4);
+    sq = vfma(qn, x2, sq);
+    sv = vfma(sn, x2, sv);
+    x2 = x1;
+    x1 = x;
+    put_v<V>(rs, r, SY, NS, x);
+  }
+  // ---- fix
+  V dl[4] = {vsub(x1, tau[0]), vsub(x2, tau[1]), vsub(sq, tau[2]), vsub(sv, tau[3])};
+  V w[4], wn[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    wn[q] = shfl_down_v(dl[q], 1);
+    if (lane == 31) wn[q] = vzero<V>();
+  }
+#pragma unroll
+  for (int step = 0; step < 2; ++step) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      V acc = dl[q];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc = vfma(pown[(q * 4 + c) * 32 + lane], wn[c], acc);
+      w[q] = acc;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      wn[q] = shfl_down_v(w[q], 1);
+      if (lane == 31) wn[q] = vzero<V>();
+    }
+  }
+  V c1 = wn[0], c2 = wn[1], cq = wn[2], cs = wn[3];
+  for (int r = nr - 1; r >= 0; --r) {
+    const int k = par + 2 * (s0 + r);
+    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), f = rs.at(r, SF, NS);
+    const double av = rs.at(r, SA, NS), bv = rs.at(r, SB, NS);
+    const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
+    const V xc = vmul(-rd, acc);
+    const double qn = __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4), sn = __ldg(a.tab + (int64_t)k * B_NCOL + B_S4);
+    cq = vfma(qn, c2, cq);
+    cs = vfma(sn, c2, cs);
+    c2 = c1;
+    c1 = xc;
+    O::st_cs(out + (int64_t)k * B + j, vadd(get_v<V>(rs, r, SY, NS), xc));
+  }
+}
+
+static size_t helm_smem(int R, int nwarp, bool cplx_rhs) {
+  return (size_t)nwarp * R * (cplx_rhs ? SlotsH<cplx>::n : SlotsH<double>::n) * 32 * sizeof(double);
+}
+static size_t bih_smem(int R, int nwarp, bool cplx_rhs) {
+  return (size_t)nwarp * (R * (cplx_rhs ? SlotsB<cplx>::n : SlotsB<double>::n) * 32 + 16 * 32) * sizeof(double);
+}
+
+template <typename K>
+static cudaError_t launch_dyn(K kernel, dim3 grid, int threads, size_t smem, cudaStream_t st, void* args) {
+  cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  void* params[] = {args};
+  return cudaLaunchKernel((const void*)kernel, grid, dim3(threads), params, smem, st);
+}
+
+cudaError_t launch_helm_chunk(const HelmChunkArgs& a, bool cplx_rhs, cudaStream_t st) {
+  if (a.batch <= 0) return cudaSuccess;
+  if (a.chunk_rows <= 0 || (int64_t)a.chunk_rows * 32 < (a.n_dir + 1) / 2) return cudaErrorInvalidValue;
+  int nwarp = 4;
+  while (nwarp > 1 && helm_smem(a.chunk_rows, nwarp, cplx_rhs) > 110 * 1024) nwarp >>= 1;
+  const size_t smem = helm_smem(a.chunk_rows, nwarp, cplx_rhs);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((a.batch + nwarp - 1) / nwarp), 2);
+  HelmChunkArgs copy = a;
+  return cplx_rhs ? launch_dyn(helm_chunk_kernel<cplx>, grid, 32 * nwarp, smem, st, &copy)
+                  : launch_dyn(helm_chunk_kernel<double>, grid, 32 * nwarp, smem, st, &copy);
+}
+
+cudaError_t launch_bih_chunk(const BihChunkArgs& a, bool cplx_rhs, cudaStream_t st) {
+  if (a.batch <= 0) return cudaSuccess;
+  if (a.chunk_rows <= 0 || (int64_t)a.chunk_rows * 32 < (a.n_bih + 1) / 2) return cudaErrorInvalidValue;
+  int nwarp = 2;
+  while (nwarp > 1 && bih_smem(a.chunk_rows, nwarp, cplx_rhs) > 110 * 1024) nwarp >>= 1;
+  const size_t smem = bih_smem(a.chunk_rows, nwarp, cplx_rhs);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((a.batch + nwarp - 1) / nwarp), 2);
+  BihChunkArgs copy = a;
+  return cplx_rhs ? launch_dyn(bih_chunk_kernel<cplx>, grid, 32 * nwarp, smem, st, &copy)
+                  : launch_dyn(bih_chunk_kernel<double>, grid, 32 * nwarp, smem, st, &copy);
+}
+
+}  // namespace shen

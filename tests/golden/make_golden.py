@@ -1,0 +1,153 @@
+"""Generate the golden fixtures in tests/golden from the REFERENCE package.
+
+Run in the build container only (needs /root/reference):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The reference is imported read-only; only its outputs (numbers) are stored.
+Nothing in the test suite reads /root/reference at run time.
+"""
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+from chebchan import matrices as RM  # noqa: E402
+from chebchan import solvers as RS  # noqa: E402
+from chebchan import transforms as RT  # noqa: E402
+from chebchan.mesh import PointFamily, Space, build_mesh, wavenumber_grid  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+FAMS = list(PointFamily)
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def z2_grid(n_y, n_z, l_y=2 * np.pi, l_z=np.pi):
+    m = 2 * np.pi * np.fft.fftfreq(n_y, 1.0 / n_y) / l_y
+    n = 2 * np.pi * np.fft.rfftfreq(n_z, 1.0 / n_z) / l_z
+    return m[:, None] ** 2 + n[None, :] ** 2
+
+
+def matrices_fixture():
+    out = {}
+    for n_x in (8, 16, 63, 64, 256):
+        for fi, fam in enumerate(FAMS):
+            m = RM.assemble(n_x, fam)
+            key = f"nx{n_x}_f{fi}"
+            out[key + "_mass_cheb"] = m.mass_cheb
+            for name in ("mass_dir", "mass_bih", "mixed_mass", "stiff_bih", "deriv_dir_to_bih", "deriv_bih_to_dir"):
+                mat = getattr(m, name)
+                for off, dg in zip(mat.offsets, mat.diagonals):
+                    out[f"{key}_{name}_{off}"] = dg
+            for name in ("stiff_dir", "deriv_dir_to_cheb"):
+                mat = getattr(m, name)
+                for off, dg in zip(mat.banded.offsets, mat.banded.diagonals):
+                    out[f"{key}_{name}_{off}"] = dg
+                out[f"{key}_{name}_tail"] = mat.tail
+            out[key + "_fourth_bih_diag"] = m.fourth_bih.diag
+    np.savez_compressed(os.path.join(OUT, "matrices.npz"), **out)
+
+
+def solver_fixture():
+    """Small cases: full factors + solutions (real and complex RHS)."""
+    out = {}
+    meta = []
+    cases = []
+    for n_x in (16, 32, 63):
+        for fi in (0, 1):
+            cases.append((n_x, fi, 1 / 5200, 1e-5, np.array([0.0, 10.0, 200.0]) ** 2))
+    cases.append((256, 0, 1 / 5200, 1e-5, np.array([5400.0]) ** 2))
+    cases.append((64, 0, 0.01, 0.1, np.linspace(0.0, 400.0, 12).reshape(3, 4)))
+    for ci, (n_x, fi, nu, dt, z2) in enumerate(cases):
+        mats = RM.assemble(n_x, FAMS[fi])
+        rng = np.random.default_rng(1000 + ci)
+        key = f"c{ci}"
+        out[key + "_z2"] = z2
+        for op, build, nm in (("h", RS.build_helmholtz, mats.n_dir), ("b", RS.build_biharmonic, mats.n_bih)):
+            lu = build(mats, nu, dt, z2)
+            fr = rng.standard_normal((nm,) + z2.shape)
+            fc = rng.standard_normal((nm,) + z2.shape) + 1j * rng.standard_normal((nm,) + z2.shape)
+            out[f"{key}_{op}_rhs_real"] = fr
+            out[f"{key}_{op}_rhs_cplx"] = fc
+            out[f"{key}_{op}_x_real"] = lu.solve(fr)
+            out[f"{key}_{op}_x_cplx"] = lu.solve(fc)
+            names = ("low", "d", "e", "tail") if op == "h" else ("low2", "low4", "d", "e", "f", "a", "b")
+            for nmf in names:
+                for p in (0, 1):
+                    out[f"{key}_{op}_{nmf}{p}"] = getattr(lu, nmf)[p]
+        meta.append({"case": ci, "n_x": n_x, "family": fi, "nu": nu, "dt": dt, "z2_shape": list(z2.shape)})
+    np.savez_compressed(os.path.join(OUT, "solvers.npz"), **out)
+    return meta
+
+
+def baseline_fixture():
+    """BASELINE configs 1 and 2 (n_x = 63, 64 x 33 wavenumbers, nu = dt = 1e-3,
+    RHS N(0,1) complex from default_rng(0), real part first): sha256 of the
+    reference's full solution plus every 16th system verbatim."""
+    mats = RM.assemble(63, PointFamily.GAUSS)
+    z2 = z2_grid(64, 64)
+    res = {}
+    arrays = {}
+    for op, build, nm in (("h", RS.build_helmholtz, mats.n_dir), ("b", RS.build_biharmonic, mats.n_bih)):
+        rng = np.random.default_rng(0)
+        f = rng.standard_normal((nm,) + z2.shape) + 1j * rng.standard_normal((nm,) + z2.shape)
+        lu = build(mats, 1e-3, 1e-3, z2)
+        x = lu.solve(f)
+        res[op] = {"rhs_sha256": sha(f), "x_sha256": sha(x), "shape": list(x.shape)}
+        flat = x.reshape(nm, -1)
+        arrays[f"{op}_x_every16"] = flat[:, ::16]
+        if op == "h":
+            res[op]["factor_sha256"] = {f"{k}{p}": sha(getattr(lu, k)[p]) for k in ("low", "d", "e", "tail")
+                                        for p in (0, 1)}
+    np.savez_compressed(os.path.join(OUT, "baseline_c1c2.npz"), **arrays)
+    return res
+
+
+def transforms_fixture():
+    out = {}
+    for n_x in (8, 16, 32):
+        for fi, fam in enumerate(FAMS):
+            mesh = build_mesh(n_x, 8, 4, 2 * np.pi, np.pi, fam)
+            rng = np.random.default_rng(7 * n_x + fi)
+            u = rng.standard_normal(mesh.shape)
+            key = f"nx{n_x}_f{fi}"
+            out[key + "_u"] = u
+            for space in Space:
+                sc = list(Space).index(space)
+                c = RT.forward_transform(RT.PhysicalField(u, mesh), space)
+                out[f"{key}_s{sc}_fwd"] = c.data
+                out[f"{key}_s{sc}_fsp"] = RT.forward_scalar_product(RT.PhysicalField(u, mesh), space).data
+                out[f"{key}_s{sc}_inv"] = RT.inverse_transform(c).data
+    # 1-D building blocks on a (n_x+1, 3) complex block
+    for fi, fam in enumerate(FAMS):
+        rng = np.random.default_rng(99 + fi)
+        v = rng.standard_normal((13, 3)) + 1j * rng.standard_normal((13, 3))
+        out[f"blk_f{fi}_v"] = v
+        out[f"blk_f{fi}_cheb_scalar"] = RT.chebyshev_scalar(v, fam)
+        out[f"blk_f{fi}_cheb_eval"] = RT.chebyshev_evaluate(v, fam)
+        for space in (Space.DIRICHLET, Space.BIHARMONIC):
+            sc = list(Space).index(space)
+            out[f"blk_f{fi}_s{sc}_shen_scalar"] = RT.shen_scalar(v, fam, space)
+            w = v[:13 - space.mode_drop]
+            out[f"blk_f{fi}_s{sc}_expand"] = RT.shen_expand(w, space, 12)
+            out[f"blk_f{fi}_s{sc}_mass"] = RT.mass_solve(w, space, 12, fam)
+    np.savez_compressed(os.path.join(OUT, "transforms.npz"), **out)
+
+
+if __name__ == "__main__":
+    matrices_fixture()
+    meta = solver_fixture()
+    base = baseline_fixture()
+    transforms_fixture()
+    with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
+        json.dump({"solver_cases": meta, "baseline": base,
+                   "generator": "tests/golden/make_golden.py from /root/reference/pkg/src (chebchan 0.1.0)",
+                   "numpy": np.__version__}, fh, indent=1)
+    print("golden fixtures written to", OUT)
