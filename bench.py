@@ -1,0 +1,421 @@
+"""Benchmark: batched fp64 Helmholtz + biharmonic solves (BASELINE config 4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c4|c5:N|c1] [--kx-rows R]
+
+One step = HelmholtzLU.solve + BiharmonicLU.solve over this rank's kx slab of
+the 2048 x 1025 wavenumber plane (n_x = 1024, nu = 1/2000, dt = 1e-4),
+complex128 N(0,1) right-hand sides resident in HBM (34 GB each at N = 1, far
+larger than L2, so no flush is needed between steps).  The LU objects are
+built once before timing, as the reference's stepper does (build time is
+reported separately).  Multi-GPU: one process per GPU, kx slabs, no
+collectives on the data path (weak scaling of the wavenumber plane would be
+'strong' here: the plane is fixed and split -- see "scaling").
+
+The reference arm (--impl reference) times the oracle port of the reference
+CPU algorithm (numpy, identical arithmetic) on all host cores over kx slabs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NU_C4, DT_C4 = 1 / 2000, 1e-4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--kx-rows", type=int, default=0, help="limit the kx rows per rank (debug)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg: str):
+    """(name, n_x, n_y, n_z, nu, dt)"""
+    if cfg == "c4":
+        return "config4: n_x=1024 (N=1025), 2048x1025 wavenumbers, nu=1/2000, dt=1e-4", 1024, 2048, 2048, NU_C4, DT_C4
+    if cfg.startswith("c5:"):
+        N = int(cfg[3:])
+        return f"config5: N={N}, 512x257 wavenumbers, nu=1/2000, dt=1e-4", N - 1, 512, 512, NU_C4, DT_C4
+    if cfg == "c1":
+        return "config1/2: n_x=63, 64x33 wavenumbers, nu=dt=1e-3", 63, 64, 64, 1e-3, 1e-3
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def slab_rows(n_y, rank, world):
+    lo = (n_y * rank) // world
+    hi = (n_y * (rank + 1)) // world
+    return lo, hi
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        smax = float(rows[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ======================================================================= B200 arm
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_03787_b200 import solvers as S
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import channel_z2
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name, n_x, n_y, n_z, nu, dt = workload(args.config)
+    z2_full = channel_z2(n_y, n_z)
+    lo, hi = slab_rows(n_y, rank, world)
+    if args.kx_rows:
+        hi = min(hi, lo + args.kx_rows)
+    z2 = np.ascontiguousarray(z2_full[lo:hi])
+    mats = assemble(n_x, 0)
+    dev = torch.device("cuda", local)
+
+    t0 = time.perf_counter()
+    hlu = S.build_helmholtz(mats, nu, dt, z2)
+    blu = S.build_biharmonic(mats, nu, dt, z2)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    # device-timed build (second build, warm)
+    eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eb0.record()
+    hlu = S.build_helmholtz(mats, nu, dt, z2)
+    blu = S.build_biharmonic(mats, nu, dt, z2)
+    eb1.record()
+    torch.cuda.synchronize()
+    build_ms = eb0.elapsed_time(eb1)
+
+    B = z2.size
+    nh, nb = mats.n_dir, mats.n_bih
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    fh = torch.randn((nh, B), dtype=torch.complex128, device=dev, generator=gen).mul_(np.sqrt(2.0))
+    fb = torch.randn((nb, B), dtype=torch.complex128, device=dev, generator=gen).mul_(np.sqrt(2.0))
+    xh = torch.empty_like(fh)
+    xb = torch.empty_like(fb)
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record()
+        hlu.solve_into(fh, xh, True)
+        if evs is not None:
+            evs[1].record()
+        blu.solve_into(fb, xb, True)
+        if evs is not None:
+            evs[2].record()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record()
+        for k in range(args.steps):
+            step(evs[k])
+        t_end.record()
+        torch.cuda.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    h_ms = np.mean([e[0].elapsed_time(e[1]) for e in evs])
+    b_ms = np.mean([e[1].elapsed_time(e[2]) for e in evs])
+    if world > 1:
+        t = torch.tensor([total_ms, h_ms, b_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, h_ms, b_ms = t.tolist()
+        bt = torch.tensor([B], dtype=torch.int64, device=dev)
+        dist.all_reduce(bt)
+        B_all = int(bt.item())
+    else:
+        B_all = B
+    unk_h = nh * B_all
+    unk_b = nb * B_all
+    value = (unk_h + unk_b) * args.steps / (total_ms / 1e3)
+
+    # correctness spot check on this rank (sampled systems vs the oracle)
+    parity = spot_parity(mats, nu, dt, z2, fh, xh, fb, xb) if rank == 0 else None
+
+    peak, peak_src = measured_peak()
+    bytes_h = 32.0 * nh * B  # per launch on this rank
+    bytes_b = 32.0 * nb * B
+    ach_h = bytes_h / (h_ms / 1e3) / 1e9
+    ach_b = bytes_b / (b_ms / 1e3) / 1e9
+    dom = "biharmonic" if b_ms >= h_ms else "helmholtz"
+    ach = ach_b if dom == "biharmonic" else ach_h
+    ckpt_bytes_h = 8.0 * hlu._ckpt.numel() if hlu._ckpt is not None else 0.0
+    ckpt_bytes_b = 8.0 * blu._ckpt.numel() if blu._ckpt is not None else 0.0
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e(S, mats, nu, dt, z2_full, n_y, args)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu = cpu_baseline(mats, nu, dt, z2_full)
+    if rank == 0:
+        line = {
+            "metric": "solved unknowns/s (batched fp64 Helmholtz+biharmonic); % of HBM roofline",
+            "value": value,
+            "unit": "unknowns/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64 (complex128 RHS/solution)",
+            "data": "synthetic: complex128 N(0,1) RHS (torch Philox, seed 1234+rank), z2 of the channel plane",
+            "config": {"workload": name, "systems_total": int(B_all), "kx_rows_per_rank": int(hi - lo),
+                       "modes": {"helmholtz": nh, "biharmonic": nb}, "parallelism": f"kx-slab x{world}",
+                       "l2_policy": "inputs (34 GB/operator at N=1) >> 126 MB L2; no flush needed",
+                       "lu": "built once before timing (stepper usage); build timed separately"},
+            "per_operator": {
+                "helmholtz": {"ms": h_ms, "unknowns_per_s": nh * B / (h_ms / 1e3), "GBps_alg": ach_h,
+                              "frac": ach_h / peak, "ckpt_read_bytes": ckpt_bytes_h},
+                "biharmonic": {"ms": b_ms, "unknowns_per_s": nb * B / (b_ms / 1e3), "GBps_alg": ach_b,
+                               "frac": ach_b / peak, "ckpt_read_bytes": ckpt_bytes_b},
+            },
+            "roofline": {"bound": "hbm", "kernel": f"{dom} chunked solve", "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes": "32 B per complex unknown (16 B RHS read + 16 B solution write)"},
+            "build_ms": build_ms,
+            "build_wall_s_first": build_s,
+            "parity": parity,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def spot_parity(mats, nu, dt, z2, fh, xh, fb, xb):
+    from oracle import shen_oracle as O
+
+    flat = z2.reshape(-1)
+    idx = np.unique(np.concatenate([np.argsort(flat)[-4:], np.linspace(0, flat.size - 1, 12).astype(int)]))
+    z = flat[idx]
+    it = __import__("torch").from_numpy(idx).to(fh.device)
+    f1 = fh[:, it].cpu().numpy()
+    x1 = xh[:, it].cpu().numpy()
+    f2 = fb[:, it].cpu().numpy()
+    x2 = xb[:, it].cpu().numpy()
+    rh = O.helmholtz_solve(O.helmholtz_factor(mats, nu, dt, z), f1)
+    rb = O.biharmonic_solve(O.biharmonic_factor(mats, nu, dt, z), f2)
+    resid = max(float(O.residual_longdouble(O.dense_biharmonic(mats, nu, dt, z[j]), x2[:, j], f2[:, j]))
+                for j in range(len(z)))
+    resid_ref = max(float(O.residual_longdouble(O.dense_biharmonic(mats, nu, dt, z[j]), rb[:, j], f2[:, j]))
+                    for j in range(len(z)))
+    return {"systems_checked": int(len(z)), "helmholtz_max_rel": float(O.max_rel_per_system(x1, rh).max()),
+            "biharmonic_max_rel": float(O.max_rel_per_system(x2, rb).max()),
+            "biharmonic_residual_max": resid, "reference_residual_max_same_systems": resid_ref}
+
+
+def run_e2e(S, mats, nu, dt, z2_full, n_y, args):
+    """Same metric through the public numpy API: host RHS -> H2D -> solve ->
+    D2H every step (pinned staging inside solve()).  Bounded sample: 64 kx
+    rows (65,600 systems; 1.07 GB per operator RHS)."""
+    import torch
+
+    rows = 64
+    z2 = np.ascontiguousarray(z2_full[:rows])
+    hlu = S.build_helmholtz(mats, nu, dt, z2)
+    blu = S.build_biharmonic(mats, nu, dt, z2)
+    rng = np.random.default_rng(5)
+    fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
+    fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
+    for _ in range(2):
+        hlu.solve(fh)
+        blu.solve(fb)
+    torch.cuda.synchronize()
+    steps = 3
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        xh = hlu.solve(fh)
+        xb = blu.solve(fb)
+    torch.cuda.synchronize()
+    dt_s = (time.perf_counter() - t0) / steps
+    unk = (mats.n_dir + mats.n_bih) * z2.size
+    return {"value": unk / dt_s, "unit": "unknowns/s", "h2d_bytes_per_step": int(fh.nbytes + fb.nbytes),
+            "d2h_bytes_per_step": int(xh.nbytes + xb.nbytes), "sample": f"{rows} kx rows x 1025 (numpy in/out)",
+            "path": "HelmholtzLU.solve / BiharmonicLU.solve with numpy arrays (wall clock incl. copies)"}
+
+
+def cpu_baseline(mats, nu, dt, z2_full):
+    """Oracle port (numpy, reference arithmetic) on one host core, bounded
+    sample of the same workload: 48 kx rows x 1025 systems."""
+    from oracle import shen_oracle as O
+
+    rows = 48
+    z2 = np.ascontiguousarray(z2_full[:rows])
+    rng = np.random.default_rng(6)
+    fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
+    fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
+    fh_f = O.helmholtz_factor(mats, nu, dt, z2)
+    fb_f = O.biharmonic_factor(mats, nu, dt, z2)
+    t0 = time.perf_counter()
+    O.helmholtz_solve(fh_f, fh)
+    O.biharmonic_solve(fb_f, fb)
+    t = time.perf_counter() - t0
+    unk = (mats.n_dir + mats.n_bih) * z2.size
+    return {"value": unk / t, "unit": "unknowns/s", "cores": 1, "kind": "port",
+            "sample": f"{rows} kx rows x 1025 systems of config 4, solve only (LU prebuilt), 1 thread"}
+
+
+# ======================================================================= reference arm
+
+def _ref_worker(task):
+    import os as _os
+
+    _os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import shen_oracle as O
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import channel_z2
+
+    cfg, lo, hi, seed = task
+    name, n_x, n_y, n_z, nu, dt = workload(cfg)
+    mats = assemble(n_x, 0)
+    z2 = np.ascontiguousarray(channel_z2(n_y, n_z)[lo:hi])
+    rng = np.random.default_rng(seed)
+    fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
+    fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
+    hf = O.helmholtz_factor(mats, nu, dt, z2)
+    bf = O.biharmonic_factor(mats, nu, dt, z2)
+    t0 = time.perf_counter()
+    O.helmholtz_solve(hf, fh)
+    O.biharmonic_solve(bf, fb)
+    return (mats.n_dir + mats.n_bih) * z2.size, time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    name, n_x, n_y, n_z, nu, dt = workload(args.config)
+    cores = os.cpu_count() or 1
+    rows_per_task = 2
+    ctx = mp.get_context("spawn")
+    results = []
+    with ctx.Pool(cores) as pool:
+        tasks = [(args.config, (r * rows_per_task) % n_y, (r * rows_per_task) % n_y + rows_per_task, r)
+                 for r in range(cores)]
+        for _ in range(max(args.warmup, 0)):
+            pool.map(_ref_worker, tasks)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            results.extend(pool.map(_ref_worker, tasks))
+        wall = time.perf_counter() - t0
+    unk = sum(r[0] for r in results)
+    value = unk / wall
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "solved unknowns/s (batched fp64 Helmholtz+biharmonic); % of HBM roofline",
+        "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)",
+        "data": "synthetic complex128 N(0,1)",
+        "config": {"workload": name, "sample_per_step": f"{cores} x {rows_per_task} kx rows x 1025 systems"},
+        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": cores, "kind": "port",
+                         "sample": f"each step: {cores} processes x {rows_per_task} kx rows of {name}; "
+                                   "oracle port of chebchan solve (numpy, identical arithmetic), LU prebuilt"},
+        "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)

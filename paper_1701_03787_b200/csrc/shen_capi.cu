@@ -54,6 +54,7 @@ int shen_pivot_reset(int* pivot_dev, void* stream) {
 int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
                      const double* md, int chunk_rows, double* ckpt, double* const* factors, int exact,
                      int* pivot_dev, void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md) return fail(SHEN_ERR_ARG, "shen_helm_factor: bad args");
   if (ckpt && chunk_rows <= 0) return fail(SHEN_ERR_ARG, "shen_helm_factor: ckpt needs chunk_rows > 0");
   shen::HelmFactorArgs a{};
@@ -72,6 +73,7 @@ int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, cons
 int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                             const double* st, const double* md, int chunk_rows, const double* ckpt,
                             const void* rhs, void* out, int is_complex, void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: bad args");
   const int rows0 = (n_dir + 1) / 2;
@@ -84,6 +86,7 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !factors || !rhs || !out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stored: bad args");
   shen::HelmSeqArgs a{};
   a.n_dir = n_dir; a.batch = batch; a.rhs = rhs; a.out = out;
@@ -96,6 +99,7 @@ int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factor
 int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                     const double* tab, int chunk_rows, double* ckpt, double* const* factors, int exact,
                     int* pivot_dev, void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab) return fail(SHEN_ERR_ARG, "shen_bih_factor: bad args");
   if (ckpt && chunk_rows <= 0) return fail(SHEN_ERR_ARG, "shen_bih_factor: ckpt needs chunk_rows > 0");
   shen::BihFactorArgs a{};
@@ -116,6 +120,7 @@ int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2,
 int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                            const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                            int is_complex, void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: bad args");
   const int rows0 = (n_bih + 1) / 2;
@@ -129,6 +134,7 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream) {
+  if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !q || !s || !factors || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stored: bad args");
   shen::BihSeqArgs a{};

@@ -44,7 +44,7 @@ def test_load_and_query_without_gpu():
 def test_argument_errors_are_reported():
     h = _lib.lib()
     # invalid sizes are rejected before any device work
-    st = h.shen_helm_factor(1, 0.0, None, 0, None, None, None, 0, None, None, 0, None, None)
+    st = h.shen_helm_factor(1, 0.0, None, 1, None, None, None, 0, None, None, 0, None, None)
     assert st == 1
     assert b"bad args" in h.shen_last_error()
 
