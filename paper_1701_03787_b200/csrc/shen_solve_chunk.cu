@@ -16,49 +16,23 @@
 //  pass 3  (rows backward) the reference back-substitution, row by row;
 //  fix     the estimate and what the right-hand neighbour actually
 //          produced differ by a few ulps; that inconsistency is pushed
-//          through two truncated neighbour steps and removed with a
+//          through SHEN_FIX_STEPS truncated neighbour steps and removed with a
 //          homogeneous correction sweep (keeps the residual at the
 //          reference's level; without it the biharmonic residual at
 //          BASELINE config 4 corners is ~10x the reference's).
 //
-// Global traffic: the RHS once in, the solution once out (32 B per complex
-// unknown) plus the chunk checkpoints (3 or 10 doubles per chunk).
+// The RHS rows of a chunk are prefetched into shared memory with cp.async
+// before the recurrences start, so no global latency sits inside the row
+// loops.  Global traffic: the RHS once in, the solution once out (32 B per
+// complex unknown) plus the chunk checkpoints (3 or 10 doubles per chunk).
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
 
 namespace shen {
 
-template <typename V> struct SlotsH { static constexpr int n = VOps<V>::ndouble + 4; };   // y, h, rd, e, t
-template <typename V> struct SlotsB { static constexpr int n = VOps<V>::ndouble + 7; };   // y, g1, g2, rd, e, f, a, b
-
-// per-warp row store: [row][slot][lane]
-struct RowStore {
-  double* base;
-  int lane;
-  __device__ __forceinline__ double& at(int r, int slot, int nslot) { return base[(r * nslot + slot) * 32 + lane]; }
-};
-
-template <typename V>
-__device__ __forceinline__ void put_v(RowStore& s, int r, int slot, int nslot, V v);
-template <>
-__device__ __forceinline__ void put_v<double>(RowStore& s, int r, int slot, int nslot, double v) {
-  s.at(r, slot, nslot) = v;
-}
-template <>
-__device__ __forceinline__ void put_v<cplx>(RowStore& s, int r, int slot, int nslot, cplx v) {
-  s.at(r, slot, nslot) = v.re;
-  s.at(r, slot + 1, nslot) = v.im;
-}
-template <typename V>
-__device__ __forceinline__ V get_v(RowStore& s, int r, int slot, int nslot);
-template <>
-__device__ __forceinline__ double get_v<double>(RowStore& s, int r, int slot, int nslot) {
-  return s.at(r, slot, nslot);
-}
-template <>
-__device__ __forceinline__ cplx get_v<cplx>(RowStore& s, int r, int slot, int nslot) {
-  return {s.at(r, slot, nslot), s.at(r, slot + 1, nslot)};
-}
+#ifndef SHEN_FIX_STEPS
+#define SHEN_FIX_STEPS 3  // truncated neighbour steps of the consistency fix
+#endif
 
 __device__ __forceinline__ cplx vfma(double s, cplx b, cplx a) { return {__fma_rn(s, b.re, a.re), __fma_rn(s, b.im, a.im)}; }
 __device__ __forceinline__ double vfma(double s, double b, double a) { return __fma_rn(s, b, a); }
@@ -72,30 +46,60 @@ template <typename V> __device__ __forceinline__ V vzero();
 template <> __device__ __forceinline__ double vzero<double>() { return 0.0; }
 template <> __device__ __forceinline__ cplx vzero<cplx>() { return {0.0, 0.0}; }
 
+// ---------------------------------------------------------------- async copies
+__device__ __forceinline__ void cp_async_v(cplx* dst, const cplx* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_v(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+
 // ======================================================================= Helmholtz
+// smem: table [R][3][32] (shared by the CTA, one parity per CTA), then per
+// warp: Y [R][32] (RHS -> y -> x, lane-contiguous V) and S [R][4][32]
+// (h, 1/d, e, t).
 template <typename V>
 __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
   using O = VOps<V>;
-  constexpr int NS = SlotsH<V>::n;
-  constexpr int SY = 0, SH = O::ndouble, SRD = SH + 1, SE = SH + 2, ST = SH + 3;
+  constexpr int ND = O::ndouble;
+  constexpr int SH = 0, SRD = 1, SE = 2, ST = 3, NS = 4;
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int par = blockIdx.y;
   const int64_t j = (int64_t)blockIdx.x * nwarp + warp;
-  if (j >= a.batch) return;
   const int64_t B = a.batch;
   const int R = a.chunk_rows;
   const int n = (a.n_dir - par + 1) / 2;
   const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
+  double* tab = smem;
+  for (int idx = threadIdx.x; idx < R * 32; idx += blockDim.x) {
+    const int r = idx >> 5, c = idx & 31, i = c * R + r;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    if (i < n) {
+      const int k = par + 2 * i;
+      v0 = __ldg(a.sd + k); v1 = __ldg(a.st + k); v2 = __ldg(a.md + k);
+    }
+    tab[(r * 3 + 0) * 32 + c] = v0;
+    tab[(r * 3 + 1) * 32 + c] = v1;
+    tab[(r * 3 + 2) * 32 + c] = v2;
+  }
+  __syncthreads();
+  if (j >= B) return;
   const int s0 = lane * R;
   const int nr = max(0, min(R, n - s0));
-  RowStore rs{smem + (size_t)warp * R * NS * 32, lane};
+  double* wb = smem + R * 3 * 32 + (size_t)warp * R * 32 * (ND + NS);
+  V* Ys = reinterpret_cast<V*>(wb);
+  double* Ss = wb + R * 32 * ND;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
+  for (int r = 0; r < nr; ++r) cp_async_v(Ys + r * 32 + lane, rhs + (int64_t)(par + 2 * (s0 + r)) * B + j);
   const double cb = __ldg(a.cb + j);
   const double sub = __dmul_rn(cb, -1.5707963267948966);
-
-  // ---- pass 1
   HelmState st{0, 0, 0, 0};
   if (s0 > 0 && nr > 0) {
     const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + j;
@@ -104,18 +108,20 @@ __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
     st.t = ck[2 * B];
     st.rd = __drcp_rn(st.d);
   }
+  cp_async_wait_all();
+
+  // ---- pass 1
   V y = vzero<V>();
   double h = 1.0;
   double p00 = 1.0, p01 = 0.0, p10 = 0.0, p11 = 1.0;
   V t0a = vzero<V>(), t0b = vzero<V>();
   double t1a = 0.0, t1b = 0.0;
-  // issue the chunk's RHS loads up front (independent of the recurrence)
   for (int r = 0; r < nr; ++r) {
     const int i = s0 + r;
-    const int k = par + 2 * i;
-    HelmRow row = helm_row(a.ca, cb, sub, __ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsup);
+    HelmRow row = helm_row(a.ca, cb, sub, tab[(r * 3 + 0) * 32 + lane], tab[(r * 3 + 1) * 32 + lane],
+                           tab[(r * 3 + 2) * 32 + lane], i < nsup);
     const double low = helm_step<false>(st, row, sub, i == 0);
-    const V b = O::ld_cs(rhs + (int64_t)k * B + j);
+    const V b = Ys[r * 32 + lane];
     if (i == 0) {
       y = b;
       h = 0.0;
@@ -123,11 +129,11 @@ __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
       y = vfma(-low, y, b);
       h = -low * h;
     }
-    put_v<V>(rs, r, SY, NS, y);
-    rs.at(r, SH, NS) = h;
-    rs.at(r, SRD, NS) = st.rd;
-    rs.at(r, SE, NS) = st.e;
-    rs.at(r, ST, NS) = st.t;
+    Ys[r * 32 + lane] = y;
+    Ss[(r * NS + SH) * 32 + lane] = h;
+    Ss[(r * NS + SRD) * 32 + lane] = st.rd;
+    Ss[(r * NS + SE) * 32 + lane] = st.e;
+    Ss[(r * NS + ST) * 32 + lane] = st.t;
     const double al = -st.rd * st.e, be = -st.rd * st.t;
     const V cy = vmul(st.rd, y);
     const double ch = st.rd * h;
@@ -157,7 +163,6 @@ __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
 
   // ---- scan B: sigma_s = P sigma_{s+R} + tau, suffix over lanes
   V ta = vfma(t1a, E, t0a), tb = vfma(t1b, E, t0b);
-  // tau is complex, t1 real: vfma(real, V, V) with real multiplier t1 times E
   const double o00 = p00, o01 = p01, o10 = p10, o11 = p11;
   {
     double q00 = p00, q01 = p01, q10 = p10, q11 = p11;
@@ -178,50 +183,51 @@ __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
     ta = ua;
     tb = ub;
   }
-  // ta/tb: estimated state entering this chunk from the left view = sigma_est(c)
   V x1 = shfl_down_v(ta, 1), S = shfl_down_v(tb, 1);
   if (lane == 31) { x1 = vzero<V>(); S = vzero<V>(); }
 
   // ---- pass 3: reference back-substitution
   for (int r = nr - 1; r >= 0; --r) {
-    const V y0 = get_v<V>(rs, r, SY, NS);
-    const double hh = rs.at(r, SH, NS);
-    const V yy = vfma(hh, E, y0);
-    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), t = rs.at(r, ST, NS);
+    const double hh = Ss[(r * NS + SH) * 32 + lane];
+    const V yy = vfma(hh, E, Ys[r * 32 + lane]);
+    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                 t = Ss[(r * NS + ST) * 32 + lane];
     const V acc = vsub(vsub(yy, vmul(e, x1)), vmul(t, S));
     const V x = vmul(rd, acc);
     S = vadd(x1, S);
     x1 = x;
-    put_v<V>(rs, r, SY, NS, x);
+    Ys[r * 32 + lane] = x;
   }
-  // ---- fix: delta = actual - estimated entering state, 2 truncated neighbour steps
+  // ---- fix: delta = actual - estimated entering state, truncated neighbour steps
   const V da = vsub(x1, ta), db = vsub(S, tb);
-  V wa = shfl_down_v(da, 1), wb = shfl_down_v(db, 1);
-  if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
-  V w1a = vfma(o00, wa, vfma(o01, wb, da)), w1b = vfma(o10, wa, vfma(o11, wb, db));
-  wa = shfl_down_v(w1a, 1); wb = shfl_down_v(w1b, 1);
-  if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
-  V w2a = vfma(o00, wa, vfma(o01, wb, da)), w2b = vfma(o10, wa, vfma(o11, wb, db));
-  V xc1 = shfl_down_v(w2a, 1), Sc = shfl_down_v(w2b, 1);
-  if (lane == 31) { xc1 = vzero<V>(); Sc = vzero<V>(); }
+  V wa = shfl_down_v(da, 1), wb2 = shfl_down_v(db, 1);
+  if (lane == 31) { wa = vzero<V>(); wb2 = vzero<V>(); }
+#pragma unroll
+  for (int it = 0; it < SHEN_FIX_STEPS; ++it) {
+    const V w1a = vfma(o00, wa, vfma(o01, wb2, da)), w1b = vfma(o10, wa, vfma(o11, wb2, db));
+    wa = shfl_down_v(w1a, 1);
+    wb2 = shfl_down_v(w1b, 1);
+    if (lane == 31) { wa = vzero<V>(); wb2 = vzero<V>(); }
+  }
+  V xc1 = wa, Sc = wb2;
   for (int r = nr - 1; r >= 0; --r) {
     const int k = par + 2 * (s0 + r);
-    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), t = rs.at(r, ST, NS);
+    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                 t = Ss[(r * NS + ST) * 32 + lane];
     const V xc = vmul(-rd, vfma(e, xc1, vmul(t, Sc)));
     Sc = vadd(xc1, Sc);
     xc1 = xc;
-    const V x = vadd(get_v<V>(rs, r, SY, NS), xc);
-    O::st_cs(out + (int64_t)k * B + j, x);
+    O::st_cs(out + (int64_t)k * B + j, vadd(Ys[r * 32 + lane], xc));
   }
 }
 
 // ======================================================================= biharmonic
+// smem per warp: Y [R][32] V, S [R][NS][32] doubles, P_own [16][32].
 template <typename V>
 __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
   using O = VOps<V>;
-  constexpr int NS = SlotsB<V>::n;
-  constexpr int SY = 0, SG1 = O::ndouble, SG2 = SG1 + 1, SRD = SG1 + 2, SE = SG1 + 3, SF = SG1 + 4, SA = SG1 + 5,
-                SB = SG1 + 6;
+  constexpr int ND = O::ndouble;
+  constexpr int SG1 = 0, SG2 = 1, SRD = 2, SE = 3, SF = 4, SA = 5, SB = 6, SQN = 7, SSN = 8, NS = 9;
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int par = blockIdx.y;
@@ -232,11 +238,13 @@ __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
   const int n = (a.n_bih - par + 1) / 2;
   const int s0 = lane * R;
   const int nr = max(0, min(R, n - s0));
-  double* wbase = smem + (size_t)warp * (R * NS * 32 + 16 * 32);
-  RowStore rs{wbase, lane};
-  double* pown = wbase + R * NS * 32;  // [16][32] own transfer matrix
+  double* wb = smem + (size_t)warp * (R * 32 * (ND + NS) + 16 * 32);
+  V* Ys = reinterpret_cast<V*>(wb);
+  double* Ss = wb + R * 32 * ND;
+  double* pown = Ss + R * NS * 32;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
+  for (int r = 0; r < nr; ++r) cp_async_v(Ys + r * 32 + lane, rhs + (int64_t)(par + 2 * (s0 + r)) * B + j);
   const double xi0 = a.xi0, xi1 = __ldg(a.xi1 + j), xi2 = __ldg(a.xi2 + j);
 
   BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
@@ -259,34 +267,45 @@ __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
 #pragma unroll
   for (int r = 0; r < 4; ++r) { t0[r] = vzero<V>(); t1[r] = 0.0; t2[r] = 0.0; }
 
+  double cn[B_NCOL];
+  if (nr > 0) {
+#pragma unroll
+    for (int q = 0; q < B_NCOL; ++q) cn[q] = __ldg(a.tab + (int64_t)(par + 2 * s0) * B_NCOL + q);
+  }
+  cp_async_wait_all();
   for (int r = 0; r < nr; ++r) {
     const int i = s0 + r;
-    const int k = par + 2 * i;
     double c[B_NCOL];
 #pragma unroll
-    for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+    for (int q = 0; q < B_NCOL; ++q) c[q] = cn[q];
+    if (r + 1 < nr) {
+#pragma unroll
+      for (int q = 0; q < B_NCOL; ++q) cn[q] = __ldg(a.tab + (int64_t)(par + 2 * (i + 1)) * B_NCOL + q);
+    }
     const BihBands hb = bih_bands(xi0, xi1, xi2, c);
     double l2, l4;
     bih_step<false>(u, u1, u2, hb, c, xi0, i, l2, l4);
     u2 = u1;
     u1 = u;
-    const V b = O::ld_cs(rhs + (int64_t)k * B + j);
+    const V b = Ys[r * 32 + lane];
     const V y = vfma(-l4, yp2, vfma(-l2, yp1, b));
     const double g1 = -fma(l2, h11, l4 * h21), g2 = -fma(l2, h12, l4 * h22);
     yp2 = yp1; yp1 = y;
     h21 = h11; h22 = h12; h11 = g1; h12 = g2;
-    put_v<V>(rs, r, SY, NS, y);
-    rs.at(r, SG1, NS) = g1;
-    rs.at(r, SG2, NS) = g2;
-    rs.at(r, SRD, NS) = u.rd;
-    rs.at(r, SE, NS) = u.e;
-    rs.at(r, SF, NS) = u.f;
-    rs.at(r, SA, NS) = u.a;
-    rs.at(r, SB, NS) = u.b;
+    Ys[r * 32 + lane] = y;
+    Ss[(r * NS + SG1) * 32 + lane] = g1;
+    Ss[(r * NS + SG2) * 32 + lane] = g2;
+    Ss[(r * NS + SRD) * 32 + lane] = u.rd;
+    Ss[(r * NS + SE) * 32 + lane] = u.e;
+    Ss[(r * NS + SF) * 32 + lane] = u.f;
+    Ss[(r * NS + SA) * 32 + lane] = u.a;
+    Ss[(r * NS + SB) * 32 + lane] = u.b;
+    const double qn = c[B_Q4], sn = c[B_S4];
+    Ss[(r * NS + SQN) * 32 + lane] = qn;
+    Ss[(r * NS + SSN) * 32 + lane] = sn;
     // backward transfer of this row, accumulated left to right
     const double al = -u.rd * u.e, be = -u.rd * u.f;
     const double ga = -u.rd * (xi0 * u.a), de = -u.rd * (xi0 * u.b);
-    const double qn = c[B_Q4], sn = c[B_S4];
     const V cy = vmul(u.rd, y);
     const double cg1 = u.rd * g1, cg2 = u.rd * g2;
 #pragma unroll
@@ -308,10 +327,10 @@ __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
 #pragma unroll
   for (int dd = 1; dd < 32; dd <<= 1) {
     const double g0 = shfl_up_d(H0, dd), g1 = shfl_up_d(H1, dd), g2 = shfl_up_d(H2, dd), g3 = shfl_up_d(H3, dd);
-    const V wa = shfl_up_v(Ya, dd), wb = shfl_up_v(Yb, dd);
+    const V wa = shfl_up_v(Ya, dd), wb3 = shfl_up_v(Yb, dd);
     if (lane >= dd) {
-      Ya = vfma(H0, wa, vfma(H1, wb, Ya));
-      Yb = vfma(H2, wa, vfma(H3, wb, Yb));
+      Ya = vfma(H0, wa, vfma(H1, wb3, Ya));
+      Yb = vfma(H2, wa, vfma(H3, wb3, Yb));
       const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
       const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
       H0 = n0; H1 = n1; H2 = n2; H3 = n3;
@@ -365,31 +384,31 @@ __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
   // ---- pass 3: reference back-substitution (Alg. 4 order)
   V x1 = sg[0], x2 = sg[1], sq = sg[2], sv = sg[3];
   for (int r = nr - 1; r >= 0; --r) {
-    const int k = par + 2 * (s0 + r);
-    const V y0 = get_v<V>(rs, r, SY, NS);
-    const V yy = vfma(rs.at(r, SG1, NS), E1, vfma(rs.at(r, SG2, NS), E2, y0));
-    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), f = rs.at(r, SF, NS);
-    const double av = rs.at(r, SA, NS), bv = rs.at(r, SB, NS);
+    const V yy = vfma(Ss[(r * NS + SG1) * 32 + lane], E1, vfma(Ss[(r * NS + SG2) * 32 + lane], E2, Ys[r * 32 + lane]));
+    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                 f = Ss[(r * NS + SF) * 32 + lane];
+    const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
     V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
     acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
     const V x = vmul(rd, acc);
-    const double qn = __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4), sn = __ldg(a.tab + (int64_t)k * B_NCOL + B_S4);
+    const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
     sq = vfma(qn, x2, sq);
     sv = vfma(sn, x2, sv);
     x2 = x1;
     x1 = x;
-    put_v<V>(rs, r, SY, NS, x);
+    Ys[r * 32 + lane] = x;
   }
   // ---- fix
   V dl[4] = {vsub(x1, tau[0]), vsub(x2, tau[1]), vsub(sq, tau[2]), vsub(sv, tau[3])};
-  V w[4], wn[4];
+  V wn[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     wn[q] = shfl_down_v(dl[q], 1);
     if (lane == 31) wn[q] = vzero<V>();
   }
 #pragma unroll
-  for (int step = 0; step < 2; ++step) {
+  for (int step = 0; step < SHEN_FIX_STEPS; ++step) {
+    V w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       V acc = dl[q];
@@ -406,24 +425,25 @@ __global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
   V c1 = wn[0], c2 = wn[1], cq = wn[2], cs = wn[3];
   for (int r = nr - 1; r >= 0; --r) {
     const int k = par + 2 * (s0 + r);
-    const double rd = rs.at(r, SRD, NS), e = rs.at(r, SE, NS), f = rs.at(r, SF, NS);
-    const double av = rs.at(r, SA, NS), bv = rs.at(r, SB, NS);
+    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                 f = Ss[(r * NS + SF) * 32 + lane];
+    const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
     const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
     const V xc = vmul(-rd, acc);
-    const double qn = __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4), sn = __ldg(a.tab + (int64_t)k * B_NCOL + B_S4);
+    const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
     cq = vfma(qn, c2, cq);
     cs = vfma(sn, c2, cs);
     c2 = c1;
     c1 = xc;
-    O::st_cs(out + (int64_t)k * B + j, vadd(get_v<V>(rs, r, SY, NS), xc));
+    O::st_cs(out + (int64_t)k * B + j, vadd(Ys[r * 32 + lane], xc));
   }
 }
 
 static size_t helm_smem(int R, int nwarp, bool cplx_rhs) {
-  return (size_t)nwarp * R * (cplx_rhs ? SlotsH<cplx>::n : SlotsH<double>::n) * 32 * sizeof(double);
+  return ((size_t)R * 3 * 32 + (size_t)nwarp * R * 32 * ((cplx_rhs ? 2 : 1) + 4)) * sizeof(double);
 }
 static size_t bih_smem(int R, int nwarp, bool cplx_rhs) {
-  return (size_t)nwarp * (R * (cplx_rhs ? SlotsB<cplx>::n : SlotsB<double>::n) * 32 + 16 * 32) * sizeof(double);
+  return (size_t)nwarp * ((size_t)R * 32 * ((cplx_rhs ? 2 : 1) + 9) + 16 * 32) * sizeof(double);
 }
 
 template <typename K>
