@@ -24,25 +24,43 @@ __global__ void __launch_bounds__(256) helm_factor_kernel(HelmFactorArgs a) {
   const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
   const double cb = __ldg(a.cb + j);
   const double sub = __dmul_rn(cb, -1.5707963267948966);  // cb * (-pi/2)
-  HelmState s{0, 0, 0, 0};
   const int64_t B = a.batch;
+  const int R = a.chunk_rows > 0 ? a.chunk_rows : (1 << 30);
+  HelmState s{0, 0, 0, 0};
+  HelmProj pj{0, 0, 0, 0, 0};
+  double dl = 0.0, el = 0.0, tl = 0.0;  // ratios of the last row (fast mode)
   for (int i = 0; i < n; ++i) {
     const int k = par + 2 * i;
     HelmRow h = helm_row(a.ca, cb, sub, __ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsup);
-    double low = helm_step<EXACT>(s, h, sub, i == 0);
-    note_pivot(a.pivot, par, i, s.d);
+    double low, d, e, t;
+    if (EXACT) {
+      low = helm_step<true>(s, h, sub, i == 0);
+      d = s.d; e = s.e; t = s.t;
+    } else {
+      const int r = i % R;
+      if (i == 0) {
+        hp_first(pj, h);
+        low = 0.0; d = h.diag; e = h.sup; t = h.tail;
+      } else {
+        if (r == 0) hp_start(pj, dl, el, tl);
+        else if ((r & 7) == 0) hp_rescale(pj);
+        low = hp_step(pj, h, sub, d, e, t);
+      }
+      dl = d; el = e; tl = t;
+    }
+    note_pivot(a.pivot, par, i, d);
     if (a.low[par] != nullptr) {
       if (i > 0) a.low[par][(int64_t)(i - 1) * B + j] = low;
-      a.d[par][(int64_t)i * B + j] = s.d;
-      a.e[par][(int64_t)i * B + j] = s.e;
-      a.t[par][(int64_t)i * B + j] = s.t;
+      a.d[par][(int64_t)i * B + j] = d;
+      a.e[par][(int64_t)i * B + j] = e;
+      a.t[par][(int64_t)i * B + j] = t;
     }
-    if (a.ckpt != nullptr && a.chunk_rows > 0 && (i + 1) % a.chunk_rows == 0 && i + 1 < n) {
-      const int c = (i + 1) / a.chunk_rows;
+    if (a.ckpt != nullptr && (i + 1) % R == 0 && i + 1 < n) {
+      const int c = (i + 1) / R;
       double* base = a.ckpt + ((int64_t)(c * 2 + par) * 3) * B + j;
-      base[0] = s.d;
-      base[B] = s.e;
-      base[2 * B] = s.t;
+      base[0] = d;
+      base[B] = e;
+      base[2 * B] = t;
     }
   }
 }

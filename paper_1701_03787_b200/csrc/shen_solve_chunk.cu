@@ -1,14 +1,17 @@
 // Chunk-parallel fused factor+solve for the wall-normal systems.
 //
-// One warp owns one (wavenumber system, parity); its 32 lanes own 32
-// consecutive chunks of R rows.  Per lane, in registers + shared memory:
+// One warp owns one (wavenumber system, parity) at a time; its 32 lanes own
+// 32 consecutive chunks of R rows (R a compile-time power of two, so every
+// row loop is fully unrolled).  Warps are persistent: while a warp works on
+// system j, the RHS rows of its next system are already streaming into the
+// second half of a double-buffered shared-memory tile (cp.async), so global
+// latency never sits on the recurrences.  Per system, per lane:
 //
 //  pass 1  (rows forward)  recompute the compressed-LU rows from the
-//          chunk's checkpoint (same recurrence as the build kernel, so the
-//          factors are bit-identical), form the forward particular
-//          solution y0 with zero entry and its homogeneous responses, and
-//          accumulate the chunk's backward transfer  sigma_s = P sigma_{s+R}
-//          + tau  (sigma = back-substitution state), all in one sweep;
+//          chunk's checkpoint (same arithmetic as the build kernel, hence
+//          bit-identical factors), form the forward particular solution y0
+//          with zero entry and its homogeneous responses, and accumulate the
+//          chunk's backward transfer  sigma_s = P sigma_{s+R} + tau;
 //  scan F  warp shuffle scan (Hillis-Steele) of the forward affine maps ->
 //          the y entering every chunk;
 //  scan B  warp shuffle suffix scan of the backward maps -> estimated
@@ -17,14 +20,15 @@
 //  fix     the estimate and what the right-hand neighbour actually
 //          produced differ by a few ulps; that inconsistency is pushed
 //          through SHEN_FIX_STEPS truncated neighbour steps and removed with a
-//          homogeneous correction sweep (keeps the residual at the
-//          reference's level; without it the biharmonic residual at
-//          BASELINE config 4 corners is ~10x the reference's).
+//          homogeneous correction sweep while the solution is streamed out
+//          (keeps the residual at the reference's level; without it the
+//          biharmonic residual at BASELINE config 4 corners is ~10x the
+//          reference's).
 //
-// The RHS rows of a chunk are prefetched into shared memory with cp.async
-// before the recurrences start, so no global latency sits inside the row
-// loops.  Global traffic: the RHS once in, the solution once out (32 B per
-// complex unknown) plus the chunk checkpoints (3 or 10 doubles per chunk).
+// Global traffic: the RHS once in, the solution once out (32 B per complex
+// unknown) plus the chunk checkpoints (3 or 10 doubles per chunk).
+#include <algorithm>
+
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
 
@@ -55,25 +59,31 @@ __device__ __forceinline__ void cp_async_v(double* dst, const double* src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// issue the RHS rows of this lane's chunk of system j into Y (one commit group)
+template <typename V, int R>
+__device__ __forceinline__ void prefetch_rows(V* Y, const V* rhs, int64_t B, int64_t j, int par, int s0, int nr,
+                                              int lane) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr) cp_async_v(Y + r * 32 + lane, rhs + (int64_t)(par + 2 * (s0 + r)) * B + j);
+  cp_async_commit();
 }
 
 // ======================================================================= Helmholtz
-// smem: table [R][3][32] (shared by the CTA, one parity per CTA), then per
-// warp: Y [R][32] (RHS -> y -> x, lane-contiguous V) and S [R][4][32]
-// (h, 1/d, e, t).
-template <typename V>
-__global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
+// smem: table [R][3][32] (one parity per CTA, loaded once), then per warp
+// Y [2][R][32] V (double-buffered RHS -> y -> x).  The per-row factor data
+// (h, 1/d, e, t) lives in registers (fully unrolled rows).
+template <typename V, int R>
+__global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
   using O = VOps<V>;
-  constexpr int ND = O::ndouble;
-  constexpr int SH = 0, SRD = 1, SE = 2, ST = 3, NS = 4;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int par = blockIdx.y;
-  const int64_t j = (int64_t)blockIdx.x * nwarp + warp;
   const int64_t B = a.batch;
-  const int R = a.chunk_rows;
   const int n = (a.n_dir - par + 1) / 2;
   const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
   double* tab = smem;
@@ -89,395 +99,443 @@ __global__ void __launch_bounds__(128) helm_chunk_kernel(HelmChunkArgs a) {
     tab[(r * 3 + 2) * 32 + c] = v2;
   }
   __syncthreads();
-  if (j >= B) return;
   const int s0 = lane * R;
   const int nr = max(0, min(R, n - s0));
-  double* wb = smem + R * 3 * 32 + (size_t)warp * R * 32 * (ND + NS);
-  V* Ys = reinterpret_cast<V*>(wb);
-  double* Ss = wb + R * 32 * ND;
+  V* Ybuf = reinterpret_cast<V*>(smem + R * 3 * 32) + (size_t)warp * 2 * R * 32;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
-  for (int r = 0; r < nr; ++r) cp_async_v(Ys + r * 32 + lane, rhs + (int64_t)(par + 2 * (s0 + r)) * B + j);
-  const double cb = __ldg(a.cb + j);
-  const double sub = __dmul_rn(cb, -1.5707963267948966);
-  HelmState st{0, 0, 0, 0};
-  if (s0 > 0 && nr > 0) {
-    const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + j;
-    st.d = ck[0];
-    st.e = ck[B];
-    st.t = ck[2 * B];
-    st.rd = __drcp_rn(st.d);
-  }
-  cp_async_wait_all();
-
-  // ---- pass 1
-  V y = vzero<V>();
-  double h = 1.0;
-  double p00 = 1.0, p01 = 0.0, p10 = 0.0, p11 = 1.0;
-  V t0a = vzero<V>(), t0b = vzero<V>();
-  double t1a = 0.0, t1b = 0.0;
-  for (int r = 0; r < nr; ++r) {
-    const int i = s0 + r;
-    HelmRow row = helm_row(a.ca, cb, sub, tab[(r * 3 + 0) * 32 + lane], tab[(r * 3 + 1) * 32 + lane],
-                           tab[(r * 3 + 2) * 32 + lane], i < nsup);
-    const double low = helm_step<false>(st, row, sub, i == 0);
-    const V b = Ys[r * 32 + lane];
-    if (i == 0) {
-      y = b;
-      h = 0.0;
-    } else {
-      y = vfma(-low, y, b);
-      h = -low * h;
+  const int64_t stride = (int64_t)gridDim.x * nwarp;
+  int64_t j = (int64_t)blockIdx.x * nwarp + warp;
+  if (j < B) prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+  int buf = 0;
+  for (; j < B; j += stride, buf ^= 1) {
+    V* Ys = Ybuf + buf * R * 32;
+    const int64_t jn = j + stride;
+    if (jn < B) prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
+    const double cb = __ldg(a.cb + j);
+    const double sub = __dmul_rn(cb, -1.5707963267948966);
+    HelmProj pj{0, 0, 0, 0, 0};
+    if (s0 > 0 && nr > 0) {
+      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + j;
+      hp_start(pj, __ldg(ck), __ldg(ck + B), __ldg(ck + 2 * B));
     }
-    Ys[r * 32 + lane] = y;
-    Ss[(r * NS + SH) * 32 + lane] = h;
-    Ss[(r * NS + SRD) * 32 + lane] = st.rd;
-    Ss[(r * NS + SE) * 32 + lane] = st.e;
-    Ss[(r * NS + ST) * 32 + lane] = st.t;
-    const double al = -st.rd * st.e, be = -st.rd * st.t;
-    const V cy = vmul(st.rd, y);
-    const double ch = st.rd * h;
-    t0a = vfma(p00, cy, t0a);
-    t0b = vfma(p10, cy, t0b);
-    t1a = fma(p00, ch, t1a);
-    t1b = fma(p10, ch, t1b);
-    const double n00 = fma(p00, al, p01), n01 = fma(p00, be, p01);
-    const double n10 = fma(p10, al, p11), n11 = fma(p10, be, p11);
-    p00 = n00; p01 = n01; p10 = n10; p11 = n11;
-  }
+    if (jn < B) cp_async_wait<1>(); else cp_async_wait<0>();
 
-  // ---- scan F: exit_c = Y_c + m_c * exit_{c-1}
-  double m = h;
-  V Y = y;
+    // ---- pass 1
+    double h_[R], rd_[R], e_[R], t_[R];
+    V y = vzero<V>();
+    double h = 1.0;
+    double p00 = 1.0, p01 = 0.0, p10 = 0.0, p11 = 1.0;
+    V t0a = vzero<V>(), t0b = vzero<V>();
+    double t1a = 0.0, t1b = 0.0;
 #pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    const double mb = shfl_up_d(m, dd);
-    const V Yb = shfl_up_v(Y, dd);
-    if (lane >= dd) {
-      Y = vfma(m, Yb, Y);
-      m = m * mb;
-    }
-  }
-  V E = shfl_up_v(Y, 1);
-  if (lane == 0) E = vzero<V>();
-
-  // ---- scan B: sigma_s = P sigma_{s+R} + tau, suffix over lanes
-  V ta = vfma(t1a, E, t0a), tb = vfma(t1b, E, t0b);
-  const double o00 = p00, o01 = p01, o10 = p10, o11 = p11;
-  {
-    double q00 = p00, q01 = p01, q10 = p10, q11 = p11;
-    V ua = ta, ub = tb;
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      const double r00 = shfl_down_d(q00, dd), r01 = shfl_down_d(q01, dd);
-      const double r10 = shfl_down_d(q10, dd), r11 = shfl_down_d(q11, dd);
-      const V va = shfl_down_v(ua, dd), vb = shfl_down_v(ub, dd);
-      if (lane + dd < 32) {
-        ua = vfma(q00, va, vfma(q01, vb, ua));
-        ub = vfma(q10, va, vfma(q11, vb, ub));
-        const double n00 = fma(q00, r00, q01 * r10), n01 = fma(q00, r01, q01 * r11);
-        const double n10 = fma(q10, r00, q11 * r10), n11 = fma(q10, r01, q11 * r11);
-        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+    for (int r = 0; r < R; ++r) {
+      h_[r] = 0.0; rd_[r] = 0.0; e_[r] = 0.0; t_[r] = 0.0;
+      if (r < nr) {
+        const int i = s0 + r;
+        const HelmRow row = helm_row(a.ca, cb, sub, tab[(r * 3 + 0) * 32 + lane], tab[(r * 3 + 1) * 32 + lane],
+                                     tab[(r * 3 + 2) * 32 + lane], i < nsup);
+        const V b = Ys[r * 32 + lane];
+        double e, t;
+        if (i == 0) {
+          hp_first(pj, row);
+          e = row.sup;
+          t = row.tail;
+          y = b;
+          h = 0.0;
+        } else {
+          if (r > 0 && (r & 7) == 0) hp_rescale(pj);
+          double d;
+          const double low = hp_step(pj, row, sub, d, e, t);
+          y = vfma(-low, y, b);
+          h = -low * h;
+        }
+        const double rd = pj.rd;
+        Ys[r * 32 + lane] = y;
+        h_[r] = h; rd_[r] = rd; e_[r] = e; t_[r] = t;
+        const double al = -rd * e, be = -rd * t;
+        const V cy = vmul(rd, y);
+        const double ch = rd * h;
+        t0a = vfma(p00, cy, t0a);
+        t0b = vfma(p10, cy, t0b);
+        t1a = fma(p00, ch, t1a);
+        t1b = fma(p10, ch, t1b);
+        const double n00 = fma(p00, al, p01), n01 = fma(p00, be, p01);
+        const double n10 = fma(p10, al, p11), n11 = fma(p10, be, p11);
+        p00 = n00; p01 = n01; p10 = n10; p11 = n11;
       }
     }
-    ta = ua;
-    tb = ub;
-  }
-  V x1 = shfl_down_v(ta, 1), S = shfl_down_v(tb, 1);
-  if (lane == 31) { x1 = vzero<V>(); S = vzero<V>(); }
 
-  // ---- pass 3: reference back-substitution
-  for (int r = nr - 1; r >= 0; --r) {
-    const double hh = Ss[(r * NS + SH) * 32 + lane];
-    const V yy = vfma(hh, E, Ys[r * 32 + lane]);
-    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                 t = Ss[(r * NS + ST) * 32 + lane];
-    const V acc = vsub(vsub(yy, vmul(e, x1)), vmul(t, S));
-    const V x = vmul(rd, acc);
-    S = vadd(x1, S);
-    x1 = x;
-    Ys[r * 32 + lane] = x;
-  }
-  // ---- fix: delta = actual - estimated entering state, truncated neighbour steps
-  const V da = vsub(x1, ta), db = vsub(S, tb);
-  V wa = shfl_down_v(da, 1), wb2 = shfl_down_v(db, 1);
-  if (lane == 31) { wa = vzero<V>(); wb2 = vzero<V>(); }
+    // ---- scan F: exit_c = Y_c + m_c * exit_{c-1}
+    double m = h;
+    V Y = y;
 #pragma unroll
-  for (int it = 0; it < SHEN_FIX_STEPS; ++it) {
-    const V w1a = vfma(o00, wa, vfma(o01, wb2, da)), w1b = vfma(o10, wa, vfma(o11, wb2, db));
-    wa = shfl_down_v(w1a, 1);
-    wb2 = shfl_down_v(w1b, 1);
-    if (lane == 31) { wa = vzero<V>(); wb2 = vzero<V>(); }
-  }
-  V xc1 = wa, Sc = wb2;
-  for (int r = nr - 1; r >= 0; --r) {
-    const int k = par + 2 * (s0 + r);
-    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                 t = Ss[(r * NS + ST) * 32 + lane];
-    const V xc = vmul(-rd, vfma(e, xc1, vmul(t, Sc)));
-    Sc = vadd(xc1, Sc);
-    xc1 = xc;
-    O::st_cs(out + (int64_t)k * B + j, vadd(Ys[r * 32 + lane], xc));
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const double mb = shfl_up_d(m, dd);
+      const V Yb = shfl_up_v(Y, dd);
+      if (lane >= dd) {
+        Y = vfma(m, Yb, Y);
+        m = m * mb;
+      }
+    }
+    V E = shfl_up_v(Y, 1);
+    if (lane == 0) E = vzero<V>();
+
+    // ---- scan B: sigma_s = P sigma_{s+R} + tau, suffix over lanes
+    V ta = vfma(t1a, E, t0a), tb = vfma(t1b, E, t0b);
+    {
+      double q00 = p00, q01 = p01, q10 = p10, q11 = p11;
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const double r00 = shfl_down_d(q00, dd), r01 = shfl_down_d(q01, dd);
+        const double r10 = shfl_down_d(q10, dd), r11 = shfl_down_d(q11, dd);
+        const V va = shfl_down_v(ta, dd), vb = shfl_down_v(tb, dd);
+        if (lane + dd < 32) {
+          ta = vfma(q00, va, vfma(q01, vb, ta));
+          tb = vfma(q10, va, vfma(q11, vb, tb));
+          const double n00 = fma(q00, r00, q01 * r10), n01 = fma(q00, r01, q01 * r11);
+          const double n10 = fma(q10, r00, q11 * r10), n11 = fma(q10, r01, q11 * r11);
+          q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        }
+      }
+    }
+    V x1 = shfl_down_v(ta, 1), S = shfl_down_v(tb, 1);
+    if (lane == 31) { x1 = vzero<V>(); S = vzero<V>(); }
+
+    // ---- pass 3: reference back-substitution
+#pragma unroll
+    for (int r = R - 1; r >= 0; --r) {
+      if (r < nr) {
+        const V yy = vfma(h_[r], E, Ys[r * 32 + lane]);
+        const V acc = vsub(vsub(yy, vmul(e_[r], x1)), vmul(t_[r], S));
+        const V x = vmul(rd_[r], acc);
+        S = vadd(x1, S);
+        x1 = x;
+        Ys[r * 32 + lane] = x;
+      }
+    }
+    // ---- fix: delta = actual - estimated entering state, truncated neighbour steps
+    const V da = vsub(x1, ta), db = vsub(S, tb);
+    V wa = shfl_down_v(da, 1), wb = shfl_down_v(db, 1);
+    if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
+#pragma unroll
+    for (int it = 0; it < SHEN_FIX_STEPS; ++it) {
+      const V w1a = vfma(p00, wa, vfma(p01, wb, da)), w1b = vfma(p10, wa, vfma(p11, wb, db));
+      wa = shfl_down_v(w1a, 1);
+      wb = shfl_down_v(w1b, 1);
+      if (lane == 31) { wa = vzero<V>(); wb = vzero<V>(); }
+    }
+    V xc1 = wa, Sc = wb;
+#pragma unroll
+    for (int r = R - 1; r >= 0; --r) {
+      if (r < nr) {
+        const V xc = vmul(-rd_[r], vfma(e_[r], xc1, vmul(t_[r], Sc)));
+        Sc = vadd(xc1, Sc);
+        xc1 = xc;
+        O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
+      }
+    }
+    __syncwarp();
   }
 }
 
 // ======================================================================= biharmonic
-// smem per warp: Y [R][32] V, S [R][NS][32] doubles, P_own [16][32].
-template <typename V>
-__global__ void __launch_bounds__(64) bih_chunk_kernel(BihChunkArgs a) {
+// smem per warp: Y [2][R][32] V, S [R][NS][32] doubles, P_own [16][32].
+template <typename V, int R>
+__global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
   using O = VOps<V>;
-  constexpr int ND = O::ndouble;
   constexpr int SG1 = 0, SG2 = 1, SRD = 2, SE = 3, SF = 4, SA = 5, SB = 6, SQN = 7, SSN = 8, NS = 9;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int par = blockIdx.y;
-  const int64_t j = (int64_t)blockIdx.x * nwarp + warp;
-  if (j >= a.batch) return;
   const int64_t B = a.batch;
-  const int R = a.chunk_rows;
   const int n = (a.n_bih - par + 1) / 2;
   const int s0 = lane * R;
   const int nr = max(0, min(R, n - s0));
-  double* wb = smem + (size_t)warp * (R * 32 * (ND + NS) + 16 * 32);
-  V* Ys = reinterpret_cast<V*>(wb);
-  double* Ss = wb + R * 32 * ND;
+  const size_t per_warp = (size_t)2 * R * 32 * VOps<V>::ndouble + (size_t)R * NS * 32 + 16 * 32;
+  double* wbase = smem + (size_t)warp * per_warp;
+  V* Ybuf = reinterpret_cast<V*>(wbase);
+  double* Ss = wbase + 2 * R * 32 * VOps<V>::ndouble;
   double* pown = Ss + R * NS * 32;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
-  for (int r = 0; r < nr; ++r) cp_async_v(Ys + r * 32 + lane, rhs + (int64_t)(par + 2 * (s0 + r)) * B + j);
-  const double xi0 = a.xi0, xi1 = __ldg(a.xi1 + j), xi2 = __ldg(a.xi2 + j);
-
-  BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
-  if (s0 > 0 && nr > 0) {
-    const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 10) * B + j;
-    u1.d = ck[0]; u1.e = ck[B]; u1.f = ck[2 * B]; u1.a = ck[3 * B]; u1.b = ck[4 * B];
-    u2.d = ck[5 * B]; u2.e = ck[6 * B]; u2.f = ck[7 * B]; u2.a = ck[8 * B]; u2.b = ck[9 * B];
-    u1.rd = __drcp_rn(u1.d);
-    u2.rd = s0 >= 2 ? __drcp_rn(u2.d) : 0.0;
-  }
-  V yp1 = vzero<V>(), yp2 = vzero<V>();
-  double h11 = 1.0, h12 = 0.0, h21 = 0.0, h22 = 1.0;
-  double P[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) P[r][c] = (r == c) ? 1.0 : 0.0;
-  V t0[4];
-  double t1[4], t2[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) { t0[r] = vzero<V>(); t1[r] = 0.0; t2[r] = 0.0; }
-
-  double cn[B_NCOL];
-  if (nr > 0) {
-#pragma unroll
-    for (int q = 0; q < B_NCOL; ++q) cn[q] = __ldg(a.tab + (int64_t)(par + 2 * s0) * B_NCOL + q);
-  }
-  cp_async_wait_all();
-  for (int r = 0; r < nr; ++r) {
-    const int i = s0 + r;
-    double c[B_NCOL];
-#pragma unroll
-    for (int q = 0; q < B_NCOL; ++q) c[q] = cn[q];
-    if (r + 1 < nr) {
-#pragma unroll
-      for (int q = 0; q < B_NCOL; ++q) cn[q] = __ldg(a.tab + (int64_t)(par + 2 * (i + 1)) * B_NCOL + q);
+  const double xi0 = a.xi0;
+  const int64_t stride = (int64_t)gridDim.x * nwarp;
+  int64_t j = (int64_t)blockIdx.x * nwarp + warp;
+  if (j < B) prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+  int buf = 0;
+  for (; j < B; j += stride, buf ^= 1) {
+    V* Ys = Ybuf + buf * R * 32;
+    const int64_t jn = j + stride;
+    if (jn < B) prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
+    const double xi1 = __ldg(a.xi1 + j), xi2 = __ldg(a.xi2 + j);
+    BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
+    if (s0 > 0 && nr > 0) {
+      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 10) * B + j;
+      u1.d = __ldg(ck); u1.e = __ldg(ck + B); u1.f = __ldg(ck + 2 * B); u1.a = __ldg(ck + 3 * B);
+      u1.b = __ldg(ck + 4 * B);
+      u2.d = __ldg(ck + 5 * B); u2.e = __ldg(ck + 6 * B); u2.f = __ldg(ck + 7 * B); u2.a = __ldg(ck + 8 * B);
+      u2.b = __ldg(ck + 9 * B);
+      u1.rd = rcp_fast(u1.d);
+      u2.rd = s0 >= 2 ? rcp_fast(u2.d) : 0.0;
     }
-    const BihBands hb = bih_bands(xi0, xi1, xi2, c);
-    double l2, l4;
-    bih_step<false>(u, u1, u2, hb, c, xi0, i, l2, l4);
-    u2 = u1;
-    u1 = u;
-    const V b = Ys[r * 32 + lane];
-    const V y = vfma(-l4, yp2, vfma(-l2, yp1, b));
-    const double g1 = -fma(l2, h11, l4 * h21), g2 = -fma(l2, h12, l4 * h22);
-    yp2 = yp1; yp1 = y;
-    h21 = h11; h22 = h12; h11 = g1; h12 = g2;
-    Ys[r * 32 + lane] = y;
-    Ss[(r * NS + SG1) * 32 + lane] = g1;
-    Ss[(r * NS + SG2) * 32 + lane] = g2;
-    Ss[(r * NS + SRD) * 32 + lane] = u.rd;
-    Ss[(r * NS + SE) * 32 + lane] = u.e;
-    Ss[(r * NS + SF) * 32 + lane] = u.f;
-    Ss[(r * NS + SA) * 32 + lane] = u.a;
-    Ss[(r * NS + SB) * 32 + lane] = u.b;
-    const double qn = c[B_Q4], sn = c[B_S4];
-    Ss[(r * NS + SQN) * 32 + lane] = qn;
-    Ss[(r * NS + SSN) * 32 + lane] = sn;
-    // backward transfer of this row, accumulated left to right
-    const double al = -u.rd * u.e, be = -u.rd * u.f;
-    const double ga = -u.rd * (xi0 * u.a), de = -u.rd * (xi0 * u.b);
-    const V cy = vmul(u.rd, y);
-    const double cg1 = u.rd * g1, cg2 = u.rd * g2;
+    V yp1 = vzero<V>(), yp2 = vzero<V>();
+    double h11 = 1.0, h12 = 0.0, h21 = 0.0, h22 = 1.0;
+    double P[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      t0[q] = vfma(P[q][0], cy, t0[q]);
-      t1[q] = fma(P[q][0], cg1, t1[q]);
-      t2[q] = fma(P[q][0], cg2, t2[q]);
-      const double p0 = P[q][0], p1 = P[q][1], p2 = P[q][2], p3 = P[q][3];
-      P[q][0] = fma(p0, al, p1);
-      P[q][1] = fma(p0, be, fma(p2, qn, p3 * sn));
-      P[q][2] = fma(p0, ga, p2);
-      P[q][3] = fma(p0, de, p3);
-    }
-  }
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) P[q][c] = (q == c) ? 1.0 : 0.0;
+    V t0[4];
+    double t1[4], t2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { t0[q] = vzero<V>(); t1[q] = 0.0; t2[q] = 0.0; }
+    if (jn < B) cp_async_wait<1>(); else cp_async_wait<0>();
 
-  // ---- scan F: (y_last, y_last-1) = Y + H (E1, E2)
-  double H0 = h11, H1 = h12, H2 = h21, H3 = h22;
-  V Ya = yp1, Yb = yp2;
 #pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    const double g0 = shfl_up_d(H0, dd), g1 = shfl_up_d(H1, dd), g2 = shfl_up_d(H2, dd), g3 = shfl_up_d(H3, dd);
-    const V wa = shfl_up_v(Ya, dd), wb3 = shfl_up_v(Yb, dd);
-    if (lane >= dd) {
-      Ya = vfma(H0, wa, vfma(H1, wb3, Ya));
-      Yb = vfma(H2, wa, vfma(H3, wb3, Yb));
-      const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
-      const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
-      H0 = n0; H1 = n1; H2 = n2; H3 = n3;
+    for (int r = 0; r < R; ++r) {
+      if (r < nr) {
+        const int i = s0 + r;
+        const int k = par + 2 * i;
+        double c[B_NCOL];
+#pragma unroll
+        for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+        const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+        double l2, l4;
+        bih_step<false>(u, u1, u2, hb, c, xi0, i, l2, l4);
+        u2 = u1;
+        u1 = u;
+        const V b = Ys[r * 32 + lane];
+        const V y = vfma(-l4, yp2, vfma(-l2, yp1, b));
+        const double g1 = -fma(l2, h11, l4 * h21), g2 = -fma(l2, h12, l4 * h22);
+        yp2 = yp1; yp1 = y;
+        h21 = h11; h22 = h12; h11 = g1; h12 = g2;
+        Ys[r * 32 + lane] = y;
+        Ss[(r * NS + SG1) * 32 + lane] = g1;
+        Ss[(r * NS + SG2) * 32 + lane] = g2;
+        Ss[(r * NS + SRD) * 32 + lane] = u.rd;
+        Ss[(r * NS + SE) * 32 + lane] = u.e;
+        Ss[(r * NS + SF) * 32 + lane] = u.f;
+        Ss[(r * NS + SA) * 32 + lane] = u.a;
+        Ss[(r * NS + SB) * 32 + lane] = u.b;
+        const double qn = c[B_Q4], sn = c[B_S4];
+        Ss[(r * NS + SQN) * 32 + lane] = qn;
+        Ss[(r * NS + SSN) * 32 + lane] = sn;
+        const double al = -u.rd * u.e, be = -u.rd * u.f;
+        const double ga = -u.rd * (xi0 * u.a), de = -u.rd * (xi0 * u.b);
+        const V cy = vmul(u.rd, y);
+        const double cg1 = u.rd * g1, cg2 = u.rd * g2;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          t0[q] = vfma(P[q][0], cy, t0[q]);
+          t1[q] = fma(P[q][0], cg1, t1[q]);
+          t2[q] = fma(P[q][0], cg2, t2[q]);
+          const double p0 = P[q][0], p1 = P[q][1], p2 = P[q][2], p3 = P[q][3];
+          P[q][0] = fma(p0, al, p1);
+          P[q][1] = fma(p0, be, fma(p2, qn, p3 * sn));
+          P[q][2] = fma(p0, ga, p2);
+          P[q][3] = fma(p0, de, p3);
+        }
+      }
     }
-  }
-  V E1 = shfl_up_v(Ya, 1), E2 = shfl_up_v(Yb, 1);
-  if (lane == 0) { E1 = vzero<V>(); E2 = vzero<V>(); }
 
-  // ---- scan B
-  V tau[4];
+    // ---- scan F: (y_last, y_last-1) = Y + H (E1, E2)
+    double H0 = h11, H1 = h12, H2 = h21, H3 = h22;
+    V Ya = yp1, Yb = yp2;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) tau[q] = vfma(t1[q], E1, vfma(t2[q], E2, t0[q]));
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) pown[(q * 4 + c) * 32 + lane] = P[q][c];
-#pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    double Q[4][4];
-    V ub[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ub[q] = shfl_down_v(tau[q], dd);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) Q[q][c] = shfl_down_d(P[q][c], dd);
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const double g0 = shfl_up_d(H0, dd), g1 = shfl_up_d(H1, dd), g2 = shfl_up_d(H2, dd), g3 = shfl_up_d(H3, dd);
+      const V wa = shfl_up_v(Ya, dd), wb3 = shfl_up_v(Yb, dd);
+      if (lane >= dd) {
+        Ya = vfma(H0, wa, vfma(H1, wb3, Ya));
+        Yb = vfma(H2, wa, vfma(H3, wb3, Yb));
+        const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
+        const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
+        H0 = n0; H1 = n1; H2 = n2; H3 = n3;
+      }
     }
-    if (lane + dd < 32) {
+    V E1 = shfl_up_v(Ya, 1), E2 = shfl_up_v(Yb, 1);
+    if (lane == 0) { E1 = vzero<V>(); E2 = vzero<V>(); }
+
+    // ---- scan B
+    V tau[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tau[q] = vfma(t1[q], E1, vfma(t2[q], E2, t0[q]));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pown[(q * 4 + c) * 32 + lane] = P[q][c];
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      double Q[4][4];
+      V ub[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        tau[q] = vfma(P[q][0], ub[0], vfma(P[q][1], ub[1], vfma(P[q][2], ub[2], vfma(P[q][3], ub[3], tau[q]))));
+        ub[q] = shfl_down_v(tau[q], dd);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Q[q][c] = shfl_down_d(P[q][c], dd);
       }
-      double N[4][4];
+      if (lane + dd < 32) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q)
+          tau[q] = vfma(P[q][0], ub[0], vfma(P[q][1], ub[1], vfma(P[q][2], ub[2], vfma(P[q][3], ub[3], tau[q]))));
+        double N[4][4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          N[q][c] = fma(P[q][0], Q[0][c], fma(P[q][1], Q[1][c], fma(P[q][2], Q[2][c], P[q][3] * Q[3][c])));
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+          for (int c = 0; c < 4; ++c)
+            N[q][c] = fma(P[q][0], Q[0][c], fma(P[q][1], Q[1][c], fma(P[q][2], Q[2][c], P[q][3] * Q[3][c])));
 #pragma unroll
-        for (int c = 0; c < 4; ++c) P[q][c] = N[q][c];
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) P[q][c] = N[q][c];
+      }
     }
-  }
-  V sg[4];
+    V sg[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    sg[q] = shfl_down_v(tau[q], 1);
-    if (lane == 31) sg[q] = vzero<V>();
-  }
+    for (int q = 0; q < 4; ++q) {
+      sg[q] = shfl_down_v(tau[q], 1);
+      if (lane == 31) sg[q] = vzero<V>();
+    }
 
-  // ---- pass 3: reference back-substitution (Alg. 4 order)
-  V x1 = sg[0], x2 = sg[1], sq = sg[2], sv = sg[3];
-  for (int r = nr - 1; r >= 0; --r) {
-    const V yy = vfma(Ss[(r * NS + SG1) * 32 + lane], E1, vfma(Ss[(r * NS + SG2) * 32 + lane], E2, Ys[r * 32 + lane]));
-    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                 f = Ss[(r * NS + SF) * 32 + lane];
-    const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
-    V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
-    acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
-    const V x = vmul(rd, acc);
-    const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
-    sq = vfma(qn, x2, sq);
-    sv = vfma(sn, x2, sv);
-    x2 = x1;
-    x1 = x;
-    Ys[r * 32 + lane] = x;
-  }
-  // ---- fix
-  V dl[4] = {vsub(x1, tau[0]), vsub(x2, tau[1]), vsub(sq, tau[2]), vsub(sv, tau[3])};
-  V wn[4];
+    // ---- pass 3: reference back-substitution (Alg. 4 order)
+    V x1 = sg[0], x2 = sg[1], sq = sg[2], sv = sg[3];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    wn[q] = shfl_down_v(dl[q], 1);
-    if (lane == 31) wn[q] = vzero<V>();
-  }
-#pragma unroll
-  for (int step = 0; step < SHEN_FIX_STEPS; ++step) {
-    V w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      V acc = dl[q];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc = vfma(pown[(q * 4 + c) * 32 + lane], wn[c], acc);
-      w[q] = acc;
+    for (int r = R - 1; r >= 0; --r) {
+      if (r < nr) {
+        const V yy = vfma(Ss[(r * NS + SG1) * 32 + lane], E1, vfma(Ss[(r * NS + SG2) * 32 + lane], E2, Ys[r * 32 + lane]));
+        const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                     f = Ss[(r * NS + SF) * 32 + lane];
+        const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
+        V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
+        acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
+        const V x = vmul(rd, acc);
+        const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
+        sq = vfma(qn, x2, sq);
+        sv = vfma(sn, x2, sv);
+        x2 = x1;
+        x1 = x;
+        Ys[r * 32 + lane] = x;
+      }
     }
+    // ---- fix
+    V dl[4] = {vsub(x1, tau[0]), vsub(x2, tau[1]), vsub(sq, tau[2]), vsub(sv, tau[3])};
+    V wn[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      wn[q] = shfl_down_v(w[q], 1);
+      wn[q] = shfl_down_v(dl[q], 1);
       if (lane == 31) wn[q] = vzero<V>();
     }
-  }
-  V c1 = wn[0], c2 = wn[1], cq = wn[2], cs = wn[3];
-  for (int r = nr - 1; r >= 0; --r) {
-    const int k = par + 2 * (s0 + r);
-    const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                 f = Ss[(r * NS + SF) * 32 + lane];
-    const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
-    const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
-    const V xc = vmul(-rd, acc);
-    const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
-    cq = vfma(qn, c2, cq);
-    cs = vfma(sn, c2, cs);
-    c2 = c1;
-    c1 = xc;
-    O::st_cs(out + (int64_t)k * B + j, vadd(Ys[r * 32 + lane], xc));
+#pragma unroll
+    for (int step = 0; step < SHEN_FIX_STEPS; ++step) {
+      V w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        V acc = dl[q];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc = vfma(pown[(q * 4 + c) * 32 + lane], wn[c], acc);
+        w[q] = acc;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        wn[q] = shfl_down_v(w[q], 1);
+        if (lane == 31) wn[q] = vzero<V>();
+      }
+    }
+    V c1 = wn[0], c2 = wn[1], cq = wn[2], cs = wn[3];
+#pragma unroll
+    for (int r = R - 1; r >= 0; --r) {
+      if (r < nr) {
+        const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                     f = Ss[(r * NS + SF) * 32 + lane];
+        const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
+        const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
+        const V xc = vmul(-rd, acc);
+        const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
+        cq = vfma(qn, c2, cq);
+        cs = vfma(sn, c2, cs);
+        c2 = c1;
+        c1 = xc;
+        O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
+      }
+    }
+    __syncwarp();
   }
 }
 
-static size_t helm_smem(int R, int nwarp, bool cplx_rhs) {
-  return ((size_t)R * 3 * 32 + (size_t)nwarp * R * 32 * ((cplx_rhs ? 2 : 1) + 4)) * sizeof(double);
-}
-static size_t bih_smem(int R, int nwarp, bool cplx_rhs) {
-  return (size_t)nwarp * ((size_t)R * 32 * ((cplx_rhs ? 2 : 1) + 9) + 16 * 32) * sizeof(double);
-}
-
+// ======================================================================= launchers
 template <typename K>
-static cudaError_t launch_dyn(K kernel, dim3 grid, int threads, size_t smem, cudaStream_t st, void* args) {
+static cudaError_t launch_persistent(K kernel, int threads, size_t smem, int64_t items_per_parity, int nwarp,
+                                     cudaStream_t st, void* args) {
   cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+  if (err != cudaSuccess) return err;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int64_t want = (items_per_parity + nwarp - 1) / nwarp;
+  const int64_t cap = std::max<int64_t>(1, (int64_t)sms * occ / 2);
+  dim3 grid((unsigned)std::min(want, cap), 2);
   void* params[] = {args};
   return cudaLaunchKernel((const void*)kernel, grid, dim3(threads), params, smem, st);
 }
 
+template <typename V, int R>
+static cudaError_t helm_launch_R(const HelmChunkArgs& a, cudaStream_t st) {
+  constexpr int nwarp = R >= 32 ? 4 : 8;
+  const size_t smem = ((size_t)R * 3 * 32 + (size_t)nwarp * 2 * R * 32 * VOps<V>::ndouble) * sizeof(double);
+  HelmChunkArgs copy = a;
+  return launch_persistent(helm_chunk_kernel<V, R>, 32 * nwarp, smem, a.batch, nwarp, st, &copy);
+}
+
+template <typename V, int R>
+static cudaError_t bih_launch_R(const BihChunkArgs& a, cudaStream_t st) {
+  constexpr int NS = 9;
+  const size_t per_warp = ((size_t)2 * R * 32 * VOps<V>::ndouble + (size_t)R * NS * 32 + 16 * 32) * sizeof(double);
+  int nwarp = 4;
+  while (nwarp > 1 && per_warp * nwarp > 200 * 1024) --nwarp;
+  BihChunkArgs copy = a;
+  return launch_persistent(bih_chunk_kernel<V, R>, 32 * nwarp, per_warp * nwarp, a.batch, nwarp, st, &copy);
+}
+
+template <typename V>
+static cudaError_t helm_dispatch(const HelmChunkArgs& a, cudaStream_t st) {
+  switch (a.chunk_rows) {
+    case 1: return helm_launch_R<V, 1>(a, st);
+    case 2: return helm_launch_R<V, 2>(a, st);
+    case 4: return helm_launch_R<V, 4>(a, st);
+    case 8: return helm_launch_R<V, 8>(a, st);
+    case 16: return helm_launch_R<V, 16>(a, st);
+    case 32: return helm_launch_R<V, 32>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename V>
+static cudaError_t bih_dispatch(const BihChunkArgs& a, cudaStream_t st) {
+  switch (a.chunk_rows) {
+    case 1: return bih_launch_R<V, 1>(a, st);
+    case 2: return bih_launch_R<V, 2>(a, st);
+    case 4: return bih_launch_R<V, 4>(a, st);
+    case 8: return bih_launch_R<V, 8>(a, st);
+    case 16: return bih_launch_R<V, 16>(a, st);
+    case 32: return bih_launch_R<V, 32>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_helm_chunk(const HelmChunkArgs& a, bool cplx_rhs, cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
-  if (a.chunk_rows <= 0 || (int64_t)a.chunk_rows * 32 < (a.n_dir + 1) / 2) return cudaErrorInvalidValue;
-  int nwarp = 4;
-  while (nwarp > 1 && helm_smem(a.chunk_rows, nwarp, cplx_rhs) > 110 * 1024) nwarp >>= 1;
-  const size_t smem = helm_smem(a.chunk_rows, nwarp, cplx_rhs);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)((a.batch + nwarp - 1) / nwarp), 2);
-  HelmChunkArgs copy = a;
-  return cplx_rhs ? launch_dyn(helm_chunk_kernel<cplx>, grid, 32 * nwarp, smem, st, &copy)
-                  : launch_dyn(helm_chunk_kernel<double>, grid, 32 * nwarp, smem, st, &copy);
+  if ((int64_t)a.chunk_rows * 32 < (a.n_dir + 1) / 2) return cudaErrorInvalidValue;
+  return cplx_rhs ? helm_dispatch<cplx>(a, st) : helm_dispatch<double>(a, st);
 }
 
 cudaError_t launch_bih_chunk(const BihChunkArgs& a, bool cplx_rhs, cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
-  if (a.chunk_rows <= 0 || (int64_t)a.chunk_rows * 32 < (a.n_bih + 1) / 2) return cudaErrorInvalidValue;
-  int nwarp = 2;
-  while (nwarp > 1 && bih_smem(a.chunk_rows, nwarp, cplx_rhs) > 110 * 1024) nwarp >>= 1;
-  const size_t smem = bih_smem(a.chunk_rows, nwarp, cplx_rhs);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)((a.batch + nwarp - 1) / nwarp), 2);
-  BihChunkArgs copy = a;
-  return cplx_rhs ? launch_dyn(bih_chunk_kernel<cplx>, grid, 32 * nwarp, smem, st, &copy)
-                  : launch_dyn(bih_chunk_kernel<double>, grid, 32 * nwarp, smem, st, &copy);
+  if ((int64_t)a.chunk_rows * 32 < (a.n_bih + 1) / 2) return cudaErrorInvalidValue;
+  return cplx_rhs ? bih_dispatch<cplx>(a, st) : bih_dispatch<double>(a, st);
 }
 
 }  // namespace shen

@@ -69,9 +69,16 @@ def biharmonic_coefficients(nu: float, dt: float, z2):
 
 
 def chunk_rows_for(n_modes: int) -> int:
-    """Rows per lane so that 32 lanes cover the larger parity."""
+    """Rows per lane (a power of two, compile-time in the kernels) so that 32
+    lanes cover the larger parity."""
     rows0 = (n_modes + 1) // 2
-    return max(1, -(-rows0 // 32))
+    need = max(1, -(-rows0 // 32))
+    R = 1
+    while R < need:
+        R *= 2
+    if R > 32:
+        raise ValueError(f"n_modes = {n_modes} exceeds the supported 2048 rows per parity")
+    return R
 
 
 def _n_chunks(n_modes: int, R: int) -> int:
