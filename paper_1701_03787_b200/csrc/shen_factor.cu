@@ -38,14 +38,10 @@ __global__ void __launch_bounds__(256) helm_factor_kernel(HelmFactorArgs a) {
       d = s.d; e = s.e; t = s.t;
     } else {
       const int r = i % R;
-      if (i == 0) {
-        hp_first(pj, h);
-        low = 0.0; d = h.diag; e = h.sup; t = h.tail;
-      } else {
-        if (r == 0) hp_start(pj, dl, el, tl);
-        else if ((r & 7) == 0) hp_rescale(pj);
-        low = hp_step(pj, h, sub, d, e, t);
-      }
+      if (i == 0) hp_origin(pj);
+      else if (r == 0) hp_start(pj, dl, el, tl);
+      else if ((r & 7) == 0) hp_rescale(pj);
+      low = hp_step(pj, h, sub, d, e, t);
       dl = d; el = e; tl = t;
     }
     note_pivot(a.pivot, par, i, d);
@@ -82,7 +78,10 @@ __global__ void __launch_bounds__(256) bih_factor_kernel(BihFactorArgs a) {
     for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
     BihBands h = bih_bands(a.xi0, xi1, xi2, c);
     double l2, l4;
-    bih_step<EXACT>(u, u1, u2, h, c, a.xi0, i, l2, l4);
+    if (EXACT)
+      bih_step<true>(u, u1, u2, h, c, a.xi0, i, l2, l4);
+    else
+      bih_step_fast(u, u1, u2, h, c, a.xi0, l2, l4);
     note_pivot(a.pivot, par, i, u.d);
     if (a.d[par] != nullptr) {
       if (i >= 1) a.low2[par][(int64_t)(i - 1) * B + j] = l2;

@@ -98,13 +98,15 @@ __device__ __forceinline__ void hp_start(HelmProj& s, double d, double e, double
   s.rd = s.rD;
 }
 
-// row 0 of the parity (no predecessor)
-__device__ __forceinline__ void hp_first(HelmProj& s, const HelmRow& h) {
-  s.D = h.diag;
-  s.E = h.sup;
-  s.T = h.tail;
-  s.rD = rcp_fast(h.diag);
-  s.rd = s.rD;
+// state "before row 0": D_{-1} = 1, E = T = 0 and 1/d_{-1} := 0, so the
+// generic step reproduces row 0 exactly (d_0 = diag_0, e_0 = sup_0,
+// t_0 = tail_0, low_0 = 0) without a branch
+__device__ __forceinline__ void hp_origin(HelmProj& s) {
+  s.D = 1.0;
+  s.E = 0.0;
+  s.T = 0.0;
+  s.rD = 1.0;
+  s.rd = 0.0;
 }
 
 // generic row: returns low_i = sub / d_{i-1}; outputs ratios e_i, t_i, d_i
@@ -131,9 +133,9 @@ __device__ __forceinline__ double hp_step(HelmProj& s, const HelmRow& h, double 
 __device__ __forceinline__ void hp_rescale(HelmProj& s) {
   const int hi = __double2hiint(s.D);
   const int ex = (hi >> 20) & 0x7ff;
-  if (ex == 0 || ex == 0x7ff) return;
-  const double sc = __hiloint2double((2046 - ex) << 20, 0);  // 2^(1023 - ex)
-  const double isc = __hiloint2double(ex << 20, 0);         // 2^(ex - 1023)
+  const bool ok = ex != 0 && ex != 0x7ff;  // branch-free: zero/inf/nan left alone
+  const double sc = ok ? __hiloint2double((2046 - ex) << 20, 0) : 1.0;  // 2^(1023 - ex)
+  const double isc = ok ? __hiloint2double(ex << 20, 0) : 1.0;         // 2^(ex - 1023)
   s.D = __dmul_rn(s.D, sc);
   s.E = __dmul_rn(s.E, sc);
   s.T = __dmul_rn(s.T, sc);
@@ -235,6 +237,25 @@ __device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2
     }
   }
   u.rd = EXACT ? 0.0 : rcp_fast(u.d);
+}
+
+// Branch-free fast-mode biharmonic step (same arithmetic as bih_step<false>
+// for i >= 2).  Rows "before row 0" are zero records with rd = 0, which makes
+// the generic formula reproduce rows 0 and 1 exactly (fma(-0, 0, x) == x).
+__device__ __forceinline__ void bih_step_fast(BihU& u, const BihU& u1, const BihU& u2, const BihBands& h,
+                                              const double* c, double xi0, double& l2, double& l4) {
+  l4 = __dmul_rn(h.hm4, u2.rd);
+  const double tmp = __fma_rn(-l4, u2.e, h.hm2);
+  l2 = __dmul_rn(tmp, u1.rd);
+  const double u42 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2])));
+  const double u44 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4])));
+  const double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
+  u.d = __fma_rn(-l2, u1.e, __fma_rn(-l4, u2.f, h.hd));
+  u.e = __fma_rn(-l2, u1.f, __fma_rn(-l4, u42, h.hp2));
+  u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
+  u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
+  u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
+  u.rd = rcp_fast(u.d);
 }
 
 }  // namespace shen

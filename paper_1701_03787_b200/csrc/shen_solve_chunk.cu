@@ -74,7 +74,7 @@ __device__ __forceinline__ void prefetch_rows(V* Y, const V* rhs, int64_t B, int
 }
 
 // ======================================================================= Helmholtz
-// smem: table [R][3][32] (one parity per CTA, loaded once), then per warp
+// smem: table [R][4][32] (one parity per CTA, loaded once), then per warp
 // Y [2][R][32] V (double-buffered RHS -> y -> x).  The per-row factor data
 // (h, 1/d, e, t) lives in registers (fully unrolled rows).
 template <typename V, int R>
@@ -86,42 +86,58 @@ __global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
   const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
-  double* tab = smem;
+  double* tab = smem;  // [R][4][32]: sd, st, md, has_sup (0/1); zero rows past the end
   for (int idx = threadIdx.x; idx < R * 32; idx += blockDim.x) {
     const int r = idx >> 5, c = idx & 31, i = c * R + r;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
     if (i < n) {
       const int k = par + 2 * i;
-      v0 = __ldg(a.sd + k); v1 = __ldg(a.st + k); v2 = __ldg(a.md + k);
+      v0 = __ldg(a.sd + k); v1 = __ldg(a.st + k); v2 = __ldg(a.md + k); v3 = i < nsup ? 1.0 : 0.0;
     }
-    tab[(r * 3 + 0) * 32 + c] = v0;
-    tab[(r * 3 + 1) * 32 + c] = v1;
-    tab[(r * 3 + 2) * 32 + c] = v2;
+    tab[(r * 4 + 0) * 32 + c] = v0;
+    tab[(r * 4 + 1) * 32 + c] = v1;
+    tab[(r * 4 + 2) * 32 + c] = v2;
+    tab[(r * 4 + 3) * 32 + c] = v3;
   }
   __syncthreads();
   const int s0 = lane * R;
   const int nr = max(0, min(R, n - s0));
-  V* Ybuf = reinterpret_cast<V*>(smem + R * 3 * 32) + (size_t)warp * 2 * R * 32;
+  V* Ybuf = reinterpret_cast<V*>(smem + R * 4 * 32) + (size_t)warp * 2 * R * 32;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const int64_t stride = (int64_t)gridDim.x * nwarp;
   int64_t j = (int64_t)blockIdx.x * nwarp + warp;
-  if (j < B) prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+  const bool use_ck = s0 > 0 && nr > 0;
+  // per-item scalars are loaded one item ahead
+  double cb_n = 0.0, ckd_n = 1.0, cke_n = 0.0, ckt_n = 0.0;
+  auto load_scalars = [&](int64_t jj) {
+    cb_n = __ldg(a.cb + jj);
+    if (use_ck) {
+      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + jj;
+      ckd_n = __ldg(ck); cke_n = __ldg(ck + B); ckt_n = __ldg(ck + 2 * B);
+    }
+  };
+  if (j < B) {
+    prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+    load_scalars(j);
+  }
   int buf = 0;
   for (; j < B; j += stride, buf ^= 1) {
     V* Ys = Ybuf + buf * R * 32;
     const int64_t jn = j + stride;
-    if (jn < B) prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
-    const double cb = __ldg(a.cb + j);
-    const double sub = __dmul_rn(cb, -1.5707963267948966);
-    HelmProj pj{0, 0, 0, 0, 0};
-    if (s0 > 0 && nr > 0) {
-      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 3) * B + j;
-      hp_start(pj, __ldg(ck), __ldg(ck + B), __ldg(ck + 2 * B));
+    const double cb = cb_n;
+    HelmProj pj;
+    if (use_ck) hp_start(pj, ckd_n, cke_n, ckt_n); else hp_origin(pj);
+    if (jn < B) {
+      prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
+      load_scalars(jn);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    if (jn < B) cp_async_wait<1>(); else cp_async_wait<0>();
+    const double sub = __dmul_rn(cb, -1.5707963267948966);
 
-    // ---- pass 1
+    // ---- pass 1 (every lane runs R rows; rows past the end are masked)
     double h_[R], rd_[R], e_[R], t_[R];
     V y = vzero<V>();
     double h = 1.0;
@@ -130,40 +146,31 @@ __global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
     double t1a = 0.0, t1b = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      h_[r] = 0.0; rd_[r] = 0.0; e_[r] = 0.0; t_[r] = 0.0;
-      if (r < nr) {
-        const int i = s0 + r;
-        const HelmRow row = helm_row(a.ca, cb, sub, tab[(r * 3 + 0) * 32 + lane], tab[(r * 3 + 1) * 32 + lane],
-                                     tab[(r * 3 + 2) * 32 + lane], i < nsup);
-        const V b = Ys[r * 32 + lane];
-        double e, t;
-        if (i == 0) {
-          hp_first(pj, row);
-          e = row.sup;
-          t = row.tail;
-          y = b;
-          h = 0.0;
-        } else {
-          if (r > 0 && (r & 7) == 0) hp_rescale(pj);
-          double d;
-          const double low = hp_step(pj, row, sub, d, e, t);
-          y = vfma(-low, y, b);
-          h = -low * h;
-        }
-        const double rd = pj.rd;
-        Ys[r * 32 + lane] = y;
-        h_[r] = h; rd_[r] = rd; e_[r] = e; t_[r] = t;
-        const double al = -rd * e, be = -rd * t;
-        const V cy = vmul(rd, y);
-        const double ch = rd * h;
-        t0a = vfma(p00, cy, t0a);
-        t0b = vfma(p10, cy, t0b);
-        t1a = fma(p00, ch, t1a);
-        t1b = fma(p10, ch, t1b);
-        const double n00 = fma(p00, al, p01), n01 = fma(p00, be, p01);
-        const double n10 = fma(p10, al, p11), n11 = fma(p10, be, p11);
-        p00 = n00; p01 = n01; p10 = n10; p11 = n11;
-      }
+      const bool valid = r < nr;
+      const HelmRow row = helm_row(a.ca, cb, sub, tab[(r * 4 + 0) * 32 + lane], tab[(r * 4 + 1) * 32 + lane],
+                                   tab[(r * 4 + 2) * 32 + lane], tab[(r * 4 + 3) * 32 + lane] != 0.0);
+      if (r > 0 && (r & 7) == 0) hp_rescale(pj);
+      double d, e, t;
+      const double low = hp_step(pj, row, sub, d, e, t);
+      const V b = Ys[r * 32 + lane];
+      const V yv = vfma(-low, y, b);
+      y = valid ? yv : vzero<V>();
+      h = valid ? -low * h : h;
+      const double rd = valid ? pj.rd : 0.0;
+      e = valid ? e : 0.0;
+      t = valid ? t : 0.0;
+      Ys[r * 32 + lane] = y;
+      h_[r] = h; rd_[r] = rd; e_[r] = e; t_[r] = t;
+      const double al = -rd * e, be = -rd * t;
+      const V cy = vmul(rd, y);
+      const double ch = rd * h;
+      t0a = vfma(p00, cy, t0a);
+      t0b = vfma(p10, cy, t0b);
+      t1a = fma(p00, ch, t1a);
+      t1b = fma(p10, ch, t1b);
+      const double n00 = fma(p00, al, p01), n01 = fma(p00, be, p01);
+      const double n10 = fma(p10, al, p11), n11 = fma(p10, be, p11);
+      p00 = n00; p01 = n01; p10 = n10; p11 = n11;
     }
 
     // ---- scan F: exit_c = Y_c + m_c * exit_{c-1}
@@ -173,10 +180,11 @@ __global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
     for (int dd = 1; dd < 32; dd <<= 1) {
       const double mb = shfl_up_d(m, dd);
       const V Yb = shfl_up_v(Y, dd);
-      if (lane >= dd) {
-        Y = vfma(m, Yb, Y);
-        m = m * mb;
-      }
+      const bool take = lane >= dd;
+      const V Yn = vfma(m, Yb, Y);
+      const double mn = m * mb;
+      Y = take ? Yn : Y;
+      m = take ? mn : m;
     }
     V E = shfl_up_v(Y, 1);
     if (lane == 0) E = vzero<V>();
@@ -190,29 +198,29 @@ __global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
         const double r00 = shfl_down_d(q00, dd), r01 = shfl_down_d(q01, dd);
         const double r10 = shfl_down_d(q10, dd), r11 = shfl_down_d(q11, dd);
         const V va = shfl_down_v(ta, dd), vb = shfl_down_v(tb, dd);
-        if (lane + dd < 32) {
-          ta = vfma(q00, va, vfma(q01, vb, ta));
-          tb = vfma(q10, va, vfma(q11, vb, tb));
-          const double n00 = fma(q00, r00, q01 * r10), n01 = fma(q00, r01, q01 * r11);
-          const double n10 = fma(q10, r00, q11 * r10), n11 = fma(q10, r01, q11 * r11);
-          q00 = n00; q01 = n01; q10 = n10; q11 = n11;
-        }
+        const bool take = lane + dd < 32;
+        const V tan = vfma(q00, va, vfma(q01, vb, ta));
+        const V tbn = vfma(q10, va, vfma(q11, vb, tb));
+        const double n00 = fma(q00, r00, q01 * r10), n01 = fma(q00, r01, q01 * r11);
+        const double n10 = fma(q10, r00, q11 * r10), n11 = fma(q10, r01, q11 * r11);
+        ta = take ? tan : ta;
+        tb = take ? tbn : tb;
+        q00 = take ? n00 : q00; q01 = take ? n01 : q01;
+        q10 = take ? n10 : q10; q11 = take ? n11 : q11;
       }
     }
     V x1 = shfl_down_v(ta, 1), S = shfl_down_v(tb, 1);
     if (lane == 31) { x1 = vzero<V>(); S = vzero<V>(); }
 
-    // ---- pass 3: reference back-substitution
+    // ---- pass 3: reference back-substitution (masked rows give x = 0)
 #pragma unroll
     for (int r = R - 1; r >= 0; --r) {
-      if (r < nr) {
-        const V yy = vfma(h_[r], E, Ys[r * 32 + lane]);
-        const V acc = vsub(vsub(yy, vmul(e_[r], x1)), vmul(t_[r], S));
-        const V x = vmul(rd_[r], acc);
-        S = vadd(x1, S);
-        x1 = x;
-        Ys[r * 32 + lane] = x;
-      }
+      const V yy = vfma(h_[r], E, Ys[r * 32 + lane]);
+      const V acc = vsub(vsub(yy, vmul(e_[r], x1)), vmul(t_[r], S));
+      const V x = vmul(rd_[r], acc);
+      S = vadd(x1, S);
+      x1 = x;
+      Ys[r * 32 + lane] = x;
     }
     // ---- fix: delta = actual - estimated entering state, truncated neighbour steps
     const V da = vsub(x1, ta), db = vsub(S, tb);
@@ -228,12 +236,10 @@ __global__ void __launch_bounds__(256) helm_chunk_kernel(HelmChunkArgs a) {
     V xc1 = wa, Sc = wb;
 #pragma unroll
     for (int r = R - 1; r >= 0; --r) {
-      if (r < nr) {
-        const V xc = vmul(-rd_[r], vfma(e_[r], xc1, vmul(t_[r], Sc)));
-        Sc = vadd(xc1, Sc);
-        xc1 = xc;
-        O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
-      }
+      const V xc = vmul(-rd_[r], vfma(e_[r], xc1, vmul(t_[r], Sc)));
+      Sc = vadd(xc1, Sc);
+      xc1 = xc;
+      if (r < nr) O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
     }
     __syncwarp();
   }
@@ -262,22 +268,41 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
   const double xi0 = a.xi0;
   const int64_t stride = (int64_t)gridDim.x * nwarp;
   int64_t j = (int64_t)blockIdx.x * nwarp + warp;
-  if (j < B) prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+  const bool use_ck = s0 > 0 && nr > 0;
+  double xi1_n = 0.0, xi2_n = 0.0, ck_n[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) ck_n[q] = 0.0;
+  auto load_scalars = [&](int64_t jj) {
+    xi1_n = __ldg(a.xi1 + jj);
+    xi2_n = __ldg(a.xi2 + jj);
+    if (use_ck) {
+      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 10) * B + jj;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) ck_n[q] = __ldg(ck + q * B);
+    }
+  };
+  if (j < B) {
+    prefetch_rows<V, R>(Ybuf, rhs, B, j, par, s0, nr, lane);
+    load_scalars(j);
+  }
   int buf = 0;
   for (; j < B; j += stride, buf ^= 1) {
     V* Ys = Ybuf + buf * R * 32;
     const int64_t jn = j + stride;
-    if (jn < B) prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
-    const double xi1 = __ldg(a.xi1 + j), xi2 = __ldg(a.xi2 + j);
+    const double xi1 = xi1_n, xi2 = xi2_n;
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
-    if (s0 > 0 && nr > 0) {
-      const double* ck = a.ckpt + ((int64_t)(lane * 2 + par) * 10) * B + j;
-      u1.d = __ldg(ck); u1.e = __ldg(ck + B); u1.f = __ldg(ck + 2 * B); u1.a = __ldg(ck + 3 * B);
-      u1.b = __ldg(ck + 4 * B);
-      u2.d = __ldg(ck + 5 * B); u2.e = __ldg(ck + 6 * B); u2.f = __ldg(ck + 7 * B); u2.a = __ldg(ck + 8 * B);
-      u2.b = __ldg(ck + 9 * B);
+    if (use_ck) {
+      u1.d = ck_n[0]; u1.e = ck_n[1]; u1.f = ck_n[2]; u1.a = ck_n[3]; u1.b = ck_n[4];
+      u2.d = ck_n[5]; u2.e = ck_n[6]; u2.f = ck_n[7]; u2.a = ck_n[8]; u2.b = ck_n[9];
       u1.rd = rcp_fast(u1.d);
       u2.rd = s0 >= 2 ? rcp_fast(u2.d) : 0.0;
+    }
+    if (jn < B) {
+      prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);
+      load_scalars(jn);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     V yp1 = vzero<V>(), yp2 = vzero<V>();
     double h11 = 1.0, h12 = 0.0, h21 = 0.0, h22 = 1.0;
@@ -290,52 +315,53 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
     double t1[4], t2[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) { t0[q] = vzero<V>(); t1[q] = 0.0; t2[q] = 0.0; }
-    if (jn < B) cp_async_wait<1>(); else cp_async_wait<0>();
 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (r < nr) {
-        const int i = s0 + r;
-        const int k = par + 2 * i;
-        double c[B_NCOL];
+      const bool valid = r < nr;
+      const int k = min(par + 2 * (s0 + r), a.n_bih - 1);
+      double c[B_NCOL];
 #pragma unroll
-        for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
-        const BihBands hb = bih_bands(xi0, xi1, xi2, c);
-        double l2, l4;
-        bih_step<false>(u, u1, u2, hb, c, xi0, i, l2, l4);
-        u2 = u1;
-        u1 = u;
-        const V b = Ys[r * 32 + lane];
-        const V y = vfma(-l4, yp2, vfma(-l2, yp1, b));
-        const double g1 = -fma(l2, h11, l4 * h21), g2 = -fma(l2, h12, l4 * h22);
-        yp2 = yp1; yp1 = y;
-        h21 = h11; h22 = h12; h11 = g1; h12 = g2;
-        Ys[r * 32 + lane] = y;
-        Ss[(r * NS + SG1) * 32 + lane] = g1;
-        Ss[(r * NS + SG2) * 32 + lane] = g2;
-        Ss[(r * NS + SRD) * 32 + lane] = u.rd;
-        Ss[(r * NS + SE) * 32 + lane] = u.e;
-        Ss[(r * NS + SF) * 32 + lane] = u.f;
-        Ss[(r * NS + SA) * 32 + lane] = u.a;
-        Ss[(r * NS + SB) * 32 + lane] = u.b;
-        const double qn = c[B_Q4], sn = c[B_S4];
-        Ss[(r * NS + SQN) * 32 + lane] = qn;
-        Ss[(r * NS + SSN) * 32 + lane] = sn;
-        const double al = -u.rd * u.e, be = -u.rd * u.f;
-        const double ga = -u.rd * (xi0 * u.a), de = -u.rd * (xi0 * u.b);
-        const V cy = vmul(u.rd, y);
-        const double cg1 = u.rd * g1, cg2 = u.rd * g2;
+      for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+      const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+      double l2, l4;
+      bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
+      u2 = u1;
+      u1 = u;
+      const V b = Ys[r * 32 + lane];
+      const V yv = vfma(-l4, yp2, vfma(-l2, yp1, b));
+      const V y = valid ? yv : vzero<V>();
+      const double g1 = valid ? -fma(l2, h11, l4 * h21) : 0.0;
+      const double g2 = valid ? -fma(l2, h12, l4 * h22) : 0.0;
+      yp2 = yp1; yp1 = y;
+      h21 = h11; h22 = h12; h11 = g1; h12 = g2;
+      const double rd = valid ? u.rd : 0.0, ue = valid ? u.e : 0.0, uf = valid ? u.f : 0.0;
+      const double ua = valid ? u.a : 0.0, ub = valid ? u.b : 0.0;
+      const double qn = valid ? c[B_Q4] : 0.0, sn = valid ? c[B_S4] : 0.0;
+      Ys[r * 32 + lane] = y;
+      Ss[(r * NS + SG1) * 32 + lane] = g1;
+      Ss[(r * NS + SG2) * 32 + lane] = g2;
+      Ss[(r * NS + SRD) * 32 + lane] = rd;
+      Ss[(r * NS + SE) * 32 + lane] = ue;
+      Ss[(r * NS + SF) * 32 + lane] = uf;
+      Ss[(r * NS + SA) * 32 + lane] = ua;
+      Ss[(r * NS + SB) * 32 + lane] = ub;
+      Ss[(r * NS + SQN) * 32 + lane] = qn;
+      Ss[(r * NS + SSN) * 32 + lane] = sn;
+      const double al = -rd * ue, be = -rd * uf;
+      const double ga = -rd * (xi0 * ua), de = -rd * (xi0 * ub);
+      const V cy = vmul(rd, y);
+      const double cg1 = rd * g1, cg2 = rd * g2;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          t0[q] = vfma(P[q][0], cy, t0[q]);
-          t1[q] = fma(P[q][0], cg1, t1[q]);
-          t2[q] = fma(P[q][0], cg2, t2[q]);
-          const double p0 = P[q][0], p1 = P[q][1], p2 = P[q][2], p3 = P[q][3];
-          P[q][0] = fma(p0, al, p1);
-          P[q][1] = fma(p0, be, fma(p2, qn, p3 * sn));
-          P[q][2] = fma(p0, ga, p2);
-          P[q][3] = fma(p0, de, p3);
-        }
+      for (int q = 0; q < 4; ++q) {
+        t0[q] = vfma(P[q][0], cy, t0[q]);
+        t1[q] = fma(P[q][0], cg1, t1[q]);
+        t2[q] = fma(P[q][0], cg2, t2[q]);
+        const double p0 = P[q][0], p1 = P[q][1], p2 = P[q][2], p3 = P[q][3];
+        P[q][0] = fma(p0, al, p1);
+        P[q][1] = fma(p0, be, fma(p2, qn, p3 * sn));
+        P[q][2] = fma(p0, ga, p2);
+        P[q][3] = fma(p0, de, p3);
       }
     }
 
@@ -346,13 +372,14 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
     for (int dd = 1; dd < 32; dd <<= 1) {
       const double g0 = shfl_up_d(H0, dd), g1 = shfl_up_d(H1, dd), g2 = shfl_up_d(H2, dd), g3 = shfl_up_d(H3, dd);
       const V wa = shfl_up_v(Ya, dd), wb3 = shfl_up_v(Yb, dd);
-      if (lane >= dd) {
-        Ya = vfma(H0, wa, vfma(H1, wb3, Ya));
-        Yb = vfma(H2, wa, vfma(H3, wb3, Yb));
-        const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
-        const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
-        H0 = n0; H1 = n1; H2 = n2; H3 = n3;
-      }
+      const bool take = lane >= dd;
+      const V Yan = vfma(H0, wa, vfma(H1, wb3, Ya));
+      const V Ybn = vfma(H2, wa, vfma(H3, wb3, Yb));
+      const double n0 = fma(H0, g0, H1 * g2), n1 = fma(H0, g1, H1 * g3);
+      const double n2 = fma(H2, g0, H3 * g2), n3 = fma(H2, g1, H3 * g3);
+      Ya = take ? Yan : Ya;
+      Yb = take ? Ybn : Yb;
+      H0 = take ? n0 : H0; H1 = take ? n1 : H1; H2 = take ? n2 : H2; H3 = take ? n3 : H3;
     }
     V E1 = shfl_up_v(Ya, 1), E2 = shfl_up_v(Yb, 1);
     if (lane == 0) { E1 = vzero<V>(); E2 = vzero<V>(); }
@@ -375,20 +402,22 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) Q[q][c] = shfl_down_d(P[q][c], dd);
       }
-      if (lane + dd < 32) {
+      const bool take = lane + dd < 32;
+      V taun[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tau[q] = vfma(P[q][0], ub[0], vfma(P[q][1], ub[1], vfma(P[q][2], ub[2], vfma(P[q][3], ub[3], tau[q]))));
-        double N[4][4];
+      for (int q = 0; q < 4; ++q)
+        taun[q] = vfma(P[q][0], ub[0], vfma(P[q][1], ub[1], vfma(P[q][2], ub[2], vfma(P[q][3], ub[3], tau[q]))));
+      double N[4][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            N[q][c] = fma(P[q][0], Q[0][c], fma(P[q][1], Q[1][c], fma(P[q][2], Q[2][c], P[q][3] * Q[3][c])));
+        for (int c = 0; c < 4; ++c)
+          N[q][c] = fma(P[q][0], Q[0][c], fma(P[q][1], Q[1][c], fma(P[q][2], Q[2][c], P[q][3] * Q[3][c])));
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q) {
+        tau[q] = take ? taun[q] : tau[q];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) P[q][c] = N[q][c];
+        for (int c = 0; c < 4; ++c) P[q][c] = take ? N[q][c] : P[q][c];
       }
     }
     V sg[4];
@@ -398,25 +427,23 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       if (lane == 31) sg[q] = vzero<V>();
     }
 
-    // ---- pass 3: reference back-substitution (Alg. 4 order)
+    // ---- pass 3: reference back-substitution (Alg. 4 order; masked rows give x = 0)
     V x1 = sg[0], x2 = sg[1], sq = sg[2], sv = sg[3];
 #pragma unroll
     for (int r = R - 1; r >= 0; --r) {
-      if (r < nr) {
-        const V yy = vfma(Ss[(r * NS + SG1) * 32 + lane], E1, vfma(Ss[(r * NS + SG2) * 32 + lane], E2, Ys[r * 32 + lane]));
-        const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                     f = Ss[(r * NS + SF) * 32 + lane];
-        const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
-        V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
-        acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
-        const V x = vmul(rd, acc);
-        const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
-        sq = vfma(qn, x2, sq);
-        sv = vfma(sn, x2, sv);
-        x2 = x1;
-        x1 = x;
-        Ys[r * 32 + lane] = x;
-      }
+      const V yy = vfma(Ss[(r * NS + SG1) * 32 + lane], E1, vfma(Ss[(r * NS + SG2) * 32 + lane], E2, Ys[r * 32 + lane]));
+      const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                   f = Ss[(r * NS + SF) * 32 + lane];
+      const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
+      V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
+      acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
+      const V x = vmul(rd, acc);
+      const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
+      sq = vfma(qn, x2, sq);
+      sv = vfma(sn, x2, sv);
+      x2 = x1;
+      x1 = x;
+      Ys[r * 32 + lane] = x;
     }
     // ---- fix
     V dl[4] = {vsub(x1, tau[0]), vsub(x2, tau[1]), vsub(sq, tau[2]), vsub(sv, tau[3])};
@@ -445,19 +472,17 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
     V c1 = wn[0], c2 = wn[1], cq = wn[2], cs = wn[3];
 #pragma unroll
     for (int r = R - 1; r >= 0; --r) {
-      if (r < nr) {
-        const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
-                     f = Ss[(r * NS + SF) * 32 + lane];
-        const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
-        const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
-        const V xc = vmul(-rd, acc);
-        const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
-        cq = vfma(qn, c2, cq);
-        cs = vfma(sn, c2, cs);
-        c2 = c1;
-        c1 = xc;
-        O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
-      }
+      const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
+                   f = Ss[(r * NS + SF) * 32 + lane];
+      const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
+      const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
+      const V xc = vmul(-rd, acc);
+      const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
+      cq = vfma(qn, c2, cq);
+      cs = vfma(sn, c2, cs);
+      c2 = c1;
+      c1 = xc;
+      if (r < nr) O::st_cs(out + (int64_t)(par + 2 * (s0 + r)) * B + j, vadd(Ys[r * 32 + lane], xc));
     }
     __syncwarp();
   }
@@ -485,7 +510,7 @@ static cudaError_t launch_persistent(K kernel, int threads, size_t smem, int64_t
 template <typename V, int R>
 static cudaError_t helm_launch_R(const HelmChunkArgs& a, cudaStream_t st) {
   constexpr int nwarp = R >= 32 ? 4 : 8;
-  const size_t smem = ((size_t)R * 3 * 32 + (size_t)nwarp * 2 * R * 32 * VOps<V>::ndouble) * sizeof(double);
+  const size_t smem = ((size_t)R * 4 * 32 + (size_t)nwarp * 2 * R * 32 * VOps<V>::ndouble) * sizeof(double);
   HelmChunkArgs copy = a;
   return launch_persistent(helm_chunk_kernel<V, R>, 32 * nwarp, smem, a.batch, nwarp, st, &copy);
 }
