@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--kx-rows", type=int, default=0, help="limit the kx rows per rank (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--method", default="stream", choices=["stream", "chunked", "stored"])
     return ap.parse_args()
 
 
@@ -154,15 +155,15 @@ def run_b200(args):
     dev = torch.device("cuda", local)
 
     t0 = time.perf_counter()
-    hlu = S.build_helmholtz(mats, nu, dt, z2)
-    blu = S.build_biharmonic(mats, nu, dt, z2)
+    hlu = S.build_helmholtz(mats, nu, dt, z2, method=args.method)
+    blu = S.build_biharmonic(mats, nu, dt, z2, method=args.method)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     # device-timed build (second build, warm)
     eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     eb0.record()
-    hlu = S.build_helmholtz(mats, nu, dt, z2)
-    blu = S.build_biharmonic(mats, nu, dt, z2)
+    hlu = S.build_helmholtz(mats, nu, dt, z2, method=args.method)
+    blu = S.build_biharmonic(mats, nu, dt, z2, method=args.method)
     eb1.record()
     torch.cuda.synchronize()
     build_ms = eb0.elapsed_time(eb1)
@@ -253,14 +254,15 @@ def run_b200(args):
             "config": {"workload": name, "systems_total": int(B_all), "kx_rows_per_rank": int(hi - lo),
                        "modes": {"helmholtz": nh, "biharmonic": nb}, "parallelism": f"kx-slab x{world}",
                        "l2_policy": "inputs (34 GB/operator at N=1) >> 126 MB L2; no flush needed",
-                       "lu": "built once before timing (stepper usage); build timed separately"},
+                       "lu": "built once before timing (stepper usage); build timed separately",
+                       "method": args.method},
             "per_operator": {
                 "helmholtz": {"ms": h_ms, "unknowns_per_s": nh * B / (h_ms / 1e3), "GBps_alg": ach_h,
                               "frac": ach_h / peak, "ckpt_read_bytes": ckpt_bytes_h},
                 "biharmonic": {"ms": b_ms, "unknowns_per_s": nb * B / (b_ms / 1e3), "GBps_alg": ach_b,
                                "frac": ach_b / peak, "ckpt_read_bytes": ckpt_bytes_b},
             },
-            "roofline": {"bound": "hbm", "kernel": f"{dom} chunked solve", "achieved": ach, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": f"{dom} {args.method} solve", "achieved": ach, "peak": peak,
                          "unit": "GB/s", "frac": ach / peak, "traffic": None,
                          "peak_source": peak_src,
                          "algorithmic_bytes": "32 B per complex unknown (16 B RHS read + 16 B solution write)"},
@@ -308,8 +310,8 @@ def run_e2e(S, mats, nu, dt, z2_full, n_y, args):
 
     rows = 64
     z2 = np.ascontiguousarray(z2_full[:rows])
-    hlu = S.build_helmholtz(mats, nu, dt, z2)
-    blu = S.build_biharmonic(mats, nu, dt, z2)
+    hlu = S.build_helmholtz(mats, nu, dt, z2, method=args.method)
+    blu = S.build_biharmonic(mats, nu, dt, z2, method=args.method)
     rng = np.random.default_rng(5)
     fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
     fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)

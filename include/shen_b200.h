@@ -67,6 +67,10 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  *                  pivot has |d| < 1e-300 (reset it first).
  * shen_helm_solve_chunked: fused factor+solve from the checkpoints
  *   (requires 32 * chunk_rows >= rows_p0; ckpt made with exact == 0).
+ * shen_helm_solve_stream: same inputs as the chunked solve (chunk_rows in
+ *   {4, 8, 16}); one thread per system with coalesced row access, y staged
+ *   in `out` through L2; warps_per_sm bounds the systems in flight
+ *   (0 = default 4).
  * shen_helm_solve_stored: solve with full stored factors (reference order).
  * rhs and out may alias only for the stored variant.
  * ------------------------------------------------------------------- */
@@ -76,6 +80,9 @@ int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, cons
 int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                             const double* st, const double* md, int chunk_rows, const double* ckpt,
                             const void* rhs, void* out, int is_complex, void* stream);
+int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                           const double* st, const double* md, int chunk_rows, const double* ckpt,
+                           const void* rhs, void* out, int is_complex, int warps_per_sm, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 
@@ -99,6 +106,9 @@ int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2,
 int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                            const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                            int is_complex, void* stream);
+int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                          const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                          int is_complex, int warps_per_sm, void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

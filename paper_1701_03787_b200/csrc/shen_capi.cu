@@ -84,6 +84,21 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
   return cuda_check(shen::launch_helm_chunk(a, is_complex != 0, S(stream)), "shen_helm_solve_chunked");
 }
 
+int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                           const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
+                           void* out, int is_complex, int warps_per_sm, void* stream) {
+  if (batch == 0) return SHEN_OK;
+  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: bad args");
+  const int rows0 = (n_dir + 1) / 2;
+  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: chunk_rows");
+  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: ckpt required");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: rhs must not alias out");
+  if (warps_per_sm <= 0) warps_per_sm = 4;
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
+  return cuda_check(shen::launch_helm_stream(a, is_complex != 0, warps_per_sm, S(stream)), "shen_helm_solve_stream");
+}
+
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream) {
   if (batch == 0) return SHEN_OK;
@@ -129,6 +144,21 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: rhs must not alias out");
   shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
   return cuda_check(shen::launch_bih_chunk(a, is_complex != 0, S(stream)), "shen_bih_solve_chunked");
+}
+
+int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                          const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                          int is_complex, int warps_per_sm, void* stream) {
+  if (batch == 0) return SHEN_OK;
+  if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: bad args");
+  const int rows0 = (n_bih + 1) / 2;
+  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: chunk_rows");
+  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: ckpt required");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: rhs must not alias out");
+  if (warps_per_sm <= 0) warps_per_sm = 4;
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
+  return cuda_check(shen::launch_bih_stream(a, is_complex != 0, warps_per_sm, S(stream)), "shen_bih_solve_stream");
 }
 
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,

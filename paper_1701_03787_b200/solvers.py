@@ -51,6 +51,16 @@ __all__ = [
 
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
+_METHODS = ("chunked", "stream", "stored")
+STREAM_ROWS_H = 16  # checkpoint spacing of the streaming solve (registers per segment)
+STREAM_ROWS_B = 8
+
+
+def stream_warps() -> int:
+    """Resident warps per SM of the streaming solve (bounds the y staged in L2)."""
+    import os
+
+    return int(os.environ.get("SHEN_STREAM_WARPS", "4"))
 
 
 class ZeroPivotError(ArithmeticError):
@@ -216,6 +226,13 @@ class HelmholtzLU:
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
             del keep
+        elif self.method == "stream":
+            sd, st, md = self._tab
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            check(h.shen_helm_solve_stream(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
+                                           md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
+                                           out_dev.data_ptr(), int(is_complex), stream_warps(), sh),
+                  "shen_helm_solve_stream")
         else:
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -234,7 +251,7 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "ch
     Raises ``ZeroPivotError`` exactly like the reference."""
     import torch
 
-    if method not in ("chunked", "stored"):
+    if method not in _METHODS:
         raise ValueError(f"unknown method {method!r}")
     if dv.is_torch(z2):
         z2 = z2.detach().cpu().numpy()
@@ -246,14 +263,14 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "ch
     tabs = tuple(torch.from_numpy(t).to(dev) for t in _helm_tables(mats))
     cb_dev = torch.from_numpy(np.ascontiguousarray(cb_flat)).to(dev)
     B = cb_flat.size
-    R = chunk_rows_for(nd)
+    R = chunk_rows_for(nd) if method == "chunked" else STREAM_ROWS_H
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method == "chunked":
+    if method in ("chunked", "stream"):
         C = _n_chunks(nd, R)
         ckpt = torch.empty((C, 2, 3, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_helm_factor(nd, float(ca), cb_dev.data_ptr(), B, tabs[0].data_ptr(), tabs[1].data_ptr(),
@@ -416,6 +433,12 @@ class BiharmonicLU:
                                           ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(), int(is_complex), sh),
                   "shen_bih_solve_stored")
             del keep
+        elif self.method == "stream":
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            check(h.shen_bih_solve_stream(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
+                                          self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
+                                          out_dev.data_ptr(), int(is_complex), stream_warps(), sh),
+                  "shen_bih_solve_stream")
         else:
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
             check(h.shen_bih_solve_chunked(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
@@ -428,7 +451,7 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "c
     """Factor the biharmonic operator for every z^2 (reference solvers.py:271-355)."""
     import torch
 
-    if method not in ("chunked", "stored"):
+    if method not in _METHODS:
         raise ValueError(f"unknown method {method!r}")
     if dv.is_torch(z2):
         z2 = z2.detach().cpu().numpy()
@@ -443,14 +466,14 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "c
     x1d = torch.from_numpy(x1).to(dev)
     x2d = torch.from_numpy(x2).to(dev)
     B = x1.size
-    R = chunk_rows_for(nb)
+    R = chunk_rows_for(nb) if method == "chunked" else STREAM_ROWS_B
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method == "chunked":
+    if method in ("chunked", "stream"):
         C = _n_chunks(nb, R)
         ckpt = torch.empty((C, 2, 10, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_bih_factor(nb, float(xi0), x1d.data_ptr(), x2d.data_ptr(), B, tab.data_ptr(), R,

@@ -65,13 +65,14 @@ def test_stored_solve_bitwise_vs_reference(golden, golden_meta, case):
 
 
 @pytest.mark.parametrize("case", range(8))
-def test_chunked_solve_parity(golden, golden_meta, case):
+@pytest.mark.parametrize("method", ["chunked", "stream"])
+def test_fused_solve_parity(golden, golden_meta, case, method):
     g = golden("solvers.npz")
     meta = golden_meta["solver_cases"][case]
     mats = assemble(meta["n_x"], meta["family"])
     z2 = g[f"c{case}_z2"]
-    hl = S.build_helmholtz(mats, meta["nu"], meta["dt"], z2)
-    bl = S.build_biharmonic(mats, meta["nu"], meta["dt"], z2)
+    hl = S.build_helmholtz(mats, meta["nu"], meta["dt"], z2, method=method)
+    bl = S.build_biharmonic(mats, meta["nu"], meta["dt"], z2, method=method)
     for kind in ("real", "cplx"):
         for op, lu in (("h", hl), ("b", bl)):
             x = lu.solve(g[f"c{case}_{op}_rhs_{kind}"])
@@ -202,7 +203,8 @@ def _corner_systems(n_y, n_z):
 
 
 @pytest.mark.parametrize("op", ["h", "b"])
-def test_config4_corners_residual(op):
+@pytest.mark.parametrize("method", ["chunked", "stream"])
+def test_config4_corners_residual(op, method):
     """BASELINE config 4 parameters (n_x = 1024, nu = 1/2000, dt = 1e-4) on
     32 systems including the largest z^2 of the 2048 x 1025 plane."""
     mats = assemble(1024, 0)
@@ -212,11 +214,11 @@ def test_config4_corners_residual(op):
     rng = np.random.default_rng(44)
     f = rng.standard_normal((nm, z2.size)) + 1j * rng.standard_normal((nm, z2.size))
     if op == "h":
-        x = S.build_helmholtz(mats, nu, dt, z2).solve(f)
+        x = S.build_helmholtz(mats, nu, dt, z2, method=method).solve(f)
         ref = O.helmholtz_solve(O.helmholtz_factor(mats, nu, dt, z2), f)
         dense = O.dense_helmholtz
     else:
-        x = S.build_biharmonic(mats, nu, dt, z2).solve(f)
+        x = S.build_biharmonic(mats, nu, dt, z2, method=method).solve(f)
         ref = O.biharmonic_solve(O.biharmonic_factor(mats, nu, dt, z2), f)
         dense = O.dense_biharmonic
     assert O.max_rel_per_system(x, ref).max() <= TOL
@@ -228,7 +230,8 @@ def test_config4_corners_residual(op):
 
 
 @pytest.mark.parametrize("N", [129, 257, 513, 1025, 2049])
-def test_config5_sizes(N):
+@pytest.mark.parametrize("method", ["chunked", "stream"])
+def test_config5_sizes(N, method):
     """BASELINE config 5 wall-normal sweep, 24 systems of the 512 x 257 plane."""
     mats = assemble(N - 1, 0)
     z2 = _corner_systems(512, 512)[:24]
@@ -237,5 +240,5 @@ def test_config5_sizes(N):
     for build, fac, sol, nm in ((S.build_helmholtz, O.helmholtz_factor, O.helmholtz_solve, mats.n_dir),
                                 (S.build_biharmonic, O.biharmonic_factor, O.biharmonic_solve, mats.n_bih)):
         f = rng.standard_normal((nm, z2.size)) + 1j * rng.standard_normal((nm, z2.size))
-        x = build(mats, nu, dt, z2).solve(f)
+        x = build(mats, nu, dt, z2, method=method).solve(f)
         assert O.max_rel_per_system(x, sol(fac(mats, nu, dt, z2), f)).max() <= TOL
