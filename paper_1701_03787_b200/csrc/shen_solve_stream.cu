@@ -70,7 +70,7 @@ template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 constexpr int kStreamThreads = 64;  // 2 warps: parity 0, parity 1
 
 // Shared-memory plan common to both operators (per CTA):
-//   stage [2][R][64] V : cp.async landing zone (forward RHS / backward y)
+//   stage [kRing][R][64] V : cp.async ring (forward RHS / backward y)
 //   tail  [T][64]    V : the last T = tail_segs*R rows of y of every thread
 //   (Helmholtz only) table [2][nseg*R] double4
 struct StreamPlan {
@@ -84,6 +84,20 @@ __device__ __forceinline__ int tail_slot(int s, int nseg, int tail_segs) {
   return s >= first ? s - first : -1;
 }
 
+constexpr int kRing = 4;  // stage buffers; prefetch distance kRing - 1 segments
+
+// cp.async the rows of segment s (parity rows s*R ...) of `src` into stage buffer b
+template <typename V, int R>
+__device__ __forceinline__ void stage_segment(V* stage, int b, const V* src, int s, int n, int par, int64_t B,
+                                              int64_t jc, bool jv, int tid) {
+  V* dst = stage + (size_t)b * R * kStreamThreads;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = s * R + r;
+    cpa(dst + r * kStreamThreads + tid, src + (int64_t)(par + 2 * min(i, n - 1)) * B + jc, jv && i < n);
+  }
+}
+
 // ======================================================================= Helmholtz
 template <typename V, int R>
 __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChunkArgs a, int tail_segs, int tab_rows) {
@@ -95,7 +109,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
   const int nseg = (n + R - 1) / R;
   const int tseg = min(tail_segs, nseg);
   V* stage = reinterpret_cast<V*>(smem);                        // [2][R][64]
-  V* tail = stage + 2 * R * kStreamThreads;                     // [tail_segs*R][64]
+  V* tail = stage + kRing * R * kStreamThreads;                 // [tail_segs*R][64]
   double4* tab = reinterpret_cast<double4*>(tail + (size_t)tail_segs * R * kStreamThreads);  // [2][tab_rows]
   for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
     const int p = idx / tab_rows, i = idx - p * tab_rows;
@@ -124,26 +138,19 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
     const double sub = __dmul_rn(cb, -1.5707963267948966);
     // ---------------- forward
 #pragma unroll
-    for (int r = 0; r < R; ++r) cpa(stage + r * kStreamThreads + tid, rowp(rhs, min(r, n - 1), jc), jv && r < n);
-    cpa_commit();
+    for (int u = 0; u < kRing - 1; ++u) {
+      if (u < nseg) stage_segment<V, R>(stage, u, rhs, u, n, par, B, jc, jv, tid);
+      cpa_commit();
+    }
     HelmProj pj;
     hp_origin(pj);
     V y = szero<V>();
     double dl = 0.0, el = 0.0, tl = 0.0;
     for (int s = 0; s < nseg; ++s) {
-      if (s + 1 < nseg) {
-        V* nb = stage + ((s + 1) & 1) * R * kStreamThreads;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = (s + 1) * R + r;
-          cpa(nb + r * kStreamThreads + tid, rowp(rhs, min(i, n - 1), jc), jv && i < n);
-        }
-        cpa_commit();
-        cpa_wait<1>();
-      } else {
-        cpa_wait<0>();
-      }
-      const V* cur = stage + (s & 1) * R * kStreamThreads;
+      if (s + kRing - 1 < nseg) stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
+      cpa_commit();
+      cpa_wait<kRing - 1>();
+      const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
       if (s > 0) hp_start(pj, dl, el, tl);
       const int ts = tail_slot(s, nseg, tseg);
 #pragma unroll
@@ -163,18 +170,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
       }
     }
     // ---------------- backward
-    // prefetch the first staged (global) segment below the tail
+    cpa_wait<0>();
+    // staged (global) segments are consumed in the order first_tail-1, ..., 0
     const int first_tail = nseg - tseg;
-    if (first_tail - 1 >= 0) {
-      const int s = first_tail - 1;
-      V* nb = stage + (s & 1) * R * kStreamThreads;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        cpa(nb + r * kStreamThreads + tid, rowp(out, min(i, n - 1), jc), jv && i < n);
-      }
+    for (int u = 0; u < kRing - 1; ++u) {
+      if (first_tail - 1 - u >= 0) stage_segment<V, R>(stage, u, out, first_tail - 1 - u, n, par, B, jc, jv, tid);
+      cpa_commit();
     }
-    cpa_commit();
     V x1 = szero<V>(), S = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
       const int ts = tail_slot(s, nseg, tseg);
@@ -203,20 +206,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
       if (ts >= 0) {
         ysrc = tail + (size_t)ts * R * kStreamThreads;
       } else {
-        // issue the next staged segment, then wait for this one
-        if (s - 1 >= 0) {
-          V* nb = stage + ((s - 1) & 1) * R * kStreamThreads;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const int i = (s - 1) * R + r;
-            cpa(nb + r * kStreamThreads + tid, rowp(out, min(i, n - 1), jc), jv && i < n);
-          }
-          cpa_commit();
-          cpa_wait<1>();
-        } else {
-          cpa_wait<0>();
-        }
-        ysrc = stage + (s & 1) * R * kStreamThreads;
+        const int u = first_tail - 1 - s;  // position in the staged sequence
+        if (s - (kRing - 1) >= 0)
+          stage_segment<V, R>(stage, (u + kRing - 1) % kRing, out, s - (kRing - 1), n, par, B, jc, jv, tid);
+        cpa_commit();
+        cpa_wait<kRing - 1>();
+        ysrc = stage + (size_t)(u % kRing) * R * kStreamThreads;
       }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
@@ -245,7 +240,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
   const int nseg = (n + R - 1) / R;
   const int tseg = min(tail_segs, nseg);
   V* stage = reinterpret_cast<V*>(smem);
-  V* tail = stage + 2 * R * kStreamThreads;
+  V* tail = stage + kRing * R * kStreamThreads;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
@@ -260,24 +255,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
     // ---------------- forward
 #pragma unroll
-    for (int r = 0; r < R; ++r) cpa(stage + r * kStreamThreads + tid, rowp(rhs, min(r, n - 1), jc), jv && r < n);
-    cpa_commit();
+    for (int q = 0; q < kRing - 1; ++q) {
+      if (q < nseg) stage_segment<V, R>(stage, q, rhs, q, n, par, B, jc, jv, tid);
+      cpa_commit();
+    }
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
     V y1 = szero<V>(), y2 = szero<V>();
     for (int s = 0; s < nseg; ++s) {
-      if (s + 1 < nseg) {
-        V* nbuf = stage + ((s + 1) & 1) * R * kStreamThreads;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = (s + 1) * R + r;
-          cpa(nbuf + r * kStreamThreads + tid, rowp(rhs, min(i, n - 1), jc), jv && i < n);
-        }
-        cpa_commit();
-        cpa_wait<1>();
-      } else {
-        cpa_wait<0>();
-      }
-      const V* cur = stage + (s & 1) * R * kStreamThreads;
+      if (s + kRing - 1 < nseg) stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
+      cpa_commit();
+      cpa_wait<kRing - 1>();
+      const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
       const int ts = tail_slot(s, nseg, tseg);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -301,17 +289,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
       }
     }
     // ---------------- backward
+    cpa_wait<0>();
     const int first_tail = nseg - tseg;
-    if (first_tail - 1 >= 0) {
-      const int s = first_tail - 1;
-      V* nbuf = stage + (s & 1) * R * kStreamThreads;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        cpa(nbuf + r * kStreamThreads + tid, rowp(out, min(i, n - 1), jc), jv && i < n);
-      }
+    for (int q = 0; q < kRing - 1; ++q) {
+      if (first_tail - 1 - q >= 0) stage_segment<V, R>(stage, q, out, first_tail - 1 - q, n, par, B, jc, jv, tid);
+      cpa_commit();
     }
-    cpa_commit();
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
       const int ts = tail_slot(s, nseg, tseg);
@@ -349,19 +333,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
       if (ts >= 0) {
         ysrc = tail + (size_t)ts * R * kStreamThreads;
       } else {
-        if (s - 1 >= 0) {
-          V* nbuf = stage + ((s - 1) & 1) * R * kStreamThreads;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const int i = (s - 1) * R + r;
-            cpa(nbuf + r * kStreamThreads + tid, rowp(out, min(i, n - 1), jc), jv && i < n);
-          }
-          cpa_commit();
-          cpa_wait<1>();
-        } else {
-          cpa_wait<0>();
-        }
-        ysrc = stage + (s & 1) * R * kStreamThreads;
+        const int u = first_tail - 1 - s;  // position in the staged sequence
+        if (s - (kRing - 1) >= 0)
+          stage_segment<V, R>(stage, (u + kRing - 1) % kRing, out, s - (kRing - 1), n, par, B, jc, jv, tid);
+        cpa_commit();
+        cpa_wait<kRing - 1>();
+        ysrc = stage + (size_t)(u % kRing) * R * kStreamThreads;
       }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
@@ -395,7 +372,7 @@ static int stream_ctas(int ctas_per_sm) {
 // shared memory for staging + tail; the tail takes what is left of `budget`
 template <typename V, int R>
 static int stream_tail_segs(int nseg_max, size_t fixed_bytes, size_t budget) {
-  const size_t stage = (size_t)2 * R * kStreamThreads * sizeof(V);
+  const size_t stage = (size_t)kRing * R * kStreamThreads * sizeof(V);
   const size_t per_seg = (size_t)R * kStreamThreads * sizeof(V);
   if (budget <= fixed_bytes + stage) return 0;
   const int t = (int)((budget - fixed_bytes - stage) / per_seg);
@@ -410,7 +387,7 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, int ctas_per_sm, cudaSt
   const size_t tab_bytes = (size_t)2 * tab_rows * sizeof(double4);
   const size_t budget = (size_t)(220 * 1024) / std::max(1, ctas_per_sm);
   const int tail = stream_tail_segs<V, R>(nseg0, tab_bytes, budget);
-  const size_t smem = (size_t)(2 + tail) * R * kStreamThreads * sizeof(V) + tab_bytes;
+  const size_t smem = (size_t)(kRing + tail) * R * kStreamThreads * sizeof(V) + tab_bytes;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t err = cudaFuncSetAttribute(helm_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
@@ -426,7 +403,7 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, int ctas_per_sm, cudaStre
   const int nseg0 = (n0 + R - 1) / R;
   const size_t budget = (size_t)(200 * 1024) / std::max(1, ctas_per_sm);
   const int tail = stream_tail_segs<V, R>(nseg0, 0, budget);
-  const size_t smem = (size_t)(2 + tail) * R * kStreamThreads * sizeof(V);
+  const size_t smem = (size_t)(kRing + tail) * R * kStreamThreads * sizeof(V);
   cudaError_t err = cudaFuncSetAttribute(bih_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int64_t groups = (a.batch + 31) / 32;
