@@ -44,6 +44,8 @@ const char* shen_version(void);
 const char* shen_last_error(void);
 /* visible CUDA devices (0 on a machine without a GPU; never aborts) */
 int shen_device_count(void);
+/* scratch bytes of shen_{helm,bih}_solve_stream (op 0 = Helmholtz, 1 = biharmonic) */
+int64_t shen_stream_scratch_bytes(int op, int n_modes, int chunk_rows, int64_t batch, int is_complex);
 /* set pivot[0] = pivot[1] = INT32_MAX on the device (stream-ordered) */
 int shen_pivot_reset(int* pivot_dev, void* stream);
 
@@ -68,9 +70,10 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  * shen_helm_solve_chunked: fused factor+solve from the checkpoints
  *   (requires 32 * chunk_rows >= rows_p0; ckpt made with exact == 0).
  * shen_helm_solve_stream: same inputs as the chunked solve (chunk_rows in
- *   {4, 8, 16}); one thread per system with coalesced row access, y staged
- *   in `out` through L2; warps_per_sm bounds the systems in flight
- *   (0 = default 4).
+ *   {4, 8, 16}); one thread per system with coalesced row access; y is
+ *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
+ *   bytes) and recomputed in the backward sweep; warps_per_sm caps the
+ *   resident warps per SM (0 = as many as fit).
  * shen_helm_solve_stored: solve with full stored factors (reference order).
  * rhs and out may alias only for the stored variant.
  * ------------------------------------------------------------------- */
@@ -82,7 +85,8 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
                             const void* rhs, void* out, int is_complex, void* stream);
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
-                           const void* rhs, void* out, int is_complex, int warps_per_sm, void* stream);
+                           const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
+                           void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 
@@ -108,7 +112,7 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
                            int is_complex, void* stream);
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          int is_complex, int warps_per_sm, void* stream);
+                          void* scratch, int is_complex, int warps_per_sm, void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

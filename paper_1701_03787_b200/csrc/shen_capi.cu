@@ -1,4 +1,5 @@
 // extern "C" boundary: argument validation, stream plumbing, error text.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -45,6 +46,14 @@ int shen_device_count(void) {
   return n;
 }
 
+int64_t shen_stream_scratch_bytes(int op, int n_modes, int chunk_rows, int64_t batch, int is_complex) {
+  if (chunk_rows <= 0 || n_modes < 2 || batch < 0) return -1;
+  const int64_t rows0 = (n_modes + 1) / 2;
+  const int64_t nseg = (rows0 + chunk_rows - 1) / chunk_rows;
+  const int64_t per = (op == 0 ? 1 : 2) * (is_complex ? 16 : 8);
+  return std::max<int64_t>(nseg - 1, 0) * 2 * per * batch;
+}
+
 int shen_pivot_reset(int* pivot_dev, void* stream) {
   if (!pivot_dev) return fail(SHEN_ERR_ARG, "pivot_dev is NULL");
   fill_int_kernel<<<1, 32, 0, S(stream)>>>(pivot_dev, 2, INT_MAX);
@@ -86,7 +95,7 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
-                           void* out, int is_complex, int warps_per_sm, void* stream) {
+                           void* out, void* scratch, int is_complex, int warps_per_sm, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: bad args");
@@ -94,9 +103,10 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
   if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: chunk_rows");
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: rhs must not alias out");
-  if (warps_per_sm <= 0) warps_per_sm = 4;
+  if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: scratch required");
   shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
-  return cuda_check(shen::launch_helm_stream(a, is_complex != 0, warps_per_sm, S(stream)), "shen_helm_solve_stream");
+  return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
+                    "shen_helm_solve_stream");
 }
 
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
@@ -148,7 +158,7 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
 
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          int is_complex, int warps_per_sm, void* stream) {
+                          void* scratch, int is_complex, int warps_per_sm, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: bad args");
@@ -156,9 +166,10 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
   if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: chunk_rows");
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: rhs must not alias out");
-  if (warps_per_sm <= 0) warps_per_sm = 4;
+  if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: scratch required");
   shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
-  return cuda_check(shen::launch_bih_stream(a, is_complex != 0, warps_per_sm, S(stream)), "shen_bih_solve_stream");
+  return cuda_check(shen::launch_bih_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
+                    "shen_bih_solve_stream");
 }
 
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,

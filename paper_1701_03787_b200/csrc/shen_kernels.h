@@ -106,7 +106,9 @@ cudaError_t launch_bih_seq(const BihSeqArgs& a, bool complex_rhs, cudaStream_t s
 cudaError_t launch_helm_chunk(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
 cudaError_t launch_bih_chunk(const BihChunkArgs& a, bool complex_rhs, cudaStream_t st);
 // streaming sequential solve (lanes = systems); warps_per_sm bounds the systems in flight
-cudaError_t launch_helm_stream(const HelmChunkArgs& a, bool complex_rhs, int warps_per_sm, cudaStream_t st);
-cudaError_t launch_bih_stream(const BihChunkArgs& a, bool complex_rhs, int warps_per_sm, cudaStream_t st);
+cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
+                               cudaStream_t st);
+cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
+                              cudaStream_t st);
 
 }  // namespace shen

@@ -69,19 +69,9 @@ template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 
 constexpr int kStreamThreads = 64;  // 2 warps: parity 0, parity 1
 
-// Shared-memory plan common to both operators (per CTA):
-//   stage [kRing][R][64] V : cp.async ring (forward RHS / backward y)
-//   tail  [T][64]    V : the last T = tail_segs*R rows of y of every thread
-//   (Helmholtz only) table [2][nseg*R] double4
-struct StreamPlan {
-  int nseg[2];      // segments per parity
-  int tail_segs;    // segments of y kept in shared memory
-};
-
-// segment s of parity `par` -> where its y lives: >= 0 -> tail segment index
-__device__ __forceinline__ int tail_slot(int s, int nseg, int tail_segs) {
-  const int first = nseg - tail_segs;
-  return s >= first ? s - first : -1;
+template <typename V>
+__device__ __forceinline__ V* rowp_out(V* base, int par, int i, int64_t B, int64_t j) {
+  return base + (int64_t)(par + 2 * i) * B + j;
 }
 
 constexpr int kRing = 4;  // stage buffers; prefetch distance kRing - 1 segments
@@ -99,18 +89,21 @@ __device__ __forceinline__ void stage_segment(V* stage, int b, const V* src, int
 }
 
 // ======================================================================= Helmholtz
+// v3 ("recompute y"): the forward sweep keeps only y at segment ends
+// (ychk, 1 value per R rows); the backward sweep re-streams the segment's
+// RHS rows and recomputes factors and y from the two checkpoints before the
+// back-substitution.  HBM traffic: 2 RHS reads + 1 solution write per row,
+// nothing depends on L2 capacity, so occupancy can be high.
 template <typename V, int R>
-__global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChunkArgs a, int tail_segs, int tab_rows) {
+__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, par = tid >> 5;
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  const int tseg = min(tail_segs, nseg);
-  V* stage = reinterpret_cast<V*>(smem);                        // [2][R][64]
-  V* tail = stage + kRing * R * kStreamThreads;                 // [tail_segs*R][64]
-  double4* tab = reinterpret_cast<double4*>(tail + (size_t)tail_segs * R * kStreamThreads);  // [2][tab_rows]
+  V* stage = reinterpret_cast<V*>(smem);                                                   // [kRing][R][64]
+  double4* tab = reinterpret_cast<double4*>(stage + (size_t)kRing * R * kStreamThreads);  // [2][tab_rows]
   for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
     const int p = idx / tab_rows, i = idx - p * tab_rows;
     const int np = (a.n_dir - p + 1) / 2;
@@ -126,17 +119,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
   const double4* mytab = tab + par * tab_rows;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
-  const uint64_t keep = policy_evict_last();
   const int64_t ngroups = (B + 31) / 32;
-  auto rowp = [&](auto* base, int i, int64_t j) { return base + (int64_t)(par + 2 * i) * B + j; };
 
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t j = g * 32 + lane;
     const bool jv = j < B;
-    const int64_t jc = jv ? j : B - 1;  // clamped (loads stay in bounds; results discarded)
+    const int64_t jc = jv ? j : B - 1;
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
-    // ---------------- forward
+    // ---------------- forward: y at segment ends only
 #pragma unroll
     for (int u = 0; u < kRing - 1; ++u) {
       if (u < nseg) stage_segment<V, R>(stage, u, rhs, u, n, par, B, jc, jv, tid);
@@ -147,48 +138,50 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
     V y = szero<V>();
     double dl = 0.0, el = 0.0, tl = 0.0;
     for (int s = 0; s < nseg; ++s) {
-      if (s + kRing - 1 < nseg) stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
+      if (s + kRing - 1 < nseg)
+        stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
       cpa_commit();
       cpa_wait<kRing - 1>();
       const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
       if (s > 0) hp_start(pj, dl, el, tl);
-      const int ts = tail_slot(s, nseg, tseg);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        const double4 tv = mytab[i];
+        const double4 tv = mytab[s * R + r];
         const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
         if (r > 0 && (r & 7) == 0) hp_rescale(pj);
         double d, e, t;
         const double low = hp_step(pj, row, sub, d, e, t);
         dl = d; el = e; tl = t;
         y = sfma(-low, y, cur[r * kStreamThreads + tid]);
-        if (ts >= 0)
-          tail[(ts * R + r) * kStreamThreads + tid] = y;
-        else if (jv && i < n)
-          st_keep(rowp(out, i, j), y, keep);
       }
+      if (jv && s + 1 < nseg) ychk[((int64_t)s * 2 + par) * B + j] = y;
     }
-    // ---------------- backward
     cpa_wait<0>();
-    // staged (global) segments are consumed in the order first_tail-1, ..., 0
-    const int first_tail = nseg - tseg;
+    // ---------------- backward: re-stream each segment (bottom first)
 #pragma unroll
     for (int u = 0; u < kRing - 1; ++u) {
-      if (first_tail - 1 - u >= 0) stage_segment<V, R>(stage, u, out, first_tail - 1 - u, n, par, B, jc, jv, tid);
+      if (nseg - 1 - u >= 0) stage_segment<V, R>(stage, u, rhs, nseg - 1 - u, n, par, B, jc, jv, tid);
       cpa_commit();
     }
     V x1 = szero<V>(), S = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
-      const int ts = tail_slot(s, nseg, tseg);
+      const int u = nseg - 1 - s;
+      if (s - (kRing - 1) >= 0)
+        stage_segment<V, R>(stage, (u + kRing - 1) % kRing, rhs, s - (kRing - 1), n, par, B, jc, jv, tid);
+      cpa_commit();
       HelmProj q;
+      V yy = szero<V>();
       if (s == 0) {
         hp_origin(q);
       } else {
         const double* ck = a.ckpt + ((int64_t)(s * 2 + par) * 3) * B + jc;
         hp_start(q, __ldg(ck), __ldg(ck + B), __ldg(ck + 2 * B));
+        yy = ychk[((int64_t)(s - 1) * 2 + par) * B + jc];
       }
+      cpa_wait<kRing - 1>();
+      const V* cur = stage + (size_t)(u % kRing) * R * kStreamThreads;
       double rd_[R], e_[R], t_[R];
+      V y_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
@@ -196,32 +189,22 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
         const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
         if (r > 0 && (r & 7) == 0) hp_rescale(q);
         double d, e, t;
-        hp_step(q, row, sub, d, e, t);
+        const double low = hp_step(q, row, sub, d, e, t);
+        yy = sfma(-low, yy, cur[r * kStreamThreads + tid]);
         const bool valid = i < n;
+        y_[r] = yy;
         rd_[r] = valid ? q.rd : 0.0;
         e_[r] = valid ? e : 0.0;
         t_[r] = valid ? t : 0.0;
       }
-      const V* ysrc;
-      if (ts >= 0) {
-        ysrc = tail + (size_t)ts * R * kStreamThreads;
-      } else {
-        const int u = first_tail - 1 - s;  // position in the staged sequence
-        if (s - (kRing - 1) >= 0)
-          stage_segment<V, R>(stage, (u + kRing - 1) % kRing, out, s - (kRing - 1), n, par, B, jc, jv, tid);
-        cpa_commit();
-        cpa_wait<kRing - 1>();
-        ysrc = stage + (size_t)(u % kRing) * R * kStreamThreads;
-      }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
         const int i = s * R + r;
-        const V yv = ysrc[r * kStreamThreads + tid];
-        const V acc = ssub(ssub(yv, smul(e_[r], x1)), smul(t_[r], S));
+        const V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(t_[r], S));
         const V x = smul(rd_[r], acc);
         S = sadd(x1, S);
         x1 = x;
-        if (jv && i < n) O::st_cs(rowp(out, i, j), x);
+        if (jv && i < n) O::st_cs(rowp_out(out, par, i, B, j), x);
       }
     }
     cpa_wait<0>();
@@ -230,7 +213,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) helm_stream_kernel(HelmChun
 
 // ======================================================================= biharmonic
 template <typename V, int R>
-__global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkArgs a, int tail_segs) {
+__global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs a, V* ychk) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, par = tid >> 5;
@@ -238,22 +221,18 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  const int tseg = min(tail_segs, nseg);
   V* stage = reinterpret_cast<V*>(smem);
-  V* tail = stage + kRing * R * kStreamThreads;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
-  const uint64_t keep = policy_evict_last();
   const int64_t ngroups = (B + 31) / 32;
-  auto rowp = [&](auto* base, int i, int64_t j) { return base + (int64_t)(par + 2 * i) * B + j; };
 
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     const int64_t j = g * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
-    // ---------------- forward
+    // ---------------- forward: (y_last, y_last-1) at segment ends only
 #pragma unroll
     for (int q = 0; q < kRing - 1; ++q) {
       if (q < nseg) stage_segment<V, R>(stage, q, rhs, q, n, par, B, jc, jv, tid);
@@ -262,11 +241,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
     V y1 = szero<V>(), y2 = szero<V>();
     for (int s = 0; s < nseg; ++s) {
-      if (s + kRing - 1 < nseg) stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
+      if (s + kRing - 1 < nseg)
+        stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
       cpa_commit();
       cpa_wait<kRing - 1>();
       const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
-      const int ts = tail_slot(s, nseg, tseg);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
@@ -282,24 +261,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
         const V y = sfma(-l4, y2, sfma(-l2, y1, cur[r * kStreamThreads + tid]));
         y2 = y1;
         y1 = y;
-        if (ts >= 0)
-          tail[(ts * R + r) * kStreamThreads + tid] = y;
-        else if (jv && i < n)
-          st_keep(rowp(out, i, j), y, keep);
+      }
+      if (jv && s + 1 < nseg) {
+        ychk[(((int64_t)s * 2 + par) * 2 + 0) * B + j] = y1;
+        ychk[(((int64_t)s * 2 + par) * 2 + 1) * B + j] = y2;
       }
     }
-    // ---------------- backward
     cpa_wait<0>();
-    const int first_tail = nseg - tseg;
+    // ---------------- backward
 #pragma unroll
     for (int q = 0; q < kRing - 1; ++q) {
-      if (first_tail - 1 - q >= 0) stage_segment<V, R>(stage, q, out, first_tail - 1 - q, n, par, B, jc, jv, tid);
+      if (nseg - 1 - q >= 0) stage_segment<V, R>(stage, q, rhs, nseg - 1 - q, n, par, B, jc, jv, tid);
       cpa_commit();
     }
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
-      const int ts = tail_slot(s, nseg, tseg);
+      const int uu = nseg - 1 - s;
+      if (s - (kRing - 1) >= 0)
+        stage_segment<V, R>(stage, (uu + kRing - 1) % kRing, rhs, s - (kRing - 1), n, par, B, jc, jv, tid);
+      cpa_commit();
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
+      V ya = szero<V>(), yb = szero<V>();
       if (s > 0) {
         const double* ck = a.ckpt + ((int64_t)(s * 2 + par) * 10) * B + jc;
         w1.d = __ldg(ck); w1.e = __ldg(ck + B); w1.f = __ldg(ck + 2 * B); w1.a = __ldg(ck + 3 * B);
@@ -308,8 +290,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
         w2.b = __ldg(ck + 9 * B);
         w1.rd = rcp_fast(w1.d);
         w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
+        ya = ychk[(((int64_t)(s - 1) * 2 + par) * 2 + 0) * B + jc];
+        yb = ychk[(((int64_t)(s - 1) * 2 + par) * 2 + 1) * B + jc];
       }
+      cpa_wait<kRing - 1>();
+      const V* cur = stage + (size_t)(uu % kRing) * R * kStreamThreads;
       double rd_[R], e_[R], f_[R], a_[R], b_[R];
+      V y_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
@@ -322,23 +309,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
         bih_step_fast(w, w1, w2, hb, c, xi0, l2, l4);
         w2 = w1;
         w1 = w;
+        const V y = sfma(-l4, yb, sfma(-l2, ya, cur[r * kStreamThreads + tid]));
+        yb = ya;
+        ya = y;
         const bool valid = i < n;
+        y_[r] = y;
         rd_[r] = valid ? w.rd : 0.0;
         e_[r] = valid ? w.e : 0.0;
         f_[r] = valid ? w.f : 0.0;
         a_[r] = valid ? w.a : 0.0;
         b_[r] = valid ? w.b : 0.0;
-      }
-      const V* ysrc;
-      if (ts >= 0) {
-        ysrc = tail + (size_t)ts * R * kStreamThreads;
-      } else {
-        const int u = first_tail - 1 - s;  // position in the staged sequence
-        if (s - (kRing - 1) >= 0)
-          stage_segment<V, R>(stage, (u + kRing - 1) % kRing, out, s - (kRing - 1), n, par, B, jc, jv, tid);
-        cpa_commit();
-        cpa_wait<kRing - 1>();
-        ysrc = stage + (size_t)(u % kRing) * R * kStreamThreads;
       }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
@@ -346,15 +326,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) bih_stream_kernel(BihChunkA
         const int k = min(par + 2 * i, nb - 1);
         const double qn = i < n ? __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4) : 0.0;
         const double sn = i < n ? __ldg(a.tab + (int64_t)k * B_NCOL + B_S4) : 0.0;
-        const V yv = ysrc[r * kStreamThreads + tid];
-        V acc = ssub(ssub(yv, smul(e_[r], x1)), smul(f_[r], x2));
+        V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(f_[r], x2));
         acc = ssub(acc, smul(xi0, sadd(smul(a_[r], sq), smul(b_[r], sv))));
         const V x = smul(rd_[r], acc);
         sq = sfma(qn, x2, sq);
         sv = sfma(sn, x2, sv);
         x2 = x1;
         x1 = x;
-        if (jv && i < n) O::st_cs(rowp(out, i, j), x);
+        if (jv && i < n) O::st_cs(rowp_out(out, par, i, B, j), x);
       }
     }
     cpa_wait<0>();
@@ -369,80 +348,73 @@ static int stream_ctas(int ctas_per_sm) {
   return sms * std::max(1, ctas_per_sm);
 }
 
-// shared memory for staging + tail; the tail takes what is left of `budget`
-template <typename V, int R>
-static int stream_tail_segs(int nseg_max, size_t fixed_bytes, size_t budget) {
-  const size_t stage = (size_t)kRing * R * kStreamThreads * sizeof(V);
-  const size_t per_seg = (size_t)R * kStreamThreads * sizeof(V);
-  if (budget <= fixed_bytes + stage) return 0;
-  const int t = (int)((budget - fixed_bytes - stage) / per_seg);
-  return std::min(t, nseg_max);
+template <typename K>
+static int resident_ctas(K kernel, size_t smem) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kStreamThreads, smem) != cudaSuccess) return 1;
+  return std::max(1, occ);
 }
 
 template <typename V, int R>
-static cudaError_t helm_stream_R(const HelmChunkArgs& a, int ctas_per_sm, cudaStream_t st) {
+static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
   const int n0 = (a.n_dir + 1) / 2;
-  const int nseg0 = (n0 + R - 1) / R;
-  const int tab_rows = nseg0 * R;
-  const size_t tab_bytes = (size_t)2 * tab_rows * sizeof(double4);
-  const size_t budget = (size_t)(220 * 1024) / std::max(1, ctas_per_sm);
-  const int tail = stream_tail_segs<V, R>(nseg0, tab_bytes, budget);
-  const size_t smem = (size_t)(kRing + tail) * R * kStreamThreads * sizeof(V) + tab_bytes;
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const int tab_rows = ((n0 + R - 1) / R) * R;
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
   cudaError_t err = cudaFuncSetAttribute(helm_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(helm_stream_kernel<V, R>, smem))
+                                  : resident_ctas(helm_stream_kernel<V, R>, smem);
   const int64_t groups = (a.batch + 31) / 32;
-  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(ctas_per_sm));
-  helm_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, tail, tab_rows);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
+  helm_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
 }
 
 template <typename V, int R>
-static cudaError_t bih_stream_R(const BihChunkArgs& a, int ctas_per_sm, cudaStream_t st) {
-  const int n0 = (a.n_bih + 1) / 2;
-  const int nseg0 = (n0 + R - 1) / R;
-  const size_t budget = (size_t)(200 * 1024) / std::max(1, ctas_per_sm);
-  const int tail = stream_tail_segs<V, R>(nseg0, 0, budget);
-  const size_t smem = (size_t)(kRing + tail) * R * kStreamThreads * sizeof(V);
+static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
   cudaError_t err = cudaFuncSetAttribute(bih_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
+  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(bih_stream_kernel<V, R>, smem))
+                                  : resident_ctas(bih_stream_kernel<V, R>, smem);
   const int64_t groups = (a.batch + 31) / 32;
-  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(ctas_per_sm));
-  bih_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, tail);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
+  bih_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
 }
 
 template <typename V>
-static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, int w, cudaStream_t st) {
+static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
   switch (a.chunk_rows) {
-    case 4: return helm_stream_R<V, 4>(a, w, st);
-    case 8: return helm_stream_R<V, 8>(a, w, st);
-    case 16: return helm_stream_R<V, 16>(a, w, st);
+    case 4: return helm_stream_R<V, 4>(a, sc, w, st);
+    case 8: return helm_stream_R<V, 8>(a, sc, w, st);
+    case 16: return helm_stream_R<V, 16>(a, sc, w, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <typename V>
-static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, int w, cudaStream_t st) {
+static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, void* sc, int w, cudaStream_t st) {
   switch (a.chunk_rows) {
-    case 4: return bih_stream_R<V, 4>(a, w, st);
-    case 8: return bih_stream_R<V, 8>(a, w, st);
-    case 16: return bih_stream_R<V, 16>(a, w, st);
+    case 4: return bih_stream_R<V, 4>(a, sc, w, st);
+    case 8: return bih_stream_R<V, 8>(a, sc, w, st);
+    case 16: return bih_stream_R<V, 16>(a, sc, w, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-// `warps_per_sm` of the C ABI: resident CTAs per SM = warps_per_sm / 2
-cudaError_t launch_helm_stream(const HelmChunkArgs& a, bool cplx_rhs, int warps_per_sm, cudaStream_t st) {
+// warps_per_sm of the C ABI: resident 2-warp CTAs per SM = warps_per_sm / 2 (0 = as many as fit)
+cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm,
+                               cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
-  const int ctas = std::max(1, warps_per_sm / 2);
-  return cplx_rhs ? helm_stream_dispatch<cplx>(a, ctas, st) : helm_stream_dispatch<double>(a, ctas, st);
+  const int ctas = warps_per_sm / 2;
+  return cplx_rhs ? helm_stream_dispatch<cplx>(a, scratch, ctas, st) : helm_stream_dispatch<double>(a, scratch, ctas, st);
 }
 
-cudaError_t launch_bih_stream(const BihChunkArgs& a, bool cplx_rhs, int warps_per_sm, cudaStream_t st) {
+cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm, cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
-  const int ctas = std::max(1, warps_per_sm / 2);
-  return cplx_rhs ? bih_stream_dispatch<cplx>(a, ctas, st) : bih_stream_dispatch<double>(a, ctas, st);
+  const int ctas = warps_per_sm / 2;
+  return cplx_rhs ? bih_stream_dispatch<cplx>(a, scratch, ctas, st) : bih_stream_dispatch<double>(a, scratch, ctas, st);
 }
 
 }  // namespace shen

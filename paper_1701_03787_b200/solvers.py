@@ -57,10 +57,22 @@ STREAM_ROWS_B = 8
 
 
 def stream_warps() -> int:
-    """Resident warps per SM of the streaming solve (bounds the y staged in L2)."""
+    """Cap on resident warps per SM of the streaming solve (0 = as many as fit)."""
     import os
 
-    return int(os.environ.get("SHEN_STREAM_WARPS", "4"))
+    return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
+
+
+def _scratch(lu, op, n_modes, batch, is_complex, device):
+    """Per-LU cached device scratch of the streaming solve (y checkpoints)."""
+    import torch
+
+    nbytes = int(lib().shen_stream_scratch_bytes(op, n_modes, lu.chunk_rows, batch, int(is_complex)))
+    buf = getattr(lu, "_scratch_buf", None)
+    if buf is None or buf.numel() < nbytes or buf.device != device:
+        buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        lu._scratch_buf = buf
+    return buf.data_ptr()
 
 
 class ZeroPivotError(ArithmeticError):
@@ -229,9 +241,10 @@ class HelmholtzLU:
         elif self.method == "stream":
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
             check(h.shen_helm_solve_stream(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
                                            md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                           out_dev.data_ptr(), int(is_complex), stream_warps(), sh),
+                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), sh),
                   "shen_helm_solve_stream")
         else:
             sd, st, md = self._tab
@@ -435,9 +448,10 @@ class BiharmonicLU:
             del keep
         elif self.method == "stream":
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
             check(h.shen_bih_solve_stream(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
                                           self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                          out_dev.data_ptr(), int(is_complex), stream_warps(), sh),
+                                          out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), sh),
                   "shen_bih_solve_stream")
         else:
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
