@@ -88,12 +88,72 @@ __device__ __forceinline__ void stage_segment(V* stage, int b, const V* src, int
   }
 }
 
+// ---------------------------------------------------------------- bulk-copy ring
+// Each warp streams its segments (R rows x 32 systems = R contiguous row
+// pieces of 32*sizeof(V) bytes) through a kRing-deep shared-memory ring with
+// cp.async.bulk (the TMA engine; one elected lane issues, an mbarrier per
+// stage counts the bytes).  The sequence of segments a warp consumes is
+// continuous across the forward sweep (segments 0..nseg-1), the backward
+// sweep (nseg-1..0) and consecutive system groups, so the next group's first
+// rows are already in flight while the current group finishes.
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// segment q of a warp's continuous stream -> (group index, segment s)
+struct SegRef {
+  int64_t g;
+  int s;
+};
+__device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_t gstride) {
+  const int64_t per = 2 * (int64_t)nseg;
+  const int64_t gi = q / per;
+  const int k = (int)(q - gi * per);
+  return {g0 + gi * gstride, k < nseg ? k : 2 * nseg - 1 - k};
+}
+
+// lane 0 issues the R row pieces of segment `ref` into ring stage `st`
+template <typename V, int R>
+__device__ __forceinline__ void ring_issue(V* ring, uint64_t* bars, int st, const V* rhs, SegRef ref, int n, int par,
+                                           int64_t B, int64_t ngroups) {
+  if (ref.g >= ngroups) return;
+  const int64_t j0 = ref.g * 32;
+  const int nsys = (int)(B - j0 < 32 ? B - j0 : 32);
+  const unsigned piece = (unsigned)(nsys * sizeof(V));
+  int rows = min(R, n - ref.s * R);
+  fence_async_smem();
+  mbar_expect(bars + st, piece * (unsigned)rows);
+  V* dst = ring + (size_t)st * R * 32;
+  for (int r = 0; r < rows; ++r)
+    bulk_g2s(dst + r * 32, rhs + (int64_t)(par + 2 * (ref.s * R + r)) * B + j0, piece, bars + st);
+}
+
 // ======================================================================= Helmholtz
-// v3 ("recompute y"): the forward sweep keeps only y at segment ends
-// (ychk, 1 value per R rows); the backward sweep re-streams the segment's
-// RHS rows and recomputes factors and y from the two checkpoints before the
-// back-substitution.  HBM traffic: 2 RHS reads + 1 solution write per row,
-// nothing depends on L2 capacity, so occupancy can be high.
+// v4: recompute-y streaming solve (see file header), TMA bulk ring, per-warp
+// persistent stream of segments.  CTA = 2 warps (parity 0 / parity 1 of the
+// same 32 systems) sharing the row table; HBM traffic per unknown: 2 RHS
+// reads + 1 solution write (+ ~3 B of checkpoints).
 template <typename V, int R>
 __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
   using O = VOps<V>;
@@ -102,8 +162,9 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  V* stage = reinterpret_cast<V*>(smem);                                                   // [kRing][R][64]
-  double4* tab = reinterpret_cast<double4*>(stage + (size_t)kRing * R * kStreamThreads);  // [2][tab_rows]
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32;                   // [2 warps][kRing][R][32]
+  double4* tab = reinterpret_cast<double4*>(reinterpret_cast<V*>(smem) + (size_t)2 * kRing * R * 32);  // [2][tab_rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 2 * tab_rows) + par * kRing;          // [2][kRing]
   for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
     const int p = idx / tab_rows, i = idx - p * tab_rows;
     const int np = (a.n_dir - p + 1) / 2;
@@ -115,35 +176,51 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
     }
     tab[idx] = v;
   }
+  if (lane == 0)
+    for (int q = 0; q < kRing; ++q) mbar_init(bars + q, 1);
+  fence_async_smem();
   __syncthreads();
   const double4* mytab = tab + par * tab_rows;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const int64_t ngroups = (B + 31) / 32;
+  const int64_t g0 = blockIdx.x, gstride = gridDim.x;
+  if (g0 >= ngroups) return;
+  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;  // segments this warp consumes
+  int64_t qi = 0;                                                            // next segment to issue
+  if (lane == 0)
+    for (; qi < kRing - 1 && qi < nq; ++qi) ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
+  int64_t qc = 0;  // next segment to consume
+  auto consume = [&]() -> const V* {
+    __syncwarp();
+    if (lane == 0 && qi < nq) {
+      ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
+    }
+    ++qi;
+    const int st = (int)(qc % kRing);
+    mbar_wait(bars + st, (unsigned)((qc / kRing) & 1));
+    ++qc;
+    return ring + (size_t)st * R * 32;
+  };
 
-  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+  for (int64_t g = g0; g < ngroups; g += gstride) {
     const int64_t j = g * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
+    V* outj = out + (int64_t)par * B + j;      // row i at outj + 2*i*B
+    V* ychkj = ychk + (int64_t)par * B + jc;   // segment s at ychkj + 2*s*B
+    const double* ckj = a.ckpt + (int64_t)par * 3 * B + jc;  // segment s at ckj + 6*s*B
     // ---------------- forward: y at segment ends only
-#pragma unroll
-    for (int u = 0; u < kRing - 1; ++u) {
-      if (u < nseg) stage_segment<V, R>(stage, u, rhs, u, n, par, B, jc, jv, tid);
-      cpa_commit();
-    }
     HelmProj pj;
     hp_origin(pj);
     V y = szero<V>();
     double dl = 0.0, el = 0.0, tl = 0.0;
     for (int s = 0; s < nseg; ++s) {
-      if (s + kRing - 1 < nseg)
-        stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
-      cpa_commit();
-      cpa_wait<kRing - 1>();
-      const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
+      const V* cur = consume();
       if (s > 0) hp_start(pj, dl, el, tl);
+      const bool full = (s + 1) * R <= n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double4 tv = mytab[s * R + r];
@@ -152,46 +229,36 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
         double d, e, t;
         const double low = hp_step(pj, row, sub, d, e, t);
         dl = d; el = e; tl = t;
-        y = sfma(-low, y, cur[r * kStreamThreads + tid]);
+        const V b = (full || s * R + r < n) ? cur[r * 32 + lane] : szero<V>();
+        y = sfma(-low, y, b);
       }
-      if (jv && s + 1 < nseg) ychk[((int64_t)s * 2 + par) * B + j] = y;
+      if (jv && s + 1 < nseg) ychkj[(int64_t)2 * s * B] = y;
     }
-    cpa_wait<0>();
     // ---------------- backward: re-stream each segment (bottom first)
-#pragma unroll
-    for (int u = 0; u < kRing - 1; ++u) {
-      if (nseg - 1 - u >= 0) stage_segment<V, R>(stage, u, rhs, nseg - 1 - u, n, par, B, jc, jv, tid);
-      cpa_commit();
-    }
     V x1 = szero<V>(), S = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
-      const int u = nseg - 1 - s;
-      if (s - (kRing - 1) >= 0)
-        stage_segment<V, R>(stage, (u + kRing - 1) % kRing, rhs, s - (kRing - 1), n, par, B, jc, jv, tid);
-      cpa_commit();
       HelmProj q;
       V yy = szero<V>();
       if (s == 0) {
         hp_origin(q);
       } else {
-        const double* ck = a.ckpt + ((int64_t)(s * 2 + par) * 3) * B + jc;
+        const double* ck = ckj + (int64_t)6 * s * B;
         hp_start(q, __ldg(ck), __ldg(ck + B), __ldg(ck + 2 * B));
-        yy = ychk[((int64_t)(s - 1) * 2 + par) * B + jc];
+        yy = ychkj[(int64_t)2 * (s - 1) * B];
       }
-      cpa_wait<kRing - 1>();
-      const V* cur = stage + (size_t)(u % kRing) * R * kStreamThreads;
+      const V* cur = consume();
+      const bool full = (s + 1) * R <= n;
       double rd_[R], e_[R], t_[R];
       V y_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        const double4 tv = mytab[i];
+        const double4 tv = mytab[s * R + r];
         const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
         if (r > 0 && (r & 7) == 0) hp_rescale(q);
         double d, e, t;
         const double low = hp_step(q, row, sub, d, e, t);
-        yy = sfma(-low, yy, cur[r * kStreamThreads + tid]);
-        const bool valid = i < n;
+        const bool valid = full || s * R + r < n;
+        yy = sfma(-low, yy, valid ? cur[r * 32 + lane] : szero<V>());
         y_[r] = yy;
         rd_[r] = valid ? q.rd : 0.0;
         e_[r] = valid ? e : 0.0;
@@ -199,15 +266,13 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
-        const int i = s * R + r;
         const V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(t_[r], S));
         const V x = smul(rd_[r], acc);
         S = sadd(x1, S);
         x1 = x;
-        if (jv && i < n) O::st_cs(rowp_out(out, par, i, B, j), x);
+        if (jv && (full || s * R + r < n)) O::st_cs(outj + (int64_t)2 * (s * R + r) * B, x);
       }
     }
-    cpa_wait<0>();
   }
 }
 
@@ -221,31 +286,49 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  V* stage = reinterpret_cast<V*>(smem);
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smem) + (size_t)2 * kRing * R * 32) + par * kRing;
+  if (lane == 0)
+    for (int q = 0; q < kRing; ++q) mbar_init(bars + q, 1);
+  fence_async_smem();
+  __syncthreads();
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
   const int64_t ngroups = (B + 31) / 32;
+  const int64_t g0 = blockIdx.x, gstride = gridDim.x;
+  if (g0 >= ngroups) return;
+  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
+  int64_t qi = 0;
+  if (lane == 0)
+    for (; qi < kRing - 1 && qi < nq; ++qi) ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
+  int64_t qc = 0;
+  auto consume = [&]() -> const V* {
+    __syncwarp();
+    if (lane == 0 && qi < nq) {
+      ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
+    }
+    ++qi;
+    const int st = (int)(qc % kRing);
+    mbar_wait(bars + st, (unsigned)((qc / kRing) & 1));
+    ++qc;
+    return ring + (size_t)st * R * 32;
+  };
 
-  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+  for (int64_t g = g0; g < ngroups; g += gstride) {
     const int64_t j = g * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
-    // ---------------- forward: (y_last, y_last-1) at segment ends only
-#pragma unroll
-    for (int q = 0; q < kRing - 1; ++q) {
-      if (q < nseg) stage_segment<V, R>(stage, q, rhs, q, n, par, B, jc, jv, tid);
-      cpa_commit();
-    }
+    V* outj = out + (int64_t)par * B + j;
+    V* ychkj = ychk + (int64_t)par * 2 * B + jc;               // segment s: ychkj + 4*s*B (+B for y_{-2})
+    const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;   // segment s: ckj + 20*s*B
+    // ---------------- forward
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
     V y1 = szero<V>(), y2 = szero<V>();
     for (int s = 0; s < nseg; ++s) {
-      if (s + kRing - 1 < nseg)
-        stage_segment<V, R>(stage, (s + kRing - 1) % kRing, rhs, s + kRing - 1, n, par, B, jc, jv, tid);
-      cpa_commit();
-      cpa_wait<kRing - 1>();
-      const V* cur = stage + (size_t)(s % kRing) * R * kStreamThreads;
+      const V* cur = consume();
+      const bool full = (s + 1) * R <= n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
@@ -258,43 +341,34 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
         u2 = u1;
         u1 = u;
-        const V y = sfma(-l4, y2, sfma(-l2, y1, cur[r * kStreamThreads + tid]));
+        const V b = (full || i < n) ? cur[r * 32 + lane] : szero<V>();
+        const V y = sfma(-l4, y2, sfma(-l2, y1, b));
         y2 = y1;
         y1 = y;
       }
       if (jv && s + 1 < nseg) {
-        ychk[(((int64_t)s * 2 + par) * 2 + 0) * B + j] = y1;
-        ychk[(((int64_t)s * 2 + par) * 2 + 1) * B + j] = y2;
+        ychkj[(int64_t)4 * s * B] = y1;
+        ychkj[(int64_t)4 * s * B + B] = y2;
       }
     }
-    cpa_wait<0>();
     // ---------------- backward
-#pragma unroll
-    for (int q = 0; q < kRing - 1; ++q) {
-      if (nseg - 1 - q >= 0) stage_segment<V, R>(stage, q, rhs, nseg - 1 - q, n, par, B, jc, jv, tid);
-      cpa_commit();
-    }
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
     for (int s = nseg - 1; s >= 0; --s) {
-      const int uu = nseg - 1 - s;
-      if (s - (kRing - 1) >= 0)
-        stage_segment<V, R>(stage, (uu + kRing - 1) % kRing, rhs, s - (kRing - 1), n, par, B, jc, jv, tid);
-      cpa_commit();
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>();
       if (s > 0) {
-        const double* ck = a.ckpt + ((int64_t)(s * 2 + par) * 10) * B + jc;
+        const double* ck = ckj + (int64_t)20 * s * B;
         w1.d = __ldg(ck); w1.e = __ldg(ck + B); w1.f = __ldg(ck + 2 * B); w1.a = __ldg(ck + 3 * B);
         w1.b = __ldg(ck + 4 * B);
         w2.d = __ldg(ck + 5 * B); w2.e = __ldg(ck + 6 * B); w2.f = __ldg(ck + 7 * B); w2.a = __ldg(ck + 8 * B);
         w2.b = __ldg(ck + 9 * B);
         w1.rd = rcp_fast(w1.d);
         w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
-        ya = ychk[(((int64_t)(s - 1) * 2 + par) * 2 + 0) * B + jc];
-        yb = ychk[(((int64_t)(s - 1) * 2 + par) * 2 + 1) * B + jc];
+        ya = ychkj[(int64_t)4 * (s - 1) * B];
+        yb = ychkj[(int64_t)4 * (s - 1) * B + B];
       }
-      cpa_wait<kRing - 1>();
-      const V* cur = stage + (size_t)(uu % kRing) * R * kStreamThreads;
+      const V* cur = consume();
+      const bool full = (s + 1) * R <= n;
       double rd_[R], e_[R], f_[R], a_[R], b_[R];
       V y_[R];
 #pragma unroll
@@ -309,10 +383,10 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         bih_step_fast(w, w1, w2, hb, c, xi0, l2, l4);
         w2 = w1;
         w1 = w;
-        const V y = sfma(-l4, yb, sfma(-l2, ya, cur[r * kStreamThreads + tid]));
+        const bool valid = full || i < n;
+        const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32 + lane] : szero<V>()));
         yb = ya;
         ya = y;
-        const bool valid = i < n;
         y_[r] = y;
         rd_[r] = valid ? w.rd : 0.0;
         e_[r] = valid ? w.e : 0.0;
@@ -324,8 +398,9 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
       for (int r = R - 1; r >= 0; --r) {
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
-        const double qn = i < n ? __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4) : 0.0;
-        const double sn = i < n ? __ldg(a.tab + (int64_t)k * B_NCOL + B_S4) : 0.0;
+        const bool valid = full || i < n;
+        const double qn = valid ? __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4) : 0.0;
+        const double sn = valid ? __ldg(a.tab + (int64_t)k * B_NCOL + B_S4) : 0.0;
         V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(f_[r], x2));
         acc = ssub(acc, smul(xi0, sadd(smul(a_[r], sq), smul(b_[r], sv))));
         const V x = smul(rd_[r], acc);
@@ -333,10 +408,9 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         sv = sfma(sn, x2, sv);
         x2 = x1;
         x1 = x;
-        if (jv && i < n) O::st_cs(rowp_out(out, par, i, B, j), x);
+        if (jv && valid) O::st_cs(outj + (int64_t)2 * i * B, x);
       }
     }
-    cpa_wait<0>();
   }
 }
 
@@ -359,7 +433,8 @@ template <typename V, int R>
 static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
   const int n0 = (a.n_dir + 1) / 2;
   const int tab_rows = ((n0 + R - 1) / R) * R;
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4) +
+                      2 * kRing * sizeof(uint64_t);
   cudaError_t err = cudaFuncSetAttribute(helm_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(helm_stream_kernel<V, R>, smem))
@@ -372,7 +447,7 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
 
 template <typename V, int R>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + 2 * kRing * sizeof(uint64_t);
   cudaError_t err = cudaFuncSetAttribute(bih_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(bih_stream_kernel<V, R>, smem))
@@ -407,12 +482,15 @@ static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, void* sc, int w, c
 cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm,
                                cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
+  // the bulk-copy ring moves 16-B aligned row pieces: real RHS needs an even batch
+  if (!cplx_rhs && ((a.batch & 1) || (reinterpret_cast<uintptr_t>(a.rhs) & 15))) return cudaErrorInvalidValue;
   const int ctas = warps_per_sm / 2;
   return cplx_rhs ? helm_stream_dispatch<cplx>(a, scratch, ctas, st) : helm_stream_dispatch<double>(a, scratch, ctas, st);
 }
 
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm, cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
+  if (!cplx_rhs && ((a.batch & 1) || (reinterpret_cast<uintptr_t>(a.rhs) & 15))) return cudaErrorInvalidValue;
   const int ctas = warps_per_sm / 2;
   return cplx_rhs ? bih_stream_dispatch<cplx>(a, scratch, ctas, st) : bih_stream_dispatch<double>(a, scratch, ctas, st);
 }

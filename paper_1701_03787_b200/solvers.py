@@ -52,8 +52,14 @@ __all__ = [
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
 _METHODS = ("chunked", "stream", "stored")
-STREAM_ROWS_H = 16  # checkpoint spacing of the streaming solve (registers per segment)
-STREAM_ROWS_B = 8
+def _env_int(name, default):
+    import os
+
+    return int(os.environ.get(name, default))
+
+
+STREAM_ROWS_H = _env_int("SHEN_STREAM_ROWS_H", 16)  # checkpoint spacing of the streaming solve
+STREAM_ROWS_B = _env_int("SHEN_STREAM_ROWS_B", 8)
 
 
 def stream_warps() -> int:
@@ -61,6 +67,20 @@ def stream_warps() -> int:
     import os
 
     return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
+
+
+def _solve_real_via_complex(lu, rhs_dev, out_dev):
+    """Real RHS whose rows are not 16-B aligned (odd batch): the streaming
+    kernel moves 16-B row pieces, so solve the complex system with zero
+    imaginary part -- every coefficient is real, so the real part is the same
+    arithmetic as the real solve."""
+    import torch
+
+    z = torch.complex(rhs_dev, torch.zeros_like(rhs_dev)).contiguous()
+    xz = torch.empty_like(z)
+    lu.solve_into(z, xz, True)
+    out_dev.copy_(xz.real)
+    return out_dev
 
 
 def _scratch(lu, op, n_modes, batch, is_complex, device):
@@ -231,6 +251,8 @@ class HelmholtzLU:
         nd, B = self.n_modes, self.batch
         if B == 0:
             return out_dev
+        if self.method == "stream" and not is_complex and (B % 2 or rhs_dev.data_ptr() % 16):
+            return _solve_real_via_complex(self, rhs_dev, out_dev)
         h = lib()
         sh = dv.stream_handle()
         if self.method == "stored":
@@ -430,14 +452,16 @@ class BiharmonicLU:
         return _finish(out, tuple(rhs.shape), from_np)
 
     def solve_into(self, rhs_dev, out_dev, is_complex):
-        import torch
-
         nb, B = self.n_modes, self.batch
         if B == 0:
             return out_dev
+        if self.method == "stream" and not is_complex and (B % 2 or rhs_dev.data_ptr() % 16):
+            return _solve_real_via_complex(self, rhs_dev, out_dev)
         h = lib()
         sh = dv.stream_handle()
         if self.method == "stored":
+            import torch
+
             if self._qs_dev is None:
                 self._qs_dev = (torch.from_numpy(np.ascontiguousarray(self.q)).to(out_dev.device),
                                 torch.from_numpy(np.ascontiguousarray(self.s)).to(out_dev.device))
