@@ -74,7 +74,7 @@ __device__ __forceinline__ V* rowp_out(V* base, int par, int i, int64_t B, int64
   return base + (int64_t)(par + 2 * i) * B + j;
 }
 
-constexpr int kRing = 4;  // stage buffers; prefetch distance kRing - 1 segments
+constexpr int kRing = 3;  // stage buffers; prefetch distance kRing - 1 segments
 
 // cp.async the rows of segment s (parity rows s*R ...) of `src` into stage buffer b
 template <typename V, int R>
@@ -88,40 +88,12 @@ __device__ __forceinline__ void stage_segment(V* stage, int b, const V* src, int
   }
 }
 
-// ---------------------------------------------------------------- bulk-copy ring
-// Each warp streams its segments (R rows x 32 systems = R contiguous row
-// pieces of 32*sizeof(V) bytes) through a kRing-deep shared-memory ring with
-// cp.async.bulk (the TMA engine; one elected lane issues, an mbarrier per
-// stage counts the bytes).  The sequence of segments a warp consumes is
-// continuous across the forward sweep (segments 0..nseg-1), the backward
-// sweep (nseg-1..0) and consecutive system groups, so the next group's first
-// rows are already in flight while the current group finishes.
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
-               : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// segment q of a warp's continuous stream -> (group index, segment s)
+// ---------------------------------------------------------------- per-thread segment stream
+// Each thread streams its own column through a kRing-deep shared-memory ring
+// with cp.async (16 B per row and thread; a warp covers whole 512-B row
+// pieces).  The sequence of segments a thread consumes is continuous across
+// the forward sweep (segments 0..nseg-1), the backward sweep (nseg-1..0) and
+// consecutive system groups, so the prefetch distance never drains.
 struct SegRef {
   int64_t g;
   int s;
@@ -133,74 +105,63 @@ __device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_
   return {g0 + gi * gstride, k < nseg ? k : 2 * nseg - 1 - k};
 }
 
-// lane 0 issues the R row pieces of segment `ref` into ring stage `st`
 template <typename V, int R>
-__device__ __forceinline__ void ring_issue(V* ring, uint64_t* bars, int st, const V* rhs, SegRef ref, int n, int par,
-                                           int64_t B, int64_t ngroups) {
-  if (ref.g >= ngroups) return;
-  const int64_t j0 = ref.g * 32;
-  const int nsys = (int)(B - j0 < 32 ? B - j0 : 32);
-  const unsigned piece = (unsigned)(nsys * sizeof(V));
-  int rows = min(R, n - ref.s * R);
-  fence_async_smem();
-  mbar_expect(bars + st, piece * (unsigned)rows);
-  V* dst = ring + (size_t)st * R * 32;
-  for (int r = 0; r < rows; ++r)
-    bulk_g2s(dst + r * 32, rhs + (int64_t)(par + 2 * (ref.s * R + r)) * B + j0, piece, bars + st);
+__device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int n, int par, int64_t B,
+                                          int64_t ngroups, int lane) {
+  if (ref.g < ngroups) {
+    const int64_t j = ref.g * 32 + lane;
+    const bool jv = j < B;
+    const int64_t jc = jv ? j : B - 1;
+    const V* src = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
+    const int64_t step = 2 * B;
+    const int rows = min(R, n - ref.s * R);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool ok = jv && r < rows;
+      cpa(slot + r * 32, ok ? src + r * step : src, ok);
+    }
+  }
+  cpa_commit();
 }
 
 // ======================================================================= Helmholtz
-// v4: recompute-y streaming solve (see file header), TMA bulk ring, per-warp
-// persistent stream of segments.  CTA = 2 warps (parity 0 / parity 1 of the
-// same 32 systems) sharing the row table; HBM traffic per unknown: 2 RHS
+// v5: recompute-y streaming solve, per-thread cp.async ring, row constants
+// read through the L1 (warp-uniform broadcast loads).  CTA = 2 warps
+// (parity 0 / 1 of the same 32 systems).  HBM traffic per unknown: 2 RHS
 // reads + 1 solution write (+ ~3 B of checkpoints).
 template <typename V, int R>
-__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
+__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int /*unused*/) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, par = tid >> 5;
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
+  const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32;                   // [2 warps][kRing][R][32]
-  double4* tab = reinterpret_cast<double4*>(reinterpret_cast<V*>(smem) + (size_t)2 * kRing * R * 32);  // [2][tab_rows]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 2 * tab_rows) + par * kRing;          // [2][kRing]
-  for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
-    const int p = idx / tab_rows, i = idx - p * tab_rows;
-    const int np = (a.n_dir - p + 1) / 2;
-    const int nsp = (a.n_dir - 2 - p + 1) / 2 > 0 ? (a.n_dir - 2 - p + 1) / 2 : 0;
-    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (i < np) {
-      const int k = p + 2 * i;
-      v = make_double4(__ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsp ? 1.0 : 0.0);
-    }
-    tab[idx] = v;
-  }
-  if (lane == 0)
-    for (int q = 0; q < kRing; ++q) mbar_init(bars + q, 1);
-  fence_async_smem();
-  __syncthreads();
-  const double4* mytab = tab + par * tab_rows;
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32 + lane;  // this thread's column
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
+  const double* sdp = a.sd + par;  // row i -> [2 i]
+  const double* stp = a.st + par;
+  const double* mdp = a.md + par;
   const int64_t ngroups = (B + 31) / 32;
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
-  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;  // segments this warp consumes
-  int64_t qi = 0;                                                            // next segment to issue
-  if (lane == 0)
-    for (; qi < kRing - 1 && qi < nq; ++qi) ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
-  int64_t qc = 0;  // next segment to consume
+  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
+  int64_t qi = 0;
+  for (; qi < kRing - 1; ++qi) {
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    else cpa_commit();
+  }
+  int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    __syncwarp();
-    if (lane == 0 && qi < nq) {
-      ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
-    }
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    else cpa_commit();
     ++qi;
-    const int st = (int)(qc % kRing);
-    mbar_wait(bars + st, (unsigned)((qc / kRing) & 1));
+    cpa_wait<kRing - 1>();
+    const V* p = ring + (qc % kRing) * R * 32;
     ++qc;
-    return ring + (size_t)st * R * 32;
+    return p;
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
@@ -209,9 +170,9 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
     const int64_t jc = jv ? j : B - 1;
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
-    V* outj = out + (int64_t)par * B + j;      // row i at outj + 2*i*B
-    V* ychkj = ychk + (int64_t)par * B + jc;   // segment s at ychkj + 2*s*B
-    const double* ckj = a.ckpt + (int64_t)par * 3 * B + jc;  // segment s at ckj + 6*s*B
+    V* outj = out + (int64_t)par * B + j;
+    V* ychkj = ychk + (int64_t)par * B + jc;
+    const double* ckj = a.ckpt + (int64_t)par * 3 * B + jc;
     // ---------------- forward: y at segment ends only
     HelmProj pj;
     hp_origin(pj);
@@ -223,28 +184,42 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       const bool full = (s + 1) * R <= n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double4 tv = mytab[s * R + r];
-        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
+        const int i = s * R + r;
+        const int ic = min(i, n - 1);
+        const HelmRow row = helm_row(a.ca, cb, sub, __ldg(sdp + 2 * ic), __ldg(stp + 2 * ic), __ldg(mdp + 2 * ic),
+                                     i < nsup);
         if (r > 0 && (r & 7) == 0) hp_rescale(pj);
         double d, e, t;
         const double low = hp_step(pj, row, sub, d, e, t);
         dl = d; el = e; tl = t;
-        const V b = (full || s * R + r < n) ? cur[r * 32 + lane] : szero<V>();
+        const V b = (full || i < n) ? cur[r * 32] : szero<V>();
         y = sfma(-low, y, b);
       }
       if (jv && s + 1 < nseg) ychkj[(int64_t)2 * s * B] = y;
     }
     // ---------------- backward: re-stream each segment (bottom first)
     V x1 = szero<V>(), S = szero<V>();
+    // scalars of the next (lower) segment, loaded one segment ahead
+    double ckd = 1.0, cke = 0.0, ckt = 0.0;
+    V ckyv = szero<V>();
+    if (nseg - 1 > 0) {
+      const double* ck = ckj + (int64_t)6 * (nseg - 1) * B;
+      ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
+      ckyv = ychkj[(int64_t)2 * (nseg - 2) * B];
+    }
     for (int s = nseg - 1; s >= 0; --s) {
       HelmProj q;
       V yy = szero<V>();
       if (s == 0) {
         hp_origin(q);
       } else {
-        const double* ck = ckj + (int64_t)6 * s * B;
-        hp_start(q, __ldg(ck), __ldg(ck + B), __ldg(ck + 2 * B));
-        yy = ychkj[(int64_t)2 * (s - 1) * B];
+        hp_start(q, ckd, cke, ckt);
+        yy = ckyv;
+      }
+      if (s - 1 > 0) {
+        const double* ck = ckj + (int64_t)6 * (s - 1) * B;
+        ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
+        ckyv = ychkj[(int64_t)2 * (s - 2) * B];
       }
       const V* cur = consume();
       const bool full = (s + 1) * R <= n;
@@ -252,13 +227,15 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       V y_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double4 tv = mytab[s * R + r];
-        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
+        const int i = s * R + r;
+        const int ic = min(i, n - 1);
+        const HelmRow row = helm_row(a.ca, cb, sub, __ldg(sdp + 2 * ic), __ldg(stp + 2 * ic), __ldg(mdp + 2 * ic),
+                                     i < nsup);
         if (r > 0 && (r & 7) == 0) hp_rescale(q);
         double d, e, t;
         const double low = hp_step(q, row, sub, d, e, t);
-        const bool valid = full || s * R + r < n;
-        yy = sfma(-low, yy, valid ? cur[r * 32 + lane] : szero<V>());
+        const bool valid = full || i < n;
+        yy = sfma(-low, yy, valid ? cur[r * 32] : szero<V>());
         y_[r] = yy;
         rd_[r] = valid ? q.rd : 0.0;
         e_[r] = valid ? e : 0.0;
@@ -274,6 +251,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       }
     }
   }
+  cpa_wait<0>();
 }
 
 // ======================================================================= biharmonic
@@ -286,12 +264,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<V*>(smem) + (size_t)2 * kRing * R * 32) + par * kRing;
-  if (lane == 0)
-    for (int q = 0; q < kRing; ++q) mbar_init(bars + q, 1);
-  fence_async_smem();
-  __syncthreads();
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32 + lane;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
@@ -300,19 +273,19 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
-  if (lane == 0)
-    for (; qi < kRing - 1 && qi < nq; ++qi) ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
+  for (; qi < kRing - 1; ++qi) {
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    else cpa_commit();
+  }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    __syncwarp();
-    if (lane == 0 && qi < nq) {
-      ring_issue<V, R>(ring, bars, (int)(qi % kRing), rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups);
-    }
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    else cpa_commit();
     ++qi;
-    const int st = (int)(qc % kRing);
-    mbar_wait(bars + st, (unsigned)((qc / kRing) & 1));
+    cpa_wait<kRing - 1>();
+    const V* p = ring + (qc % kRing) * R * 32;
     ++qc;
-    return ring + (size_t)st * R * 32;
+    return p;
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
@@ -321,8 +294,8 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
     const int64_t jc = jv ? j : B - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
     V* outj = out + (int64_t)par * B + j;
-    V* ychkj = ychk + (int64_t)par * 2 * B + jc;               // segment s: ychkj + 4*s*B (+B for y_{-2})
-    const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;   // segment s: ckj + 20*s*B
+    V* ychkj = ychk + (int64_t)par * 2 * B + jc;
+    const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;
     // ---------------- forward
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
     V y1 = szero<V>(), y2 = szero<V>();
@@ -341,7 +314,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
         u2 = u1;
         u1 = u;
-        const V b = (full || i < n) ? cur[r * 32 + lane] : szero<V>();
+        const V b = (full || i < n) ? cur[r * 32] : szero<V>();
         const V y = sfma(-l4, y2, sfma(-l2, y1, b));
         y2 = y1;
         y1 = y;
@@ -353,19 +326,34 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
     }
     // ---------------- backward
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
+    double ck[10];
+    V cya = szero<V>(), cyb = szero<V>();
+#pragma unroll
+    for (int q = 0; q < 10; ++q) ck[q] = 0.0;
+    if (nseg - 1 > 0) {
+      const double* cp = ckj + (int64_t)20 * (nseg - 1) * B;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
+      cya = ychkj[(int64_t)4 * (nseg - 2) * B];
+      cyb = ychkj[(int64_t)4 * (nseg - 2) * B + B];
+    }
     for (int s = nseg - 1; s >= 0; --s) {
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>();
       if (s > 0) {
-        const double* ck = ckj + (int64_t)20 * s * B;
-        w1.d = __ldg(ck); w1.e = __ldg(ck + B); w1.f = __ldg(ck + 2 * B); w1.a = __ldg(ck + 3 * B);
-        w1.b = __ldg(ck + 4 * B);
-        w2.d = __ldg(ck + 5 * B); w2.e = __ldg(ck + 6 * B); w2.f = __ldg(ck + 7 * B); w2.a = __ldg(ck + 8 * B);
-        w2.b = __ldg(ck + 9 * B);
+        w1.d = ck[0]; w1.e = ck[1]; w1.f = ck[2]; w1.a = ck[3]; w1.b = ck[4];
+        w2.d = ck[5]; w2.e = ck[6]; w2.f = ck[7]; w2.a = ck[8]; w2.b = ck[9];
         w1.rd = rcp_fast(w1.d);
         w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
-        ya = ychkj[(int64_t)4 * (s - 1) * B];
-        yb = ychkj[(int64_t)4 * (s - 1) * B + B];
+        ya = cya;
+        yb = cyb;
+      }
+      if (s - 1 > 0) {
+        const double* cp = ckj + (int64_t)20 * (s - 1) * B;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
+        cya = ychkj[(int64_t)4 * (s - 2) * B];
+        cyb = ychkj[(int64_t)4 * (s - 2) * B + B];
       }
       const V* cur = consume();
       const bool full = (s + 1) * R <= n;
@@ -384,7 +372,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         w2 = w1;
         w1 = w;
         const bool valid = full || i < n;
-        const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32 + lane] : szero<V>()));
+        const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32] : szero<V>()));
         yb = ya;
         ya = y;
         y_[r] = y;
@@ -412,6 +400,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
       }
     }
   }
+  cpa_wait<0>();
 }
 
 // ======================================================================= launchers
@@ -431,10 +420,8 @@ static int resident_ctas(K kernel, size_t smem) {
 
 template <typename V, int R>
 static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  const int n0 = (a.n_dir + 1) / 2;
-  const int tab_rows = ((n0 + R - 1) / R) * R;
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4) +
-                      2 * kRing * sizeof(uint64_t);
+  const int tab_rows = 0;
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
   cudaError_t err = cudaFuncSetAttribute(helm_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(helm_stream_kernel<V, R>, smem))
@@ -447,7 +434,7 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
 
 template <typename V, int R>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V) + 2 * kRing * sizeof(uint64_t);
+  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
   cudaError_t err = cudaFuncSetAttribute(bih_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(bih_stream_kernel<V, R>, smem))
