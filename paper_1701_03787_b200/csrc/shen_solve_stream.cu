@@ -67,7 +67,8 @@ template <typename V> __device__ __forceinline__ V szero();
 template <> __device__ __forceinline__ double szero<double>() { return 0.0; }
 template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 
-constexpr int kStreamThreads = 64;  // 2 warps: parity 0, parity 1
+constexpr int kSG = 4;                    // 32-system groups per CTA (128 consecutive systems)
+constexpr int kStreamThreads = 64 * kSG;  // warp w: parity w & 1, system group w >> 1
 
 template <typename V>
 __device__ __forceinline__ V* rowp_out(V* base, int par, int i, int64_t B, int64_t j) {
@@ -75,18 +76,6 @@ __device__ __forceinline__ V* rowp_out(V* base, int par, int i, int64_t B, int64
 }
 
 constexpr int kRing = 3;  // stage buffers; prefetch distance kRing - 1 segments
-
-// cp.async the rows of segment s (parity rows s*R ...) of `src` into stage buffer b
-template <typename V, int R>
-__device__ __forceinline__ void stage_segment(V* stage, int b, const V* src, int s, int n, int par, int64_t B,
-                                              int64_t jc, bool jv, int tid) {
-  V* dst = stage + (size_t)b * R * kStreamThreads;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = s * R + r;
-    cpa(dst + r * kStreamThreads + tid, src + (int64_t)(par + 2 * min(i, n - 1)) * B + jc, jv && i < n);
-  }
-}
 
 // ---------------------------------------------------------------- per-thread segment stream
 // Each thread streams its own column through a kRing-deep shared-memory ring
@@ -107,9 +96,9 @@ __device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_
 
 template <typename V, int R>
 __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int n, int par, int64_t B,
-                                          int64_t ngroups, int lane) {
+                                          int64_t ngroups, int sgi, int lane) {
   if (ref.g < ngroups) {
-    const int64_t j = ref.g * 32 + lane;
+    const int64_t j = ref.g * (32 * kSG) + sgi * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const V* src = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
@@ -133,29 +122,29 @@ template <typename V, int R>
 __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int /*unused*/) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
-  const int tid = threadIdx.x, lane = tid & 31, par = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
   const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32 + lane;  // this thread's column
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * kRing * R * 32 + lane;  // this thread's column
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double* sdp = a.sd + par;  // row i -> [2 i]
   const double* stp = a.st + par;
   const double* mdp = a.md + par;
-  const int64_t ngroups = (B + 31) / 32;
+  const int64_t ngroups = (B + 32 * kSG - 1) / (32 * kSG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < kRing - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<kRing - 1>();
@@ -165,7 +154,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = g * 32 + lane;
+    const int64_t j = g * (32 * kSG) + sgi * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const double cb = __ldg(a.cb + jc);
@@ -259,27 +248,27 @@ template <typename V, int R>
 __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs a, V* ychk) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
-  const int tid = threadIdx.x, lane = tid & 31, par = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
   const int64_t B = a.batch;
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)par * kRing * R * 32 + lane;
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * kRing * R * 32 + lane;
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
-  const int64_t ngroups = (B + 31) / 32;
+  const int64_t ngroups = (B + 32 * kSG - 1) / (32 * kSG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < kRing - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<kRing - 1>();
@@ -289,7 +278,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = g * 32 + lane;
+    const int64_t j = g * (32 * kSG) + sgi * 32 + lane;
     const bool jv = j < B;
     const int64_t jc = jv ? j : B - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
@@ -426,7 +415,7 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(helm_stream_kernel<V, R>, smem))
                                   : resident_ctas(helm_stream_kernel<V, R>, smem);
-  const int64_t groups = (a.batch + 31) / 32;
+  const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   helm_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
@@ -439,7 +428,7 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
   if (err != cudaSuccess) return err;
   const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(bih_stream_kernel<V, R>, smem))
                                   : resident_ctas(bih_stream_kernel<V, R>, smem);
-  const int64_t groups = (a.batch + 31) / 32;
+  const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   bih_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
