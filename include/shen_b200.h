@@ -36,9 +36,9 @@ enum shen_status {
   SHEN_ERR_CUDA = 2,  /* CUDA runtime error (message via shen_last_error) */
 };
 
-/* number of biharmonic row constants per mode in the table passed to the
- * biharmonic entry points (see shen_rows.cuh: BihCol) */
-#define SHEN_BIH_NCOL 17
+/* row pitch (doubles) of the biharmonic row-constant table: 17 constants per
+ * mode (see shen_rows.cuh: BihCol) + 1 pad so rows are 16-B aligned */
+#define SHEN_BIH_NCOL 18
 
 const char* shen_version(void);
 const char* shen_last_error(void);
@@ -95,7 +95,7 @@ int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factor
  * replaces build_biharmonic (solvers.py:244-355) and BiharmonicLU.solve
  * (solvers.py:162-198).
  *   xi1[batch], xi2[batch] : biharmonic_coefficients (solvers.py:72-75).
- *   tab[n_bih][17]         : per-mode row constants
+ *   tab[n_bih][18]         : per-mode row constants (last column padding)
  *      {q0, -A0, B0, tail2, -A+2, B+2, tail4, B+4, -A-2(k-2), B+2(k-2),
  *       B+4(k-4), p, r, q(k+2), s(k+2), q(k+4), s(k+4)}
  *      with entries outside the band set to 0 (solvers.py:244-268).

@@ -9,7 +9,7 @@
 #include "shen_kernels.h"
 #include "shen_rows.cuh"
 
-static_assert(SHEN_BIH_NCOL == shen::B_NCOL, "table width mismatch");
+static_assert(SHEN_BIH_NCOL == shen::B_STRIDE, "table pitch mismatch");
 
 namespace {
 thread_local std::string g_err;

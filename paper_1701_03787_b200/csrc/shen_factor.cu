@@ -74,8 +74,7 @@ __global__ void __launch_bounds__(256) bih_factor_kernel(BihFactorArgs a) {
   double c[B_NCOL];
   for (int i = 0; i < n; ++i) {
     const int k = par + 2 * i;
-#pragma unroll
-    for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+    load_bih_row(a.tab, k, c);
     BihBands h = bih_bands(a.xi0, xi1, xi2, c);
     double l2, l4;
     if (EXACT)

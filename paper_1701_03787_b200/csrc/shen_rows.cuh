@@ -156,6 +156,18 @@ enum BihCol {
   B_Q2, B_S2, B_Q4, B_S4,          // q, s at k+2 and k+4 (0 past the end)
   B_NCOL
 };
+constexpr int B_STRIDE = 18;  // table row pitch in doubles (17 used + 1 pad: 16-B aligned rows)
+
+// the row constants of full mode k: 9 vector loads through the read-only path
+__device__ __forceinline__ void load_bih_row(const double* tab, int k, double* c) {
+  const double2* p = reinterpret_cast<const double2*>(tab + (int64_t)k * B_STRIDE);
+#pragma unroll
+  for (int q = 0; q < B_STRIDE / 2; ++q) {
+    const double2 v = __ldg(p + q);
+    c[2 * q] = v.x;
+    if (2 * q + 1 < B_NCOL) c[2 * q + 1] = v.y;
+  }
+}
 
 struct BihBands {
   double hd, hp2, hp4, hm2, hm4;

@@ -321,8 +321,7 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       const bool valid = r < nr;
       const int k = min(par + 2 * (s0 + r), a.n_bih - 1);
       double c[B_NCOL];
-#pragma unroll
-      for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+      load_bih_row(a.tab, k, c);
       const BihBands hb = bih_bands(xi0, xi1, xi2, c);
       double l2, l4;
       bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);

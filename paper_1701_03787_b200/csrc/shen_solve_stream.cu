@@ -296,8 +296,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-#pragma unroll
-        for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+        load_bih_row(a.tab, k, c);
         const BihBands hb = bih_bands(xi0, xi1, xi2, c);
         double l2, l4;
         bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
@@ -353,8 +352,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-#pragma unroll
-        for (int q = 0; q < B_NCOL; ++q) c[q] = __ldg(a.tab + (int64_t)k * B_NCOL + q);
+        load_bih_row(a.tab, k, c);
         const BihBands hb = bih_bands(xi0, xi1, xi2, c);
         double l2, l4;
         bih_step_fast(w, w1, w2, hb, c, xi0, l2, l4);
@@ -376,8 +374,8 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         const bool valid = full || i < n;
-        const double qn = valid ? __ldg(a.tab + (int64_t)k * B_NCOL + B_Q4) : 0.0;
-        const double sn = valid ? __ldg(a.tab + (int64_t)k * B_NCOL + B_S4) : 0.0;
+        const double qn = valid ? __ldg(a.tab + (int64_t)k * B_STRIDE + B_Q4) : 0.0;
+        const double sn = valid ? __ldg(a.tab + (int64_t)k * B_STRIDE + B_S4) : 0.0;
         V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(f_[r], x2));
         acc = ssub(acc, smul(xi0, sadd(smul(a_[r], sq), smul(b_[r], sv))));
         const V x = smul(rd_[r], acc);

@@ -329,7 +329,7 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "ch
 
 # ------------------------------------------------------------------ biharmonic
 
-BIH_NCOL = 17
+BIH_NCOL = 18  # 17 constants + 1 pad (16-B aligned rows on the device)
 
 
 def _bih_table(mats):
