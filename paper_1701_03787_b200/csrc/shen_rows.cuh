@@ -168,6 +168,16 @@ __device__ __forceinline__ void load_bih_row(const double* tab, int k, double* c
     if (2 * q + 1 < B_NCOL) c[2 * q + 1] = v.y;
   }
 }
+// same from a shared-memory copy of the table
+__device__ __forceinline__ void load_bih_row_smem(const double* tab, int k, double* c) {
+  const double2* p = reinterpret_cast<const double2*>(tab + (int64_t)k * B_STRIDE);
+#pragma unroll
+  for (int q = 0; q < B_STRIDE / 2; ++q) {
+    const double2 v = p[q];
+    c[2 * q] = v.x;
+    if (2 * q + 1 < B_NCOL) c[2 * q + 1] = v.y;
+  }
+}
 
 struct BihBands {
   double hd, hp2, hp4, hm2, hm4;

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
 }
 
 // ======================================================================= biharmonic
-template <typename V, int R>
+template <typename V, int R, bool SMEM_TAB, int RING>
 __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs a, V* ychk) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
@@ -253,7 +253,21 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * kRing * R * 32 + lane;
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * R * 32 + lane;
+  // row-constant table: a shared-memory copy when it fits (loaded once per
+  // persistent CTA), else the read-only path
+  double* stab = smem + (size_t)kStreamThreads / 32 * RING * R * 32 * VOps<V>::ndouble;
+  const double* tab = a.tab;
+  if (SMEM_TAB) {
+    const double2* src = reinterpret_cast<const double2*>(a.tab);
+    double2* dst = reinterpret_cast<double2*>(stab);
+    for (int q = tid; q < nb * B_STRIDE / 2; q += kStreamThreads) dst[q] = __ldg(src + q);
+    __syncthreads();
+    tab = stab;
+  }
+  auto row_consts = [&](int k, double* c) {
+    if (SMEM_TAB) load_bih_row_smem(tab, k, c); else load_bih_row(tab, k, c);
+  };
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
@@ -262,17 +276,17 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
-  for (; qi < kRing - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+  for (; qi < RING - 1; ++qi) {
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
     ++qi;
-    cpa_wait<kRing - 1>();
-    const V* p = ring + (qc % kRing) * R * 32;
+    cpa_wait<RING - 1>();
+    const V* p = ring + (qc % RING) * R * 32;
     ++qc;
     return p;
   };
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-        load_bih_row(a.tab, k, c);
+        row_consts(k, c);
         const BihBands hb = bih_bands(xi0, xi1, xi2, c);
         double l2, l4;
         bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-        load_bih_row(a.tab, k, c);
+        row_consts(k, c);
         const BihBands hb = bih_bands(xi0, xi1, xi2, c);
         double l2, l4;
         bih_step_fast(w, w1, w2, hb, c, xi0, l2, l4);
@@ -374,8 +388,8 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         const bool valid = full || i < n;
-        const double qn = valid ? __ldg(a.tab + (int64_t)k * B_STRIDE + B_Q4) : 0.0;
-        const double sn = valid ? __ldg(a.tab + (int64_t)k * B_STRIDE + B_S4) : 0.0;
+        const double qn = valid ? tab[(int64_t)k * B_STRIDE + B_Q4] : 0.0;
+        const double sn = valid ? tab[(int64_t)k * B_STRIDE + B_S4] : 0.0;
         V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(f_[r], x2));
         acc = ssub(acc, smul(xi0, sadd(smul(a_[r], sq), smul(b_[r], sv))));
         const V x = smul(rd_[r], acc);
@@ -419,17 +433,27 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   return cudaGetLastError();
 }
 
-template <typename V, int R>
-static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
-  cudaError_t err = cudaFuncSetAttribute(bih_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <typename V, int R, bool SMEM_TAB, int RING>
+static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int ctas_per_sm, size_t smem,
+                                     cudaStream_t st) {
+  auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(bih_stream_kernel<V, R>, smem))
-                                  : resident_ctas(bih_stream_kernel<V, R>, smem);
+  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem);
   const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
-  bih_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
+  kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
+}
+
+template <typename V, int R>
+static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
+  // the table in shared memory beats a deeper ring: the biharmonic rows are
+  // slow enough that one segment of prefetch covers HBM latency
+  const size_t ring2 = (size_t)2 * R * kStreamThreads * sizeof(V);
+  const size_t tabb = (size_t)a.n_bih * B_STRIDE * sizeof(double);
+  if (ring2 + tabb <= 220 * 1024) return bih_stream_launch<V, R, true, 2>(a, scratch, ctas_per_sm, ring2 + tabb, st);
+  return bih_stream_launch<V, R, false, kRing>(a, scratch, ctas_per_sm, (size_t)kRing * R * kStreamThreads * sizeof(V), st);
 }
 
 template <typename V>
