@@ -118,37 +118,49 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
 // read through the L1 (warp-uniform broadcast loads).  CTA = 2 warps
 // (parity 0 / 1 of the same 32 systems).  HBM traffic per unknown: 2 RHS
 // reads + 1 solution write (+ ~3 B of checkpoints).
-template <typename V, int R>
-__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int /*unused*/) {
+template <typename V, int R, int RING>
+__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
   const int64_t B = a.batch;
   const int n = (a.n_dir - par + 1) / 2;
-  const int nsup = (a.n_dir - 2 - par + 1) / 2 > 0 ? (a.n_dir - 2 - par + 1) / 2 : 0;
   const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * kRing * R * 32 + lane;  // this thread's column
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * R * 32 + lane;  // this thread's column
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
-  const double* sdp = a.sd + par;  // row i -> [2 i]
-  const double* stp = a.st + par;
-  const double* mdp = a.md + par;
+  // row constants (sd, st, md, has_sup) of both parities in shared memory,
+  // loaded once per persistent CTA
+  double4* tab = reinterpret_cast<double4*>(smem + (size_t)kStreamThreads / 32 * RING * R * 32 * VOps<V>::ndouble);
+  for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
+    const int p = idx / tab_rows, i = idx - p * tab_rows;
+    const int np = (a.n_dir - p + 1) / 2;
+    const int nsp = (a.n_dir - 2 - p + 1) / 2 > 0 ? (a.n_dir - 2 - p + 1) / 2 : 0;
+    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (i < np) {
+      const int k = p + 2 * i;
+      v = make_double4(__ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsp ? 1.0 : 0.0);
+    }
+    tab[idx] = v;
+  }
+  __syncthreads();
+  const double4* mytab = tab + par * tab_rows;
   const int64_t ngroups = (B + 32 * kSG - 1) / (32 * kSG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
-  for (; qi < kRing - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+  for (; qi < RING - 1; ++qi) {
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % kRing) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
     else cpa_commit();
     ++qi;
-    cpa_wait<kRing - 1>();
-    const V* p = ring + (qc % kRing) * R * 32;
+    cpa_wait<RING - 1>();
+    const V* p = ring + (qc % RING) * R * 32;
     ++qc;
     return p;
   };
@@ -174,9 +186,8 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int ic = min(i, n - 1);
-        const HelmRow row = helm_row(a.ca, cb, sub, __ldg(sdp + 2 * ic), __ldg(stp + 2 * ic), __ldg(mdp + 2 * ic),
-                                     i < nsup);
+        const double4 tv = mytab[i];
+        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
         if (r > 0 && (r & 7) == 0) hp_rescale(pj);
         double d, e, t;
         const double low = hp_step(pj, row, sub, d, e, t);
@@ -217,9 +228,8 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int ic = min(i, n - 1);
-        const HelmRow row = helm_row(a.ca, cb, sub, __ldg(sdp + 2 * ic), __ldg(stp + 2 * ic), __ldg(mdp + 2 * ic),
-                                     i < nsup);
+        const double4 tv = mytab[i];
+        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
         if (r > 0 && (r & 7) == 0) hp_rescale(q);
         double d, e, t;
         const double low = hp_step(q, row, sub, d, e, t);
@@ -421,15 +431,18 @@ static int resident_ctas(K kernel, size_t smem) {
 
 template <typename V, int R>
 static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  const int tab_rows = 0;
-  const size_t smem = (size_t)kRing * R * kStreamThreads * sizeof(V);
-  cudaError_t err = cudaFuncSetAttribute(helm_stream_kernel<V, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  constexpr int RING = 2;
+  const int n0 = (a.n_dir + 1) / 2;
+  const int tab_rows = ((n0 + R - 1) / R) * R;
+  const size_t smem = (size_t)RING * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = helm_stream_kernel<V, R, RING>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(helm_stream_kernel<V, R>, smem))
-                                  : resident_ctas(helm_stream_kernel<V, R>, smem);
+  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem);
   const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
-  helm_stream_kernel<V, R><<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
+  kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
 }
 
