@@ -48,10 +48,7 @@ int shen_device_count(void) {
 
 int64_t shen_stream_scratch_bytes(int op, int n_modes, int chunk_rows, int64_t batch, int is_complex) {
   if (chunk_rows <= 0 || n_modes < 2 || batch < 0) return -1;
-  const int64_t rows0 = (n_modes + 1) / 2;
-  const int64_t nseg = (rows0 + chunk_rows - 1) / chunk_rows;
-  const int64_t per = (op == 0 ? 1 : 2) * (is_complex ? 16 : 8);
-  return std::max<int64_t>(nseg - 1, 0) * 2 * per * batch;
+  return shen::stream_scratch_bytes(op, n_modes, chunk_rows, is_complex != 0);
 }
 
 int shen_pivot_reset(int* pivot_dev, void* stream) {

@@ -110,5 +110,6 @@ cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool compl
                                cudaStream_t st);
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
                               cudaStream_t st);
+int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
 
 }  // namespace shen

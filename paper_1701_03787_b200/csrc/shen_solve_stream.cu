@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
     V* outj = out + (int64_t)par * B + j;
-    V* ychkj = ychk + (int64_t)par * B + jc;
+    // y checkpoints: per-CTA scratch, [segment][thread] (only the group in flight)
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((a.n_dir + 1) / 2 + R - 1) / R) * kStreamThreads + tid;
     const double* ckj = a.ckpt + (int64_t)par * 3 * B + jc;
     // ---------------- forward: y at segment ends only
     HelmProj pj;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
         const V b = (full || i < n) ? cur[r * 32] : szero<V>();
         y = sfma(-low, y, b);
       }
-      if (jv && s + 1 < nseg) ychkj[(int64_t)2 * s * B] = y;
+      if (s + 1 < nseg) ychkj[s * kStreamThreads] = y;
     }
     // ---------------- backward: re-stream each segment (bottom first)
     V x1 = szero<V>(), S = szero<V>();
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
     if (nseg - 1 > 0) {
       const double* ck = ckj + (int64_t)6 * (nseg - 1) * B;
       ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-      ckyv = ychkj[(int64_t)2 * (nseg - 2) * B];
+      ckyv = ychkj[(nseg - 2) * kStreamThreads];
     }
     for (int s = nseg - 1; s >= 0; --s) {
       HelmProj q;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       if (s - 1 > 0) {
         const double* ck = ckj + (int64_t)6 * (s - 1) * B;
         ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-        ckyv = ychkj[(int64_t)2 * (s - 2) * B];
+        ckyv = ychkj[(s - 2) * kStreamThreads];
       }
       const V* cur = consume();
       const bool full = (s + 1) * R <= n;
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
     const int64_t jc = jv ? j : B - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
     V* outj = out + (int64_t)par * B + j;
-    V* ychkj = ychk + (int64_t)par * 2 * B + jc;
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 2 * kStreamThreads + tid;
     const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;
     // ---------------- forward
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
@@ -331,9 +332,9 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         y2 = y1;
         y1 = y;
       }
-      if (jv && s + 1 < nseg) {
-        ychkj[(int64_t)4 * s * B] = y1;
-        ychkj[(int64_t)4 * s * B + B] = y2;
+      if (s + 1 < nseg) {
+        ychkj[(2 * s) * kStreamThreads] = y1;
+        ychkj[(2 * s + 1) * kStreamThreads] = y2;
       }
     }
     // ---------------- backward
@@ -346,8 +347,8 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
       const double* cp = ckj + (int64_t)20 * (nseg - 1) * B;
 #pragma unroll
       for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
-      cya = ychkj[(int64_t)4 * (nseg - 2) * B];
-      cyb = ychkj[(int64_t)4 * (nseg - 2) * B + B];
+      cya = ychkj[(2 * (nseg - 2)) * kStreamThreads];
+      cyb = ychkj[(2 * (nseg - 2) + 1) * kStreamThreads];
     }
     for (int s = nseg - 1; s >= 0; --s) {
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const double* cp = ckj + (int64_t)20 * (s - 1) * B;
 #pragma unroll
         for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
-        cya = ychkj[(int64_t)4 * (s - 2) * B];
-        cyb = ychkj[(int64_t)4 * (s - 2) * B + B];
+        cya = ychkj[(2 * (s - 2)) * kStreamThreads];
+        cyb = ychkj[(2 * (s - 2) + 1) * kStreamThreads];
       }
       const V* cur = consume();
       const bool full = (s + 1) * R <= n;
@@ -439,7 +440,7 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   auto kern = helm_stream_kernel<V, R, RING>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem);
+  const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
   const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
@@ -452,7 +453,7 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
   auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  const int occ = ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem);
+  const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
   const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
@@ -487,6 +488,18 @@ static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, void* sc, int w, c
     case 16: return bih_stream_R<V, 16>(a, sc, w, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// per-CTA y-checkpoint scratch: grid is at most (#SMs x 8) CTAs
+int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool cplx_rhs) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 160;
+  }
+  const int64_t nseg0 = (((int64_t)n_modes + 1) / 2 + chunk_rows - 1) / chunk_rows;
+  return (int64_t)sms * 8 * nseg0 * (op == 0 ? 1 : 2) * kStreamThreads * (cplx_rhs ? 16 : 8);
 }
 
 // warps_per_sm of the C ABI: resident 2-warp CTAs per SM = warps_per_sm / 2 (0 = as many as fit)

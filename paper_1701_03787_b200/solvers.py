@@ -58,7 +58,7 @@ def _env_int(name, default):
     return int(os.environ.get(name, default))
 
 
-STREAM_ROWS_H = _env_int("SHEN_STREAM_ROWS_H", 16)  # checkpoint spacing of the streaming solve
+STREAM_ROWS_H = _env_int("SHEN_STREAM_ROWS_H", 8)  # checkpoint spacing of the streaming solve
 STREAM_ROWS_B = _env_int("SHEN_STREAM_ROWS_B", 8)
 
 
@@ -278,10 +278,12 @@ class HelmholtzLU:
         return out_dev
 
 
-def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "chunked") -> HelmholtzLU:
+def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "stream") -> HelmholtzLU:
     """Factor the Helmholtz operator for every z^2 (reference solvers.py:201-241).
 
-    ``method="chunked"`` (default): checkpoints for the fused chunked solve.
+    ``method="stream"`` (default): checkpoints every 8 rows for the streaming
+    fused solve (one thread per system, coalesced rows).
+    ``method="chunked"``: checkpoints for the warp-per-system chunked solve.
     ``method="stored"``: full reference-exact factors kept on the device.
     Raises ``ZeroPivotError`` exactly like the reference."""
     import torch
@@ -485,7 +487,7 @@ class BiharmonicLU:
         return out_dev
 
 
-def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "chunked") -> BiharmonicLU:
+def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "stream") -> BiharmonicLU:
     """Factor the biharmonic operator for every z^2 (reference solvers.py:271-355)."""
     import torch
 
