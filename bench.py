@@ -66,12 +66,6 @@ def dist_env():
     return rank, world, local
 
 
-def slab_rows(n_y, rank, world):
-    lo = (n_y * rank) // world
-    hi = (n_y * (rank + 1)) // world
-    return lo, hi
-
-
 def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -147,7 +141,9 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     name, n_x, n_y, n_z, nu, dt = workload(args.config)
     z2_full = channel_z2(n_y, n_z)
-    lo, hi = slab_rows(n_y, rank, world)
+    from paper_1701_03787_b200.shard import kx_slab
+
+    lo, hi = kx_slab(n_y, rank, world)
     if args.kx_rows:
         hi = min(hi, lo + args.kx_rows)
     z2 = np.ascontiguousarray(z2_full[lo:hi])

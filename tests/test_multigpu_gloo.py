@@ -1,0 +1,73 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): the kx-slab split used
+by bench.py / multi-GPU runs covers the plane exactly, per-rank solves of the
+slabs reassemble into the single-process result, and the timing reduction is
+a max over ranks.  The per-rank solver here is the CPU oracle (the product has
+no CPU path); on GPUs each rank runs the same slab through the B200 solver."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1701_03787_b200.shard import assemble_slabs, kx_slab, slab_of
+
+
+def test_kx_slab_partition():
+    for n_y in (1, 7, 64, 2048):
+        for world in (1, 2, 3, 8):
+            spans = [kx_slab(n_y, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n_y
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        kx_slab(8, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+
+    from oracle import shen_oracle as O
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import channel_z2
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mats = assemble(32, 0)
+    n_y, n_z = 12, 8
+    z2 = channel_z2(n_y, n_z)
+    rng = np.random.default_rng(0)
+    f = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
+    z2s = slab_of(z2, n_y, rank, world, axis=0)
+    fs = np.ascontiguousarray(slab_of(f, n_y, rank, world, axis=1))
+    xs = O.biharmonic_solve(O.biharmonic_factor(mats, 1e-3, 1e-3, z2s), fs)
+    parts = [None] * world
+    dist.all_gather_object(parts, xs)
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        full = O.biharmonic_solve(O.biharmonic_factor(mats, 1e-3, 1e-3, z2), f)
+        np.save(os.path.join(out_dir, "ok.npy"),
+                np.array([np.array_equal(assemble_slabs(parts, axis=1), full), t.item() == world]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_solve_gloo(tmp_path):
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    ok = np.load(tmp_path / "ok.npy")
+    assert ok.all(), ok
