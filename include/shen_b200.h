@@ -46,6 +46,10 @@ const char* shen_last_error(void);
 int shen_device_count(void);
 /* scratch bytes of shen_{helm,bih}_solve_stream (op 0 = Helmholtz, 1 = biharmonic) */
 int64_t shen_stream_scratch_bytes(int op, int n_modes, int chunk_rows, int64_t batch, int is_complex);
+/* cudaMemcpy2DAsync (kind 0 = H2D, 1 = D2H, 2 = D2D): column slabs of
+ * (n_modes, batch) arrays for pipelined host<->device solves */
+int shen_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                        int64_t height, int kind, void* stream);
 /* set pivot[0] = pivot[1] = INT32_MAX on the device (stream-ordered) */
 int shen_pivot_reset(int* pivot_dev, void* stream);
 
@@ -73,7 +77,10 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  *   {4, 8, 16}); one thread per system with coalesced row access; y is
  *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
  *   bytes) and recomputed in the backward sweep; warps_per_sm caps the
- *   resident warps per SM (0 = as many as fit).
+ *   resident warps per SM (0 = as many as fit).  [j_begin, j_end) restricts
+ *   the solve to a range of systems (j_end < 0: the whole batch) -- the row
+ *   pitch stays `batch`, so host<->device copies of column slabs can be
+ *   pipelined against the solve (see shen_memcpy2d_async).
  * shen_helm_solve_stored: solve with full stored factors (reference order).
  * rhs and out may alias only for the stored variant.
  * ------------------------------------------------------------------- */
@@ -86,7 +93,7 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
-                           void* stream);
+                           int64_t j_begin, int64_t j_end, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 
@@ -112,7 +119,8 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
                            int is_complex, void* stream);
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          void* scratch, int is_complex, int warps_per_sm, void* stream);
+                          void* scratch, int is_complex, int warps_per_sm, int64_t j_begin, int64_t j_end,
+                          void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

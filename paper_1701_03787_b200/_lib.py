@@ -32,20 +32,23 @@ _SIGS = {
     "shen_last_error": (ctypes.c_char_p, []),
     "shen_device_count": (ctypes.c_int, []),
     "shen_pivot_reset": (ctypes.c_int, [_vp, _vp]),
+    "shen_memcpy2d_async": (ctypes.c_int, [_vp, _c_int64, _vp, _c_int64, _c_int64, _c_int64, ctypes.c_int, _vp]),
     "shen_stream_scratch_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int]),
     "shen_helm_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                         ctypes.c_int, _vp, _pp, ctypes.c_int, _vp, _vp]),
     "shen_helm_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                                ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_helm_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                              ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp]),
+                                              ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
+                                              _c_int64, _c_int64, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp, ctypes.c_int,
                                        _vp, _pp, ctypes.c_int, _vp, _vp]),
     "shen_bih_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
                                               ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
-                                             ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _vp]),
+                                             ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
+                                             _c_int64, _c_int64, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
 }

@@ -51,6 +51,17 @@ int64_t shen_stream_scratch_bytes(int op, int n_modes, int chunk_rows, int64_t b
   return shen::stream_scratch_bytes(op, n_modes, chunk_rows, is_complex != 0);
 }
 
+int shen_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                        int64_t height, int kind, void* stream) {
+  if (height == 0 || width_bytes == 0) return SHEN_OK;
+  if (!dst || !src || width_bytes < 0 || height < 0 || kind < 0 || kind > 2)
+    return fail(SHEN_ERR_ARG, "shen_memcpy2d_async: bad args");
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  return cuda_check(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes, (size_t)height, k,
+                                      S(stream)),
+                    "shen_memcpy2d_async");
+}
+
 int shen_pivot_reset(int* pivot_dev, void* stream) {
   if (!pivot_dev) return fail(SHEN_ERR_ARG, "pivot_dev is NULL");
   fill_int_kernel<<<1, 32, 0, S(stream)>>>(pivot_dev, 2, INT_MAX);
@@ -92,7 +103,8 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
-                           void* out, void* scratch, int is_complex, int warps_per_sm, void* stream) {
+                           void* out, void* scratch, int is_complex, int warps_per_sm, int64_t j_begin,
+                           int64_t j_end, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: bad args");
@@ -101,7 +113,9 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: rhs must not alias out");
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: scratch required");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
+  if (j_end < 0) j_end = batch;
+  if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: range");
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end};
   return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
                     "shen_helm_solve_stream");
 }
@@ -155,7 +169,8 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
 
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          void* scratch, int is_complex, int warps_per_sm, void* stream) {
+                          void* scratch, int is_complex, int warps_per_sm, int64_t j_begin, int64_t j_end,
+                          void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: bad args");
@@ -164,7 +179,9 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: rhs must not alias out");
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: scratch required");
-  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
+  if (j_end < 0) j_end = batch;
+  if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: range");
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, j_begin, j_end};
   return cuda_check(shen::launch_bih_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
                     "shen_bih_solve_stream");
 }

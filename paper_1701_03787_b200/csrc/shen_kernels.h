@@ -84,6 +84,7 @@ struct HelmChunkArgs {
   const double* ckpt;
   const void* rhs;
   void* out;
+  int64_t jb = 0, je = -1;  // system range [jb, je) of the streaming solve (je < 0: whole batch)
 };
 
 struct BihChunkArgs {
@@ -97,6 +98,7 @@ struct BihChunkArgs {
   const double* ckpt;
   const void* rhs;
   void* out;
+  int64_t jb = 0, je = -1;
 };
 
 cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);

@@ -96,11 +96,11 @@ __device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_
 
 template <typename V, int R>
 __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int n, int par, int64_t B,
-                                          int64_t ngroups, int sgi, int lane) {
+                                          int64_t ngroups, int64_t jb, int64_t je, int sgi, int lane) {
   if (ref.g < ngroups) {
-    const int64_t j = ref.g * (32 * kSG) + sgi * 32 + lane;
-    const bool jv = j < B;
-    const int64_t jc = jv ? j : B - 1;
+    const int64_t j = jb + ref.g * (32 * kSG) + sgi * 32 + lane;
+    const bool jv = j < je;
+    const int64_t jc = jv ? j : je - 1;
     const V* src = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
     const int64_t step = 2 * B;
     const int rows = min(R, n - ref.s * R);
@@ -145,18 +145,19 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   }
   __syncthreads();
   const double4* mytab = tab + par * tab_rows;
-  const int64_t ngroups = (B + 32 * kSG - 1) / (32 * kSG);
+  const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;
+  const int64_t ngroups = (je - jb + 32 * kSG - 1) / (32 * kSG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<RING - 1>();
@@ -166,9 +167,9 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = g * (32 * kSG) + sgi * 32 + lane;
-    const bool jv = j < B;
-    const int64_t jc = jv ? j : B - 1;
+    const int64_t j = jb + g * (32 * kSG) + sgi * 32 + lane;
+    const bool jv = j < je;
+    const int64_t jc = jv ? j : je - 1;
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
     V* outj = out + (int64_t)par * B + j;
@@ -282,18 +283,19 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
-  const int64_t ngroups = (B + 32 * kSG - 1) / (32 * kSG);
+  const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;
+  const int64_t ngroups = (je - jb + 32 * kSG - 1) / (32 * kSG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, sgi, lane);
+    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<RING - 1>();
@@ -303,9 +305,9 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = g * (32 * kSG) + sgi * 32 + lane;
-    const bool jv = j < B;
-    const int64_t jc = jv ? j : B - 1;
+    const int64_t j = jb + g * (32 * kSG) + sgi * 32 + lane;
+    const bool jv = j < je;
+    const int64_t jc = jv ? j : je - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
     V* outj = out + (int64_t)par * B + j;
     V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 2 * kStreamThreads + tid;
@@ -441,7 +443,9 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
-  const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
+  const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
+  if (nsys <= 0) return cudaSuccess;
+  const int64_t groups = (nsys + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
@@ -454,7 +458,9 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
-  const int64_t groups = (a.batch + 32 * kSG - 1) / (32 * kSG);
+  const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
+  if (nsys <= 0) return cudaSuccess;
+  const int64_t groups = (nsys + 32 * kSG - 1) / (32 * kSG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
   kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();

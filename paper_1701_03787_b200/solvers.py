@@ -69,6 +69,82 @@ def stream_warps() -> int:
     return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
 
 
+# ------------------------------------------------------------------ host <-> device
+
+def _solve_api(lu, rhs, out):
+    import torch
+
+    _check_rhs_shape(rhs, lu.n_modes, lu.z2_shape)
+    if dv.is_torch(rhs) and rhs.is_cuda:
+        r, cplx, _ = dv.as_rhs(rhs)
+        flat = r.reshape(lu.n_modes, -1)
+        res = torch.empty_like(flat) if out is None else out.reshape(lu.n_modes, -1)
+        lu.solve_into(flat, res, cplx)
+        return res.reshape(tuple(rhs.shape))
+    a = rhs.numpy() if dv.is_torch(rhs) else np.asarray(rhs)
+    cplx = np.iscomplexobj(a)
+    a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+    if out is None:
+        out = np.empty(a.shape, dtype=a.dtype)
+    elif out.shape != a.shape or out.dtype != a.dtype or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous {a.dtype} array of shape {a.shape}")
+    if lu.batch == 0:
+        return out
+    _host_pipeline(lu, a.reshape(lu.n_modes, -1), out.reshape(lu.n_modes, -1), cplx)
+    return out
+
+
+_PIPE_MIN_SLAB = 4096
+
+
+def _host_pipeline(lu, h_rhs, h_out, cplx):
+    """Column-slab pipeline: H2D copy of slab k+1 and D2H copy of slab k-1 run
+    on their own streams while slab k is solved (stream method; the other
+    methods solve the whole batch after one copy).  Page-locked host arrays
+    make the copies asynchronous; pageable ones still work (staged)."""
+    import torch
+
+    n, B = h_rhs.shape
+    es = h_rhs.itemsize
+    dev = dv.device()
+    dtype = torch.complex128 if cplx else torch.float64
+    cache = getattr(lu, "_pipe", None)
+    if cache is None or cache[0].shape != (n, B) or cache[0].dtype != dtype:
+        cache = (torch.empty((n, B), dtype=dtype, device=dev), torch.empty((n, B), dtype=dtype, device=dev),
+                 torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        lu._pipe = cache
+    d_rhs, d_out, s_in, s_out = cache
+    h = lib()
+    comp = torch.cuda.current_stream(dev)
+    if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
+        bounds = [(0, B)]
+    else:
+        nslab = min(8, B // _PIPE_MIN_SLAB)
+        step = -(-B // nslab)
+        step = -(-step // 128) * 128
+        bounds = [(a, min(a + step, B)) for a in range(0, B, step)]
+    pitch = B * es
+    s_in.wait_stream(comp)
+    for a, b in bounds:
+        ev_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            check(h.shen_memcpy2d_async(d_rhs.data_ptr() + a * es, pitch, h_rhs.ctypes.data + a * es, pitch,
+                                        (b - a) * es, n, 0, s_in.cuda_stream), "H2D slab")
+            ev_in.record(s_in)
+        comp.wait_event(ev_in)
+        if len(bounds) == 1:
+            lu.solve_into(d_rhs, d_out, cplx)
+        else:
+            lu.solve_into(d_rhs, d_out, cplx, a, b)
+        ev_c = torch.cuda.Event()
+        ev_c.record(comp)
+        s_out.wait_event(ev_c)
+        with torch.cuda.stream(s_out):
+            check(h.shen_memcpy2d_async(h_out.ctypes.data + a * es, pitch, d_out.data_ptr() + a * es, pitch,
+                                        (b - a) * es, n, 1, s_out.cuda_stream), "D2H slab")
+    s_out.synchronize()
+
+
 def _solve_real_via_complex(lu, rhs_dev, out_dev):
     """Real RHS whose rows are not 16-B aligned (odd batch): the streaming
     kernel moves 16-B row pieces, so solve the complex system with zero
@@ -234,20 +310,16 @@ class HelmholtzLU:
         n = sum(int(t.numel()) for t in (self._stored or []))
         return 8 * (n + (int(self._ckpt.numel()) if self._ckpt is not None else 0) + self.batch)
 
-    def solve(self, rhs):
+    def solve(self, rhs, out=None):
         """Solve H x = rhs; rhs shape (n_modes, *z2_shape); numpy in -> numpy
-        out, torch CUDA in -> torch out (reference solvers.py:100-109)."""
-        import torch
+        out, torch CUDA in -> torch out (reference solvers.py:100-109).
+        ``out`` (optional, numpy) receives the result; with page-locked host
+        buffers the copies overlap the solve slab by slab."""
+        return _solve_api(self, rhs, out)
 
-        _check_rhs_shape(rhs, self.n_modes, self.z2_shape)
-        r, cplx, from_np = dv.as_rhs(rhs)
-        flat = r.reshape(self.n_modes, -1)
-        out = torch.empty_like(flat)
-        self.solve_into(flat, out, cplx)
-        return _finish(out, tuple(rhs.shape), from_np)
-
-    def solve_into(self, rhs_dev, out_dev, is_complex):
-        """Device-to-device solve on (n_modes, batch) contiguous tensors."""
+    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1):
+        """Device-to-device solve on (n_modes, batch) contiguous tensors
+        (systems [j0, j1) only with the stream method)."""
         nd, B = self.n_modes, self.batch
         if B == 0:
             return out_dev
@@ -266,7 +338,7 @@ class HelmholtzLU:
             scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
             check(h.shen_helm_solve_stream(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
                                            md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), sh),
+                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), j0, j1, sh),
                   "shen_helm_solve_stream")
         else:
             sd, st, md = self._tab
@@ -442,18 +514,11 @@ class BiharmonicLU:
     a = property(lambda self: self._host_factors()["a"])
     b = property(lambda self: self._host_factors()["b"])
 
-    def solve(self, rhs):
-        """Solve H x = rhs (reference solvers.py:162-170)."""
-        import torch
+    def solve(self, rhs, out=None):
+        """Solve H x = rhs (reference solvers.py:162-170); see HelmholtzLU.solve."""
+        return _solve_api(self, rhs, out)
 
-        _check_rhs_shape(rhs, self.n_modes, self.z2_shape)
-        r, cplx, from_np = dv.as_rhs(rhs)
-        flat = r.reshape(self.n_modes, -1)
-        out = torch.empty_like(flat)
-        self.solve_into(flat, out, cplx)
-        return _finish(out, tuple(rhs.shape), from_np)
-
-    def solve_into(self, rhs_dev, out_dev, is_complex):
+    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1):
         nb, B = self.n_modes, self.batch
         if B == 0:
             return out_dev
@@ -477,7 +542,7 @@ class BiharmonicLU:
             scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
             check(h.shen_bih_solve_stream(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
                                           self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                          out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), sh),
+                                          out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), j0, j1, sh),
                   "shen_bih_solve_stream")
         else:
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
