@@ -125,6 +125,42 @@ int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);
 
+/* ---------------------------------------------------------------------
+ * Wall-normal transform stages (reference transforms.py:81-205).
+ * Arrays are (rows, L) complex128 with the L Fourier lines contiguous.
+ * The DCT itself is an FFT of an extended sequence along the rows, done by
+ * the caller's FFT library (cuFFT) between the stages below:
+ *   forward  : shen_xform_extend -> FFT (forward, along rows) -> shen_xform_fwd_post
+ *              -> shen_xform_mass_solve (transforms.py:178-196)
+ *   inverse  : shen_xform_inv_pre -> FFT (Gauss: unnormalised inverse, GL:
+ *              forward) -> shen_xform_inv_post (transforms.py:199-205)
+ * family: 0 = Gauss (DCT-II/III via 2N-point FFT), 1 = Gauss-Lobatto (DCT-I
+ * via 2(N-1)-point FFT); N = n_x + 1 points; space 0/1/2 = Chebyshev /
+ * Dirichlet / biharmonic.
+ * ------------------------------------------------------------------- */
+/* x[N][L] -> e[M][L], M = 2N (Gauss, symmetric) or 2N-2 (GL, even). */
+int shen_xform_extend(int family, int N, int64_t L, const void* x, void* e, void* stream);
+/* Y[>=N][L] (FFT of the extension) -> out[n_modes][L]: Chebyshev scalar
+ * products scaled by `scale` (pi/(2N) Gauss, pi/(2(N-1)) GL), twiddled by
+ * tw[N] (exp(-i pi k / 2N), Gauss only), then the `space` stencil
+ * (transforms.py:93-110); space 3 = the raw scalar products (chebyshev_scalar
+ * transforms.py:81-86). */
+int shen_xform_fwd_post(int family, int space, int N, int64_t L, double scale, const void* tw, const void* Y,
+                        void* out, void* stream);
+/* coef[n][L] of `space` -> FFT input Z[M][L] and cends[2][L] = {c_0, c_{N-1}}
+ * of the Chebyshev expansion (shen_expand transforms.py:113-126).
+ * family 2 writes the expanded Chebyshev coefficients Z[N][L] themselves
+ * (shen_expand alone; cends may be NULL). */
+int shen_xform_inv_pre(int family, int space, int n, int N, int64_t L, const void* tw, const void* coef, void* Z,
+                       void* cends, void* stream);
+/* F[>=N][L] -> point values out[N][L] (chebyshev_evaluate transforms.py:129-137). */
+int shen_xform_inv_post(int family, int N, int64_t L, const void* F, const void* cends, void* out, void* stream);
+/* Per-parity banded Cholesky solve U^T U x = s (transforms.py:163-175):
+ * fac[2][nband+1][mmax] LAPACK upper band storage per parity (scipy
+ * cholesky_banded), n rows, s and x may alias. */
+int shen_xform_mass_solve(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,14 @@ _SIGS = {
                                              _c_int64, _c_int64, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
+    "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
+    "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,
+                                           _vp, _vp, _vp, _vp]),
+    "shen_xform_inv_pre": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, _vp,
+                                          _vp, _vp, _vp, _vp]),
+    "shen_xform_inv_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp, _vp]),
+    "shen_xform_mass_solve": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp,
+                                             _vp]),
 }
 
 _lock = threading.Lock()

@@ -201,4 +201,45 @@ int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q,
   return cuda_check(shen::launch_bih_seq(a, is_complex != 0, S(stream)), "shen_bih_solve_stored");
 }
 
+int shen_xform_extend(int family, int N, int64_t L, const void* x, void* e, void* stream) {
+  if (L == 0) return SHEN_OK;
+  if ((family != 0 && family != 1) || N < 2 || L < 0 || !x || !e) return fail(SHEN_ERR_ARG, "shen_xform_extend: bad args");
+  return cuda_check(shen::launch_xf_extend(family, N, L, x, e, S(stream)), "shen_xform_extend");
+}
+
+int shen_xform_fwd_post(int family, int space, int N, int64_t L, double scale, const void* tw, const void* Y,
+                        void* out, void* stream) {
+  if (L == 0) return SHEN_OK;
+  if ((family != 0 && family != 1) || space < 0 || space > 3 || N < (space == 2 ? 5 : space == 1 ? 3 : 2) || L < 0 ||
+      !Y || !out ||
+      (family == 0 && !tw))
+    return fail(SHEN_ERR_ARG, "shen_xform_fwd_post: bad args");
+  return cuda_check(shen::launch_xf_fwd_post(family, space, N, L, scale, tw, Y, out, S(stream)), "shen_xform_fwd_post");
+}
+
+int shen_xform_inv_pre(int family, int space, int n, int N, int64_t L, const void* tw, const void* coef, void* Z,
+                       void* cends, void* stream) {
+  if (L == 0) return SHEN_OK;
+  if (family < 0 || family > 2 || space < 0 || space > 2 || N < 2 || n < 1 ||
+      n + (space == 2 ? 4 : space == 1 ? 2 : 0) > N || L < 0 || !coef || !Z || (family != 2 && !cends) ||
+      (family == 0 && !tw))
+    return fail(SHEN_ERR_ARG, "shen_xform_inv_pre: bad args");
+  return cuda_check(shen::launch_xf_inv_pre(family, space, n, N, L, tw, coef, Z, cends, S(stream)), "shen_xform_inv_pre");
+}
+
+int shen_xform_inv_post(int family, int N, int64_t L, const void* F, const void* cends, void* out, void* stream) {
+  if (L == 0) return SHEN_OK;
+  if ((family != 0 && family != 1) || N < 2 || L < 0 || !F || !cends || !out)
+    return fail(SHEN_ERR_ARG, "shen_xform_inv_post: bad args");
+  return cuda_check(shen::launch_xf_inv_post(family, N, L, F, cends, out, S(stream)), "shen_xform_inv_post");
+}
+
+int shen_xform_mass_solve(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
+                          void* stream) {
+  if (L == 0) return SHEN_OK;
+  if ((nband != 1 && nband != 2) || n < 2 || mmax < (n + 1) / 2 || L < 0 || !fac || !s || !x)
+    return fail(SHEN_ERR_ARG, "shen_xform_mass_solve: bad args");
+  return cuda_check(shen::launch_xf_mass(nband, n, mmax, L, fac, s, x, S(stream)), "shen_xform_mass_solve");
+}
+
 }  // extern "C"

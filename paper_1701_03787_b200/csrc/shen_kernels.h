@@ -114,4 +114,14 @@ cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex
                               cudaStream_t st);
 int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
 
+// transforms (shen_transform.cu)
+cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
+cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,
+                               void* out, cudaStream_t st);
+cudaError_t launch_xf_inv_pre(int gl, int space, int n, int N, int64_t L, const void* tw, const void* coef, void* Z,
+                              void* cends, cudaStream_t st);
+cudaError_t launch_xf_inv_post(int gl, int N, int64_t L, const void* F, const void* cends, void* out, cudaStream_t st);
+cudaError_t launch_xf_mass(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
+                           cudaStream_t st);
+
 }  // namespace shen

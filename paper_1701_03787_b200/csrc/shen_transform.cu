@@ -1,0 +1,238 @@
+// Wall-normal (axis 0) pieces of the Shen transforms, reference
+// transforms.py:81-205.  Layout: arrays (rows, L) with the L = n_y*(n_z/2+1)
+// Fourier lines contiguous, complex128; one thread per line walks the rows,
+// so every row access of a warp is a coalesced 512-B piece.
+//
+// The DCTs along axis 0 go through an FFT of an extended sequence (cuFFT,
+// called from the host layer) with these kernels doing everything around it:
+//   Gauss  (DCT-II / DCT-III, N = n_x+1 points):
+//     forward : symmetric extension e = [x_0..x_{N-1}, x_{N-1}..x_0] (2N rows),
+//               Y = FFT_2N(e), DCT-II_k = w_k Y_k with w_k = exp(-i pi k / 2N);
+//     inverse : Z_k = c_k conj(w_k) (k < N), Z_{2N-k} = c_k w_k, Z_N = 0,
+//               sum_k c_k cos(pi k (2n+1)/2N) = (IFFT_2N^unnormalised(Z)_n + c_0) / 2.
+//   Gauss-Lobatto (DCT-I, N = n_x+1 points):
+//     even extension [x_0..x_{N-1}, x_{N-2}..x_1] (2 n_x rows), DCT-I = FFT.
+// Post-processing fuses the Chebyshev scaling and the Shen stencil
+// (transforms.py:81-110) and the inverse pre-processing fuses shen_expand
+// (transforms.py:113-126).  mass_solve is the per-parity banded Cholesky
+// solve (transforms.py:163-175) with the host's LAPACK factors.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "shen_common.cuh"
+
+namespace shen {
+
+struct c2 {
+  double x, y;
+};
+__device__ __forceinline__ c2 ld2(const double2* p) {
+  const double2 v = __ldg(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void st2(double2* p, c2 v) { *p = make_double2(v.x, v.y); }
+__device__ __forceinline__ c2 cmul(c2 a, c2 b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ c2 cadd(c2 a, c2 b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ c2 csub(c2 a, c2 b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ c2 cscale(double s, c2 a) { return {s * a.x, s * a.y}; }
+
+// ---------------------------------------------------------------- extensions
+// kind 0: Gauss forward symmetric extension (N -> 2N rows)
+// kind 1: Gauss-Lobatto even extension (N -> 2N-2 rows)
+__global__ void xf_extend_kernel(int kind, int N, int64_t L, const double2* __restrict__ x, double2* __restrict__ e) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const int M = kind == 0 ? 2 * N : 2 * N - 2;
+  for (int m = 0; m < M; ++m) {
+    int src;
+    if (m < N) src = m;
+    else src = kind == 0 ? 2 * N - 1 - m : 2 * N - 2 - m;
+    e[(int64_t)m * L + l] = __ldg(x + (int64_t)src * L + l);
+  }
+}
+
+// ---------------------------------------------------------------- forward post
+// Y: FFT of the extension (rows 0..N-1 used).  w_k = scale * (Gauss: tw_k Y_k,
+// GL: Y_k); then space 0: Chebyshev coefficients (2/pi, halved ends), 1:
+// Dirichlet w_k - w_{k+2}, 2: biharmonic w_k - c2_k w_{k+2} + c4_k w_{k+4},
+// 3: the raw scalar products w (chebyshev_scalar).
+// tw: [N] complex twiddles exp(-i pi k/2N) (host precomputed).
+__global__ void xf_fwd_post_kernel(int gl, int space, int N, int64_t L, double scale, const double2* __restrict__ tw,
+                                   const double2* __restrict__ Y, double2* __restrict__ out) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const int n_x = N - 1;
+  auto w_at = [&](int k) -> c2 {
+    c2 y = ld2(Y + (int64_t)k * L + l);
+    if (!gl) y = cmul(ld2(tw + k), y);
+    return cscale(scale, y);
+  };
+  if (space == 0 || space == 3) {
+    for (int k = 0; k < N; ++k) {
+      c2 v = w_at(k);
+      if (space == 3) {
+        st2(out + (int64_t)k * L + l, v);
+        continue;
+      }
+      v = cscale(2.0 / 3.141592653589793, v);
+      if (k == 0 || (gl && k == n_x)) v = cscale(0.5, v);
+      st2(out + (int64_t)k * L + l, v);
+    }
+    return;
+  }
+  if (space == 1) {
+    c2 wk = w_at(0), wk1 = w_at(1);
+    for (int k = 0; k < n_x - 1; ++k) {
+      const c2 wk2 = w_at(k + 2);
+      st2(out + (int64_t)k * L + l, csub(wk, wk2));
+      wk = wk1;
+      wk1 = wk2;
+    }
+    return;
+  }
+  c2 w0 = w_at(0), w1 = w_at(1), w2 = w_at(2), w3 = w_at(3);
+  for (int k = 0; k < n_x - 3; ++k) {
+    const c2 w4 = w_at(k + 4);
+    const double kk = (double)k;
+    const double c2k = 2 * (kk + 2) / (kk + 3), c4k = (kk + 1) / (kk + 3);
+    st2(out + (int64_t)k * L + l, cadd(csub(w0, cscale(c2k, w2)), cscale(c4k, w4)));
+    w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+  }
+}
+
+// ---------------------------------------------------------------- inverse pre
+// coefficients of `space` (n rows) -> Chebyshev coefficients c (N = n_x+1)
+// (shen_expand) -> FFT input: Gauss Z (2N rows, twiddled), GL even extension
+// (2N-2 rows), or (gl == 2) the expanded coefficients themselves (N rows).
+// Also writes c_0 and c_{n_x} per line into cends[2][L] (may be NULL).
+__global__ void xf_inv_pre_kernel(int gl, int space, int n, int N, int64_t L, const double2* __restrict__ tw,
+                                  const double2* __restrict__ coef, double2* __restrict__ Z, double2* __restrict__ cends) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  auto a_at = [&](int k) -> c2 {
+    if (k < 0 || k >= n) return {0.0, 0.0};
+    return ld2(coef + (int64_t)k * L + l);
+  };
+  const int M = gl ? 2 * N - 2 : 2 * N;
+  for (int k = 0; k < N; ++k) {
+    c2 c = a_at(k);
+    if (space == 1) {
+      c = csub(c, a_at(k - 2));
+    } else if (space == 2) {
+      const double j2 = (double)(k - 2), j4 = (double)(k - 4);
+      if (k >= 2 && k - 2 < n) c = csub(c, cscale(2 * (j2 + 2) / (j2 + 3), a_at(k - 2)));
+      if (k >= 4 && k - 4 < n) c = cadd(c, cscale((j4 + 1) / (j4 + 3), a_at(k - 4)));
+    }
+    if (cends && k == 0) st2(cends + l, c);
+    if (cends && k == N - 1) st2(cends + L + l, c);
+    if (gl == 2) {  // plain shen_expand output (N rows)
+      st2(Z + (int64_t)k * L + l, c);
+    } else if (gl) {
+      st2(Z + (int64_t)k * L + l, c);
+      if (k > 0 && k < N - 1) st2(Z + (int64_t)(M - k) * L + l, c);
+    } else {
+      const c2 w = ld2(tw + k);
+      st2(Z + (int64_t)k * L + l, cmul({w.x, -w.y}, c));
+      if (k > 0) st2(Z + (int64_t)(M - k) * L + l, cmul(w, c));
+    }
+  }
+  if (!gl) st2(Z + (int64_t)N * L + l, {0.0, 0.0});
+}
+
+// ---------------------------------------------------------------- inverse post
+// F: unnormalised inverse FFT (Gauss) / FFT (GL) of Z; lines out (N rows):
+//   Gauss: (F_n + c_0)/2 ; GL: F_n/2 + c_0/2 + (-1)^n c_{n_x}/2
+// (transforms.py:129-137)
+__global__ void xf_inv_post_kernel(int gl, int N, int64_t L, const double2* __restrict__ F,
+                                   const double2* __restrict__ cends, double2* __restrict__ out) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L) return;
+  const c2 c0 = ld2(cends + l), cN = ld2(cends + L + l);
+  for (int m = 0; m < N; ++m) {
+    c2 f = ld2(F + (int64_t)m * L + l);
+    c2 v;
+    if (!gl) {
+      v = cscale(0.5, cadd(f, c0));
+    } else {
+      v = cadd(cscale(0.5, f), cscale(0.5, c0));
+      v = (m & 1) ? csub(v, cscale(0.5, cN)) : cadd(v, cscale(0.5, cN));
+    }
+    st2(out + (int64_t)m * L + l, v);
+  }
+}
+
+// ---------------------------------------------------------------- mass solve
+// Per parity p, the banded SPD system U^T U x = s (upper Cholesky factor U of
+// bandwidth nb = 1 or 2, LAPACK band storage rows (nb+1) x m per parity):
+// forward U^T y = s, backward U x = y (zpbtrs).  fac layout: [2][nb+1][mmax].
+__global__ void xf_mass_kernel(int nband, int n, int mmax, int64_t L, const double* __restrict__ fac,
+                               const double2* __restrict__ s, double2* __restrict__ x) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * L) return;
+  const int par = (int)(t / L);
+  const int64_t l = t - (int64_t)par * L;
+  const int m = (n - par + 1) / 2;
+  const double* ab = fac + (int64_t)par * (nband + 1) * mmax;
+  auto U = [&](int i, int j) -> double {  // U[i][j], j - i in [0, nband]
+    return __ldg(ab + (int64_t)(nband - (j - i)) * mmax + j);
+  };
+  auto row = [&](int i) -> int64_t { return (int64_t)(par + 2 * i) * L + l; };
+  c2 y1 = {0, 0}, y2 = {0, 0};
+  for (int i = 0; i < m; ++i) {
+    c2 acc = ld2(s + row(i));
+    if (i >= 1) acc = csub(acc, cscale(U(i - 1, i), y1));
+    if (nband == 2 && i >= 2) acc = csub(acc, cscale(U(i - 2, i), y2));
+    const c2 y = cscale(1.0 / U(i, i), acc);
+    st2(x + row(i), y);
+    y2 = y1;
+    y1 = y;
+  }
+  c2 x1 = {0, 0}, x2 = {0, 0};
+  for (int i = m - 1; i >= 0; --i) {
+    c2 acc = {x[row(i)].x, x[row(i)].y};
+    if (i + 1 < m) acc = csub(acc, cscale(U(i, i + 1), x1));
+    if (nband == 2 && i + 2 < m) acc = csub(acc, cscale(U(i, i + 2), x2));
+    const c2 v = cscale(1.0 / U(i, i), acc);
+    st2(x + row(i), v);
+    x2 = x1;
+    x1 = v;
+  }
+}
+
+static unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  xf_extend_kernel<<<blocks_for(L), 256, 0, st>>>(kind, N, L, static_cast<const double2*>(x), static_cast<double2*>(e));
+  return cudaGetLastError();
+}
+cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,
+                               void* out, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  xf_fwd_post_kernel<<<blocks_for(L), 256, 0, st>>>(gl, space, N, L, scale, static_cast<const double2*>(tw),
+                                                    static_cast<const double2*>(Y), static_cast<double2*>(out));
+  return cudaGetLastError();
+}
+cudaError_t launch_xf_inv_pre(int gl, int space, int n, int N, int64_t L, const void* tw, const void* coef, void* Z,
+                              void* cends, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  xf_inv_pre_kernel<<<blocks_for(L), 256, 0, st>>>(gl, space, n, N, L, static_cast<const double2*>(tw),
+                                                   static_cast<const double2*>(coef), static_cast<double2*>(Z),
+                                                   static_cast<double2*>(cends));
+  return cudaGetLastError();
+}
+cudaError_t launch_xf_inv_post(int gl, int N, int64_t L, const void* F, const void* cends, void* out, cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  xf_inv_post_kernel<<<blocks_for(L), 256, 0, st>>>(gl, N, L, static_cast<const double2*>(F),
+                                                    static_cast<const double2*>(cends), static_cast<double2*>(out));
+  return cudaGetLastError();
+}
+cudaError_t launch_xf_mass(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
+                           cudaStream_t st) {
+  if (L <= 0) return cudaSuccess;
+  xf_mass_kernel<<<blocks_for(2 * L), 256, 0, st>>>(nband, n, mmax, L, fac, static_cast<const double2*>(s),
+                                                    static_cast<double2*>(x));
+  return cudaGetLastError();
+}
+
+}  // namespace shen
