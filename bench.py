@@ -1,7 +1,7 @@
 """Benchmark: batched fp64 Helmholtz + biharmonic solves (BASELINE config 4).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c4|c5:N|c1] [--kx-rows R]
+                    [--config c4|c5:N|c1|c3] [--kx-rows R]
 
 One step = HelmholtzLU.solve + BiharmonicLU.solve over this rank's kx slab of
 the 2048 x 1025 wavenumber plane (n_x = 1024, nu = 1/2000, dt = 1e-4),
@@ -356,6 +356,113 @@ def cpu_baseline(mats, nu, dt, z2_full):
             "sample": f"{rows} kx rows x 1025 systems of config 4, solve only (LU prebuilt), 1 thread"}
 
 
+# ======================================================================= config 3
+
+def run_c3(args):
+    """BASELINE config 3: real U(-1,1) field on the 257 x 256 x 256 mesh
+    (n_x = 256, Gauss points); one step = forward Dirichlet transform ->
+    Helmholtz solve per wavenumber -> inverse, then forward biharmonic
+    transform -> biharmonic solve -> inverse, all on device-resident data.
+    Single GPU (the transforms do not shard without a transpose)."""
+    import torch
+
+    from paper_1701_03787_b200 import solvers as S
+    from paper_1701_03787_b200 import transforms as T
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    nu, dt = 1e-3, 1e-3
+    mesh = build_mesh(256, 256, 256, 2 * np.pi, np.pi)
+    mats = assemble(256, 0)
+    z2 = wavenumber_grid(mesh, Space.DIRICHLET).z2()
+    hlu = S.build_helmholtz(mats, nu, dt, z2)
+    blu = S.build_biharmonic(mats, nu, dt, z2)
+    g = torch.Generator(device="cuda").manual_seed(33)
+    u = (torch.rand(mesh.shape, generator=g, device="cuda", dtype=torch.float64) * 2 - 1)
+    B = z2.size
+    xh = torch.empty((mats.n_dir, B), dtype=torch.complex128, device="cuda")
+    xb = torch.empty((mats.n_bih, B), dtype=torch.complex128, device="cuda")
+    out = {}
+
+    def step(ev=None):
+        rec = (lambda i: ev[i].record()) if ev else (lambda i: None)
+        rec(0)
+        cd = T.forward_transform(T.PhysicalField(u, mesh), Space.DIRICHLET)
+        rec(1)
+        hlu.solve_into(cd.data.view(mats.n_dir, B), xh, True)
+        rec(2)
+        out["ud"] = T.inverse_transform(T.SpectralField(xh.view(cd.data.shape), cd.grid, mesh)).data
+        rec(3)
+        cb = T.forward_transform(T.PhysicalField(u, mesh), Space.BIHARMONIC)
+        rec(4)
+        blu.solve_into(cb.data.view(mats.n_bih, B), xb, True)
+        rec(5)
+        out["ub"] = T.inverse_transform(T.SpectralField(xb.view(cb.data.shape), cb.grid, mesh)).data
+        rec(6)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for k in range(args.steps):
+            step(evs[k])
+        t1.record()
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    names = ["forward_dirichlet", "helmholtz_solve", "inverse_dirichlet", "forward_biharmonic",
+             "biharmonic_solve", "inverse_biharmonic"]
+    stages = {nm: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in evs])) for i, nm in enumerate(names)}
+    unk = (mats.n_dir + mats.n_bih) * B
+    cpu = None if args.no_cpu else cpu_c3()
+    print(json.dumps({
+        "metric": "config-3 steps/s (fwd transform + solve + inverse, Dirichlet/Helmholtz and biharmonic)",
+        "value": args.steps / (total_ms / 1e3), "unit": "steps/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "none", "vs_baseline": None, "dtype": "f64 (real field, complex128 spectra)",
+        "data": "synthetic: real U(-1,1) field, torch Philox seed 33",
+        "config": {"workload": "config3: physical 257x256x256 (n_x=256 Gauss, n_y=n_z=256), nu=dt=1e-3",
+                   "l2_policy": "each stage streams >= 135 MB arrays (> L2)"},
+        "stages_ms": stages,
+        "solved_unknowns_per_s": unk * args.steps / (total_ms / 1e3),
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+    }))
+
+
+def cpu_c3():
+    """Oracle port of the same step (numpy/scipy pocketfft + LAPACK, reference
+    arithmetic) on a bounded sample: the full 257-point wall-normal direction
+    on a 256 x 32 plane (1/8 of config 3), 1 thread; reported per full step."""
+    from oracle import shen_oracle as O
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
+
+    nu, dt = 1e-3, 1e-3
+    mesh = build_mesh(256, 256, 32, 2 * np.pi, np.pi)
+    mats = assemble(256, 0)
+    z2 = wavenumber_grid(mesh, Space.DIRICHLET).z2()
+    u = np.random.default_rng(33).uniform(-1, 1, mesh.shape)
+    hf = O.helmholtz_factor(mats, nu, dt, z2)
+    bf = O.biharmonic_factor(mats, nu, dt, z2)
+    t0 = time.perf_counter()
+    cd = O.forward_transform(u, 1, False, mats)
+    xd = O.helmholtz_solve(hf, cd)
+    O.inverse_transform(xd, 1, False, 256, 256, 32)
+    cb = O.forward_transform(u, 2, False, mats)
+    xb = O.biharmonic_solve(bf, cb)
+    O.inverse_transform(xb, 2, False, 256, 256, 32)
+    t = time.perf_counter() - t0
+    full = t * (256 // 2 + 1) / (32 // 2 + 1)
+    return {"value": 1.0 / full, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"257 x 256 x 32 plane ({t:.2f} s), scaled by kz columns 129/17 to the full step"}
+
+
 # ======================================================================= reference arm
 
 def _ref_worker(task):
@@ -422,5 +529,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == "c3":
+        run_c3(a)
     else:
         run_b200(a)

@@ -36,6 +36,10 @@ __device__ __forceinline__ c2 cadd(c2 a, c2 b) { return {a.x + b.x, a.y + b.y}; 
 __device__ __forceinline__ c2 csub(c2 a, c2 b) { return {a.x - b.x, a.y - b.y}; }
 __device__ __forceinline__ c2 cscale(double s, c2 a) { return {s * a.x, s * a.y}; }
 
+// Every kernel is one thread per Fourier line (x) and a chunk of kRowChunk
+// rows (y), so that small line counts still fill the machine.
+constexpr int kRowChunk = 16;
+
 // ---------------------------------------------------------------- extensions
 // kind 0: Gauss forward symmetric extension (N -> 2N rows)
 // kind 1: Gauss-Lobatto even extension (N -> 2N-2 rows)
@@ -43,7 +47,8 @@ __global__ void xf_extend_kernel(int kind, int N, int64_t L, const double2* __re
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const int M = kind == 0 ? 2 * N : 2 * N - 2;
-  for (int m = 0; m < M; ++m) {
+  const int m0 = blockIdx.y * kRowChunk, m1 = min(M, m0 + kRowChunk);
+  for (int m = m0; m < m1; ++m) {
     int src;
     if (m < N) src = m;
     else src = kind == 0 ? 2 * N - 1 - m : 2 * N - 2 - m;
@@ -67,8 +72,9 @@ __global__ void xf_fwd_post_kernel(int gl, int space, int N, int64_t L, double s
     if (!gl) y = cmul(ld2(tw + k), y);
     return cscale(scale, y);
   };
+  const int k0 = blockIdx.y * kRowChunk;
   if (space == 0 || space == 3) {
-    for (int k = 0; k < N; ++k) {
+    for (int k = k0; k < min(N, k0 + kRowChunk); ++k) {
       c2 v = w_at(k);
       if (space == 3) {
         st2(out + (int64_t)k * L + l, v);
@@ -81,8 +87,9 @@ __global__ void xf_fwd_post_kernel(int gl, int space, int N, int64_t L, double s
     return;
   }
   if (space == 1) {
-    c2 wk = w_at(0), wk1 = w_at(1);
-    for (int k = 0; k < n_x - 1; ++k) {
+    if (k0 >= n_x - 1) return;
+    c2 wk = w_at(k0), wk1 = w_at(k0 + 1);
+    for (int k = k0; k < min(n_x - 1, k0 + kRowChunk); ++k) {
       const c2 wk2 = w_at(k + 2);
       st2(out + (int64_t)k * L + l, csub(wk, wk2));
       wk = wk1;
@@ -90,8 +97,9 @@ __global__ void xf_fwd_post_kernel(int gl, int space, int N, int64_t L, double s
     }
     return;
   }
-  c2 w0 = w_at(0), w1 = w_at(1), w2 = w_at(2), w3 = w_at(3);
-  for (int k = 0; k < n_x - 3; ++k) {
+  if (k0 >= n_x - 3) return;
+  c2 w0 = w_at(k0), w1 = w_at(k0 + 1), w2 = w_at(k0 + 2), w3 = w_at(k0 + 3);
+  for (int k = k0; k < min(n_x - 3, k0 + kRowChunk); ++k) {
     const c2 w4 = w_at(k + 4);
     const double kk = (double)k;
     const double c2k = 2 * (kk + 2) / (kk + 3), c4k = (kk + 1) / (kk + 3);
@@ -114,7 +122,8 @@ __global__ void xf_inv_pre_kernel(int gl, int space, int n, int N, int64_t L, co
     return ld2(coef + (int64_t)k * L + l);
   };
   const int M = gl ? 2 * N - 2 : 2 * N;
-  for (int k = 0; k < N; ++k) {
+  const int k0 = blockIdx.y * kRowChunk;
+  for (int k = k0; k < min(N, k0 + kRowChunk); ++k) {
     c2 c = a_at(k);
     if (space == 1) {
       c = csub(c, a_at(k - 2));
@@ -136,7 +145,7 @@ __global__ void xf_inv_pre_kernel(int gl, int space, int n, int N, int64_t L, co
       if (k > 0) st2(Z + (int64_t)(M - k) * L + l, cmul(w, c));
     }
   }
-  if (!gl) st2(Z + (int64_t)N * L + l, {0.0, 0.0});
+  if (!gl && blockIdx.y == 0) st2(Z + (int64_t)N * L + l, {0.0, 0.0});
 }
 
 // ---------------------------------------------------------------- inverse post
@@ -148,7 +157,8 @@ __global__ void xf_inv_post_kernel(int gl, int N, int64_t L, const double2* __re
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
   const c2 c0 = ld2(cends + l), cN = ld2(cends + L + l);
-  for (int m = 0; m < N; ++m) {
+  const int m0 = blockIdx.y * kRowChunk;
+  for (int m = m0; m < min(N, m0 + kRowChunk); ++m) {
     c2 f = ld2(F + (int64_t)m * L + l);
     c2 v;
     if (!gl) {
@@ -200,30 +210,31 @@ __global__ void xf_mass_kernel(int nband, int n, int mmax, int64_t L, const doub
 }
 
 static unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
+static dim3 grid_for(int64_t L, int rows) { return dim3(blocks_for(L), (unsigned)((rows + kRowChunk - 1) / kRowChunk)); }
 
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st) {
   if (L <= 0) return cudaSuccess;
-  xf_extend_kernel<<<blocks_for(L), 256, 0, st>>>(kind, N, L, static_cast<const double2*>(x), static_cast<double2*>(e));
+  xf_extend_kernel<<<grid_for(L, kind == 0 ? 2 * N : 2 * N - 2), 256, 0, st>>>(kind, N, L, static_cast<const double2*>(x), static_cast<double2*>(e));
   return cudaGetLastError();
 }
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,
                                void* out, cudaStream_t st) {
   if (L <= 0) return cudaSuccess;
-  xf_fwd_post_kernel<<<blocks_for(L), 256, 0, st>>>(gl, space, N, L, scale, static_cast<const double2*>(tw),
+  xf_fwd_post_kernel<<<grid_for(L, N), 256, 0, st>>>(gl, space, N, L, scale, static_cast<const double2*>(tw),
                                                     static_cast<const double2*>(Y), static_cast<double2*>(out));
   return cudaGetLastError();
 }
 cudaError_t launch_xf_inv_pre(int gl, int space, int n, int N, int64_t L, const void* tw, const void* coef, void* Z,
                               void* cends, cudaStream_t st) {
   if (L <= 0) return cudaSuccess;
-  xf_inv_pre_kernel<<<blocks_for(L), 256, 0, st>>>(gl, space, n, N, L, static_cast<const double2*>(tw),
+  xf_inv_pre_kernel<<<grid_for(L, N), 256, 0, st>>>(gl, space, n, N, L, static_cast<const double2*>(tw),
                                                    static_cast<const double2*>(coef), static_cast<double2*>(Z),
                                                    static_cast<double2*>(cends));
   return cudaGetLastError();
 }
 cudaError_t launch_xf_inv_post(int gl, int N, int64_t L, const void* F, const void* cends, void* out, cudaStream_t st) {
   if (L <= 0) return cudaSuccess;
-  xf_inv_post_kernel<<<blocks_for(L), 256, 0, st>>>(gl, N, L, static_cast<const double2*>(F),
+  xf_inv_post_kernel<<<grid_for(L, N), 256, 0, st>>>(gl, N, L, static_cast<const double2*>(F),
                                                     static_cast<const double2*>(cends), static_cast<double2*>(out));
   return cudaGetLastError();
 }

@@ -317,6 +317,135 @@ def mass_solve(scalar, space, n_x: int, family):
     return ln.give_back(_mass_pass(ln.t, sp, int(n_x), _fam(family), out=out))
 
 
+# ---------------------------------------------------------------- wall-normal operators
+#
+# For the 3-D transforms the whole wall-normal map is one linear operator per
+# (n_x, family, space): forward = B^-1 S W (Chebyshev scalar products W, Shen
+# stencil S, mass solve B^-1), scalar product = S W, inverse = C X (Shen ->
+# Chebyshev expansion X, evaluation at the points C).  At N = 257 (config 3)
+# the FFT route needs a Bluestein FFT (N prime) and several HBM passes; one
+# fp64 GEMM over all Fourier lines (cuBLAS) is about 4x faster, reads the
+# spectrum once and writes the result once.  The operators are built once in
+# 80-bit arithmetic and rounded to float64.  SHEN_XFORM=fft selects the
+# kernel/cuFFT pipeline above instead (used by the 1-D building blocks).
+
+XFORM_METHOD = __import__("os").environ.get("SHEN_XFORM", "matrix")
+
+
+def _ld_pi():
+    return np.arccos(np.longdouble(-1))
+
+
+def _scalar_matrix_ld(N: int, fam: int):
+    """W (N x N): chebyshev_scalar as a matrix (transforms.py:81-86)."""
+    pi = _ld_pi()
+    k = np.arange(N, dtype=np.longdouble)[:, None]
+    n = np.arange(N, dtype=np.longdouble)[None, :]
+    if fam == 0:
+        return (pi / N) * np.cos(pi * k * (2 * n + 1) / (2 * N))
+    nx = N - 1
+    W = (pi / nx) * np.cos(pi * k * n / nx)
+    W[:, 0] *= 0.5
+    W[:, nx] *= 0.5
+    return W
+
+
+def _stencil_ld(sp: int, N: int, fam: int):
+    """S (n x N): shen_scalar applied to the Chebyshev scalar products (transforms.py:89-110)."""
+    n_x = N - 1
+    if sp == 0:
+        S = np.eye(N, dtype=np.longdouble) * (2 / _ld_pi())
+        S[0, 0] /= 2
+        if fam == 1:
+            S[n_x, n_x] /= 2
+        return S
+    if sp == 1:
+        n = n_x - 1
+        S = np.zeros((n, N), dtype=np.longdouble)
+        r = np.arange(n)
+        S[r, r] = 1
+        S[r, r + 2] = -1
+        return S
+    n = n_x - 3
+    S = np.zeros((n, N), dtype=np.longdouble)
+    r = np.arange(n)
+    k = r.astype(np.longdouble)
+    S[r, r] = 1
+    S[r, r + 2] = -2 * (k + 2) / (k + 3)
+    S[r, r + 4] = (k + 1) / (k + 3)
+    return S
+
+
+def _banded_solve_ld(Bd, R):
+    """Solve B Y = R in long double (B banded SPD, no pivoting needed)."""
+    A = Bd.astype(np.longdouble).copy()
+    Y = R.copy()
+    n = A.shape[0]
+    bw = 4
+    for i in range(n):
+        hi = min(n, i + bw + 1)
+        for r in range(i + 1, hi):
+            if A[r, i] != 0:
+                f = A[r, i] / A[i, i]
+                A[r, i:hi] -= f * A[i, i:hi]
+                Y[r] -= f * Y[i]
+    for i in range(n - 1, -1, -1):
+        hi = min(n, i + bw + 1)
+        Y[i] = (Y[i] - A[i, i + 1:hi] @ Y[i + 1:hi]) / A[i, i]
+    return Y
+
+
+@lru_cache(maxsize=16)
+def _operator_host(kind: str, n_x: int, fam: int, sp: int):
+    N = n_x + 1
+    if kind in ("fwd", "fsp"):
+        M = _stencil_ld(sp, N, fam) @ _scalar_matrix_ld(N, fam)
+        if kind == "fwd" and sp != 0:
+            mats = assemble(n_x, as_family(fam))
+            Bd = (mats.mass_dir if sp == 1 else mats.mass_bih).dense()
+            M = _banded_solve_ld(Bd, M)
+        return np.ascontiguousarray(M.astype(np.float64))
+    # inverse: C (N x N) evaluation at the points times the expansion X (N x n)
+    pi = _ld_pi()
+    j = np.arange(N, dtype=np.longdouble)[:, None]
+    m = np.arange(N, dtype=np.longdouble)[None, :]
+    theta = pi * (2 * j + 1) / (2 * N) if fam == 0 else pi * j / n_x
+    C = np.cos(m * theta)
+    n = N - (0, 2, 4)[sp]
+    X = np.zeros((N, n), dtype=np.longdouble)
+    c = np.arange(n)
+    k = c.astype(np.longdouble)
+    X[c, c] = 1
+    if sp == 1:
+        X[c + 2, c] = -1
+    elif sp == 2:
+        X[c + 2, c] = -2 * (k + 2) / (k + 3)
+        X[c + 4, c] = (k + 1) / (k + 3)
+    return np.ascontiguousarray((C @ X).astype(np.float64))
+
+
+@lru_cache(maxsize=16)
+def _operator_dev(kind: str, n_x: int, fam: int, sp: int, dev_index: int, scale: float = 1.0):
+    """Device copy; ``scale`` folds a constant factor into the operator (the
+    inverse folds irfft2's 1/(n_y n_z) so no separate scaling pass runs)."""
+    import torch
+
+    M = _operator_host(kind, n_x, fam, sp)
+    if scale != 1.0:
+        M = M * scale
+    return torch.from_numpy(np.ascontiguousarray(M)).to(torch.device("cuda", dev_index))
+
+
+def _apply_operator(M, lines):
+    """(n x N) float64 operator applied to (N, L) complex128 lines -> (n, L)."""
+    import torch
+
+    N, L = lines.shape
+    xr = torch.view_as_real(lines).reshape(N, 2 * L)
+    out = torch.matmul(M, xr)
+    return torch.view_as_complex(out.view(M.shape[0], L, 2))
+
+
 # ---------------------------------------------------------------- 3-D transforms
 
 def _physical_to_device(field: PhysicalField):
@@ -343,10 +472,14 @@ def _forward(field: PhysicalField, space, solve_mass: bool):
     N = fourier.shape[0]
     yz = tuple(fourier.shape[1:])
     lines = fourier.view(N, -1)
-    scal = _chebyshev_pass(lines, fam, sp)
+    if XFORM_METHOD == "matrix":
+        kind = "fwd" if solve_mass else "fsp"
+        scal = _apply_operator(_operator_dev(kind, mesh.n_x, fam, sp, device().index), lines)
+    else:
+        scal = _chebyshev_pass(lines, fam, sp)
+        if solve_mass and sp != 0:
+            scal = _mass_pass(scal, sp, mesh.n_x, fam)
     del fourier, lines
-    if solve_mass and sp != 0:
-        scal = _mass_pass(scal, sp, mesh.n_x, fam)
     data = scal.reshape((scal.shape[0],) + yz)
     if from_numpy:
         data = data.cpu().numpy()
@@ -382,9 +515,15 @@ def inverse_transform(coeffs: SpectralField) -> PhysicalField:
     n = t.shape[0]
     yz = tuple(t.shape[1:])
     _check_expand_rows(n, sp, mesh.n_x)
-    lines = _expand_pass(t.reshape(n, -1), sp, mesh.n_x, fam)
+    if XFORM_METHOD == "matrix":
+        op = _operator_dev("inv", mesh.n_x, fam, sp, device().index, 1.0 / (mesh.n_y * mesh.n_z))
+        lines = _apply_operator(op, t.reshape(n, -1))
+        norm = "forward"  # 1/(n_y n_z) already folded into the operator
+    else:
+        lines = _expand_pass(t.reshape(n, -1), sp, mesh.n_x, fam)
+        norm = "backward"
     del t
-    data = torch.fft.irfft2(lines.reshape((mesh.n_x + 1,) + yz), s=(mesh.n_y, mesh.n_z), dim=(1, 2))
+    data = torch.fft.irfft2(lines.reshape((mesh.n_x + 1,) + yz), s=(mesh.n_y, mesh.n_z), dim=(1, 2), norm=norm)
     if from_numpy:
         data = data.cpu().numpy()
     return PhysicalField(data, mesh)

@@ -32,7 +32,7 @@ def _close(got, want, tol=TOL):
 
 @pytest.mark.parametrize("n_x", [8, 16, 32])
 @pytest.mark.parametrize("fi", [0, 1])
-def test_transforms_vs_reference_golden(golden, n_x, fi):
+def test_transforms_vs_reference_golden(golden, n_x, fi, xform_method):
     g = golden("transforms.npz")
     mesh = build_mesh(n_x, 8, 4, 2 * np.pi, np.pi, FAMS[fi])
     key = f"nx{n_x}_f{fi}"
@@ -71,10 +71,21 @@ def test_mass_factors_match_oracle(fi):
             assert np.array_equal(mine[p], want[p])
 
 
+@pytest.fixture(params=["matrix", "fft"])
+def xform_method(request, monkeypatch):
+    monkeypatch.setattr(T, "XFORM_METHOD", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("fi", [0, 1])
 @pytest.mark.parametrize("n_x", [64, 256])
-def test_transforms_vs_oracle_larger(fi, n_x):
-    """Larger wall-normal sizes (cfg3's n_x = 256) on a small y/z plane."""
+def test_transforms_vs_oracle_larger(fi, n_x, xform_method):
+    """Larger wall-normal sizes (cfg3's n_x = 256) on a small y/z plane.
+    The biharmonic forward transform is ill-conditioned: at n_x = 256 the
+    reference itself is 1.6e-11..2.4e-11 away from an 80-bit evaluation
+    (test_transform_operators.py), the matrix route ~1.6e-15, so the two
+    differ by the reference's own error; the gate there is BASELINE.json's
+    1e-10."""
     mesh = build_mesh(n_x, 12, 10, 2 * np.pi, np.pi, FAMS[fi])
     mats = assemble(n_x, fi)
     rng = np.random.default_rng(n_x + fi)
@@ -82,7 +93,7 @@ def test_transforms_vs_oracle_larger(fi, n_x):
     for sc, space in enumerate(SPACES):
         c = T.forward_transform(T.PhysicalField(u, mesh), space)
         want = O.forward_transform(u, sc, fi == 1, mats)
-        _close(c.data, want)
+        _close(c.data, want, 1e-10 if (sc == 2 and xform_method == "matrix") else TOL)
         _close(T.forward_scalar_product(T.PhysicalField(u, mesh), space).data,
                O.forward_scalar_product(u, sc, fi == 1))
         back = T.inverse_transform(T.SpectralField(want, c.grid, mesh))
@@ -136,7 +147,7 @@ def test_errors_match_reference():
 
 @pytest.mark.parametrize("fi", [0, 1])
 @pytest.mark.parametrize("space", [Space.DIRICHLET, Space.BIHARMONIC, Space.CHEBYSHEV])
-def test_cfg3_projection_round_trip(fi, space):
+def test_cfg3_projection_round_trip(fi, space, xform_method):
     """BASELINE config 3 sizes (physical 257 x 256 x 256): forward(inverse(c))
     recovers any coefficient field of the space (size-independent property),
     and inverse(forward(u)) recovers u for the Chebyshev space."""
@@ -156,8 +167,10 @@ def test_cfg3_projection_round_trip(fi, space):
     assert err < 1e-12, err
     c2 = T.forward_transform(T.PhysicalField(u2, mesh), space).data
     err_c = float((c2 - c_herm).abs().max() / c_herm.abs().max())
-    # The biharmonic coefficient round trip is ill-conditioned at n_x = 256:
-    # the reference itself (oracle, same property, 8 x 8 plane) loses
-    # 5.5e-11 (Gauss) / 5.8e-11 (Lobatto); Chebyshev/Dirichlet lose < 1e-13.
+    # The biharmonic coefficient round trip is ill-conditioned at n_x = 256
+    # (rounding of the point values is amplified by the forward map): the
+    # reference itself (oracle, same property, 8 x 8 plane) loses 5.5e-11
+    # (Gauss) / 5.8e-11 (Lobatto), both device routes the same.
+    # Chebyshev/Dirichlet lose < 1e-13.
     tol_c = 2e-10 if space is Space.BIHARMONIC else 1e-12
     assert err_c < tol_c, err_c
