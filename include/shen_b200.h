@@ -76,8 +76,9 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  * shen_helm_solve_stream: same inputs as the chunked solve (chunk_rows in
  *   {4, 8, 16}); one thread per system with coalesced row access; y is
  *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
- *   bytes) and recomputed in the backward sweep; warps_per_sm caps the
- *   resident warps per SM (0 = as many as fit).  [j_begin, j_end) restricts
+ *   bytes) and recomputed in the backward sweep; warps_per_sm selects the
+ *   persistent CTA size (8 or 12 warps per SM; 0 = the per-operator default,
+ *   12 for Helmholtz, 8 for the biharmonic).  [j_begin, j_end) restricts
  *   the solve to a range of systems (j_end < 0: the whole batch) -- the row
  *   pitch stays `batch`, so host<->device copies of column slabs can be
  *   pipelined against the solve (see shen_memcpy2d_async).

@@ -75,12 +75,15 @@ __global__ void __launch_bounds__(256) bih_factor_kernel(BihFactorArgs a) {
   for (int i = 0; i < n; ++i) {
     const int k = par + 2 * i;
     load_bih_row(a.tab, k, c);
-    BihBands h = bih_bands(a.xi0, xi1, xi2, c);
     double l2, l4;
-    if (EXACT)
+    if (EXACT) {
+      const BihBands h = bih_bands(a.xi0, xi1, xi2, c);
       bih_step<true>(u, u1, u2, h, c, a.xi0, i, l2, l4);
-    else
-      bih_step_fast(u, u1, u2, h, c, a.xi0, l2, l4);
+    } else {
+      const BihBands h = bih_bands_fast(a.xi0, xi1, xi2, c);
+      bih_fast_scale_tail(c, a.xi0);
+      bih_step_fast(u, u1, u2, h, c, l2, l4);
+    }
     note_pivot(a.pivot, par, i, u.d);
     if (a.d[par] != nullptr) {
       if (i >= 1) a.low2[par][(int64_t)(i - 1) * B + j] = l2;

@@ -179,6 +179,40 @@ __device__ __forceinline__ void load_bih_row_smem(const double* tab, int k, doub
   }
 }
 
+// Compact shared-memory row (BC_STRIDE doubles per mode, 4 virtual zero rows
+// in front): the 13 per-mode values; BB2M/BB4M/Q2/S2 of mode k are the BB2 /
+// BB4 / Q4 / S4 entries of modes k-2 / k-4 (virtual rows -2, -1 carry q, s of
+// modes 2, 3 so that Q2/S2 of modes 0, 1 come out right).
+enum BihCompactCol { BC_Q0 = 0, BC_AR0, BC_BB0, BC_T2, BC_AR2, BC_BB2, BC_T4, BC_BB4, BC_ARM2, BC_P, BC_Q4, BC_S4, BC_R,
+                     BC_NCOL };
+constexpr int BC_STRIDE = 14;
+__host__ __device__ constexpr int bc_src(int col) {  // 18-column source of compact column `col`
+  return col == BC_Q4 ? B_Q4 : col == BC_S4 ? B_S4 : col == BC_R ? B_R : col == BC_P ? B_P
+       : col == BC_ARM2 ? B_ARM2 : col;  // BC_Q0..BC_BB4 coincide with B_Q0..B_BB4
+}
+static_assert(BC_BB4 == B_BB4 && BC_Q0 == B_Q0, "compact columns 0..7 mirror the full table");
+
+__device__ __forceinline__ void load_bih_row_compact(const double* stab, int k, double* c) {
+  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE);
+  double v[BC_STRIDE];
+#pragma unroll
+  for (int q = 0; q < BC_STRIDE / 2; ++q) {
+    const double2 t = r0[q];
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+  c[B_Q0] = v[BC_Q0]; c[B_AR0] = v[BC_AR0]; c[B_BB0] = v[BC_BB0];
+  c[B_T2] = v[BC_T2]; c[B_AR2] = v[BC_AR2]; c[B_BB2] = v[BC_BB2];
+  c[B_T4] = v[BC_T4]; c[B_BB4] = v[BC_BB4]; c[B_ARM2] = v[BC_ARM2];
+  c[B_P] = v[BC_P]; c[B_R] = v[BC_R]; c[B_Q4] = v[BC_Q4]; c[B_S4] = v[BC_S4];
+  const double* rm2 = stab + (int64_t)(k + 2) * BC_STRIDE;
+  const double2 qs = *reinterpret_cast<const double2*>(rm2 + BC_Q4);
+  c[B_Q2] = qs.x;
+  c[B_S2] = qs.y;
+  c[B_BB2M] = rm2[BC_BB2];
+  c[B_BB4M] = stab[(int64_t)k * BC_STRIDE + BC_BB4];
+}
+
 struct BihBands {
   double hd, hp2, hp4, hm2, hm4;
 };
@@ -261,17 +295,37 @@ __device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2
   u.rd = EXACT ? 0.0 : rcp_fast(u.d);
 }
 
-// Branch-free fast-mode biharmonic step (same arithmetic as bih_step<false>
-// for i >= 2).  Rows "before row 0" are zero records with rd = 0, which makes
-// the generic formula reproduce rows 0 and 1 exactly (fma(-0, 0, x) == x).
+// ---- fast mode (build checkpoints, chunked and streaming solves) ----------
+// Own arithmetic, shared bit for bit by every fast-mode kernel: bands with
+// FMAs, and the tail factors carried pre-scaled by xi0 (a~ = xi0 a,
+// b~ = xi0 b), which removes the xi0 products from every row.  Callers
+// replace c[B_P], c[B_R] by xi0 * p_k, xi0 * r_k (bih_fast_scale_tail) before
+// bih_step_fast; checkpoints therefore hold a~, b~.
+__device__ __forceinline__ BihBands bih_bands_fast(double xi0, double xi1, double xi2, const double* c) {
+  BihBands b;
+  b.hd = __fma_rn(xi0, c[B_Q0], __fma_rn(xi1, c[B_AR0], __dmul_rn(xi2, c[B_BB0])));
+  b.hp2 = __fma_rn(xi0, c[B_T2], __fma_rn(xi1, c[B_AR2], __dmul_rn(xi2, c[B_BB2])));
+  b.hp4 = __fma_rn(xi0, c[B_T4], __dmul_rn(xi2, c[B_BB4]));
+  b.hm2 = __fma_rn(xi1, c[B_ARM2], __dmul_rn(xi2, c[B_BB2M]));
+  b.hm4 = __dmul_rn(xi2, c[B_BB4M]);
+  return b;
+}
+__device__ __forceinline__ void bih_fast_scale_tail(double* c, double xi0) {
+  c[B_P] = __dmul_rn(xi0, c[B_P]);
+  c[B_R] = __dmul_rn(xi0, c[B_R]);
+}
+
+// Branch-free fast-mode biharmonic step.  Rows "before row 0" are zero
+// records with rd = 0, which makes the generic formula reproduce rows 0 and 1
+// (fma(-0, 0, x) == x).
 __device__ __forceinline__ void bih_step_fast(BihU& u, const BihU& u1, const BihU& u2, const BihBands& h,
-                                              const double* c, double xi0, double& l2, double& l4) {
+                                              const double* c, double& l2, double& l4) {
   l4 = __dmul_rn(h.hm4, u2.rd);
   const double tmp = __fma_rn(-l4, u2.e, h.hm2);
   l2 = __dmul_rn(tmp, u1.rd);
-  const double u42 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2])));
-  const double u44 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4])));
-  const double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
+  const double u42 = __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2]));
+  const double u44 = __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4]));
+  const double u24 = __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4]));
   u.d = __fma_rn(-l2, u1.e, __fma_rn(-l4, u2.f, h.hd));
   u.e = __fma_rn(-l2, u1.f, __fma_rn(-l4, u42, h.hp2));
   u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));

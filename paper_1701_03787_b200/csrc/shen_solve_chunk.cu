@@ -322,9 +322,10 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       const int k = min(par + 2 * (s0 + r), a.n_bih - 1);
       double c[B_NCOL];
       load_bih_row(a.tab, k, c);
-      const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+      const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
+      bih_fast_scale_tail(c, xi0);
       double l2, l4;
-      bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
+      bih_step_fast(u, u1, u2, hb, c, l2, l4);
       u2 = u1;
       u1 = u;
       const V b = Ys[r * 32 + lane];
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       Ss[(r * NS + SQN) * 32 + lane] = qn;
       Ss[(r * NS + SSN) * 32 + lane] = sn;
       const double al = -rd * ue, be = -rd * uf;
-      const double ga = -rd * (xi0 * ua), de = -rd * (xi0 * ub);
+      const double ga = -rd * ua, de = -rd * ub;  // ua, ub carry xi0 (fast mode)
       const V cy = vmul(rd, y);
       const double cg1 = rd * g1, cg2 = rd * g2;
 #pragma unroll
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
                    f = Ss[(r * NS + SF) * 32 + lane];
       const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
       V acc = vsub(vsub(yy, vmul(e, x1)), vmul(f, x2));
-      acc = vsub(acc, vmul(xi0, vadd(vmul(av, sq), vmul(bv, sv))));
+      acc = vsub(acc, vadd(vmul(av, sq), vmul(bv, sv)));
       const V x = vmul(rd, acc);
       const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
       sq = vfma(qn, x2, sq);
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       const double rd = Ss[(r * NS + SRD) * 32 + lane], e = Ss[(r * NS + SE) * 32 + lane],
                    f = Ss[(r * NS + SF) * 32 + lane];
       const double av = Ss[(r * NS + SA) * 32 + lane], bv = Ss[(r * NS + SB) * 32 + lane];
-      const V acc = vfma(e, c1, vfma(f, c2, vmul(xi0, vfma(av, cq, vmul(bv, cs)))));
+      const V acc = vfma(e, c1, vfma(f, c2, vfma(av, cq, vmul(bv, cs))));
       const V xc = vmul(-rd, acc);
       const double qn = Ss[(r * NS + SQN) * 32 + lane], sn = Ss[(r * NS + SSN) * 32 + lane];
       cq = vfma(qn, c2, cq);

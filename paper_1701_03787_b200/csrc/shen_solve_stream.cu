@@ -23,6 +23,7 @@
 // not HBM.  Latency is hidden by cp.async prefetch of the next segment (RHS
 // rows in the forward, staged y in the backward) instead of by occupancy.
 #include <algorithm>
+#include <cstdlib>
 
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
@@ -94,11 +95,12 @@ __device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_
   return {g0 + gi * gstride, k < nseg ? k : 2 * nseg - 1 - k};
 }
 
-template <typename V, int R>
+
+template <typename V, int R, int SG>
 __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int n, int par, int64_t B,
                                           int64_t ngroups, int64_t jb, int64_t je, int sgi, int lane) {
   if (ref.g < ngroups) {
-    const int64_t j = jb + ref.g * (32 * kSG) + sgi * 32 + lane;
+    const int64_t j = jb + ref.g * (32 * SG) + sgi * 32 + lane;
     const bool jv = j < je;
     const int64_t jc = jv ? j : je - 1;
     const V* src = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
@@ -118,8 +120,9 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
 // read through the L1 (warp-uniform broadcast loads).  CTA = 2 warps
 // (parity 0 / 1 of the same 32 systems).  HBM traffic per unknown: 2 RHS
 // reads + 1 solution write (+ ~3 B of checkpoints).
-template <typename V, int R, int RING>
-__global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
+template <typename V, int R, int RING, int SG>
+__global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
+  constexpr int kT = 64 * SG;
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
@@ -131,8 +134,8 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   V* out = static_cast<V*>(a.out);
   // row constants (sd, st, md, has_sup) of both parities in shared memory,
   // loaded once per persistent CTA
-  double4* tab = reinterpret_cast<double4*>(smem + (size_t)kStreamThreads / 32 * RING * R * 32 * VOps<V>::ndouble);
-  for (int idx = tid; idx < 2 * tab_rows; idx += kStreamThreads) {
+  double4* tab = reinterpret_cast<double4*>(smem + (size_t)kT / 32 * RING * R * 32 * VOps<V>::ndouble);
+  for (int idx = tid; idx < 2 * tab_rows; idx += kT) {
     const int p = idx / tab_rows, i = idx - p * tab_rows;
     const int np = (a.n_dir - p + 1) / 2;
     const int nsp = (a.n_dir - 2 - p + 1) / 2 > 0 ? (a.n_dir - 2 - p + 1) / 2 : 0;
@@ -146,18 +149,18 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   __syncthreads();
   const double4* mytab = tab + par * tab_rows;
   const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;
-  const int64_t ngroups = (je - jb + 32 * kSG - 1) / (32 * kSG);
+  const int64_t ngroups = (je - jb + 32 * SG - 1) / (32 * SG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<RING - 1>();
@@ -167,14 +170,14 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = jb + g * (32 * kSG) + sgi * 32 + lane;
+    const int64_t j = jb + g * (32 * SG) + sgi * 32 + lane;
     const bool jv = j < je;
     const int64_t jc = jv ? j : je - 1;
     const double cb = __ldg(a.cb + jc);
     const double sub = __dmul_rn(cb, -1.5707963267948966);
     V* outj = out + (int64_t)par * B + j;
     // y checkpoints: per-CTA scratch, [segment][thread] (only the group in flight)
-    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((a.n_dir + 1) / 2 + R - 1) / R) * kStreamThreads + tid;
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((a.n_dir + 1) / 2 + R - 1) / R) * kT + tid;
     const double* ckj = a.ckpt + (int64_t)par * 3 * B + jc;
     // ---------------- forward: y at segment ends only
     HelmProj pj;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
         const V b = (full || i < n) ? cur[r * 32] : szero<V>();
         y = sfma(-low, y, b);
       }
-      if (s + 1 < nseg) ychkj[s * kStreamThreads] = y;
+      if (s + 1 < nseg) ychkj[s * kT] = y;
     }
     // ---------------- backward: re-stream each segment (bottom first)
     V x1 = szero<V>(), S = szero<V>();
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
     if (nseg - 1 > 0) {
       const double* ck = ckj + (int64_t)6 * (nseg - 1) * B;
       ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-      ckyv = ychkj[(nseg - 2) * kStreamThreads];
+      ckyv = ychkj[(nseg - 2) * kT];
     }
     for (int s = nseg - 1; s >= 0; --s) {
       HelmProj q;
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
       if (s - 1 > 0) {
         const double* ck = ckj + (int64_t)6 * (s - 1) * B;
         ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-        ckyv = ychkj[(s - 2) * kStreamThreads];
+        ckyv = ychkj[(s - 2) * kT];
       }
       const V* cur = consume();
       const bool full = (s + 1) * R <= n;
@@ -256,8 +259,9 @@ __global__ void __launch_bounds__(kStreamThreads) helm_stream_kernel(HelmChunkAr
 }
 
 // ======================================================================= biharmonic
-template <typename V, int R, bool SMEM_TAB, int RING>
-__global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs a, V* ychk) {
+template <typename V, int R, bool SMEM_TAB, int RING, int SG>
+__global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, V* ychk) {
+  constexpr int kT = 64 * SG;
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
@@ -266,51 +270,69 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
   const int n = (nb - par + 1) / 2;
   const int nseg = (n + R - 1) / R;
   V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * R * 32 + lane;
-  // row-constant table: a shared-memory copy when it fits (loaded once per
-  // persistent CTA), else the read-only path
-  double* stab = smem + (size_t)kStreamThreads / 32 * RING * R * 32 * VOps<V>::ndouble;
-  const double* tab = a.tab;
+  // row-constant table: a compact shared-memory copy when it fits (loaded
+  // once per persistent CTA), else the 18-column table through the read-only
+  // path.  The compact rows keep the 13 per-mode values; the m-band and q/s
+  // lookahead entries are read from rows k-2 / k-4 (4 virtual rows in front).
+  double* stab = smem + (size_t)kT / 32 * RING * R * 32 * VOps<V>::ndouble;
   if (SMEM_TAB) {
-    const double2* src = reinterpret_cast<const double2*>(a.tab);
-    double2* dst = reinterpret_cast<double2*>(stab);
-    for (int q = tid; q < nb * B_STRIDE / 2; q += kStreamThreads) dst[q] = __ldg(src + q);
+    for (int q = tid; q < (nb + 4) * BC_STRIDE; q += kT) {
+      const int kk = q / BC_STRIDE - 4, col = q - (kk + 4) * BC_STRIDE;
+      double v = 0.0;
+      if (kk >= 0 && col < BC_NCOL) {
+        v = __ldg(a.tab + (int64_t)kk * B_STRIDE + bc_src(col));
+        if (col == BC_P || col == BC_R) v = __dmul_rn(a.xi0, v);  // == bih_fast_scale_tail
+      }
+      else if (kk >= -2 && (col == BC_Q4 || col == BC_S4))
+        v = __ldg(a.tab + (int64_t)(kk + 2) * B_STRIDE + (col == BC_Q4 ? B_Q2 : B_S2));
+      stab[q] = v;
+    }
     __syncthreads();
-    tab = stab;
   }
+  const double* tab = a.tab;
   auto row_consts = [&](int k, double* c) {
-    if (SMEM_TAB) load_bih_row_smem(tab, k, c); else load_bih_row(tab, k, c);
+    if (SMEM_TAB) load_bih_row_compact(stab, k, c); else load_bih_row(tab, k, c);
+  };
+  auto q4s4 = [&](int k, double& q4, double& s4) {
+    if (SMEM_TAB) {
+      const double2 v = *reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE + BC_Q4);
+      q4 = v.x; s4 = v.y;
+    } else {
+      q4 = tab[(int64_t)k * B_STRIDE + B_Q4];
+      s4 = tab[(int64_t)k * B_STRIDE + B_S4];
+    }
   };
   const V* rhs = static_cast<const V*>(a.rhs);
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
   const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;
-  const int64_t ngroups = (je - jb + 32 * kSG - 1) / (32 * kSG);
+  const int64_t ngroups = (je - jb + 32 * SG - 1) / (32 * SG);
   const int64_t g0 = blockIdx.x, gstride = gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
   }
   int64_t qc = 0;
-  auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+  auto consume = [&]() -> V* {
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     ++qi;
     cpa_wait<RING - 1>();
-    const V* p = ring + (qc % RING) * R * 32;
+    V* p = ring + (qc % RING) * R * 32;
     ++qc;
     return p;
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = jb + g * (32 * kSG) + sgi * 32 + lane;
+    const int64_t j = jb + g * (32 * SG) + sgi * 32 + lane;
     const bool jv = j < je;
     const int64_t jc = jv ? j : je - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
     V* outj = out + (int64_t)par * B + j;
-    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 2 * kStreamThreads + tid;
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 2 * kT + tid;
     const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;
     // ---------------- forward
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
@@ -324,9 +346,10 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
-        const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+        const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
+        if (!SMEM_TAB) bih_fast_scale_tail(c, xi0);  // the compact table holds xi0 p, xi0 r
         double l2, l4;
-        bih_step_fast(u, u1, u2, hb, c, xi0, l2, l4);
+        bih_step_fast(u, u1, u2, hb, c, l2, l4);
         u2 = u1;
         u1 = u;
         const V b = (full || i < n) ? cur[r * 32] : szero<V>();
@@ -335,77 +358,79 @@ __global__ void __launch_bounds__(kStreamThreads) bih_stream_kernel(BihChunkArgs
         y1 = y;
       }
       if (s + 1 < nseg) {
-        ychkj[(2 * s) * kStreamThreads] = y1;
-        ychkj[(2 * s + 1) * kStreamThreads] = y2;
+        ychkj[(2 * s) * kT] = y1;
+        ychkj[(2 * s + 1) * kT] = y2;
       }
     }
     // ---------------- backward
+    // Checkpoint of the segment below the one being processed is prefetched
+    // into registers (8-warp CTA); the 12-warp CTA has no registers to spare
+    // and loads it at segment start.
+    constexpr bool PF = (SG == 4);
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
     double ck[10];
     V cya = szero<V>(), cyb = szero<V>();
-#pragma unroll
-    for (int q = 0; q < 10; ++q) ck[q] = 0.0;
-    if (nseg - 1 > 0) {
-      const double* cp = ckj + (int64_t)20 * (nseg - 1) * B;
+    auto load_ck = [&](int s) {
+      const double* cp = ckj + (int64_t)20 * s * B;
 #pragma unroll
       for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
-      cya = ychkj[(2 * (nseg - 2)) * kStreamThreads];
-      cyb = ychkj[(2 * (nseg - 2) + 1) * kStreamThreads];
-    }
+      cya = ychkj[(2 * (s - 1)) * kT];
+      cyb = ychkj[(2 * (s - 1) + 1) * kT];
+    };
+    if (PF && nseg - 1 > 0) load_ck(nseg - 1);
     for (int s = nseg - 1; s >= 0; --s) {
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>();
-      if (s > 0) {
+      if (s > 0) {  // factor state and y entering the segment
+        if (!PF) load_ck(s);
         w1.d = ck[0]; w1.e = ck[1]; w1.f = ck[2]; w1.a = ck[3]; w1.b = ck[4];
         w2.d = ck[5]; w2.e = ck[6]; w2.f = ck[7]; w2.a = ck[8]; w2.b = ck[9];
-        w1.rd = rcp_fast(w1.d);
-        w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
         ya = cya;
         yb = cyb;
+        w1.rd = rcp_fast(w1.d);
+        w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
       }
-      if (s - 1 > 0) {
-        const double* cp = ckj + (int64_t)20 * (s - 1) * B;
-#pragma unroll
-        for (int q = 0; q < 10; ++q) ck[q] = __ldg(cp + q * B);
-        cya = ychkj[(2 * (s - 2)) * kStreamThreads];
-        cyb = ychkj[(2 * (s - 2) + 1) * kStreamThreads];
-      }
-      const V* cur = consume();
+      if (PF && s - 1 > 0) load_ck(s - 1);
+      V* cur = consume();
       const bool full = (s + 1) * R <= n;
-      double rd_[R], e_[R], f_[R], a_[R], b_[R];
-      V y_[R];
+      // U-row entries pre-multiplied by 1/d (rows past n get 0, so x = 0 there):
+      // x_i = y~_i - e~_i x_{i+1} - f~_i x_{i+2} - a~_i S_q - b~_i S_s
+      double e_[R], f_[R], a_[R], b_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
-        const BihBands hb = bih_bands(xi0, xi1, xi2, c);
+        const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
+        if (!SMEM_TAB) bih_fast_scale_tail(c, xi0);
         double l2, l4;
-        bih_step_fast(w, w1, w2, hb, c, xi0, l2, l4);
+        bih_step_fast(w, w1, w2, hb, c, l2, l4);
         w2 = w1;
         w1 = w;
         const bool valid = full || i < n;
         const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32] : szero<V>()));
         yb = ya;
         ya = y;
-        y_[r] = y;
-        rd_[r] = valid ? w.rd : 0.0;
-        e_[r] = valid ? w.e : 0.0;
-        f_[r] = valid ? w.f : 0.0;
-        a_[r] = valid ? w.a : 0.0;
-        b_[r] = valid ? w.b : 0.0;
+        const double rd = valid ? w.rd : 0.0;
+        cur[r * 32] = smul(rd, y);  // y~ replaces b in this thread's ring slot (frees R registers)
+        e_[r] = rd * w.e;
+        f_[r] = rd * w.f;
+        a_[r] = rd * w.a;
+        b_[r] = rd * w.b;
       }
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
         const int i = s * R + r;
         const int k = min(par + 2 * i, nb - 1);
         const bool valid = full || i < n;
-        const double qn = valid ? tab[(int64_t)k * B_STRIDE + B_Q4] : 0.0;
-        const double sn = valid ? tab[(int64_t)k * B_STRIDE + B_S4] : 0.0;
-        V acc = ssub(ssub(y_[r], smul(e_[r], x1)), smul(f_[r], x2));
-        acc = ssub(acc, smul(xi0, sadd(smul(a_[r], sq), smul(b_[r], sv))));
-        const V x = smul(rd_[r], acc);
+        double qn, sn;
+        q4s4(k, qn, sn);
+        if (!valid) qn = sn = 0.0;
+        V x = sfma(-e_[r], x1, cur[r * 32]);
+        x = sfma(-f_[r], x2, x);
+        x = sfma(-a_[r], sq, x);  // a~, b~ carry xi0
+        x = sfma(-b_[r], sv, x);
         sq = sfma(qn, x2, sq);
         sv = sfma(sn, x2, sv);
         x2 = x1;
@@ -432,66 +457,85 @@ static int resident_ctas(K kernel, size_t smem) {
   return std::max(1, occ);
 }
 
-template <typename V, int R>
-static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  constexpr int RING = 2;
+template <typename V, int R, int SG, int RING>
+static cudaError_t helm_stream_RR(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
+  constexpr int kT = 64 * SG;
   const int n0 = (a.n_dir + 1) / 2;
   const int tab_rows = ((n0 + R - 1) / R) * R;
-  const size_t smem = (size_t)RING * R * kStreamThreads * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
+  const size_t smem = (size_t)RING * R * kT * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = helm_stream_kernel<V, R, RING>;
+  auto kern = helm_stream_kernel<V, R, RING, SG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
   const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
   if (nsys <= 0) return cudaSuccess;
-  const int64_t groups = (nsys + 32 * kSG - 1) / (32 * kSG);
+  const int64_t groups = (nsys + 32 * SG - 1) / (32 * SG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
-  kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
 }
 
-template <typename V, int R, bool SMEM_TAB, int RING>
+template <typename V, int R, int SG>
+static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
+  // deepest ring that fits next to the row table (bytes in flight per SM)
+  const int n0 = (a.n_dir + 1) / 2;
+  const size_t tabb = (size_t)2 * (((n0 + R - 1) / R) * R) * sizeof(double4);
+  if ((size_t)3 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
+    return helm_stream_RR<V, R, SG, 3>(a, scratch, ctas_per_sm, st);
+  return helm_stream_RR<V, R, SG, 2>(a, scratch, ctas_per_sm, st);
+}
+
+template <typename V, int R, bool SMEM_TAB, int RING, int SG>
 static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int ctas_per_sm, size_t smem,
                                      cudaStream_t st) {
-  auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING>;
+  constexpr int kT = 64 * SG;
+  auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING, SG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
   const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
   if (nsys <= 0) return cudaSuccess;
-  const int64_t groups = (nsys + 32 * kSG - 1) / (32 * kSG);
+  const int64_t groups = (nsys + 32 * SG - 1) / (32 * SG);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
-  kern<<<grid, kStreamThreads, smem, st>>>(a, static_cast<V*>(scratch));
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
 }
 
-template <typename V, int R>
+template <typename V, int R, int SG>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency
-  const size_t ring2 = (size_t)2 * R * kStreamThreads * sizeof(V);
-  const size_t tabb = (size_t)a.n_bih * B_STRIDE * sizeof(double);
-  if (ring2 + tabb <= 220 * 1024) return bih_stream_launch<V, R, true, 2>(a, scratch, ctas_per_sm, ring2 + tabb, st);
-  return bih_stream_launch<V, R, false, kRing>(a, scratch, ctas_per_sm, (size_t)kRing * R * kStreamThreads * sizeof(V), st);
+  // (a 3-deep ring measured slower at config 4: 29.5 vs 28.6 ms)
+  const size_t ring2 = (size_t)2 * R * 64 * SG * sizeof(V);
+  const size_t tabb = (size_t)(a.n_bih + 4) * BC_STRIDE * sizeof(double);
+  if (ring2 + tabb <= 220 * 1024) return bih_stream_launch<V, R, true, 2, SG>(a, scratch, ctas_per_sm, ring2 + tabb, st);
+  return bih_stream_launch<V, R, false, kRing, 4>(a, scratch, ctas_per_sm, (size_t)kRing * R * 256 * sizeof(V), st);
 }
 
+// CTA size (one persistent CTA per SM either way -- registers and shared
+// memory): warps_per_sm 8 -> 4 system groups (8 warps), 12 -> 6 (12 warps),
+// 0 -> the measured best at BASELINE config 4: 12 warps for Helmholtz
+// (18.2 vs 19.8 ms), 8 for the biharmonic (28.6 vs 30.2 ms; its 8-warp CTA
+// can afford to prefetch the segment checkpoints into registers).
 template <typename V>
 static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
+  const bool small = (w == 8);
   switch (a.chunk_rows) {
-    case 4: return helm_stream_R<V, 4>(a, sc, w, st);
-    case 8: return helm_stream_R<V, 8>(a, sc, w, st);
-    case 16: return helm_stream_R<V, 16>(a, sc, w, st);
+    case 4: return small ? helm_stream_R<V, 4, 4>(a, sc, 1, st) : helm_stream_R<V, 4, 6>(a, sc, 1, st);
+    case 8: return small ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
+    case 16: return helm_stream_R<V, 16, 4>(a, sc, 1, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <typename V>
 static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, void* sc, int w, cudaStream_t st) {
+  const bool small = (w != 12);
   switch (a.chunk_rows) {
-    case 4: return bih_stream_R<V, 4>(a, sc, w, st);
-    case 8: return bih_stream_R<V, 8>(a, sc, w, st);
-    case 16: return bih_stream_R<V, 16>(a, sc, w, st);
+    case 4: return small ? bih_stream_R<V, 4, 4>(a, sc, 1, st) : bih_stream_R<V, 4, 6>(a, sc, 1, st);
+    case 8: return small ? bih_stream_R<V, 8, 4>(a, sc, 1, st) : bih_stream_R<V, 8, 6>(a, sc, 1, st);
+    case 16: return bih_stream_R<V, 16, 4>(a, sc, 1, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -508,21 +552,21 @@ int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool cplx_rhs)
   return (int64_t)sms * 8 * nseg0 * (op == 0 ? 1 : 2) * kStreamThreads * (cplx_rhs ? 16 : 8);
 }
 
-// warps_per_sm of the C ABI: resident 2-warp CTAs per SM = warps_per_sm / 2 (0 = as many as fit)
+// warps_per_sm of the C ABI: 8 / 12 select the CTA size, 0 the per-operator default
 cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm,
                                cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
   // the bulk-copy ring moves 16-B aligned row pieces: real RHS needs an even batch
   if (!cplx_rhs && ((a.batch & 1) || (reinterpret_cast<uintptr_t>(a.rhs) & 15))) return cudaErrorInvalidValue;
-  const int ctas = warps_per_sm / 2;
-  return cplx_rhs ? helm_stream_dispatch<cplx>(a, scratch, ctas, st) : helm_stream_dispatch<double>(a, scratch, ctas, st);
+  return cplx_rhs ? helm_stream_dispatch<cplx>(a, scratch, warps_per_sm, st)
+                  : helm_stream_dispatch<double>(a, scratch, warps_per_sm, st);
 }
 
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool cplx_rhs, int warps_per_sm, cudaStream_t st) {
   if (a.batch <= 0) return cudaSuccess;
   if (!cplx_rhs && ((a.batch & 1) || (reinterpret_cast<uintptr_t>(a.rhs) & 15))) return cudaErrorInvalidValue;
-  const int ctas = warps_per_sm / 2;
-  return cplx_rhs ? bih_stream_dispatch<cplx>(a, scratch, ctas, st) : bih_stream_dispatch<double>(a, scratch, ctas, st);
+  return cplx_rhs ? bih_stream_dispatch<cplx>(a, scratch, warps_per_sm, st)
+                  : bih_stream_dispatch<double>(a, scratch, warps_per_sm, st);
 }
 
 }  // namespace shen

@@ -63,7 +63,8 @@ STREAM_ROWS_B = _env_int("SHEN_STREAM_ROWS_B", 8)
 
 
 def stream_warps() -> int:
-    """Cap on resident warps per SM of the streaming solve (0 = as many as fit)."""
+    """CTA size of the streaming solve in warps per SM (8 or 12; 0 = the
+    per-operator default measured best at BASELINE config 4)."""
     import os
 
     return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
