@@ -13,8 +13,11 @@ What changes is where and how the work happens:
   wavenumber system and parity) and keeps only *chunk checkpoints* -- the
   factor state entering every chunk of R rows -- instead of the reference's
   4 (Helmholtz) or 7 (biharmonic) full factor vectors per system;
-* ``solve`` is the chunk-parallel fused factor+solve kernel
-  (``csrc/shen_solve_chunk.cu``): RHS read once, solution written once;
+* ``solve`` (default ``method="stream"``) is the streaming fused
+  factor+solve kernel (``csrc/shen_solve_stream.cu``): one thread per
+  (system, parity), coalesced row pieces, the factors recomputed from the
+  checkpoints in both sweeps; ``method="chunked"`` is the chunk-parallel
+  variant (lanes = row chunks, ``csrc/shen_solve_chunk.cu``);
 * the full factors ``low``/``d``/``e``/``tail`` (and ``low2`` ... ``b``) are
   materialised lazily, bit-identical to the reference, only when accessed;
 * ``method="stored"`` keeps full reference-exact factors on the device and
