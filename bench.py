@@ -76,6 +76,22 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_traffic(cfg, method, op, unknowns):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    committed ncu --set full capture (profiles/traffic_c4.json: bytes per
+    unknown measured on a 512-kx-row slab of config 4, scaled to this launch's
+    unknowns -- the kernels stream, so bytes per unknown do not depend on the
+    slab width)."""
+    path = os.path.join(ROOT, "profiles", "traffic_c4.json")
+    if cfg != "c4" or method != "stream" or not os.path.exists(path):
+        return None, None
+    try:
+        t = json.load(open(path))[op]
+        return float(t["bytes_per_unknown"]) * unknowns, f"{t['source']} ({t['bytes_per_unknown']:.1f} B/unknown)"
+    except Exception:
+        return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -218,6 +234,8 @@ def run_b200(args):
     parity = spot_parity(mats, nu, dt, z2, fh, xh, fb, xb) if rank == 0 else None
 
     peak, peak_src = measured_peak()
+    traffic, traffic_src = measured_traffic(args.config, args.method, "biharmonic" if b_ms >= h_ms else "helmholtz",
+                                            (nb if b_ms >= h_ms else nh) * B)
     bytes_h = 32.0 * nh * B  # per launch on this rank
     bytes_b = 32.0 * nb * B
     ach_h = bytes_h / (h_ms / 1e3) / 1e9
@@ -259,7 +277,7 @@ def run_b200(args):
                                "frac": ach_b / peak, "ckpt_read_bytes": ckpt_bytes_b},
             },
             "roofline": {"bound": "hbm", "kernel": f"{dom} {args.method} solve", "achieved": ach, "peak": peak,
-                         "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
                          "algorithmic_bytes": "32 B per complex unknown (16 B RHS read + 16 B solution write)"},
             "build_ms": build_ms,
