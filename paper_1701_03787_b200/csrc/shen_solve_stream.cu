@@ -13,15 +13,16 @@
 //             recomputed from the build's checkpoint into registers, then the
 //             reference back-substitution turns y into x.
 //
-// Where y lives between the sweeps decides the HBM traffic.  A CTA is two
-// warps (parity 0 and parity 1 of the same 32 systems) and there is ONE
-// persistent CTA per SM, so only 64 systems-parities per SM are in flight:
-// the last `tail` rows of every y stay in shared memory (they are the first
-// ones the backward sweep needs) and the rest is staged in the output array
-// with an L2 evict-last policy -- at BASELINE config 4 that is ~58 MB over the
-// whole chip, inside the 126 MB L2, so the y round trip costs L2 bandwidth,
-// not HBM.  Latency is hidden by cp.async prefetch of the next segment (RHS
-// rows in the forward, staged y in the backward) instead of by occupancy.
+// Where y lives between the sweeps decides the HBM traffic.  Keeping it
+// (in L2 or HBM) needs one y round trip per unknown; at the concurrency
+// needed to hide the recurrences' latency (8-12 warps per SM) the y of the
+// systems in flight does not fit L2, so the backward sweep instead re-reads
+// the RHS segment and recomputes y from a per-segment y checkpoint (per-CTA
+// scratch).  Traffic per unknown: 2 RHS reads + 1 solution write + the
+// factor checkpoints (3 doubles per 8 rows for Helmholtz, 10 for the
+// biharmonic) -- DESIGN.md section 4.2 has the measured numbers.  Latency is
+// hidden by a per-thread cp.async ring that prefetches segments continuously
+// across both sweeps and across system groups.
 #include <algorithm>
 #include <cstdlib>
 
