@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--kx-rows", type=int, default=0, help="limit the kx rows per rank (debug)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--method", default="stream", choices=["stream", "chunked", "stored"])
+    ap.add_argument("--method", default="stream", choices=["stream", "chunked", "stored", "tile"])
     return ap.parse_args()
 
 

@@ -95,6 +95,14 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
                            int64_t j_begin, int64_t j_end, void* stream);
+/* Tiled chunk-parallel solve: a CTA holds 4 consecutive systems (all rows)
+ * in shared memory, warps = (system, parity), lanes = 32 chunks of
+ * chunk_rows rows; the RHS is read once.  Same inputs as
+ * shen_helm_solve_chunked (ckpt from shen_helm_factor with the same
+ * chunk_rows, exact == 0); chunk_rows <= 16. */
+int shen_helm_solve_tile(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
+                         const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                         int is_complex, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 

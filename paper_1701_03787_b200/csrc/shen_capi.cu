@@ -120,6 +120,19 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                     "shen_helm_solve_stream");
 }
 
+int shen_helm_solve_tile(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
+                         const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                         int is_complex, void* stream) {
+  if (batch == 0) return SHEN_OK;
+  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out || chunk_rows <= 0 || chunk_rows > 16 ||
+      32 * chunk_rows < (n_dir + 1) / 2 || (!ckpt && (n_dir + 1) / 2 > chunk_rows))
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_tile: bad args (needs 32 * chunk_rows >= rows of parity 0, chunk_rows <= 16)");
+  shen::HelmChunkArgs a{};
+  a.n_dir = n_dir; a.ca = ca; a.cb = cb; a.batch = batch; a.sd = sd; a.st = st; a.md = md;
+  a.chunk_rows = chunk_rows; a.ckpt = ckpt; a.rhs = rhs; a.out = out;
+  return cuda_check(shen::launch_helm_tile(a, is_complex != 0, S(stream)), "shen_helm_solve_tile");
+}
+
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream) {
   if (batch == 0) return SHEN_OK;

@@ -114,6 +114,9 @@ cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex
                               cudaStream_t st);
 int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
 
+// tiled chunk-parallel Helmholtz solve (shen_solve_tile.cu); ckpt made with chunk_rows = R, 32 R >= rows_p0
+cudaError_t launch_helm_tile(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
+
 // transforms (shen_transform.cu)
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,

@@ -54,7 +54,7 @@ __all__ = [
 
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
-_METHODS = ("chunked", "stream", "stored")
+_METHODS = ("chunked", "stream", "stored", "tile")
 def _env_int(name, default):
     import os
 
@@ -344,6 +344,12 @@ class HelmholtzLU:
                                            md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
                                            out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), j0, j1, sh),
                   "shen_helm_solve_stream")
+        elif self.method == "tile":
+            sd, st, md = self._tab
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            check(h.shen_helm_solve_tile(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
+                                         md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(), out_dev.data_ptr(),
+                                         int(is_complex), sh), "shen_helm_solve_tile")
         else:
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -360,6 +366,8 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
     ``method="stream"`` (default): checkpoints every 8 rows for the streaming
     fused solve (one thread per system, coalesced rows).
     ``method="chunked"``: checkpoints for the warp-per-system chunked solve.
+    ``method="tile"``: the same checkpoints for the tiled chunk-parallel
+    solve (RHS read once; rows of parity 0 <= 512, else the stream solve).
     ``method="stored"``: full reference-exact factors kept on the device.
     Raises ``ZeroPivotError`` exactly like the reference."""
     import torch
@@ -376,14 +384,16 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
     tabs = tuple(torch.from_numpy(t).to(dev) for t in _helm_tables(mats))
     cb_dev = torch.from_numpy(np.ascontiguousarray(cb_flat)).to(dev)
     B = cb_flat.size
-    R = chunk_rows_for(nd) if method == "chunked" else STREAM_ROWS_H
+    if method == "tile" and chunk_rows_for(nd) > 16:
+        method = "stream"  # the tile kernel keeps at most 32 x 16 rows per parity in a warp
+    R = chunk_rows_for(nd) if method in ("chunked", "tile") else STREAM_ROWS_H
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method in ("chunked", "stream"):
+    if method in ("chunked", "stream", "tile"):
         C = _n_chunks(nd, R)
         ckpt = torch.empty((C, 2, 3, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_helm_factor(nd, float(ca), cb_dev.data_ptr(), B, tabs[0].data_ptr(), tabs[1].data_ptr(),
@@ -575,6 +585,8 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
     x1d = torch.from_numpy(x1).to(dev)
     x2d = torch.from_numpy(x2).to(dev)
     B = x1.size
+    if method == "tile":
+        method = "stream"  # no tiled biharmonic variant (its chunk state does not fit a tile CTA)
     R = chunk_rows_for(nb) if method == "chunked" else STREAM_ROWS_B
     h = lib()
     sh = dv.stream_handle()

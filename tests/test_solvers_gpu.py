@@ -65,7 +65,7 @@ def test_stored_solve_bitwise_vs_reference(golden, golden_meta, case):
 
 
 @pytest.mark.parametrize("case", range(8))
-@pytest.mark.parametrize("method", ["chunked", "stream"])
+@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
 def test_fused_solve_parity(golden, golden_meta, case, method):
     g = golden("solvers.npz")
     meta = golden_meta["solver_cases"][case]
@@ -203,7 +203,7 @@ def _corner_systems(n_y, n_z):
 
 
 @pytest.mark.parametrize("op", ["h", "b"])
-@pytest.mark.parametrize("method", ["chunked", "stream"])
+@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
 def test_config4_corners_residual(op, method):
     """BASELINE config 4 parameters (n_x = 1024, nu = 1/2000, dt = 1e-4) on
     32 systems including the largest z^2 of the 2048 x 1025 plane."""
@@ -230,7 +230,7 @@ def test_config4_corners_residual(op, method):
 
 
 @pytest.mark.parametrize("N", [129, 257, 513, 1025, 2049])
-@pytest.mark.parametrize("method", ["chunked", "stream"])
+@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
 def test_config5_sizes(N, method):
     """BASELINE config 5 wall-normal sweep, 24 systems of the 512 x 257 plane."""
     mats = assemble(N - 1, 0)
