@@ -78,7 +78,9 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
  *   bytes) and recomputed in the backward sweep; warps_per_sm selects the
  *   persistent CTA size (8 or 12 warps per SM; 0 = the per-operator default,
- *   12 for Helmholtz, 8 for the biharmonic).  [j_begin, j_end) restricts
+ *   12 for Helmholtz, 8 for the biharmonic); max_ctas > 0 caps the persistent
+ *   grid (one CTA per SM) so that a second solve can run concurrently on the
+ *   remaining SMs (0 = all SMs).  [j_begin, j_end) restricts
  *   the solve to a range of systems (j_end < 0: the whole batch) -- the row
  *   pitch stays `batch`, so host<->device copies of column slabs can be
  *   pipelined against the solve (see shen_memcpy2d_async).
@@ -94,7 +96,7 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
-                           int64_t j_begin, int64_t j_end, void* stream);
+                           int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
 /* Tiled chunk-parallel solve: a CTA holds 4 consecutive systems (all rows)
  * in shared memory, warps = (system, parity), lanes = 32 chunks of
  * chunk_rows rows; the RHS is read once.  Same inputs as
@@ -128,8 +130,8 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
                            int is_complex, void* stream);
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          void* scratch, int is_complex, int warps_per_sm, int64_t j_begin, int64_t j_end,
-                          void* stream);
+                          void* scratch, int is_complex, int warps_per_sm, int max_ctas, int64_t j_begin,
+                          int64_t j_end, void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

@@ -40,7 +40,7 @@ _SIGS = {
                                                ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_helm_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                               ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
-                                              _c_int64, _c_int64, _vp]),
+                                              ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_helm_solve_tile": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                             ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
@@ -50,7 +50,7 @@ _SIGS = {
                                               ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
                                              ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
-                                             _c_int64, _c_int64, _vp]),
+                                             ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),

@@ -103,8 +103,8 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
-                           void* out, void* scratch, int is_complex, int warps_per_sm, int64_t j_begin,
-                           int64_t j_end, void* stream) {
+                           void* out, void* scratch, int is_complex, int warps_per_sm, int max_ctas,
+                           int64_t j_begin, int64_t j_end, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: bad args");
@@ -115,7 +115,8 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: scratch required");
   if (j_end < 0) j_end = batch;
   if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: range");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end};
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: max_ctas");
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end, max_ctas};
   return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
                     "shen_helm_solve_stream");
 }
@@ -182,8 +183,8 @@ int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const doubl
 
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          void* scratch, int is_complex, int warps_per_sm, int64_t j_begin, int64_t j_end,
-                          void* stream) {
+                          void* scratch, int is_complex, int warps_per_sm, int max_ctas, int64_t j_begin,
+                          int64_t j_end, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: bad args");
@@ -194,7 +195,8 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: scratch required");
   if (j_end < 0) j_end = batch;
   if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: range");
-  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, j_begin, j_end};
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: max_ctas");
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, j_begin, j_end, max_ctas};
   return cuda_check(shen::launch_bih_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
                     "shen_bih_solve_stream");
 }

@@ -85,6 +85,7 @@ struct HelmChunkArgs {
   const void* rhs;
   void* out;
   int64_t jb = 0, je = -1;  // system range [jb, je) of the streaming solve (je < 0: whole batch)
+  int max_ctas = 0;          // streaming solve: cap on persistent CTAs (0: one per SM)
 };
 
 struct BihChunkArgs {
@@ -99,6 +100,7 @@ struct BihChunkArgs {
   const void* rhs;
   void* out;
   int64_t jb = 0, je = -1;
+  int max_ctas = 0;
 };
 
 cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);

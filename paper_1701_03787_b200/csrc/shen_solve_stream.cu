@@ -25,6 +25,7 @@
 // across both sweeps and across system groups.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
@@ -89,12 +90,18 @@ struct SegRef {
   int64_t g;
   int s;
 };
-__device__ __forceinline__ SegRef seg_of(int64_t q, int nseg, int64_t g0, int64_t gstride) {
-  const int64_t per = 2 * (int64_t)nseg;
-  const int64_t gi = q / per;
-  const int k = (int)(q - gi * per);
-  return {g0 + gi * gstride, k < nseg ? k : 2 * nseg - 1 - k};
-}
+// issue-side cursor over that sequence (no 64-bit division per segment)
+struct SegIt {
+  int64_t g;
+  int k;  // position within the group's 2 nseg segments
+  __device__ __forceinline__ SegRef ref(int nseg) const { return {g, k < nseg ? k : 2 * nseg - 1 - k}; }
+  __device__ __forceinline__ void next(int nseg, int64_t gstride) {
+    if (++k == 2 * nseg) {
+      k = 0;
+      g += gstride;
+    }
+  }
+};
 
 
 template <typename V, int R, int SG>
@@ -155,14 +162,17 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
+  SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
+    it.next(nseg, gstride);
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
+    it.next(nseg, gstride);
     ++qi;
     cpa_wait<RING - 1>();
     const V* p = ring + (qc % RING) * R * 32;
@@ -312,14 +322,17 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
+  SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
+    it.next(nseg, gstride);
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, seg_of(qi, nseg, g0, gstride), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
+    it.next(nseg, gstride);
     ++qi;
     cpa_wait<RING - 1>();
     V* p = ring + (qc % RING) * R * 32;
@@ -335,16 +348,21 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     V* outj = out + (int64_t)par * B + j;
     V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 2 * kT + tid;
     const double* ckj = a.ckpt + (int64_t)par * 10 * B + jc;
+    // Segments are processed by generic lambdas instantiated twice: FULL
+    // segments (all R rows valid -- every segment but possibly the last) run
+    // without row masks or row-index clamps; the last one is masked.
+    using Full = std::integral_constant<bool, true>;
+    using Part = std::integral_constant<bool, false>;
     // ---------------- forward
     BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
     V y1 = szero<V>(), y2 = szero<V>();
-    for (int s = 0; s < nseg; ++s) {
+    auto fwd_seg = [&](int s, auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
       const V* cur = consume();
-      const bool full = (s + 1) * R <= n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int k = min(par + 2 * i, nb - 1);
+        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
         const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
@@ -353,11 +371,15 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         bih_step_fast(u, u1, u2, hb, c, l2, l4);
         u2 = u1;
         u1 = u;
-        const V b = (full || i < n) ? cur[r * 32] : szero<V>();
+        const V b = (FULL || i < n) ? cur[r * 32] : szero<V>();
         const V y = sfma(-l4, y2, sfma(-l2, y1, b));
         y2 = y1;
         y1 = y;
       }
+    };
+    const int nfull = n / R;  // segments with all R rows valid
+    for (int s = 0; s < nseg; ++s) {
+      if (s < nfull) fwd_seg(s, Full{}); else fwd_seg(s, Part{});
       if (s + 1 < nseg) {
         ychkj[(2 * s) * kT] = y1;
         ychkj[(2 * s + 1) * kT] = y2;
@@ -378,8 +400,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       cya = ychkj[(2 * (s - 1)) * kT];
       cyb = ychkj[(2 * (s - 1) + 1) * kT];
     };
-    if (PF && nseg - 1 > 0) load_ck(nseg - 1);
-    for (int s = nseg - 1; s >= 0; --s) {
+    auto bwd_seg = [&](int s, auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>();
       if (s > 0) {  // factor state and y entering the segment
@@ -393,14 +415,13 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       }
       if (PF && s - 1 > 0) load_ck(s - 1);
       V* cur = consume();
-      const bool full = (s + 1) * R <= n;
       // U-row entries pre-multiplied by 1/d (rows past n get 0, so x = 0 there):
       // x_i = y~_i - e~_i x_{i+1} - f~_i x_{i+2} - a~_i S_q - b~_i S_s
       double e_[R], f_[R], a_[R], b_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int k = min(par + 2 * i, nb - 1);
+        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
         const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
@@ -409,7 +430,7 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         bih_step_fast(w, w1, w2, hb, c, l2, l4);
         w2 = w1;
         w1 = w;
-        const bool valid = full || i < n;
+        const bool valid = FULL || i < n;
         const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32] : szero<V>()));
         yb = ya;
         ya = y;
@@ -420,11 +441,12 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         a_[r] = rd * w.a;
         b_[r] = rd * w.b;
       }
+      V* op = outj + (int64_t)2 * (s * R) * B;
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
         const int i = s * R + r;
-        const int k = min(par + 2 * i, nb - 1);
-        const bool valid = full || i < n;
+        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
+        const bool valid = FULL || i < n;
         double qn, sn;
         q4s4(k, qn, sn);
         if (!valid) qn = sn = 0.0;
@@ -436,8 +458,12 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         sv = sfma(sn, x2, sv);
         x2 = x1;
         x1 = x;
-        if (jv && valid) O::st_cs(outj + (int64_t)2 * i * B, x);
+        if (jv && valid) O::st_cs(op + (int64_t)2 * r * B, x);
       }
+    };
+    if (PF && nseg - 1 > 0) load_ck(nseg - 1);
+    for (int s = nseg - 1; s >= 0; --s) {
+      if (s < nfull) bwd_seg(s, Full{}); else bwd_seg(s, Part{});
     }
   }
   cpa_wait<0>();
@@ -472,7 +498,9 @@ static cudaError_t helm_stream_RR(const HelmChunkArgs& a, void* scratch, int cta
   const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
   if (nsys <= 0) return cudaSuccess;
   const int64_t groups = (nsys + 32 * SG - 1) / (32 * SG);
-  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
+  int64_t cap = stream_ctas(occ);
+  if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
   kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
 }
@@ -498,7 +526,9 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
   const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
   if (nsys <= 0) return cudaSuccess;
   const int64_t groups = (nsys + 32 * SG - 1) / (32 * SG);
-  const unsigned grid = (unsigned)std::min<int64_t>(groups, stream_ctas(occ));
+  int64_t cap = stream_ctas(occ);
+  if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
   kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
 }

@@ -321,7 +321,7 @@ class HelmholtzLU:
         buffers the copies overlap the solve slab by slab."""
         return _solve_api(self, rhs, out)
 
-    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1):
+    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1, max_ctas=0):
         """Device-to-device solve on (n_modes, batch) contiguous tensors
         (systems [j0, j1) only with the stream method)."""
         nd, B = self.n_modes, self.batch
@@ -342,7 +342,8 @@ class HelmholtzLU:
             scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
             check(h.shen_helm_solve_stream(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
                                            md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), j0, j1, sh),
+                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), max_ctas,
+                                           j0, j1, sh),
                   "shen_helm_solve_stream")
         elif self.method == "tile":
             sd, st, md = self._tab
@@ -532,7 +533,7 @@ class BiharmonicLU:
         """Solve H x = rhs (reference solvers.py:162-170); see HelmholtzLU.solve."""
         return _solve_api(self, rhs, out)
 
-    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1):
+    def solve_into(self, rhs_dev, out_dev, is_complex, j0=0, j1=-1, max_ctas=0):
         nb, B = self.n_modes, self.batch
         if B == 0:
             return out_dev
@@ -556,7 +557,8 @@ class BiharmonicLU:
             scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
             check(h.shen_bih_solve_stream(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
                                           self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                          out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), j0, j1, sh),
+                                          out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), max_ctas,
+                                          j0, j1, sh),
                   "shen_bih_solve_stream")
         else:
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
