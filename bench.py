@@ -483,7 +483,14 @@ def cpu_c3():
 
 # ======================================================================= reference arm
 
+_REF_CACHE = {}
+
+
 def _ref_worker(task):
+    """One pool task: the oracle port's solve of a 2-kx-row slab.  LU objects
+    and right-hand sides are built on first use and cached in the
+    (persistent) worker process, so the timed steps contain only the solves
+    -- the same split as the B200 arm (LU built once before timing)."""
     import os as _os
 
     _os.environ["OMP_NUM_THREADS"] = "1"
@@ -492,18 +499,23 @@ def _ref_worker(task):
     from paper_1701_03787_b200.mesh import channel_z2
 
     cfg, lo, hi, seed = task
-    name, n_x, n_y, n_z, nu, dt = workload(cfg)
-    mats = assemble(n_x, 0)
-    z2 = np.ascontiguousarray(channel_z2(n_y, n_z)[lo:hi])
-    rng = np.random.default_rng(seed)
-    fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
-    fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
-    hf = O.helmholtz_factor(mats, nu, dt, z2)
-    bf = O.biharmonic_factor(mats, nu, dt, z2)
+    # tasks are equal-sized slabs; a worker keeps the first slab it was given
+    # (pool scheduling does not pin tasks to workers) and solves it every step
+    key = cfg
+    if key not in _REF_CACHE:
+        name, n_x, n_y, n_z, nu, dt = workload(cfg)
+        mats = assemble(n_x, 0)
+        z2 = np.ascontiguousarray(channel_z2(n_y, n_z)[lo:hi])
+        rng = np.random.default_rng(seed)
+        fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)
+        fb = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
+        _REF_CACHE[key] = (O.helmholtz_factor(mats, nu, dt, z2), O.biharmonic_factor(mats, nu, dt, z2), fh, fb,
+                           (mats.n_dir + mats.n_bih) * z2.size)
+    hf, bf, fh, fb, unk = _REF_CACHE[key]
     t0 = time.perf_counter()
     O.helmholtz_solve(hf, fh)
     O.biharmonic_solve(bf, fb)
-    return (mats.n_dir + mats.n_bih) * z2.size, time.perf_counter() - t0
+    return unk, time.perf_counter() - t0
 
 
 def run_reference(args):
@@ -520,11 +532,11 @@ def run_reference(args):
     with ctx.Pool(cores) as pool:
         tasks = [(args.config, (r * rows_per_task) % n_y, (r * rows_per_task) % n_y + rows_per_task, r)
                  for r in range(cores)]
-        for _ in range(max(args.warmup, 0)):
-            pool.map(_ref_worker, tasks)
+        for _ in range(max(args.warmup, 1)):  # first pass builds and caches each worker's LU + RHS
+            pool.map(_ref_worker, tasks, chunksize=1)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            results.extend(pool.map(_ref_worker, tasks))
+            results.extend(pool.map(_ref_worker, tasks, chunksize=1))
         wall = time.perf_counter() - t0
     unk = sum(r[0] for r in results)
     value = unk / wall

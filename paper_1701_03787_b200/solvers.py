@@ -99,6 +99,7 @@ def _solve_api(lu, rhs, out):
 
 
 _PIPE_MIN_SLAB = 4096
+_PIPE_MAX_SLABS = _env_int("SHEN_PIPE_SLABS", 16)  # fewer slabs = longer first-copy-in / last-copy-out bubbles
 
 
 def _host_pipeline(lu, h_rhs, h_out, cplx):
@@ -123,7 +124,7 @@ def _host_pipeline(lu, h_rhs, h_out, cplx):
     if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
         bounds = [(0, B)]
     else:
-        nslab = min(8, B // _PIPE_MIN_SLAB)
+        nslab = min(_PIPE_MAX_SLABS, B // _PIPE_MIN_SLAB)
         step = -(-B // nslab)
         step = -(-step // 128) * 128
         bounds = [(a, min(a + step, B)) for a in range(0, B, step)]
