@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(256) bih_factor_kernel(BihFactorArgs a) {
       const BihBands h = bih_bands(a.xi0, xi1, xi2, c);
       bih_step<true>(u, u1, u2, h, c, a.xi0, i, l2, l4);
     } else {
-      const BihBands h = bih_bands_fast(a.xi0, xi1, xi2, c);
-      bih_fast_scale_tail(c, a.xi0);
+      bih_fast_prescale(c, a.xi0);
+      const BihBands h = bih_bands_fast(xi1, xi2, c);
       bih_step_fast(u, u1, u2, h, c, l2, l4);
     }
     note_pivot(a.pivot, par, i, u.d);

@@ -296,23 +296,27 @@ __device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2
 }
 
 // ---- fast mode (build checkpoints, chunked and streaming solves) ----------
-// Own arithmetic, shared bit for bit by every fast-mode kernel: bands with
-// FMAs, and the tail factors carried pre-scaled by xi0 (a~ = xi0 a,
-// b~ = xi0 b), which removes the xi0 products from every row.  Callers
-// replace c[B_P], c[B_R] by xi0 * p_k, xi0 * r_k (bih_fast_scale_tail) before
-// bih_step_fast; checkpoints therefore hold a~, b~.
-__device__ __forceinline__ BihBands bih_bands_fast(double xi0, double xi1, double xi2, const double* c) {
+// Own arithmetic, shared bit for bit by every fast-mode kernel: the row
+// constants that multiply xi0 (Q0, T2, T4 of the bands, p_k and r_k of the
+// tail) are pre-scaled by xi0 (bih_fast_prescale), the bands are formed with
+// FMAs, and the tail factors are carried pre-scaled by xi0 (a~ = xi0 a,
+// b~ = xi0 b), which removes every xi0 product from the rows.  Checkpoints
+// therefore hold a~, b~.
+__device__ __forceinline__ void bih_fast_prescale(double* c, double xi0) {
+  c[B_Q0] = __dmul_rn(xi0, c[B_Q0]);
+  c[B_T2] = __dmul_rn(xi0, c[B_T2]);
+  c[B_T4] = __dmul_rn(xi0, c[B_T4]);
+  c[B_P] = __dmul_rn(xi0, c[B_P]);
+  c[B_R] = __dmul_rn(xi0, c[B_R]);
+}
+__device__ __forceinline__ BihBands bih_bands_fast(double xi1, double xi2, const double* c) {
   BihBands b;
-  b.hd = __fma_rn(xi0, c[B_Q0], __fma_rn(xi1, c[B_AR0], __dmul_rn(xi2, c[B_BB0])));
-  b.hp2 = __fma_rn(xi0, c[B_T2], __fma_rn(xi1, c[B_AR2], __dmul_rn(xi2, c[B_BB2])));
-  b.hp4 = __fma_rn(xi0, c[B_T4], __dmul_rn(xi2, c[B_BB4]));
+  b.hd = __fma_rn(xi1, c[B_AR0], __fma_rn(xi2, c[B_BB0], c[B_Q0]));
+  b.hp2 = __fma_rn(xi1, c[B_AR2], __fma_rn(xi2, c[B_BB2], c[B_T2]));
+  b.hp4 = __fma_rn(xi2, c[B_BB4], c[B_T4]);
   b.hm2 = __fma_rn(xi1, c[B_ARM2], __dmul_rn(xi2, c[B_BB2M]));
   b.hm4 = __dmul_rn(xi2, c[B_BB4M]);
   return b;
-}
-__device__ __forceinline__ void bih_fast_scale_tail(double* c, double xi0) {
-  c[B_P] = __dmul_rn(xi0, c[B_P]);
-  c[B_R] = __dmul_rn(xi0, c[B_R]);
 }
 
 // Branch-free fast-mode biharmonic step.  Rows "before row 0" are zero

@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
       const int k = min(par + 2 * (s0 + r), a.n_bih - 1);
       double c[B_NCOL];
       load_bih_row(a.tab, k, c);
-      const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
-      bih_fast_scale_tail(c, xi0);
+      bih_fast_prescale(c, xi0);
+      const BihBands hb = bih_bands_fast(xi1, xi2, c);
       double l2, l4;
       bih_step_fast(u, u1, u2, hb, c, l2, l4);
       u2 = u1;

@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       double v = 0.0;
       if (kk >= 0 && col < BC_NCOL) {
         v = __ldg(a.tab + (int64_t)kk * B_STRIDE + bc_src(col));
-        if (col == BC_P || col == BC_R) v = __dmul_rn(a.xi0, v);  // == bih_fast_scale_tail
+        if (col == BC_P || col == BC_R || col == BC_Q0 || col == BC_T2 || col == BC_T4)
+          v = __dmul_rn(a.xi0, v);  // == bih_fast_prescale
       }
       else if (kk >= -2 && (col == BC_Q4 || col == BC_S4))
         v = __ldg(a.tab + (int64_t)(kk + 2) * B_STRIDE + (col == BC_Q4 ? B_Q2 : B_S2));
@@ -365,8 +366,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
-        const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
-        if (!SMEM_TAB) bih_fast_scale_tail(c, xi0);  // the compact table holds xi0 p, xi0 r
+        if (!SMEM_TAB) bih_fast_prescale(c, xi0);  // the compact table is pre-scaled
+        const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
         bih_step_fast(u, u1, u2, hb, c, l2, l4);
         u2 = u1;
@@ -424,8 +425,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
         row_consts(k, c);
-        const BihBands hb = bih_bands_fast(xi0, xi1, xi2, c);
-        if (!SMEM_TAB) bih_fast_scale_tail(c, xi0);
+        if (!SMEM_TAB) bih_fast_prescale(c, xi0);
+        const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
         bih_step_fast(w, w1, w2, hb, c, l2, l4);
         w2 = w1;
