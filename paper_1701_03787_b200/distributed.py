@@ -1,0 +1,124 @@
+"""Slab-decomposed 3-D Shen transforms over several GPUs.
+
+The solves need no communication (kx slabs, ``shard.py``).  A 3-D transform
+does: the periodic FFTs want whole (y, z) planes, the wall-normal stage wants
+whole x columns.  The paper's slab decomposition (one all-to-all per
+transform) is used:
+
+forward   physical x-planes [p0, p1) of rank r  --rfft2 over (y, z)-->
+          (planes_r, n_y, n_z/2+1)  --all-to-all-->  (N, kx slab_r, n_z/2+1)
+          --wall-normal stage (transforms.wall_forward)-->
+          (n_modes, kx slab_r, n_z/2+1): exactly the rank's solver slab.
+inverse   the mirror image.
+
+With NCCL the exchange is ``all_to_all_single`` over NVLink on device
+tensors; the same code runs on CPU tensors under ``gloo`` (exchange tests).
+Plane split: balanced contiguous (sizes differ by at most one), the kx split
+is ``shard.kx_slab``.
+"""
+
+from __future__ import annotations
+
+from .shard import kx_slab
+
+__all__ = ["plane_slab", "planes_to_kx", "kx_to_planes", "forward_transform_slab", "inverse_transform_slab"]
+
+
+def plane_slab(n_planes: int, rank: int, world: int) -> tuple:
+    """[lo, hi) physical x-planes of `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    return (n_planes * rank) // world, (n_planes * (rank + 1)) // world
+
+
+def _world(group):
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def planes_to_kx(x, n_planes: int, group=None):
+    """(planes_r, n_y, K) on rank r -> (n_planes, kx slab_r, K): all-to-all of
+    the rank's planes to the kx slabs of every rank."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world(group)
+    p, n_y, K = x.shape
+    if world == 1:
+        return x.contiguous()
+    lo_p, hi_p = plane_slab(n_planes, rank, world)
+    if hi_p - lo_p != p:
+        raise ValueError(f"rank {rank} holds {p} planes, expected {hi_p - lo_p}")
+    blocks = []
+    send_sizes = []
+    for q in range(world):
+        a, b = kx_slab(n_y, q, world)
+        blocks.append(x[:, a:b, :].reshape(-1))
+        send_sizes.append(p * (b - a) * K)
+    send = torch.cat(blocks)
+    a, b = kx_slab(n_y, rank, world)
+    recv_sizes = [(plane_slab(n_planes, q, world)[1] - plane_slab(n_planes, q, world)[0]) * (b - a) * K
+                  for q in range(world)]
+    recv = torch.empty(sum(recv_sizes), dtype=x.dtype, device=x.device)
+    dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+    # blocks arrive in rank order = plane order: already (n_planes, slab, K)
+    return recv.view(n_planes, b - a, K)
+
+
+def kx_to_planes(y, n_y: int, group=None):
+    """(n_planes, kx slab_r, K) -> (planes_r, n_y, K): inverse of planes_to_kx."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world(group)
+    n_planes, m, K = y.shape
+    if world == 1:
+        return y.contiguous()
+    y = y.contiguous()
+    send_sizes = []
+    for q in range(world):
+        lo, hi = plane_slab(n_planes, q, world)
+        send_sizes.append((hi - lo) * m * K)  # axis-0 ranges are contiguous chunks
+    lo_p, hi_p = plane_slab(n_planes, rank, world)
+    p = hi_p - lo_p
+    widths = [kx_slab(n_y, q, world)[1] - kx_slab(n_y, q, world)[0] for q in range(world)]
+    recv_sizes = [p * w * K for w in widths]
+    recv = torch.empty(sum(recv_sizes), dtype=y.dtype, device=y.device)
+    dist.all_to_all_single(recv, y.view(-1), recv_sizes, send_sizes, group=group)
+    parts = torch.split(recv, recv_sizes)
+    return torch.cat([part.view(p, w, K) for part, w in zip(parts, widths)], dim=1)
+
+
+def forward_transform_slab(u_planes, mesh, space, group=None, solve_mass: bool = True):
+    """Rank's physical planes (planes_r, n_y, n_z) (torch CUDA, float64) ->
+    rank's kx slab of the coefficients (n_modes, slab_r, n_z/2+1), complex128.
+    ``solve_mass=False`` stops at the scalar products (forward_scalar_product)."""
+    import torch
+
+    from .mesh import family_code, space_code
+    from .transforms import wall_forward
+
+    N = mesh.n_x + 1
+    fourier = torch.fft.rfft2(u_planes.to(torch.float64), dim=(1, 2)).contiguous()
+    cols = planes_to_kx(fourier, N, group)
+    m, K = cols.shape[1], cols.shape[2]
+    out = wall_forward(cols.reshape(N, m * K), mesh.n_x, family_code(mesh.family), space_code(space), solve_mass)
+    return out.reshape(out.shape[0], m, K)
+
+
+def inverse_transform_slab(c_slab, mesh, space, group=None):
+    """Rank's kx slab of coefficients (n_modes, slab_r, n_z/2+1) -> the rank's
+    physical planes (planes_r, n_y, n_z), float64."""
+    import torch
+
+    from .mesh import family_code, space_code
+    from .transforms import wall_inverse
+
+    n, m, K = c_slab.shape
+    lines, norm = wall_inverse(c_slab.to(torch.complex128).reshape(n, m * K).contiguous(), mesh.n_x,
+                               family_code(mesh.family), space_code(space), mesh.n_y * mesh.n_z)
+    planes = kx_to_planes(lines.reshape(mesh.n_x + 1, m, K), mesh.n_y, group)
+    return torch.fft.irfft2(planes, s=(mesh.n_y, mesh.n_z), dim=(1, 2), norm=norm)

@@ -55,6 +55,8 @@ __all__ = [
     "forward_transform",
     "forward_scalar_product",
     "inverse_transform",
+    "wall_forward",
+    "wall_inverse",
 ]
 
 _RAW = 3  # fwd_post "space" code for the plain chebyshev_scalar products
@@ -446,6 +448,30 @@ def _apply_operator(M, lines):
     return torch.view_as_complex(out.view(M.shape[0], L, 2))
 
 
+# ---------------------------------------------------------------- wall-normal stage on lines
+
+def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
+    """(N, L) complex128 Fourier lines on the device -> (n_modes, L) Shen
+    coefficients (scalar products if ``solve_mass`` is False)."""
+    if XFORM_METHOD == "matrix":
+        kind = "fwd" if solve_mass else "fsp"
+        return _apply_operator(_operator_dev(kind, n_x, fam, sp, device().index), lines)
+    scal = _chebyshev_pass(lines, fam, sp)
+    if solve_mass and sp != 0:
+        scal = _mass_pass(scal, sp, n_x, fam)
+    return scal
+
+
+def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
+    """(n, L) coefficients -> (N, L) values on the Chebyshev points, and the
+    ``norm`` for the following ``irfft2`` (the matrix route folds the
+    1/(n_y n_z) of the inverse FFT into its operator)."""
+    if XFORM_METHOD == "matrix":
+        op = _operator_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)
+        return _apply_operator(op, coef), "forward"
+    return _expand_pass(coef, sp, n_x, fam), "backward"
+
+
 # ---------------------------------------------------------------- 3-D transforms
 
 def _physical_to_device(field: PhysicalField):
@@ -472,13 +498,7 @@ def _forward(field: PhysicalField, space, solve_mass: bool):
     N = fourier.shape[0]
     yz = tuple(fourier.shape[1:])
     lines = fourier.view(N, -1)
-    if XFORM_METHOD == "matrix":
-        kind = "fwd" if solve_mass else "fsp"
-        scal = _apply_operator(_operator_dev(kind, mesh.n_x, fam, sp, device().index), lines)
-    else:
-        scal = _chebyshev_pass(lines, fam, sp)
-        if solve_mass and sp != 0:
-            scal = _mass_pass(scal, sp, mesh.n_x, fam)
+    scal = wall_forward(lines, mesh.n_x, fam, sp, solve_mass)
     del fourier, lines
     data = scal.reshape((scal.shape[0],) + yz)
     if from_numpy:
@@ -515,13 +535,7 @@ def inverse_transform(coeffs: SpectralField) -> PhysicalField:
     n = t.shape[0]
     yz = tuple(t.shape[1:])
     _check_expand_rows(n, sp, mesh.n_x)
-    if XFORM_METHOD == "matrix":
-        op = _operator_dev("inv", mesh.n_x, fam, sp, device().index, 1.0 / (mesh.n_y * mesh.n_z))
-        lines = _apply_operator(op, t.reshape(n, -1))
-        norm = "forward"  # 1/(n_y n_z) already folded into the operator
-    else:
-        lines = _expand_pass(t.reshape(n, -1), sp, mesh.n_x, fam)
-        norm = "backward"
+    lines, norm = wall_inverse(t.reshape(n, -1), mesh.n_x, fam, sp, mesh.n_y * mesh.n_z)
     del t
     data = torch.fft.irfft2(lines.reshape((mesh.n_x + 1,) + yz), s=(mesh.n_y, mesh.n_z), dim=(1, 2), norm=norm)
     if from_numpy:

@@ -174,3 +174,20 @@ def test_cfg3_projection_round_trip(fi, space, xform_method):
     # Chebyshev/Dirichlet lose < 1e-13.
     tol_c = 2e-10 if space is Space.BIHARMONIC else 1e-12
     assert err_c < tol_c, err_c
+
+
+@pytest.mark.parametrize("space", [Space.DIRICHLET, Space.BIHARMONIC])
+def test_slab_transforms_single_rank(space):
+    """distributed.forward/inverse_transform_slab on one rank equal the
+    single-GPU transforms (the all-to-all itself is tested under gloo)."""
+    import torch
+
+    from paper_1701_03787_b200 import distributed as D
+
+    mesh = build_mesh(64, 16, 12, 2 * np.pi, np.pi, PointFamily.GAUSS)
+    u = torch.rand(mesh.shape, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    c = D.forward_transform_slab(u, mesh, space)
+    want = T.forward_transform(T.PhysicalField(u, mesh), space).data
+    assert torch.equal(c, want)
+    back = D.inverse_transform_slab(c, mesh, space)
+    assert torch.equal(back, T.inverse_transform(T.SpectralField(want, wavenumber_grid(mesh, space), mesh)).data)
