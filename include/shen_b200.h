@@ -172,6 +172,24 @@ int shen_xform_inv_post(int family, int N, int64_t L, const void* F, const void*
 int shen_xform_mass_solve(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
                           void* stream);
 
+/* ---------------------------------------------------------------------
+ * Structured matrix-vector products y = M x along the rows of (rows, L)
+ * arrays (reference matrices.py:62-71, 109-117, 145-152; the
+ * _parity_suffix_sum of :84-90), bit-identical to the reference's.
+ *   offsets[n_off] (host array), diag[n_off][nr] (device, row-indexed:
+ *   entry (k, k + offsets[i]) at diag[i][k] for the offset's valid rows).
+ *   constant tail: row k also gets tail[k] * sum_{j >= k + tail_start,
+ *   j = k + tail_start mod 2} x[j].
+ *   rank-2 tail (square n): diag[k] x[k] + p[k] sum_{j>=k+2} q[j] x[j]
+ *   + r[k] sum_{j>=k+2} s[j] x[j] (same-parity j).
+ * ------------------------------------------------------------------- */
+int shen_apply_banded(int nr, int nc, int64_t L, int n_off, const int* offsets, const double* diag, const void* x,
+                      void* y, int is_complex, void* stream);
+int shen_apply_const_tail(int nr, int nc, int64_t L, int n_off, const int* offsets, const double* diag,
+                          const double* tail, int tail_start, const void* x, void* y, int is_complex, void* stream);
+int shen_apply_rank2_tail(int n, int64_t L, const double* diag, const double* p, const double* q, const double* r,
+                          const double* s, const void* x, void* y, int is_complex, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

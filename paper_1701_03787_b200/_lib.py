@@ -53,6 +53,12 @@ _SIGS = {
                                              ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
+    "shen_apply_banded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                         ctypes.c_int, _vp]),
+    "shen_apply_const_tail": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int, _vp, _vp, _vp,
+                                             ctypes.c_int, _vp, _vp, ctypes.c_int, _vp]),
+    "shen_apply_rank2_tail": (ctypes.c_int, [ctypes.c_int, _c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                             ctypes.c_int, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
     "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,
                                            _vp, _vp, _vp, _vp]),

@@ -257,4 +257,35 @@ int shen_xform_mass_solve(int nband, int n, int mmax, int64_t L, const double* f
   return cuda_check(shen::launch_xf_mass(nband, n, mmax, L, fac, s, x, S(stream)), "shen_xform_mass_solve");
 }
 
+int shen_apply_banded(int nr, int nc, int64_t L, int n_off, const int* offsets, const double* diag, const void* x,
+                      void* y, int is_complex, void* stream) {
+  if (L == 0 || nr == 0) return SHEN_OK;
+  if (nr < 0 || nc <= 0 || L < 0 || n_off < 0 || n_off > 6 || (n_off > 0 && (!offsets || !diag)) || !x || !y)
+    return fail(SHEN_ERR_ARG, "shen_apply_banded: bad args");
+  return cuda_check(shen::launch_apply(0, nr, nc, L, n_off, offsets, diag, nullptr, 0, nullptr, nullptr, nullptr,
+                                       nullptr, nullptr, x, y, is_complex != 0, S(stream)),
+                    "shen_apply_banded");
+}
+
+int shen_apply_const_tail(int nr, int nc, int64_t L, int n_off, const int* offsets, const double* diag,
+                          const double* tail, int tail_start, const void* x, void* y, int is_complex, void* stream) {
+  if (L == 0 || nr == 0) return SHEN_OK;
+  if (nr < 0 || nc <= 0 || L < 0 || n_off < 0 || n_off > 6 || (n_off > 0 && (!offsets || !diag)) || !tail ||
+      tail_start < 0 || !x || !y)
+    return fail(SHEN_ERR_ARG, "shen_apply_const_tail: bad args");
+  return cuda_check(shen::launch_apply(1, nr, nc, L, n_off, offsets, diag, tail, tail_start, nullptr, nullptr,
+                                       nullptr, nullptr, nullptr, x, y, is_complex != 0, S(stream)),
+                    "shen_apply_const_tail");
+}
+
+int shen_apply_rank2_tail(int n, int64_t L, const double* diag, const double* p, const double* q, const double* r,
+                          const double* s, const void* x, void* y, int is_complex, void* stream) {
+  if (L == 0 || n == 0) return SHEN_OK;
+  if (n < 0 || L < 0 || !diag || !p || !q || !r || !s || !x || !y)
+    return fail(SHEN_ERR_ARG, "shen_apply_rank2_tail: bad args");
+  return cuda_check(shen::launch_apply(2, n, n, L, 0, nullptr, nullptr, nullptr, 0, diag, p, q, r, s, x, y,
+                                       is_complex != 0, S(stream)),
+                    "shen_apply_rank2_tail");
+}
+
 }  // extern "C"

@@ -119,6 +119,11 @@ int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_r
 // tiled chunk-parallel Helmholtz solve (shen_solve_tile.cu); ckpt made with chunk_rows = R, 32 R >= rows_p0
 cudaError_t launch_helm_tile(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
 
+// structured apply along the rows (shen_apply.cu): kind 0 banded, 1 constant tail, 2 rank-2 tail
+cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const int* offs, const double* diag,
+                         const double* tail, int tail_start, const double* d, const double* p, const double* q,
+                         const double* r, const double* s, const void* x, void* y, bool cplx_data, cudaStream_t st);
+
 // transforms (shen_transform.cu)
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,

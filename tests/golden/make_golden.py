@@ -141,11 +141,32 @@ def transforms_fixture():
     np.savez_compressed(os.path.join(OUT, "transforms.npz"), **out)
 
 
+def apply_fixture():
+    """Reference structured apply (matrices.py apply) on seeded inputs."""
+    out = {}
+    names = ("mass_dir", "mass_bih", "mixed_mass", "stiff_dir", "stiff_bih", "fourth_bih", "deriv_dir_to_bih",
+             "deriv_bih_to_dir", "deriv_dir_to_cheb")
+    for n_x in (16, 33):
+        for fi, fam in enumerate(FAMS):
+            m = RM.assemble(n_x, fam)
+            for name in names:
+                M = getattr(m, name)
+                rng = np.random.default_rng([n_x, fi, names.index(name)])
+                x = rng.standard_normal((M.shape[1], 6)) + 1j * rng.standard_normal((M.shape[1], 6))
+                out[f"nx{n_x}_f{fi}_{name}_x"] = x
+                out[f"nx{n_x}_f{fi}_{name}_y"] = M.apply(x)
+    np.savez_compressed(os.path.join(OUT, "apply.npz"), **out)
+
+
 if __name__ == "__main__":
+    if "--apply-only" in sys.argv:
+        apply_fixture()
+        sys.exit(0)
     matrices_fixture()
     meta = solver_fixture()
     base = baseline_fixture()
     transforms_fixture()
+    apply_fixture()
     with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
         json.dump({"solver_cases": meta, "baseline": base,
                    "generator": "tests/golden/make_golden.py from /root/reference/pkg/src (chebchan 0.1.0)",

@@ -76,3 +76,16 @@ def test_fourth_diag_positive():
 def test_assemble_rejects_small():
     with pytest.raises(ValueError):
         assemble(7, 0)
+
+
+@pytest.mark.parametrize("n_x", [16, 33])
+@pytest.mark.parametrize("fam", [0, 1])
+def test_host_apply_vs_reference_golden(golden, n_x, fam):
+    """The host restatement of matrices.py apply (used by the oracle and the
+    residual checks) is bit-identical to the reference's."""
+    g = golden("apply.npz")
+    mats = assemble(n_x, fam)
+    for name in ("mass_dir", "mass_bih", "mixed_mass", "stiff_dir", "stiff_bih", "fourth_bih", "deriv_dir_to_bih",
+                 "deriv_bih_to_dir", "deriv_dir_to_cheb"):
+        x = g[f"nx{n_x}_f{fam}_{name}_x"]
+        assert np.array_equal(getattr(mats, name).apply(x), g[f"nx{n_x}_f{fam}_{name}_y"]), name
