@@ -190,6 +190,51 @@ int shen_apply_const_tail(int nr, int nc, int64_t L, int n_off, const int* offse
 int shen_apply_rank2_tail(int n, int64_t L, const double* diag, const double* p, const double* q, const double* r,
                           const double* s, const void* x, void* y, int is_complex, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Stepper right-hand sides, fused (reference stepper.py:189-219): AB2
+ * combination of the nonlinear terms and the explicit operators in one pass
+ * per Fourier line, bit-identical to the reference.  Arrays are (rows, L)
+ * complex128 with L = n_y (n_z/2+1) lines; per-line coefficient arrays are
+ * the reference's numpy expressions evaluated on the host (see
+ * paper_1701_03787_b200/rhs.py).  Matrices: row-indexed diagonal tables as
+ * for shen_apply_banded (device), offsets inline.
+ * ------------------------------------------------------------------- */
+typedef struct shen_band {
+  int nr, nc, n_off;
+  int off[6];
+  const double* diag; /* [n_off][nr] */
+} shen_band;
+
+typedef struct shen_rhs_g_args {
+  int n_dir;
+  int64_t L;
+  shen_band stiff, mass; /* stiff_dir banded part, mass_dir */
+  const double* tail;    /* stiff_dir tail */
+  int tail_start;
+  double c_stiff, dt;    /* -(nu dt/2), dt */
+  const double* cg;      /* [L] 1 - nu dt z2 / 2 */
+  const double *im_m_re, *im_m_im, *im_n_re, *im_n_im; /* [L] 1j m, 1j n */
+  const void *g, *hcy, *hpy, *hcz, *hpz;                /* g, h_curr/h_prev y and z */
+  void* out;
+} shen_rhs_g_args;
+
+typedef struct shen_rhs_u_args {
+  int n_bih;
+  int64_t L;
+  const double *d, *p, *q, *r, *s; /* fourth_bih */
+  double c_fourth;                 /* nu dt / 2 */
+  shen_band stiff, mass, mixed, deriv; /* stiff_bih, mass_bih, mixed_mass, deriv_dir_to_bih */
+  const double *c_stiff, *c_mass, *c_mixed;             /* [L] 1 - nu dt z2, -z2 + nu dt z2^2/2, dt z2 */
+  const double *c_dy_re, *c_dy_im, *c_dz_re, *c_dz_im;  /* [L] dt 1j m, dt 1j n */
+  const void *u, *hcx, *hpx, *hcy, *hpy, *hcz, *hpz;
+  void* out;
+} shen_rhs_u_args;
+
+/* assemble_rhs_g (stepper.py:209-219) with _ab2 (:189-191) folded in */
+int shen_rhs_g(const shen_rhs_g_args* args, void* stream);
+/* assemble_rhs_u (stepper.py:193-207) with _ab2 folded in */
+int shen_rhs_u(const shen_rhs_u_args* args, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

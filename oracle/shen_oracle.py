@@ -411,3 +411,32 @@ def inverse_transform(coeffs, space, family_gl, n_x, n_y, n_z):
     cheb = shen_expand(coeffs, space, n_x)
     lines = chebyshev_evaluate(cheb, family_gl)
     return sfft.irfftn(lines, s=(n_y, n_z), axes=(1, 2))
+
+
+# ---------------------------------------------------------------- stepper right-hand sides
+
+def ab2(h_curr, h_prev):
+    """stepper.py:189-191"""
+    return tuple(1.5 * c - 0.5 * p for c, p in zip(h_curr, h_prev))
+
+
+def assemble_rhs_u(mats, nu, dt, z2, m, n, u, h_ab):
+    """stepper.py:193-207 (m, n, z2 as the stepper holds them)."""
+    rhs = (nu * dt / 2) * mats.fourth_bih.apply(u)
+    rhs -= (1 - nu * dt * z2) * mats.stiff_bih.apply(u)
+    rhs += (-z2 + nu * dt * z2 ** 2 / 2) * mats.mass_bih.apply(u)
+    h_x, h_y, h_z = h_ab
+    rhs -= dt * z2 * mats.mixed_mass.apply(h_x)
+    rhs -= dt * 1j * m * mats.deriv_dir_to_bih.apply(h_y)
+    rhs -= dt * 1j * n * mats.deriv_dir_to_bih.apply(h_z)
+    return rhs
+
+
+def assemble_rhs_g(mats, nu, dt, z2, m, n, g, h_ab):
+    """stepper.py:209-219"""
+    rhs = -(nu * dt / 2) * mats.stiff_dir.apply(g)
+    rhs += (1 - nu * dt * z2 / 2) * mats.mass_dir.apply(g)
+    _, h_y, h_z = h_ab
+    src = 1j * m * h_z - 1j * n * h_y
+    rhs += dt * mats.mass_dir.apply(src)
+    return rhs

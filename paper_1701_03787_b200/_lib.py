@@ -27,6 +27,31 @@ _vp = ctypes.c_void_p
 _pp = ctypes.POINTER(ctypes.c_void_p)
 
 # name -> (restype, argtypes); mirrors include/shen_b200.h
+class ShenBand(ctypes.Structure):
+    _fields_ = [("nr", ctypes.c_int), ("nc", ctypes.c_int), ("n_off", ctypes.c_int), ("off", ctypes.c_int * 6),
+                ("diag", ctypes.c_void_p)]
+
+
+class ShenRhsGArgs(ctypes.Structure):
+    _fields_ = [("n_dir", ctypes.c_int), ("L", ctypes.c_int64), ("stiff", ShenBand), ("mass", ShenBand),
+                ("tail", ctypes.c_void_p), ("tail_start", ctypes.c_int), ("c_stiff", ctypes.c_double),
+                ("dt", ctypes.c_double), ("cg", ctypes.c_void_p), ("im_m_re", ctypes.c_void_p),
+                ("im_m_im", ctypes.c_void_p), ("im_n_re", ctypes.c_void_p), ("im_n_im", ctypes.c_void_p),
+                ("g", ctypes.c_void_p), ("hcy", ctypes.c_void_p), ("hpy", ctypes.c_void_p), ("hcz", ctypes.c_void_p),
+                ("hpz", ctypes.c_void_p), ("out", ctypes.c_void_p)]
+
+
+class ShenRhsUArgs(ctypes.Structure):
+    _fields_ = [("n_bih", ctypes.c_int), ("L", ctypes.c_int64), ("d", ctypes.c_void_p), ("p", ctypes.c_void_p),
+                ("q", ctypes.c_void_p), ("r", ctypes.c_void_p), ("s", ctypes.c_void_p), ("c_fourth", ctypes.c_double),
+                ("stiff", ShenBand), ("mass", ShenBand), ("mixed", ShenBand), ("deriv", ShenBand),
+                ("c_stiff", ctypes.c_void_p), ("c_mass", ctypes.c_void_p), ("c_mixed", ctypes.c_void_p),
+                ("c_dy_re", ctypes.c_void_p), ("c_dy_im", ctypes.c_void_p), ("c_dz_re", ctypes.c_void_p),
+                ("c_dz_im", ctypes.c_void_p), ("u", ctypes.c_void_p), ("hcx", ctypes.c_void_p),
+                ("hpx", ctypes.c_void_p), ("hcy", ctypes.c_void_p), ("hpy", ctypes.c_void_p), ("hcz", ctypes.c_void_p),
+                ("hpz", ctypes.c_void_p), ("out", ctypes.c_void_p)]
+
+
 _SIGS = {
     "shen_version": (ctypes.c_char_p, []),
     "shen_last_error": (ctypes.c_char_p, []),
@@ -59,6 +84,8 @@ _SIGS = {
                                              ctypes.c_int, _vp, _vp, ctypes.c_int, _vp]),
     "shen_apply_rank2_tail": (ctypes.c_int, [ctypes.c_int, _c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                              ctypes.c_int, _vp]),
+    "shen_rhs_g": (ctypes.c_int, [ctypes.POINTER(ShenRhsGArgs), _vp]),
+    "shen_rhs_u": (ctypes.c_int, [ctypes.POINTER(ShenRhsUArgs), _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
     "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,
                                            _vp, _vp, _vp, _vp]),

@@ -288,4 +288,45 @@ int shen_apply_rank2_tail(int n, int64_t L, const double* diag, const double* p,
                     "shen_apply_rank2_tail");
 }
 
+static bool band_ok(const shen_band& b) { return b.nr >= 0 && b.nc > 0 && b.n_off >= 0 && b.n_off <= 6 && (b.n_off == 0 || b.diag); }
+static shen::RhsBand to_band(const shen_band& b) {
+  shen::RhsBand o{};
+  o.nr = b.nr; o.nc = b.nc; o.n_off = b.n_off; o.diag = b.diag;
+  for (int i = 0; i < 6; ++i) o.off[i] = b.off[i];
+  return o;
+}
+
+int shen_rhs_g(const shen_rhs_g_args* g, void* stream) {
+  if (!g) return fail(SHEN_ERR_ARG, "shen_rhs_g: NULL args");
+  if (g->L == 0 || g->n_dir == 0) return SHEN_OK;
+  if (g->n_dir < 0 || g->L < 0 || !band_ok(g->stiff) || !band_ok(g->mass) || !g->tail || !g->cg || !g->im_m_re ||
+      !g->im_m_im || !g->im_n_re || !g->im_n_im || !g->g || !g->hcy || !g->hpy || !g->hcz || !g->hpz || !g->out ||
+      g->stiff.nr != g->n_dir || g->mass.nr != g->n_dir)
+    return fail(SHEN_ERR_ARG, "shen_rhs_g: bad args");
+  shen::RhsGArgs a{};
+  a.n_dir = g->n_dir; a.L = g->L; a.stiff = to_band(g->stiff); a.mass = to_band(g->mass);
+  a.tail = g->tail; a.tail_start = g->tail_start; a.c_stiff = g->c_stiff; a.dt = g->dt; a.cg = g->cg;
+  a.im_m_re = g->im_m_re; a.im_m_im = g->im_m_im; a.im_n_re = g->im_n_re; a.im_n_im = g->im_n_im;
+  a.g = g->g; a.hcy = g->hcy; a.hpy = g->hpy; a.hcz = g->hcz; a.hpz = g->hpz; a.out = g->out;
+  return cuda_check(shen::launch_rhs_g(a, S(stream)), "shen_rhs_g");
+}
+
+int shen_rhs_u(const shen_rhs_u_args* u, void* stream) {
+  if (!u) return fail(SHEN_ERR_ARG, "shen_rhs_u: NULL args");
+  if (u->L == 0 || u->n_bih == 0) return SHEN_OK;
+  if (u->n_bih < 0 || u->L < 0 || !u->d || !u->p || !u->q || !u->r || !u->s || !band_ok(u->stiff) ||
+      !band_ok(u->mass) || !band_ok(u->mixed) || !band_ok(u->deriv) || !u->c_stiff || !u->c_mass || !u->c_mixed ||
+      !u->c_dy_re || !u->c_dy_im || !u->c_dz_re || !u->c_dz_im || !u->u || !u->hcx || !u->hpx || !u->hcy ||
+      !u->hpy || !u->hcz || !u->hpz || !u->out)
+    return fail(SHEN_ERR_ARG, "shen_rhs_u: bad args");
+  shen::RhsUArgs a{};
+  a.n_bih = u->n_bih; a.L = u->L; a.d = u->d; a.p = u->p; a.q = u->q; a.r = u->r; a.s = u->s;
+  a.c_fourth = u->c_fourth; a.stiff = to_band(u->stiff); a.mass = to_band(u->mass); a.mixed = to_band(u->mixed);
+  a.deriv = to_band(u->deriv); a.c_stiff = u->c_stiff; a.c_mass = u->c_mass; a.c_mixed = u->c_mixed;
+  a.c_dy_re = u->c_dy_re; a.c_dy_im = u->c_dy_im; a.c_dz_re = u->c_dz_re; a.c_dz_im = u->c_dz_im;
+  a.u = u->u; a.hcx = u->hcx; a.hpx = u->hpx; a.hcy = u->hcy; a.hpy = u->hpy; a.hcz = u->hcz; a.hpz = u->hpz;
+  a.out = u->out;
+  return cuda_check(shen::launch_rhs_u(a, S(stream)), "shen_rhs_u");
+}
+
 }  // extern "C"

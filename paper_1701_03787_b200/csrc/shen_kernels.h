@@ -124,6 +124,38 @@ cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const i
                          const double* tail, int tail_start, const double* d, const double* p, const double* q,
                          const double* r, const double* s, const void* x, void* y, bool cplx_data, cudaStream_t st);
 
+// stepper right-hand sides (shen_rhs.cu)
+struct RhsBand {  // banded matrix, row-indexed diagonals [n_off][nr] (device)
+  int nr, nc, n_off;
+  int off[6];
+  const double* diag;
+};
+struct RhsGArgs {
+  int n_dir;
+  int64_t L;
+  RhsBand stiff, mass;        // stiff_dir banded part, mass_dir
+  const double* tail;         // stiff_dir tail
+  int tail_start;
+  double c_stiff, dt;         // -(nu dt / 2), dt
+  const double* cg;           // per line: 1 - nu dt z2 / 2
+  const double *im_m_re, *im_m_im, *im_n_re, *im_n_im;  // per line: 1j m, 1j n
+  const void *g, *hcy, *hpy, *hcz, *hpz;
+  void* out;
+};
+struct RhsUArgs {
+  int n_bih;
+  int64_t L;
+  const double *d, *p, *q, *r, *s;  // fourth_bih
+  double c_fourth;                  // nu dt / 2
+  RhsBand stiff, mass, mixed, deriv;
+  const double *c_stiff, *c_mass, *c_mixed;            // per line: 1 - nu dt z2, -z2 + nu dt z2^2 / 2, dt z2
+  const double *c_dy_re, *c_dy_im, *c_dz_re, *c_dz_im;  // per line: dt 1j m, dt 1j n
+  const void *u, *hcx, *hpx, *hcy, *hpy, *hcz, *hpz;
+  void* out;
+};
+cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st);
+cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st);
+
 // transforms (shen_transform.cu)
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,

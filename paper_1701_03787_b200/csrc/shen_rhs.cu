@@ -1,0 +1,331 @@
+// Right-hand-side assembly of the stepper's implicit updates, fused into one
+// pass per Fourier line (reference stepper.py:189-219):
+//
+//   h_ab  = 1.5 h_curr - 0.5 h_prev                          (_ab2, :189-191)
+//   rhs_g = -(nu dt/2) A_D g + (1 - nu dt z2/2) B_D g
+//           + dt B_D (i m h_z - i n h_y)                       (assemble_rhs_g, :209-219)
+//   rhs_u = (nu dt/2) S u - (1 - nu dt z2) A_B u + (-z2 + nu dt z2^2/2) B_B u
+//           - dt z2 C h_x - dt i m D h_y - dt i n D h_z        (assemble_rhs_u, :193-207)
+//
+// A_D = stiff_dir (constant tail), B_D = mass_dir, S = fourth_bih (rank-2
+// tail), A_B = stiff_bih, B_B = mass_bih, C = mixed_mass, D = deriv_dir_to_bih.
+// The reference materialises every product and temporary (numpy); here one
+// thread per line walks its rows bottom-up once (the tails' parity suffix
+// sums ride along in registers), reading each input row once from HBM and
+// writing each rhs row once.  Every product, sum and complex multiply is
+// issued in the reference's order without contraction, and the per-line
+// coefficients are computed on the host with the reference's numpy
+// expressions, so the result is bit-identical (tests/test_rhs_gpu.py).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <initializer_list>
+
+#include "shen_common.cuh"
+#include "shen_kernels.h"
+
+namespace shen {
+namespace {
+
+struct C2 {
+  double re, im;
+};
+__device__ __forceinline__ C2 ld(const double2* p) {
+  const double2 v = __ldg(p);
+  return {v.x, v.y};
+}
+__device__ __forceinline__ C2 add(C2 a, C2 b) { return {__dadd_rn(a.re, b.re), __dadd_rn(a.im, b.im)}; }
+__device__ __forceinline__ C2 sub(C2 a, C2 b) { return {__dsub_rn(a.re, b.re), __dsub_rn(a.im, b.im)}; }
+__device__ __forceinline__ C2 rmul(double c, C2 v) { return {__dmul_rn(c, v.re), __dmul_rn(c, v.im)}; }
+// numpy complex product (a.re b.re - a.im b.im, a.re b.im + a.im b.re)
+__device__ __forceinline__ C2 cmul(C2 a, C2 b) {
+  return {__dsub_rn(__dmul_rn(a.re, b.re), __dmul_rn(a.im, b.im)), __dadd_rn(__dmul_rn(a.re, b.im), __dmul_rn(a.im, b.re))};
+}
+
+// y[k] of a banded matrix (offsets in the reference's order, each on its
+// valid row range, added to an exact zero)
+template <typename F>
+__device__ __forceinline__ C2 banded_row(const RhsBand& m, int k, F X) {
+  C2 v = {0.0, 0.0};
+  for (int q = 0; q < m.n_off; ++q) {
+    const int dk = m.off[q];
+    const int k0 = dk < 0 ? -dk : 0, k1 = min(m.nr, m.nc - dk);
+    if (k >= k0 && k < k1) v = add(v, rmul(__ldg(m.diag + (int64_t)q * m.nr + k), X(k + dk)));
+  }
+  return v;
+}
+
+__global__ void rhs_g_kernel(RhsGArgs a) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.L) return;
+  const int64_t L = a.L;
+  const int n = a.n_dir;
+  const double2* g = static_cast<const double2*>(a.g) + l;
+  auto G = [&](int j) { return ld(g + (int64_t)j * L); };
+  auto H = [&](const void* c, const void* p, int j) {  // h_ab row j
+    const C2 hc = ld(static_cast<const double2*>(c) + (int64_t)j * L + l);
+    const C2 hp = ld(static_cast<const double2*>(p) + (int64_t)j * L + l);
+    return sub(rmul(1.5, hc), rmul(0.5, hp));
+  };
+  const C2 im_m = {__ldg(a.im_m_re + l), __ldg(a.im_m_im + l)}, im_n = {__ldg(a.im_n_re + l), __ldg(a.im_n_im + l)};
+  auto SRC = [&](int j) {  // 1j m h_z - 1j n h_y
+    return sub(cmul(im_m, H(a.hcz, a.hpz, j)), cmul(im_n, H(a.hcy, a.hpy, j)));
+  };
+  const double cg = __ldg(a.cg + l);
+  C2 S[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  bool have[2] = {false, false};
+  int next_j = n - 1;
+  double2* out = static_cast<double2*>(a.out) + l;
+  for (int k = n - 1; k >= 0; --k) {
+    // stiff_dir.apply(g)[k]: banded part, then tail[k] * parity suffix sum from k + tail_start
+    C2 st = banded_row(a.stiff, k, G);
+    const int j = k + a.tail_start;
+    if (j < n) {
+      for (; next_j >= j; --next_j) {
+        const int pj = next_j & 1;
+        S[pj] = have[pj] ? add(G(next_j), S[pj]) : G(next_j);
+        have[pj] = true;
+      }
+      st = add(st, rmul(__ldg(a.tail + k), S[j & 1]));
+    }
+    C2 r = rmul(a.c_stiff, st);                              // -(nu dt/2) A_D g
+    r = add(r, rmul(cg, banded_row(a.mass, k, G)));          // += (1 - nu dt z2/2) B_D g
+    r = add(r, rmul(a.dt, banded_row(a.mass, k, SRC)));      // += dt B_D src
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+  }
+}
+
+__global__ void rhs_u_kernel(RhsUArgs a) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.L) return;
+  const int64_t L = a.L;
+  const int n = a.n_bih;
+  const double2* u = static_cast<const double2*>(a.u) + l;
+  auto U = [&](int j) { return ld(u + (int64_t)j * L); };
+  auto Hc = [&](const void* c, const void* p) {
+    return [=](int j) {
+      const C2 hc = ld(static_cast<const double2*>(c) + (int64_t)j * L + l);
+      const C2 hp = ld(static_cast<const double2*>(p) + (int64_t)j * L + l);
+      return sub(rmul(1.5, hc), rmul(0.5, hp));
+    };
+  };
+  const auto HX = Hc(a.hcx, a.hpx), HY = Hc(a.hcy, a.hpy), HZ = Hc(a.hcz, a.hpz);
+  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
+  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
+  C2 sq[2] = {{0.0, 0.0}, {0.0, 0.0}}, ss[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  bool have[2] = {false, false};
+  double2* out = static_cast<double2*>(a.out) + l;
+  for (int k = n - 1; k >= 0; --k) {
+    const int j = k + 2;
+    if (j < n) {
+      const C2 uj = U(j);
+      const C2 qx = rmul(__ldg(a.q + j), uj), sx = rmul(__ldg(a.s + j), uj);
+      const int pj = j & 1;
+      sq[pj] = have[pj] ? add(qx, sq[pj]) : qx;
+      ss[pj] = have[pj] ? add(sx, ss[pj]) : sx;
+      have[pj] = true;
+    }
+    C2 f = rmul(__ldg(a.d + k), U(k));  // fourth_bih.apply(u)[k]
+    if (k < n - 2) {
+      f = add(f, rmul(__ldg(a.p + k), sq[k & 1]));
+      f = add(f, rmul(__ldg(a.r + k), ss[k & 1]));
+    }
+    C2 r = rmul(a.c_fourth, f);
+    r = sub(r, rmul(cs, banded_row(a.stiff, k, U)));
+    r = add(r, rmul(cm, banded_row(a.mass, k, U)));
+    r = sub(r, rmul(cx, banded_row(a.mixed, k, HX)));
+    r = sub(r, cmul(cy, banded_row(a.deriv, k, HY)));
+    r = sub(r, cmul(cz, banded_row(a.deriv, k, HZ)));
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+  }
+}
+
+
+// ---------------------------------------------------------------- fast path
+#ifndef SHEN_RHS_PF
+#define SHEN_RHS_PF 0  // extra prefetch rows of the rhs_u windows (measured: none is best)
+#endif
+#ifndef SHEN_RHS_UNROLL
+#define SHEN_RHS_UNROLL 1  // rows per loop trip (measured: unrolling 2-4 is slower)
+#endif
+constexpr int kRhsUnroll = SHEN_RHS_UNROLL;
+#ifndef SHEN_RHS_U_MINB
+#define SHEN_RHS_U_MINB 3  // resident 128-thread blocks per SM the register budget targets
+#endif
+// The reference's matrices have fixed structure: mass_dir / stiff_bih
+// offsets (-2, 0, 2), stiff_dir banded part (0) + tail from k+2, mass_bih
+// (-4, -2, 0, 2, 4), mixed_mass (-2, 0, 2, 4), deriv_dir_to_bih (-1, 1, 3).
+// For that structure each input row is loaded ONCE into a register window
+// that slides down with k (the generic kernel above re-reads neighbours and
+// recombines AB2 per use).  Same operations in the same order -> same bits.
+template <int LO, int HI>
+struct Win {  // values at rows k+LO .. k+HI
+  C2 v[HI - LO + 1];
+  __device__ __forceinline__ C2 at(int d) const { return v[d - LO]; }
+  // k -> k-1: everything moves one slot up, row (k-1)+LO enters at the bottom
+  __device__ __forceinline__ void shift(C2 fresh) {
+#pragma unroll
+    for (int i = HI - LO; i > 0; --i) v[i] = v[i - 1];
+    v[0] = fresh;
+  }
+};
+
+__device__ __forceinline__ C2 term(const RhsBand& m, int q, int k, C2 x) {
+  return rmul(__ldg(m.diag + (int64_t)q * m.nr + k), x);
+}
+// banded row with the window; the offsets are compile-time (the launcher
+// checks that the matrix has exactly these, in this order)
+template <int Q, int LO, int HI>
+__device__ __forceinline__ void band_terms(const RhsBand&, int, const Win<LO, HI>&, C2&) {}
+template <int Q, int LO, int HI, int D, int... Ds>
+__device__ __forceinline__ void band_terms(const RhsBand& m, int k, const Win<LO, HI>& w, C2& v) {
+  constexpr int k0 = D < 0 ? -D : 0;
+  if (k >= k0 && k < m.nc - D && k < m.nr) v = add(v, term(m, Q, k, w.at(D)));
+  band_terms<Q + 1, LO, HI, Ds...>(m, k, w, v);
+}
+template <int... Ds, int LO, int HI>
+__device__ __forceinline__ C2 band_win(const RhsBand& m, int k, const Win<LO, HI>& w) {
+  C2 v = {0.0, 0.0};
+  band_terms<0, LO, HI, Ds...>(m, k, w, v);
+  return v;
+}
+
+__global__ void __launch_bounds__(128) rhs_g_fast_kernel(RhsGArgs a) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.L) return;
+  const int64_t L = a.L;
+  const int n = a.n_dir;
+  auto ldr = [&](const void* base, int j) -> C2 {
+    return (j >= 0 && j < n) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
+  };
+  const C2 im_m = {__ldg(a.im_m_re + l), __ldg(a.im_m_im + l)}, im_n = {__ldg(a.im_n_re + l), __ldg(a.im_n_im + l)};
+  auto src_row = [&](int j) -> C2 {
+    if (j < 0 || j >= n) return {0.0, 0.0};
+    const C2 hy = sub(rmul(1.5, ldr(a.hcy, j)), rmul(0.5, ldr(a.hpy, j)));
+    const C2 hz = sub(rmul(1.5, ldr(a.hcz, j)), rmul(0.5, ldr(a.hpz, j)));
+    return sub(cmul(im_m, hz), cmul(im_n, hy));
+  };
+  const double cg = __ldg(a.cg + l);
+  Win<-2, 2> G, R;  // g and src at rows k-2 .. k+2
+#pragma unroll
+  for (int d = -2; d <= 2; ++d) {
+    G.v[d + 2] = ldr(a.g, n - 1 + d);
+    R.v[d + 2] = src_row(n - 1 + d);
+  }
+  C2 S[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  bool have[2] = {false, false};
+  double2* out = static_cast<double2*>(a.out) + l;
+#pragma unroll kRhsUnroll
+  for (int k = n - 1; k >= 0; --k) {
+    C2 st = band_win<0>(a.stiff, k, G);
+    const int j = k + 2;  // tail_start == 2 (checked on the host side)
+    if (j < n) {
+      const int pj = j & 1;
+      S[pj] = have[pj] ? add(G.at(2), S[pj]) : G.at(2);
+      have[pj] = true;
+      st = add(st, rmul(__ldg(a.tail + k), S[pj]));
+    }
+    C2 r = rmul(a.c_stiff, st);
+    r = add(r, rmul(cg, band_win<-2, 0, 2>(a.mass, k, G)));
+    r = add(r, rmul(a.dt, band_win<-2, 0, 2>(a.mass, k, R)));
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+    G.shift(ldr(a.g, k - 3));
+    R.shift(src_row(k - 3));
+  }
+}
+
+__global__ void __launch_bounds__(128, SHEN_RHS_U_MINB) rhs_u_fast_kernel(RhsUArgs a) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= a.L) return;
+  const int64_t L = a.L;
+  const int n = a.n_bih, nd = a.mixed.nc;
+  auto ldr = [&](const void* base, int j, int rows) -> C2 {
+    return (j >= 0 && j < rows) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
+  };
+  auto hrow = [&](const void* c, const void* p, int j) -> C2 {
+    if (j < 0 || j >= nd) return {0.0, 0.0};
+    return sub(rmul(1.5, ldr(c, j, nd)), rmul(0.5, ldr(p, j, nd)));
+  };
+  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
+  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
+  // windows extended PF rows below what the bands use: those slots are a
+  // prefetch FIFO, so a row's loads are issued PF+1 iterations before use
+  constexpr int PF = SHEN_RHS_PF;
+  Win<-4 - PF, 4> U;   // u rows k-4 .. k+4 (+ prefetch)
+  Win<-2 - PF, 4> HX;  // h_x rows k-2 .. k+4
+  Win<-1 - PF, 3> HY, HZ;
+  const int k = n - 1;
+#pragma unroll
+  for (int d = -4 - PF; d <= 4; ++d) U.v[d + 4 + PF] = ldr(a.u, k + d, n);
+#pragma unroll
+  for (int d = -2 - PF; d <= 4; ++d) HX.v[d + 2 + PF] = hrow(a.hcx, a.hpx, k + d);
+#pragma unroll
+  for (int d = -1 - PF; d <= 3; ++d) {
+    HY.v[d + 1 + PF] = hrow(a.hcy, a.hpy, k + d);
+    HZ.v[d + 1 + PF] = hrow(a.hcz, a.hpz, k + d);
+  }
+  C2 sq[2] = {{0.0, 0.0}, {0.0, 0.0}}, ss[2] = {{0.0, 0.0}, {0.0, 0.0}};
+  bool have[2] = {false, false};
+  double2* out = static_cast<double2*>(a.out) + l;
+#pragma unroll kRhsUnroll
+  for (int k = n - 1; k >= 0; --k) {
+    const int j = k + 2;
+    if (j < n) {
+      const C2 uj = U.at(2);
+      const C2 qx = rmul(__ldg(a.q + j), uj), sx = rmul(__ldg(a.s + j), uj);
+      const int pj = j & 1;
+      sq[pj] = have[pj] ? add(qx, sq[pj]) : qx;
+      ss[pj] = have[pj] ? add(sx, ss[pj]) : sx;
+      have[pj] = true;
+    }
+    C2 f = rmul(__ldg(a.d + k), U.at(0));
+    if (k < n - 2) {
+      f = add(f, rmul(__ldg(a.p + k), sq[k & 1]));
+      f = add(f, rmul(__ldg(a.r + k), ss[k & 1]));
+    }
+    C2 r = rmul(a.c_fourth, f);
+    r = sub(r, rmul(cs, band_win<-2, 0, 2>(a.stiff, k, U)));
+    r = add(r, rmul(cm, band_win<-4, -2, 0, 2, 4>(a.mass, k, U)));
+    r = sub(r, rmul(cx, band_win<-2, 0, 2, 4>(a.mixed, k, HX)));
+    r = sub(r, cmul(cy, band_win<-1, 1, 3>(a.deriv, k, HY)));
+    r = sub(r, cmul(cz, band_win<-1, 1, 3>(a.deriv, k, HZ)));
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+    U.shift(ldr(a.u, k - 5 - PF, n));
+    HX.shift(hrow(a.hcx, a.hpx, k - 3 - PF));
+    HY.shift(hrow(a.hcy, a.hpy, k - 2 - PF));
+    HZ.shift(hrow(a.hcz, a.hpz, k - 2 - PF));
+  }
+}
+
+static bool offs_are(const RhsBand& m, std::initializer_list<int> o) {
+  if (m.n_off != (int)o.size()) return false;
+  int i = 0;
+  for (int v : o)
+    if (m.off[i++] != v) return false;
+  return true;
+}
+
+}  // namespace
+
+cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
+  if (a.L <= 0 || a.n_dir <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((a.L + 127) / 128);
+  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}))
+    rhs_g_fast_kernel<<<blocks, 128, 0, st>>>(a);
+  else
+    rhs_g_kernel<<<blocks, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st) {
+  if (a.L <= 0 || a.n_bih <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((a.L + 127) / 128);
+  if (offs_are(a.stiff, {-2, 0, 2}) && offs_are(a.mass, {-4, -2, 0, 2, 4}) && offs_are(a.mixed, {-2, 0, 2, 4}) &&
+      offs_are(a.deriv, {-1, 1, 3}))
+    rhs_u_fast_kernel<<<blocks, 128, 0, st>>>(a);
+  else
+    rhs_u_kernel<<<blocks, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace shen

@@ -158,15 +158,51 @@ def apply_fixture():
     np.savez_compressed(os.path.join(OUT, "apply.npz"), **out)
 
 
+def rhs_fixture():
+    """Reference ChannelStepper._ab2 / assemble_rhs_u / assemble_rhs_g on a
+    seeded state (n_x = 16, 8 x 8 plane, both families)."""
+    from chebchan.stepper import ChannelStepper, FlowState, StepperConfig
+    from chebchan.transforms import SpectralField
+
+    out = {}
+    for fi, fam in enumerate(FAMS):
+        mesh = build_mesh(16, 8, 8, 2 * np.pi, np.pi, fam)
+        st = ChannelStepper(mesh, StepperConfig(nu=1e-2, dt=1e-3))
+        gd, gb = wavenumber_grid(mesh, Space.DIRICHLET), wavenumber_grid(mesh, Space.BIHARMONIC)
+        rng = np.random.default_rng(50 + fi)
+
+        def cf(grid):
+            shp = (grid.n_modes,) + mesh.spectral_shape_yz
+            return SpectralField(rng.standard_normal(shp) + 1j * rng.standard_normal(shp), grid, mesh)
+
+        u, v, w, g = cf(gb), cf(gd), cf(gd), cf(gd)
+        hc = tuple(cf(gd) for _ in range(3))
+        hp = tuple(cf(gd) for _ in range(3))
+        state = FlowState(u, v, w, g, hc, hp, 0.0, 0.0, 0)
+        h_ab = st._ab2(state)
+        key = f"f{fi}"
+        out[key + "_u"], out[key + "_g"] = u.data, g.data
+        for i in range(3):
+            out[f"{key}_hc{i}"], out[f"{key}_hp{i}"], out[f"{key}_hab{i}"] = hc[i].data, hp[i].data, h_ab[i]
+        out[key + "_rhs_u"] = st.assemble_rhs_u(state, h_ab)
+        out[key + "_rhs_g"] = st.assemble_rhs_g(state, h_ab)
+        out[key + "_m"], out[key + "_n"], out[key + "_z2"] = st.m, st.n, st.z2
+    np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
+
+
 if __name__ == "__main__":
     if "--apply-only" in sys.argv:
         apply_fixture()
+        sys.exit(0)
+    if "--rhs-only" in sys.argv:
+        rhs_fixture()
         sys.exit(0)
     matrices_fixture()
     meta = solver_fixture()
     base = baseline_fixture()
     transforms_fixture()
     apply_fixture()
+    rhs_fixture()
     with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
         json.dump({"solver_cases": meta, "baseline": base,
                    "generator": "tests/golden/make_golden.py from /root/reference/pkg/src (chebchan 0.1.0)",

@@ -116,3 +116,20 @@ def test_oracle_pivot_error(rows, want):
     mats = degenerate_mats(16, rows)
     with pytest.raises(O.OraclePivotError, match=f"at row {want}$"):
         O.helmholtz_factor(mats, 0.0, 1.0, np.array([0.0, 1.0]))
+
+
+@pytest.mark.parametrize("fi", [0, 1])
+def test_oracle_rhs_assembly_bitwise(golden, fi):
+    """stepper.py:189-219 restated: AB2 and both right-hand sides equal the
+    reference's ChannelStepper outputs bit for bit."""
+    g = golden("rhs.npz")
+    k = f"f{fi}"
+    mats = assemble(16, fi)
+    hc = [g[f"{k}_hc{i}"] for i in range(3)]
+    hp = [g[f"{k}_hp{i}"] for i in range(3)]
+    hab = O.ab2(hc, hp)
+    for i in range(3):
+        assert np.array_equal(hab[i], g[f"{k}_hab{i}"])
+    args = (mats, 1e-2, 1e-3, g[k + "_z2"], g[k + "_m"], g[k + "_n"])
+    assert np.array_equal(O.assemble_rhs_u(*args, g[k + "_u"], hab), g[k + "_rhs_u"])
+    assert np.array_equal(O.assemble_rhs_g(*args, g[k + "_g"], hab), g[k + "_rhs_g"])
