@@ -186,7 +186,7 @@ def _degenerate(n_x, rows):
 
 
 @pytest.mark.parametrize("rows,want", [([0], 0), ([1], 1), ([0, 1], 0)])
-@pytest.mark.parametrize("method", ["chunked", "stored"])
+@pytest.mark.parametrize("method", ["stream", "chunked", "stored", "tile"])
 def test_zero_pivot_raises(rows, want, method):
     with pytest.raises(S.ZeroPivotError, match=f"Helmholtz factorization hit a near-zero pivot at row {want}$"):
         S.build_helmholtz(_degenerate(16, rows), 0.0, 1.0, np.array([0.0, 1.0]), method=method)
