@@ -440,3 +440,38 @@ def assemble_rhs_g(mats, nu, dt, z2, m, n, g, h_ab):
     src = 1j * m * h_z - 1j * n * h_y
     rhs += dt * mats.mass_dir.apply(src)
     return rhs
+
+
+def compute_nonlinear(mats, family_gl, n_y, n_z, m, n, mask, u_hat, v_hat, w_hat, g_hat):
+    """stepper.py:148-185: Dirichlet coefficients of H = u x omega, masked.
+    m, n, mask as the stepper holds them ((n_y, 1), (1, n_z//2+1), plane)."""
+    n_x = mats.n_x
+    mass_inv = 1.0 / mats.mass_cheb
+
+    def ddx(d):
+        c = mats.deriv_dir_to_cheb.apply(d)
+        c *= mass_inv.reshape(-1, 1, 1)
+        return c
+
+    def inv(c, sp):
+        return inverse_transform(c, sp, family_gl, n_x, n_y, n_z)
+
+    u = inv(u_hat, 2)
+    v = inv(v_hat, 1)
+    w = inv(w_hat, 1)
+    om_x = inv(g_hat, 1)
+    dv_dx = inv(ddx(v_hat), 0)
+    dw_dx = inv(ddx(w_hat), 0)
+    du_dy = inv(1j * m * u_hat, 2)
+    du_dz = inv(1j * n * u_hat, 2)
+    om_y = du_dz - dw_dx
+    om_z = dv_dx - du_dy
+    h_x = v * om_z - w * om_y
+    h_y = w * om_x - u * om_z
+    h_z = u * om_y - v * om_x
+    out = []
+    for h in (h_x, h_y, h_z):
+        c = forward_transform(h, 1, family_gl, mats)
+        c *= mask
+        out.append(c)
+    return tuple(out)

@@ -86,6 +86,8 @@ _SIGS = {
                                              ctypes.c_int, _vp]),
     "shen_rhs_g": (ctypes.c_int, [ctypes.POINTER(ShenRhsGArgs), _vp]),
     "shen_rhs_u": (ctypes.c_int, [ctypes.POINTER(ShenRhsUArgs), _vp]),
+    "shen_scale_lines": (ctypes.c_int, [_c_int64, _c_int64, _vp, _vp, _vp, _vp, _vp]),
+    "shen_cross": (ctypes.c_int, [_c_int64, _vp, _vp, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
     "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,
                                            _vp, _vp, _vp, _vp]),

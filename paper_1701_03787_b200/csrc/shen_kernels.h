@@ -156,6 +156,11 @@ struct RhsUArgs {
 cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st);
 cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st);
 
+// nonlinear-term pointwise kernels (shen_nonlinear.cu)
+cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const double* cre, const double* cim, void* y,
+                               cudaStream_t st);
+cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
+
 // transforms (shen_transform.cu)
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,

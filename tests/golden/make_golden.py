@@ -187,6 +187,11 @@ def rhs_fixture():
         out[key + "_rhs_u"] = st.assemble_rhs_u(state, h_ab)
         out[key + "_rhs_g"] = st.assemble_rhs_g(state, h_ab)
         out[key + "_m"], out[key + "_n"], out[key + "_z2"] = st.m, st.n, st.z2
+        # nonlinear term of the same state (dealiased)
+        nl = st.compute_nonlinear(state)
+        for i in range(3):
+            out[f"{key}_nl{i}"] = nl[i].data
+        out[key + "_v"], out[key + "_w"], out[key + "_mask"] = v.data, w.data, st.mask
     np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
 
 
