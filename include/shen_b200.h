@@ -236,6 +236,24 @@ int shen_rhs_g(const shen_rhs_g_args* args, void* stream);
 int shen_rhs_u(const shen_rhs_u_args* args, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Velocity recovery (reference stepper.py:296-303): f = B_D^-1 (D u_new),
+ * v = (1j m f + 1j n g) / z2', w = (1j n f - 1j m g) / z2' per line
+ * (z2' = z2, 1 on the mean mode).  fac = per-parity LAPACK upper band
+ * Cholesky factors of mass_dir, [2][2][mmax] (as for shen_xform_mass_solve).
+ * ------------------------------------------------------------------- */
+typedef struct shen_recover_args {
+  int n_dir;
+  int64_t L;
+  shen_band deriv;    /* deriv_bih_to_dir (n_dir x n_bih) */
+  const double* fac;
+  int mmax;
+  const double *im_m_re, *im_m_im, *im_n_re, *im_n_im, *safe_z2; /* [L] */
+  const void *u, *g;  /* u_new (n_bih, L), g_new (n_dir, L) */
+  void *v, *w;        /* (n_dir, L) outputs */
+} shen_recover_args;
+int shen_recover_velocity(const shen_recover_args* args, void* stream);
+
+/* ---------------------------------------------------------------------
  * Nonlinear term H = u x omega (reference stepper.py:148-185), pointwise
  * pieces; the transforms around them are wall-normal GEMMs + cuFFT.
  * shen_scale_lines: y[r][l] = c_l x[r][l] for rows x L complex128 (numpy

@@ -475,3 +475,15 @@ def compute_nonlinear(mats, family_gl, n_y, n_z, m, n, mask, u_hat, v_hat, w_hat
         c *= mask
         out.append(c)
     return tuple(out)
+
+
+def recover_velocity(mats, z2, m, n, u_new, g_new):
+    """stepper.py:296-303: divergence variable f = mass_solve(D u) and the
+    horizontal velocities (the mean mode (m = n = 0) is overwritten by the
+    stepper's mean-flow solve afterwards)."""
+    f_scal = mats.deriv_bih_to_dir.apply(u_new)
+    f_hat = mass_solve(f_scal, 1, mats)
+    safe_z2 = np.where(z2 > 0, z2, 1.0)
+    v_new = (1j * m * f_hat + 1j * n * g_new) / safe_z2
+    w_new = (1j * n * f_hat - 1j * m * g_new) / safe_z2
+    return v_new, w_new

@@ -52,6 +52,13 @@ class ShenRhsUArgs(ctypes.Structure):
                 ("hpz", ctypes.c_void_p), ("out", ctypes.c_void_p)]
 
 
+class ShenRecoverArgs(ctypes.Structure):
+    _fields_ = [("n_dir", ctypes.c_int), ("L", ctypes.c_int64), ("deriv", ShenBand), ("fac", ctypes.c_void_p),
+                ("mmax", ctypes.c_int), ("im_m_re", ctypes.c_void_p), ("im_m_im", ctypes.c_void_p),
+                ("im_n_re", ctypes.c_void_p), ("im_n_im", ctypes.c_void_p), ("safe_z2", ctypes.c_void_p),
+                ("u", ctypes.c_void_p), ("g", ctypes.c_void_p), ("v", ctypes.c_void_p), ("w", ctypes.c_void_p)]
+
+
 _SIGS = {
     "shen_version": (ctypes.c_char_p, []),
     "shen_last_error": (ctypes.c_char_p, []),
@@ -86,6 +93,7 @@ _SIGS = {
                                              ctypes.c_int, _vp]),
     "shen_rhs_g": (ctypes.c_int, [ctypes.POINTER(ShenRhsGArgs), _vp]),
     "shen_rhs_u": (ctypes.c_int, [ctypes.POINTER(ShenRhsUArgs), _vp]),
+    "shen_recover_velocity": (ctypes.c_int, [ctypes.POINTER(ShenRecoverArgs), _vp]),
     "shen_scale_lines": (ctypes.c_int, [_c_int64, _c_int64, _vp, _vp, _vp, _vp, _vp]),
     "shen_cross": (ctypes.c_int, [_c_int64, _vp, _vp, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),

@@ -342,4 +342,18 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream) {
   return cuda_check(shen::launch_cross(n, fields, h, S(stream)), "shen_cross");
 }
 
+int shen_recover_velocity(const shen_recover_args* r, void* stream) {
+  if (!r) return fail(SHEN_ERR_ARG, "shen_recover_velocity: NULL args");
+  if (r->L == 0 || r->n_dir == 0) return SHEN_OK;
+  if (r->n_dir < 0 || r->L < 0 || !band_ok(r->deriv) || r->deriv.nr != r->n_dir || !r->fac ||
+      r->mmax < (r->n_dir + 1) / 2 || !r->im_m_re || !r->im_m_im || !r->im_n_re || !r->im_n_im || !r->safe_z2 ||
+      !r->u || !r->g || !r->v || !r->w)
+    return fail(SHEN_ERR_ARG, "shen_recover_velocity: bad args");
+  shen::RecoverArgs a{};
+  a.n_dir = r->n_dir; a.L = r->L; a.d = to_band(r->deriv); a.fac = r->fac; a.mmax = r->mmax;
+  a.im_m_re = r->im_m_re; a.im_m_im = r->im_m_im; a.im_n_re = r->im_n_re; a.im_n_im = r->im_n_im;
+  a.safe_z2 = r->safe_z2; a.u = r->u; a.g = r->g; a.v = r->v; a.w = r->w;
+  return cuda_check(shen::launch_recover(a, S(stream)), "shen_recover_velocity");
+}
+
 }  // extern "C"

@@ -156,6 +156,19 @@ struct RhsUArgs {
 cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st);
 cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st);
 
+// velocity recovery (shen_recover.cu)
+struct RecoverArgs {
+  int n_dir;
+  int64_t L;
+  RhsBand d;          // deriv_bih_to_dir
+  const double* fac;  // mass_dir per-parity Cholesky, [2][2][mmax] upper band storage
+  int mmax;
+  const double *im_m_re, *im_m_im, *im_n_re, *im_n_im, *safe_z2;  // per line
+  const void *u, *g;
+  void *v, *w;
+};
+cudaError_t launch_recover(const RecoverArgs& a, cudaStream_t st);
+
 // nonlinear-term pointwise kernels (shen_nonlinear.cu)
 cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const double* cre, const double* cim, void* y,
                                cudaStream_t st);

@@ -192,6 +192,12 @@ def rhs_fixture():
         for i in range(3):
             out[f"{key}_nl{i}"] = nl[i].data
         out[key + "_v"], out[key + "_w"], out[key + "_mask"] = v.data, w.data, st.mask
+        # velocity recovery lines of stepper.py:296-303 with the reference's own functions
+        f_scal = st.mats.deriv_bih_to_dir.apply(u.data)
+        f_hat = RT.mass_solve(f_scal, Space.DIRICHLET, mesh.n_x, mesh.family)
+        safe_z2 = np.where(st.z2 > 0, st.z2, 1.0)
+        out[key + "_vrec"] = (1j * st.m * f_hat + 1j * st.n * g.data) / safe_z2
+        out[key + "_wrec"] = (1j * st.n * f_hat - 1j * st.m * g.data) / safe_z2
     np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
 
 

@@ -133,3 +133,18 @@ def test_oracle_rhs_assembly_bitwise(golden, fi):
     args = (mats, 1e-2, 1e-3, g[k + "_z2"], g[k + "_m"], g[k + "_n"])
     assert np.array_equal(O.assemble_rhs_u(*args, g[k + "_u"], hab), g[k + "_rhs_u"])
     assert np.array_equal(O.assemble_rhs_g(*args, g[k + "_g"], hab), g[k + "_rhs_g"])
+
+
+@pytest.mark.parametrize("fi", [0, 1])
+def test_oracle_nonlinear_and_recovery_bitwise(golden, fi):
+    """stepper.py:148-185 (compute_nonlinear) and :296-303 (velocity
+    recovery) restated: equal to the reference's outputs bit for bit."""
+    g = golden("rhs.npz")
+    k = f"f{fi}"
+    mats = assemble(16, fi)
+    nl = O.compute_nonlinear(mats, fi == 1, 8, 8, g[k + "_m"], g[k + "_n"], g[k + "_mask"], g[k + "_u"],
+                             g[k + "_v"], g[k + "_w"], g[k + "_g"])
+    for i in range(3):
+        assert np.array_equal(nl[i], g[f"{k}_nl{i}"])
+    v, w = O.recover_velocity(mats, g[k + "_z2"], g[k + "_m"], g[k + "_n"], g[k + "_u"], g[k + "_g"])
+    assert np.array_equal(v, g[k + "_vrec"]) and np.array_equal(w, g[k + "_wrec"])
