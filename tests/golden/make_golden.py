@@ -198,6 +198,11 @@ def rhs_fixture():
         safe_z2 = np.where(st.z2 > 0, st.z2, 1.0)
         out[key + "_vrec"] = (1j * st.m * f_hat + 1j * st.n * g.data) / safe_z2
         out[key + "_wrec"] = (1j * st.n * f_hat - 1j * st.m * g.data) / safe_z2
+        # a reference checkpoint of the same state (wire-format fixture)
+        from chebchan.stepper import save_checkpoint
+
+        save_checkpoint(os.path.join(OUT, f"checkpoint_f{fi}.bin"),
+                        FlowState(u, v, w, g, hc, hp, 0.25, 1.5, 7), StepperConfig(nu=1e-2, dt=1e-3))
     np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
 
 
