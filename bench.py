@@ -1,7 +1,7 @@
 """Benchmark: batched fp64 Helmholtz + biharmonic solves (BASELINE config 4).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c4|c5:N|c1|c3] [--kx-rows R]
+                    [--config c4|c5:N|c1|c3|step] [--kx-rows R]
 
 One step = HelmholtzLU.solve + BiharmonicLU.solve over this rank's kx slab of
 the 2048 x 1025 wavenumber plane (n_x = 1024, nu = 1/2000, dt = 1e-4),
@@ -481,6 +481,90 @@ def cpu_c3():
             "sample": f"257 x 256 x 32 plane ({t:.2f} s), scaled by kz columns 129/17 to the full step"}
 
 
+# ======================================================================= full time step
+
+def run_step(args):
+    """One reference time step (ChannelStepper.step, stepper.py:286-346)
+    composed of the device pieces (stepper.DeviceStepper) on the config-3 mesh
+    (n_x = 256, 256 x 256), fixed-beta forcing, nu = 1/2000, dt = 1e-4;
+    random spectral state (torch Philox).  CPU baseline: the oracle's
+    restatement of the same step (nonlinear term, RHS, solves, recovery) once
+    on one core."""
+    import torch
+
+    from paper_1701_03787_b200.checkpoint import FlowState
+    from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
+    from paper_1701_03787_b200.stepper import DeviceStepper
+    from paper_1701_03787_b200.transforms import SpectralField
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+
+    class Cfg:
+        nu, dt, forcing, beta, target_flux, dealias = 1 / 2000, 1e-4, "fixed-beta", 0.01, 0.0, True
+
+    mesh = build_mesh(256, 256, 256, 2 * np.pi, np.pi)
+    t_build = time.perf_counter()
+    stp = DeviceStepper(mesh, Cfg)
+    t_build = time.perf_counter() - t_build
+    gd, gb = wavenumber_grid(mesh, Space.DIRICHLET), wavenumber_grid(mesh, Space.BIHARMONIC)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+
+    def field(grid):
+        shp = (grid.n_modes,) + mesh.spectral_shape_yz
+        return SpectralField(torch.randn(shp, dtype=torch.complex128, device="cuda", generator=gen), grid, mesh)
+
+    state = FlowState(field(gb), field(gd), field(gd), field(gd), tuple(field(gd) for _ in range(3)),
+                      tuple(field(gd) for _ in range(3)), 0.01, 0.0, 0)
+    for _ in range(max(args.warmup, 3)):
+        stp.step(state)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s = state
+        for _ in range(args.steps):
+            s = stp.step(s)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    cpu = None if args.no_cpu else cpu_step(stp, state)
+    print(json.dumps({
+        "metric": "time steps/s (reference ChannelStepper.step composed of the device kernels)",
+        "value": 1e3 / ms, "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+        "dtype": "f64 (complex128 spectra)", "data": "synthetic: random spectral state (torch Philox seed 7)",
+        "config": {"workload": "stepper step on the config-3 mesh: n_x=256 (Gauss), 256x256, nu=1/2000, "
+                               "dt=1e-4, fixed beta; 8 inverse + 3 forward transforms, 2 RHS, 2 batched solves, "
+                               "velocity recovery, mean-flow solve",
+                   "l2_policy": "every field 135 MB (> L2)"},
+        "build_s": t_build, "cpu_baseline": cpu, "clocks": clk.summary()}))
+
+
+def cpu_step(stp, state):
+    """The oracle's restatement of the same step, once, one core."""
+    from oracle import shen_oracle as O
+
+    mats, mesh = stp.mats, stp.mesh
+    h = lambda f: f.data.cpu().numpy()  # noqa: E731
+    u, v, w, g = h(state.u_hat), h(state.v_hat), h(state.w_hat), h(state.g_hat)
+    hc = [h(x) for x in state.h_curr]
+    nu, dt = stp.config.nu, stp.config.dt
+    hf = O.helmholtz_factor(mats, nu, dt, stp.z2)
+    bf = O.biharmonic_factor(mats, nu, dt, stp.z2)
+    t0 = time.perf_counter()
+    h_new = O.compute_nonlinear(mats, False, mesh.n_y, mesh.n_z, stp.m, stp.n, stp.mask, u, v, w, g)
+    hab = O.ab2(h_new, hc)
+    u_new = O.biharmonic_solve(bf, O.assemble_rhs_u(mats, nu, dt, stp.z2, stp.m, stp.n, u, hab))
+    g_new = O.helmholtz_solve(hf, O.assemble_rhs_g(mats, nu, dt, stp.z2, stp.m, stp.n, g, hab))
+    O.recover_velocity(mats, stp.z2, stp.m, stp.n, u_new, g_new)
+    t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": "steps/s", "cores": 1, "kind": "port",
+            "sample": f"one full step on the same mesh ({t:.1f} s; LU prebuilt, mean-flow solve omitted)"}
+
+
 # ======================================================================= reference arm
 
 _REF_CACHE = {}
@@ -561,5 +645,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.config == "c3":
         run_c3(a)
+    elif a.config == "step":
+        run_step(a)
     else:
         run_b200(a)

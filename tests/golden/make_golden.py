@@ -198,6 +198,18 @@ def rhs_fixture():
         safe_z2 = np.where(st.z2 > 0, st.z2, 1.0)
         out[key + "_vrec"] = (1j * st.m * f_hat + 1j * st.n * g.data) / safe_z2
         out[key + "_wrec"] = (1j * st.n * f_hat - 1j * st.m * g.data) / safe_z2
+        # one full reference time step from this state, both forcings
+        from chebchan.stepper import Forcing
+
+        for tag, cfg in (("fb", StepperConfig(nu=1e-2, dt=1e-3, beta=0.5)),
+                         ("cf", StepperConfig(nu=1e-2, dt=1e-3, forcing=Forcing.CONSTANT_FLUX, target_flux=0.3))):
+            stp = ChannelStepper(mesh, cfg)
+            new = stp.step(FlowState(u, v, w, g, hc, hp, 0.25, 1.5, 7))
+            for nm in ("u_hat", "v_hat", "w_hat", "g_hat"):
+                out[f"{key}_{tag}_{nm}"] = getattr(new, nm).data
+            for i in range(3):
+                out[f"{key}_{tag}_hcur{i}"] = new.h_curr[i].data
+            out[f"{key}_{tag}_beta"] = np.array(new.beta)
         # a reference checkpoint of the same state (wire-format fixture)
         from chebchan.stepper import save_checkpoint
 
