@@ -213,6 +213,46 @@ __device__ __forceinline__ void load_bih_row_compact(const double* stab, int k, 
   c[B_BB4M] = stab[(int64_t)k * BC_STRIDE + BC_BB4];
 }
 
+// Sliding variant for consecutive rows k, k+2, k+4, ... of one parity: the
+// row-(k-2) / row-(k-4) entries are the previous rows' own values, so they
+// are carried in registers instead of re-read (7 instead of 10 shared loads
+// per row).  bih_carry_init loads them for the first row of a run.
+struct BihCarry {
+  double q4, s4, bb2, bb4, bb4_prev;  // rows k-2 (q4, s4, bb2, bb4) and k-4 (bb4_prev)
+};
+__device__ __forceinline__ void bih_carry_init(const double* stab, int k, BihCarry& cr) {
+  const double* rm2 = stab + (int64_t)(k + 2) * BC_STRIDE;
+  const double2 qs = *reinterpret_cast<const double2*>(rm2 + BC_Q4);
+  cr.q4 = qs.x;
+  cr.s4 = qs.y;
+  cr.bb2 = rm2[BC_BB2];
+  cr.bb4 = rm2[BC_BB4];
+  cr.bb4_prev = stab[(int64_t)k * BC_STRIDE + BC_BB4];
+}
+__device__ __forceinline__ void load_bih_row_carry(const double* stab, int k, double* c, BihCarry& cr) {
+  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE);
+  double v[BC_STRIDE];
+#pragma unroll
+  for (int q = 0; q < BC_STRIDE / 2; ++q) {
+    const double2 t = r0[q];
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+  c[B_Q0] = v[BC_Q0]; c[B_AR0] = v[BC_AR0]; c[B_BB0] = v[BC_BB0];
+  c[B_T2] = v[BC_T2]; c[B_AR2] = v[BC_AR2]; c[B_BB2] = v[BC_BB2];
+  c[B_T4] = v[BC_T4]; c[B_BB4] = v[BC_BB4]; c[B_ARM2] = v[BC_ARM2];
+  c[B_P] = v[BC_P]; c[B_R] = v[BC_R]; c[B_Q4] = v[BC_Q4]; c[B_S4] = v[BC_S4];
+  c[B_Q2] = cr.q4;
+  c[B_S2] = cr.s4;
+  c[B_BB2M] = cr.bb2;
+  c[B_BB4M] = cr.bb4_prev;
+  cr.bb4_prev = cr.bb4;
+  cr.q4 = v[BC_Q4];
+  cr.s4 = v[BC_S4];
+  cr.bb2 = v[BC_BB2];
+  cr.bb4 = v[BC_BB4];
+}
+
 struct BihBands {
   double hd, hp2, hp4, hm2, hm4;
 };

@@ -111,13 +111,15 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
     const int64_t j = jb + ref.g * (32 * SG) + sgi * 32 + lane;
     const bool jv = j < je;
     const int64_t jc = jv ? j : je - 1;
-    const V* src = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
+    const V* p = rhs + (int64_t)(par + 2 * ref.s * R) * B + jc;
     const int64_t step = 2 * B;
     const int rows = min(R, n - ref.s * R);
+    // walk the rows with pointer increments; rows past the end re-use the
+    // last valid address with a zero-fill (src-size 0) copy
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool ok = jv && r < rows;
-      cpa(slot + r * 32, ok ? src + r * step : src, ok);
+      cpa(slot + r * 32, p, jv && r < rows);
+      if (r + 1 < rows) p += step;
     }
   }
   cpa_commit();
@@ -359,13 +361,16 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     V y1 = szero<V>(), y2 = szero<V>();
     auto fwd_seg = [&](int s, auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
+      constexpr bool CARRY = FULL && SMEM_TAB;  // k-2 / k-4 entries from registers
       const V* cur = consume();
+      BihCarry cr;
+      if (CARRY) bih_carry_init(stab, par + 2 * s * R, cr);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
         const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-        row_consts(k, c);
+        if (CARRY) load_bih_row_carry(stab, k, c, cr); else row_consts(k, c);
         if (!SMEM_TAB) bih_fast_prescale(c, xi0);  // the compact table is pre-scaled
         const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
@@ -416,6 +421,9 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       }
       if (PF && s - 1 > 0) load_ck(s - 1);
       V* cur = consume();
+      constexpr bool CARRY = FULL && SMEM_TAB;
+      BihCarry cr;
+      if (CARRY) bih_carry_init(stab, par + 2 * s * R, cr);
       // U-row entries pre-multiplied by 1/d (rows past n get 0, so x = 0 there):
       // x_i = y~_i - e~_i x_{i+1} - f~_i x_{i+2} - a~_i S_q - b~_i S_s
       double e_[R], f_[R], a_[R], b_[R];
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         const int i = s * R + r;
         const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         double c[B_NCOL];
-        row_consts(k, c);
+        if (CARRY) load_bih_row_carry(stab, k, c, cr); else row_consts(k, c);
         if (!SMEM_TAB) bih_fast_prescale(c, xi0);
         const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
