@@ -54,6 +54,17 @@ __device__ __forceinline__ void cpa(double* dst, const double* src, bool pred) {
   const int n = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(n) : "memory");
 }
+// y checkpoints: written in the forward sweep, read once in the backward;
+// kept in L2 (evict_last) so the small per-CTA scratch does not round-trip
+// through HBM (SHEN_YCKPT_KEEP=0 disables the hint)
+#ifndef SHEN_YCKPT_KEEP
+#define SHEN_YCKPT_KEEP 1
+#endif
+template <typename V>
+__device__ __forceinline__ void ystore(V* p, V v) {
+  if (SHEN_YCKPT_KEEP) st_keep(p, v, policy_evict_last());
+  else *p = v;
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
         const V b = (full || i < n) ? cur[r * 32] : szero<V>();
         y = sfma(-low, y, b);
       }
-      if (s + 1 < nseg) ychkj[s * kT] = y;
+      if (s + 1 < nseg) ystore(ychkj + s * kT, y);
     }
     // ---------------- backward: re-stream each segment (bottom first)
     V x1 = szero<V>(), S = szero<V>();
@@ -387,8 +398,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     for (int s = 0; s < nseg; ++s) {
       if (s < nfull) fwd_seg(s, Full{}); else fwd_seg(s, Part{});
       if (s + 1 < nseg) {
-        ychkj[(2 * s) * kT] = y1;
-        ychkj[(2 * s + 1) * kT] = y2;
+        ystore(ychkj + (2 * s) * kT, y1);
+        ystore(ychkj + (2 * s + 1) * kT, y2);
       }
     }
     // ---------------- backward
