@@ -192,8 +192,10 @@ __host__ __device__ constexpr int bc_src(int col) {  // 18-column source of comp
 }
 static_assert(BC_BB4 == B_BB4 && BC_Q0 == B_Q0, "compact columns 0..7 mirror the full table");
 
-__device__ __forceinline__ void load_bih_row_compact(const double* stab, int k, double* c) {
-  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE);
+// pos = table position of the row, step = positions between rows k-2 and k
+// (2 in the both-parity table, whose position is k + 4; 1 in a one-parity table)
+__device__ __forceinline__ void load_bih_row_compact(const double* stab, int pos, int step, double* c) {
+  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)pos * BC_STRIDE);
   double v[BC_STRIDE];
 #pragma unroll
   for (int q = 0; q < BC_STRIDE / 2; ++q) {
@@ -205,12 +207,12 @@ __device__ __forceinline__ void load_bih_row_compact(const double* stab, int k, 
   c[B_T2] = v[BC_T2]; c[B_AR2] = v[BC_AR2]; c[B_BB2] = v[BC_BB2];
   c[B_T4] = v[BC_T4]; c[B_BB4] = v[BC_BB4]; c[B_ARM2] = v[BC_ARM2];
   c[B_P] = v[BC_P]; c[B_R] = v[BC_R]; c[B_Q4] = v[BC_Q4]; c[B_S4] = v[BC_S4];
-  const double* rm2 = stab + (int64_t)(k + 2) * BC_STRIDE;
+  const double* rm2 = stab + (int64_t)(pos - step) * BC_STRIDE;
   const double2 qs = *reinterpret_cast<const double2*>(rm2 + BC_Q4);
   c[B_Q2] = qs.x;
   c[B_S2] = qs.y;
   c[B_BB2M] = rm2[BC_BB2];
-  c[B_BB4M] = stab[(int64_t)k * BC_STRIDE + BC_BB4];
+  c[B_BB4M] = stab[(int64_t)(pos - 2 * step) * BC_STRIDE + BC_BB4];
 }
 
 // Sliding variant for consecutive rows k, k+2, k+4, ... of one parity: the
@@ -220,17 +222,17 @@ __device__ __forceinline__ void load_bih_row_compact(const double* stab, int k, 
 struct BihCarry {
   double q4, s4, bb2, bb4, bb4_prev;  // rows k-2 (q4, s4, bb2, bb4) and k-4 (bb4_prev)
 };
-__device__ __forceinline__ void bih_carry_init(const double* stab, int k, BihCarry& cr) {
-  const double* rm2 = stab + (int64_t)(k + 2) * BC_STRIDE;
+__device__ __forceinline__ void bih_carry_init(const double* stab, int pos, int step, BihCarry& cr) {
+  const double* rm2 = stab + (int64_t)(pos - step) * BC_STRIDE;
   const double2 qs = *reinterpret_cast<const double2*>(rm2 + BC_Q4);
   cr.q4 = qs.x;
   cr.s4 = qs.y;
   cr.bb2 = rm2[BC_BB2];
   cr.bb4 = rm2[BC_BB4];
-  cr.bb4_prev = stab[(int64_t)k * BC_STRIDE + BC_BB4];
+  cr.bb4_prev = stab[(int64_t)(pos - 2 * step) * BC_STRIDE + BC_BB4];
 }
-__device__ __forceinline__ void load_bih_row_carry(const double* stab, int k, double* c, BihCarry& cr) {
-  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE);
+__device__ __forceinline__ void load_bih_row_carry(const double* stab, int pos, double* c, BihCarry& cr) {
+  const double2* r0 = reinterpret_cast<const double2*>(stab + (int64_t)pos * BC_STRIDE);
   double v[BC_STRIDE];
 #pragma unroll
   for (int q = 0; q < BC_STRIDE / 2; ++q) {

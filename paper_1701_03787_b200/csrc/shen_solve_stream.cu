@@ -283,12 +283,17 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
 }
 
 // ======================================================================= biharmonic
-template <typename V, int R, bool SMEM_TAB, int RING, int SG>
+// PP: one parity per CTA (even CTAs parity 0, odd parity 1) with a one-parity
+// row table -- half the shared memory, used when the both-parity table does
+// not fit (n_x >= ~1800).
+template <typename V, int R, bool SMEM_TAB, int RING, int SG, bool PP>
 __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, V* ychk) {
   constexpr int kT = 64 * SG;
+  constexpr int SGE = PP ? 2 * SG : SG;  // 32-system groups per CTA work item
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int par = PP ? (int)(blockIdx.x & 1) : (warp & 1), sgi = PP ? warp : (warp >> 1);
   const int64_t B = a.batch;
   const int nb = a.n_bih;
   const int n = (nb - par + 1) / 2;
@@ -299,7 +304,22 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   // path.  The compact rows keep the 13 per-mode values; the m-band and q/s
   // lookahead entries are read from rows k-2 / k-4 (4 virtual rows in front).
   double* stab = smem + (size_t)kT / 32 * RING * R * 32 * VOps<V>::ndouble;
-  if (SMEM_TAB) {
+  if (SMEM_TAB && PP) {
+    // one parity: position i + 2 holds parity row i (mode par + 2 i); two virtual rows in front
+    for (int q = tid; q < (n + 2) * BC_STRIDE; q += kT) {
+      const int pos = q / BC_STRIDE, col = q - pos * BC_STRIDE, i = pos - 2;
+      double v = 0.0;
+      if (i >= 0 && col < BC_NCOL) {
+        v = __ldg(a.tab + (int64_t)(par + 2 * i) * B_STRIDE + bc_src(col));
+        if (col == BC_P || col == BC_R || col == BC_Q0 || col == BC_T2 || col == BC_T4)
+          v = __dmul_rn(a.xi0, v);  // == bih_fast_prescale
+      } else if (i == -1 && (col == BC_Q4 || col == BC_S4)) {
+        v = __ldg(a.tab + (int64_t)par * B_STRIDE + (col == BC_Q4 ? B_Q2 : B_S2));
+      }
+      stab[q] = v;
+    }
+    __syncthreads();
+  } else if (SMEM_TAB) {
     for (int q = tid; q < (nb + 4) * BC_STRIDE; q += kT) {
       const int kk = q / BC_STRIDE - 4, col = q - (kk + 4) * BC_STRIDE;
       double v = 0.0;
@@ -315,14 +335,18 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     __syncthreads();
   }
   const double* tab = a.tab;
-  auto row_consts = [&](int k, double* c) {
-    if (SMEM_TAB) load_bih_row_compact(stab, k, c); else load_bih_row(tab, k, c);
+  // table position of parity row i and the position step between rows k-2 and k
+  auto tpos = [&](int i) { return PP ? i + 2 : par + 2 * i + 4; };
+  constexpr int tstep = PP ? 1 : 2;
+  auto row_consts = [&](int i, double* c) {  // parity row i (mode par + 2 i)
+    if (SMEM_TAB) load_bih_row_compact(stab, tpos(i), tstep, c); else load_bih_row(tab, par + 2 * i, c);
   };
-  auto q4s4 = [&](int k, double& q4, double& s4) {
+  auto q4s4 = [&](int i, double& q4, double& s4) {
     if (SMEM_TAB) {
-      const double2 v = *reinterpret_cast<const double2*>(stab + (int64_t)(k + 4) * BC_STRIDE + BC_Q4);
+      const double2 v = *reinterpret_cast<const double2*>(stab + (int64_t)tpos(i) * BC_STRIDE + BC_Q4);
       q4 = v.x; s4 = v.y;
     } else {
+      const int k = par + 2 * i;
       q4 = tab[(int64_t)k * B_STRIDE + B_Q4];
       s4 = tab[(int64_t)k * B_STRIDE + B_S4];
     }
@@ -331,20 +355,21 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   V* out = static_cast<V*>(a.out);
   const double xi0 = a.xi0;
   const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;
-  const int64_t ngroups = (je - jb + 32 * SG - 1) / (32 * SG);
-  const int64_t g0 = blockIdx.x, gstride = gridDim.x;
+  const int64_t ngroups = (je - jb + 32 * SGE - 1) / (32 * SGE);
+  const int64_t g0 = PP ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t gstride = PP ? ((gridDim.x + 1 - par) >> 1) : gridDim.x;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SGE>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SGE>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
@@ -355,7 +380,7 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   };
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t j = jb + g * (32 * SG) + sgi * 32 + lane;
+    const int64_t j = jb + g * (32 * SGE) + sgi * 32 + lane;
     const bool jv = j < je;
     const int64_t jc = jv ? j : je - 1;
     const double xi1 = __ldg(a.xi1 + jc), xi2 = __ldg(a.xi2 + jc);
@@ -375,13 +400,13 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       constexpr bool CARRY = FULL && SMEM_TAB;  // k-2 / k-4 entries from registers
       const V* cur = consume();
       BihCarry cr;
-      if (CARRY) bih_carry_init(stab, par + 2 * s * R, cr);
+      if (CARRY) bih_carry_init(stab, tpos(s * R), tstep, cr);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
+        const int ic = FULL ? i : min(i, n - 1);
         double c[B_NCOL];
-        if (CARRY) load_bih_row_carry(stab, k, c, cr); else row_consts(k, c);
+        if (CARRY) load_bih_row_carry(stab, tpos(ic), c, cr); else row_consts(ic, c);
         if (!SMEM_TAB) bih_fast_prescale(c, xi0);  // the compact table is pre-scaled
         const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
@@ -434,16 +459,16 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       V* cur = consume();
       constexpr bool CARRY = FULL && SMEM_TAB;
       BihCarry cr;
-      if (CARRY) bih_carry_init(stab, par + 2 * s * R, cr);
+      if (CARRY) bih_carry_init(stab, tpos(s * R), tstep, cr);
       // U-row entries pre-multiplied by 1/d (rows past n get 0, so x = 0 there):
       // x_i = y~_i - e~_i x_{i+1} - f~_i x_{i+2} - a~_i S_q - b~_i S_s
       double e_[R], f_[R], a_[R], b_[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
-        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
+        const int ic = FULL ? i : min(i, n - 1);
         double c[B_NCOL];
-        if (CARRY) load_bih_row_carry(stab, k, c, cr); else row_consts(k, c);
+        if (CARRY) load_bih_row_carry(stab, tpos(ic), c, cr); else row_consts(ic, c);
         if (!SMEM_TAB) bih_fast_prescale(c, xi0);
         const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
@@ -465,10 +490,9 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
 #pragma unroll
       for (int r = R - 1; r >= 0; --r) {
         const int i = s * R + r;
-        const int k = FULL ? par + 2 * i : min(par + 2 * i, nb - 1);
         const bool valid = FULL || i < n;
         double qn, sn;
-        q4s4(k, qn, sn);
+        q4s4(FULL ? i : min(i, n - 1), qn, sn);
         if (!valid) qn = sn = 0.0;
         V x = sfma(-e_[r], x1, cur[r * 32]);
         x = sfma(-f_[r], x2, x);
@@ -535,17 +559,18 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   return helm_stream_RR<V, R, SG, 2>(a, scratch, ctas_per_sm, st);
 }
 
-template <typename V, int R, bool SMEM_TAB, int RING, int SG>
+template <typename V, int R, bool SMEM_TAB, int RING, int SG, bool PP = false>
 static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int ctas_per_sm, size_t smem,
                                      cudaStream_t st) {
   constexpr int kT = 64 * SG;
-  auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING, SG>;
+  constexpr int SGE = PP ? 2 * SG : SG;
+  auto kern = bih_stream_kernel<V, R, SMEM_TAB, RING, SG, PP>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const int occ = std::min(8, ctas_per_sm > 0 ? std::min(ctas_per_sm, resident_ctas(kern, smem)) : resident_ctas(kern, smem));
   const int64_t nsys = (a.je < 0 ? a.batch : a.je) - a.jb;
   if (nsys <= 0) return cudaSuccess;
-  const int64_t groups = (nsys + 32 * SG - 1) / (32 * SG);
+  const int64_t groups = (PP ? 2 : 1) * ((nsys + 32 * SGE - 1) / (32 * SGE));  // PP: one item per parity
   int64_t cap = stream_ctas(occ);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
@@ -560,7 +585,12 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
   // (a 3-deep ring measured slower at config 4: 29.5 vs 28.6 ms)
   const size_t ring2 = (size_t)2 * R * 64 * SG * sizeof(V);
   const size_t tabb = (size_t)(a.n_bih + 4) * BC_STRIDE * sizeof(double);
-  if (ring2 + tabb <= 220 * 1024) return bih_stream_launch<V, R, true, 2, SG>(a, scratch, ctas_per_sm, ring2 + tabb, st);
+  static const bool force_pp = getenv("SHEN_BIH_PP") != nullptr && atoi(getenv("SHEN_BIH_PP")) != 0;
+  if (!force_pp && ring2 + tabb <= 220 * 1024)
+    return bih_stream_launch<V, R, true, 2, SG>(a, scratch, ctas_per_sm, ring2 + tabb, st);
+  const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);  // one parity
+  if (ring2 + tabp <= 220 * 1024)
+    return bih_stream_launch<V, R, true, 2, SG, true>(a, scratch, ctas_per_sm, ring2 + tabp, st);
   return bih_stream_launch<V, R, false, kRing, 4>(a, scratch, ctas_per_sm, (size_t)kRing * R * 256 * sizeof(V), st);
 }
 
