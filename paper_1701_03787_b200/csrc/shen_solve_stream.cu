@@ -127,10 +127,18 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
     const int rows = min(R, n - ref.s * R);
     // walk the rows with pointer increments; rows past the end re-use the
     // last valid address with a zero-fill (src-size 0) copy
+    if (jv && rows == R) {  // every segment but the last: no per-row predicates
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      cpa(slot + r * 32, p, jv && r < rows);
-      if (r + 1 < rows) p += step;
+      for (int r = 0; r < R; ++r) {
+        cpa(slot + r * 32, p, true);
+        p += step;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        cpa(slot + r * 32, p, jv && r < rows);
+        if (r + 1 < rows) p += step;
+      }
     }
   }
   cpa_commit();
