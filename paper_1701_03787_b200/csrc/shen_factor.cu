@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) helm_factor_kernel(HelmFactorArgs a) {
   const double sub = __dmul_rn(cb, -1.5707963267948966);  // cb * (-pi/2)
   const int64_t B = a.batch;
   const int R = a.chunk_rows > 0 ? a.chunk_rows : (1 << 30);
-  HelmState s{0, 0, 0, 0};
+  HelmState s{0, 0, 0};
   HelmProj pj{0, 0, 0, 0, 0};
   double dl = 0.0, el = 0.0, tl = 0.0;  // ratios of the last row (fast mode)
   for (int i = 0; i < n; ++i) {
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) helm_factor_kernel(HelmFactorArgs a) {
     HelmRow h = helm_row(a.ca, cb, sub, __ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsup);
     double low, d, e, t;
     if (EXACT) {
-      low = helm_step<true>(s, h, sub, i == 0);
+      low = helm_step_exact(s, h, sub, i == 0);
       d = s.d; e = s.e; t = s.t;
     } else {
       const int r = i % R;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) bih_factor_kernel(BihFactorArgs a) {
     double l2, l4;
     if (EXACT) {
       const BihBands h = bih_bands(a.xi0, xi1, xi2, c);
-      bih_step<true>(u, u1, u2, h, c, a.xi0, i, l2, l4);
+      bih_step_exact(u, u1, u2, h, c, a.xi0, i, l2, l4);
     } else {
       bih_fast_prescale(c, a.xi0);
       const BihBands h = bih_bands_fast(xi1, xi2, c);

@@ -29,34 +29,25 @@ __device__ __forceinline__ HelmRow helm_row(double ca, double cb, double sub, do
   return h;
 }
 
-// Factor state after row i: d, e, t (+ reciprocal of d for the fast mode).
+// Factor state after row i: d, e, t.
 struct HelmState {
-  double d, e, t, rd;
+  double d, e, t;
 };
 
-// One elimination step (solvers.py:231-236).  Returns low (0 for row 0).
-template <bool EXACT>
-__device__ __forceinline__ double helm_step(HelmState& s, const HelmRow& h, double sub, bool first) {
+// One exact-mode elimination step (solvers.py:231-236): numpy's evaluation
+// order, IEEE division, no contraction.  Returns low (0 for row 0).  The fast
+// mode is the projective walk below (hp_step).
+__device__ __forceinline__ double helm_step_exact(HelmState& s, const HelmRow& h, double sub, bool first) {
   if (first) {
     s.d = h.diag;
     s.e = h.sup;
     s.t = h.tail;
-    s.rd = EXACT ? 0.0 : __drcp_rn(s.d);
     return 0.0;
   }
-  double low;
-  if (EXACT) {
-    low = __ddiv_rn(sub, s.d);
-    s.d = __dsub_rn(h.diag, __dmul_rn(low, s.e));
-    s.e = __dsub_rn(h.sup, __dmul_rn(low, s.t));
-    s.t = __dsub_rn(h.tail, __dmul_rn(low, s.t));
-  } else {
-    low = __dmul_rn(sub, s.rd);
-    s.d = __fma_rn(-low, s.e, h.diag);
-    s.e = __fma_rn(-low, s.t, h.sup);
-    s.t = __fma_rn(-low, s.t, h.tail);
-    s.rd = __drcp_rn(s.d);
-  }
+  const double low = __ddiv_rn(sub, s.d);
+  s.d = __dsub_rn(h.diag, __dmul_rn(low, s.e));
+  s.e = __dsub_rn(h.sup, __dmul_rn(low, s.t));
+  s.t = __dsub_rn(h.tail, __dmul_rn(low, s.t));
   return low;
 }
 
@@ -275,11 +266,11 @@ struct BihU {
   double d, e, f, a, b, rd;
 };
 
-// One elimination step, rows i-1 (u1) and i-2 (u2) already eliminated
-// (solvers.py:314-346).  i is the row within the parity.  Returns l2, l4.
-template <bool EXACT>
-__device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2, const BihBands& h, const double* c,
-                                         double xi0, int i, double& l2, double& l4) {
+// One exact-mode elimination step, rows i-1 (u1) and i-2 (u2) already
+// eliminated (solvers.py:314-346), numpy's evaluation order.  i is the row
+// within the parity.  Returns l2, l4.  (Fast mode: bih_step_fast below.)
+__device__ __forceinline__ void bih_step_exact(BihU& u, const BihU& u1, const BihU& u2, const BihBands& h,
+                                               const double* c, double xi0, int i, double& l2, double& l4) {
   if (i == 0) {
     u.d = h.hd;
     u.e = h.hp2;
@@ -290,51 +281,27 @@ __device__ __forceinline__ void bih_step(BihU& u, const BihU& u1, const BihU& u2
     l4 = 0.0;
   } else if (i == 1) {
     l4 = 0.0;
-    if (EXACT) {
-      l2 = __ddiv_rn(h.hm2, u1.d);
-      double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
-      u.d = __dsub_rn(h.hd, __dmul_rn(l2, u1.e));
-      u.e = __dsub_rn(h.hp2, __dmul_rn(l2, u1.f));
-      u.f = __dsub_rn(h.hp4, __dmul_rn(l2, u24));
-      u.a = __dsub_rn(c[B_P], __dmul_rn(l2, u1.a));
-      u.b = __dsub_rn(c[B_R], __dmul_rn(l2, u1.b));
-    } else {
-      l2 = __dmul_rn(h.hm2, u1.rd);
-      double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
-      u.d = __fma_rn(-l2, u1.e, h.hd);
-      u.e = __fma_rn(-l2, u1.f, h.hp2);
-      u.f = __fma_rn(-l2, u24, h.hp4);
-      u.a = __fma_rn(-l2, u1.a, c[B_P]);
-      u.b = __fma_rn(-l2, u1.b, c[B_R]);
-    }
+    l2 = __ddiv_rn(h.hm2, u1.d);
+    const double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
+    u.d = __dsub_rn(h.hd, __dmul_rn(l2, u1.e));
+    u.e = __dsub_rn(h.hp2, __dmul_rn(l2, u1.f));
+    u.f = __dsub_rn(h.hp4, __dmul_rn(l2, u24));
+    u.a = __dsub_rn(c[B_P], __dmul_rn(l2, u1.a));
+    u.b = __dsub_rn(c[B_R], __dmul_rn(l2, u1.b));
   } else {
-    if (EXACT) {
-      l4 = __ddiv_rn(h.hm4, u2.d);
-      double tmp = __dsub_rn(h.hm2, __dmul_rn(l4, u2.e));
-      l2 = __ddiv_rn(tmp, u1.d);
-      double u42 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q2]), __dmul_rn(u2.b, c[B_S2])));
-      double u44 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q4]), __dmul_rn(u2.b, c[B_S4])));
-      double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
-      u.d = __dsub_rn(__dsub_rn(h.hd, __dmul_rn(l4, u2.f)), __dmul_rn(l2, u1.e));
-      u.e = __dsub_rn(__dsub_rn(h.hp2, __dmul_rn(l4, u42)), __dmul_rn(l2, u1.f));
-      u.f = __dsub_rn(__dsub_rn(h.hp4, __dmul_rn(l4, u44)), __dmul_rn(l2, u24));
-      u.a = __dsub_rn(__dsub_rn(c[B_P], __dmul_rn(l2, u1.a)), __dmul_rn(l4, u2.a));
-      u.b = __dsub_rn(__dsub_rn(c[B_R], __dmul_rn(l2, u1.b)), __dmul_rn(l4, u2.b));
-    } else {
-      l4 = __dmul_rn(h.hm4, u2.rd);
-      double tmp = __fma_rn(-l4, u2.e, h.hm2);
-      l2 = __dmul_rn(tmp, u1.rd);
-      double u42 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2])));
-      double u44 = __dmul_rn(xi0, __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4])));
-      double u24 = __dmul_rn(xi0, __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4])));
-      u.d = __fma_rn(-l2, u1.e, __fma_rn(-l4, u2.f, h.hd));
-      u.e = __fma_rn(-l2, u1.f, __fma_rn(-l4, u42, h.hp2));
-      u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
-      u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
-      u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
-    }
+    l4 = __ddiv_rn(h.hm4, u2.d);
+    const double tmp = __dsub_rn(h.hm2, __dmul_rn(l4, u2.e));
+    l2 = __ddiv_rn(tmp, u1.d);
+    const double u42 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q2]), __dmul_rn(u2.b, c[B_S2])));
+    const double u44 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u2.a, c[B_Q4]), __dmul_rn(u2.b, c[B_S4])));
+    const double u24 = __dmul_rn(xi0, __dadd_rn(__dmul_rn(u1.a, c[B_Q4]), __dmul_rn(u1.b, c[B_S4])));
+    u.d = __dsub_rn(__dsub_rn(h.hd, __dmul_rn(l4, u2.f)), __dmul_rn(l2, u1.e));
+    u.e = __dsub_rn(__dsub_rn(h.hp2, __dmul_rn(l4, u42)), __dmul_rn(l2, u1.f));
+    u.f = __dsub_rn(__dsub_rn(h.hp4, __dmul_rn(l4, u44)), __dmul_rn(l2, u24));
+    u.a = __dsub_rn(__dsub_rn(c[B_P], __dmul_rn(l2, u1.a)), __dmul_rn(l4, u2.a));
+    u.b = __dsub_rn(__dsub_rn(c[B_R], __dmul_rn(l2, u1.b)), __dmul_rn(l4, u2.b));
   }
-  u.rd = EXACT ? 0.0 : rcp_fast(u.d);
+  u.rd = 0.0;
 }
 
 // ---- fast mode (build checkpoints, chunked and streaming solves) ----------

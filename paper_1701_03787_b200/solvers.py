@@ -35,7 +35,6 @@ import numpy as np
 from . import _device as dv
 from ._lib import check, lib, ptr_array
 from .matrices import MatrixSet, tail_factors
-from .mesh import as_family
 
 __all__ = [
     "HelmholtzLU",
@@ -653,5 +652,3 @@ def solve_field(lu, field):
 
     return SpectralField(lu.solve(field.data), field.grid, field.mesh)
 
-
-_ = as_family  # re-exported helper used by callers that pass foreign enums
