@@ -353,4 +353,48 @@ __device__ __forceinline__ void bih_step_fast(BihU& u, const BihU& u1, const Bih
   u.rd = rcp_fast(u.d);
 }
 
+// Row step for consecutive rows of one parity with the products that repeat
+// between rows carried in registers (same operations on the same operands as
+// bih_bands_fast + bih_step_fast, so bit-identical results):
+//   xi2 BB2(k-2) and xi2 BB4(k-4) of hm2 / hm4 are the previous rows'
+//   xi2 BB2 / xi2 BB4 products of hp2 / hp4;
+//   u42 of row i (a, b of row i-2 against q, s of mode k+2) is u24 of row i-1.
+struct BihProd {
+  double x2bb2, x2bb4, x2bb4_prev, u42;
+};
+__device__ __forceinline__ void bih_prod_init(double xi2, const BihCarry& cr, BihProd& pr) {
+  pr.x2bb2 = __dmul_rn(xi2, cr.bb2);
+  pr.x2bb4 = __dmul_rn(xi2, cr.bb4);
+  pr.x2bb4_prev = __dmul_rn(xi2, cr.bb4_prev);
+  pr.u42 = 0.0;
+}
+__device__ __forceinline__ void bih_row_fast_carried(BihU& u, const BihU& u1, const BihU& u2, const double* c,
+                                                     double xi1, double xi2, BihProd& pr, bool first, double& l2,
+                                                     double& l4) {
+  const double x2bb2 = __dmul_rn(xi2, c[B_BB2]);
+  const double x2bb4 = __dmul_rn(xi2, c[B_BB4]);
+  BihBands h;
+  h.hd = __dadd_rn(__dadd_rn(c[B_Q0], __dmul_rn(xi1, c[B_AR0])), __dmul_rn(xi2, c[B_BB0]));
+  h.hp2 = __dadd_rn(__dadd_rn(c[B_T2], __dmul_rn(xi1, c[B_AR2])), x2bb2);
+  h.hp4 = __dadd_rn(c[B_T4], x2bb4);
+  h.hm2 = __dadd_rn(__dmul_rn(xi1, c[B_ARM2]), pr.x2bb2);
+  h.hm4 = pr.x2bb4_prev;
+  l4 = __dmul_rn(h.hm4, u2.rd);
+  const double tmp = __fma_rn(-l4, u2.e, h.hm2);
+  l2 = __dmul_rn(tmp, u1.rd);
+  const double u42 = first ? __fma_rn(u2.a, c[B_Q2], __dmul_rn(u2.b, c[B_S2])) : pr.u42;
+  const double u44 = __fma_rn(u2.a, c[B_Q4], __dmul_rn(u2.b, c[B_S4]));
+  const double u24 = __fma_rn(u1.a, c[B_Q4], __dmul_rn(u1.b, c[B_S4]));
+  u.d = __fma_rn(-l2, u1.e, __fma_rn(-l4, u2.f, h.hd));
+  u.e = __fma_rn(-l2, u1.f, __fma_rn(-l4, u42, h.hp2));
+  u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
+  u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
+  u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
+  u.rd = rcp_fast(u.d);
+  pr.u42 = u24;
+  pr.x2bb4_prev = pr.x2bb4;
+  pr.x2bb4 = x2bb4;
+  pr.x2bb2 = x2bb2;
+}
+
 }  // namespace shen

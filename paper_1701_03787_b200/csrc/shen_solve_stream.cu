@@ -408,17 +408,26 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       constexpr bool CARRY = FULL && SMEM_TAB;  // k-2 / k-4 entries from registers
       const V* cur = consume();
       BihCarry cr;
-      if (CARRY) bih_carry_init(stab, tpos(s * R), tstep, cr);
+      BihProd pr;
+      if (CARRY) {
+        bih_carry_init(stab, tpos(s * R), tstep, cr);
+        bih_prod_init(xi2, cr, pr);
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = s * R + r;
         const int ic = FULL ? i : min(i, n - 1);
         double c[B_NCOL];
-        if (CARRY) load_bih_row_carry(stab, tpos(ic), c, cr); else row_consts(ic, c);
-        if (!SMEM_TAB) bih_fast_prescale(c, xi0);  // the compact table is pre-scaled
-        const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
-        bih_step_fast(u, u1, u2, hb, c, l2, l4);
+        if (CARRY) {
+          load_bih_row_carry(stab, tpos(ic), c, cr);
+          bih_row_fast_carried(u, u1, u2, c, xi1, xi2, pr, r == 0, l2, l4);
+        } else {
+          row_consts(ic, c);
+          if (!SMEM_TAB) bih_fast_prescale(c, xi0);  // the compact table is pre-scaled
+          const BihBands hb = bih_bands_fast(xi1, xi2, c);
+          bih_step_fast(u, u1, u2, hb, c, l2, l4);
+        }
         u2 = u1;
         u1 = u;
         const V b = (FULL || i < n) ? cur[r * 32] : szero<V>();
@@ -467,7 +476,11 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
       V* cur = consume();
       constexpr bool CARRY = FULL && SMEM_TAB;
       BihCarry cr;
-      if (CARRY) bih_carry_init(stab, tpos(s * R), tstep, cr);
+      BihProd pr;
+      if (CARRY) {
+        bih_carry_init(stab, tpos(s * R), tstep, cr);
+        bih_prod_init(xi2, cr, pr);
+      }
       // U-row entries pre-multiplied by 1/d (rows past n get 0, so x = 0 there):
       // x_i = y~_i - e~_i x_{i+1} - f~_i x_{i+2} - a~_i S_q - b~_i S_s
       double e_[R], f_[R], a_[R], b_[R];
@@ -476,11 +489,16 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         const int i = s * R + r;
         const int ic = FULL ? i : min(i, n - 1);
         double c[B_NCOL];
-        if (CARRY) load_bih_row_carry(stab, tpos(ic), c, cr); else row_consts(ic, c);
-        if (!SMEM_TAB) bih_fast_prescale(c, xi0);
-        const BihBands hb = bih_bands_fast(xi1, xi2, c);
         double l2, l4;
-        bih_step_fast(w, w1, w2, hb, c, l2, l4);
+        if (CARRY) {
+          load_bih_row_carry(stab, tpos(ic), c, cr);
+          bih_row_fast_carried(w, w1, w2, c, xi1, xi2, pr, r == 0, l2, l4);
+        } else {
+          row_consts(ic, c);
+          if (!SMEM_TAB) bih_fast_prescale(c, xi0);
+          const BihBands hb = bih_bands_fast(xi1, xi2, c);
+          bih_step_fast(w, w1, w2, hb, c, l2, l4);
+        }
         w2 = w1;
         w1 = w;
         const bool valid = FULL || i < n;
