@@ -48,6 +48,7 @@ __all__ = [
     "dense_biharmonic",
     "lu_nopivot",
     "solve_field",
+    "solve_many",
     "chunk_rows_for",
 ]
 
@@ -102,51 +103,99 @@ _PIPE_MAX_SLABS = _env_int("SHEN_PIPE_SLABS", 16)  # fewer slabs = longer first-
 
 
 def _host_pipeline(lu, h_rhs, h_out, cplx):
-    """Column-slab pipeline: H2D copy of slab k+1 and D2H copy of slab k-1 run
-    on their own streams while slab k is solved (stream method; the other
-    methods solve the whole batch after one copy).  Page-locked host arrays
-    make the copies asynchronous; pageable ones still work (staged)."""
+    _host_pipeline_many([(lu, h_rhs, h_out, cplx)])
+
+
+_STREAMS = {}
+
+
+def _pipe_streams(dev):
     import torch
 
-    n, B = h_rhs.shape
-    es = h_rhs.itemsize
+    st = _STREAMS.get(dev)
+    if st is None:
+        st = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        _STREAMS[dev] = st
+    return st
+
+
+def _host_pipeline_many(jobs):
+    """Column-slab pipeline over one or several solves: the H2D copy of slab
+    k+1 and the D2H copy of slab k-1 run on their own streams while slab k is
+    solved (stream method; the other methods solve each batch after one copy).
+    Consecutive jobs share the pipeline, so the next operator's first copy-in
+    overlaps the previous one's last copy-out.  Page-locked host arrays make
+    the copies asynchronous; pageable ones still work (staged)."""
+    import torch
+
     dev = dv.device()
-    dtype = torch.complex128 if cplx else torch.float64
-    cache = getattr(lu, "_pipe", None)
-    if cache is None or cache[0].shape != (n, B) or cache[0].dtype != dtype:
-        cache = (torch.empty((n, B), dtype=dtype, device=dev), torch.empty((n, B), dtype=dtype, device=dev),
-                 torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-        lu._pipe = cache
-    d_rhs, d_out, s_in, s_out = cache
-    h = lib()
+    s_in, s_out = _pipe_streams(dev)
     comp = torch.cuda.current_stream(dev)
-    if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
-        bounds = [(0, B)]
-    else:
-        nslab = min(_PIPE_MAX_SLABS, B // _PIPE_MIN_SLAB)
-        step = -(-B // nslab)
-        step = -(-step // 128) * 128
-        bounds = [(a, min(a + step, B)) for a in range(0, B, step)]
-    pitch = B * es
+    h = lib()
     s_in.wait_stream(comp)
-    for a, b in bounds:
-        ev_in = torch.cuda.Event()
-        with torch.cuda.stream(s_in):
-            check(h.shen_memcpy2d_async(d_rhs.data_ptr() + a * es, pitch, h_rhs.ctypes.data + a * es, pitch,
-                                        (b - a) * es, n, 0, s_in.cuda_stream), "H2D slab")
-            ev_in.record(s_in)
-        comp.wait_event(ev_in)
-        if len(bounds) == 1:
-            lu.solve_into(d_rhs, d_out, cplx)
+    for lu, h_rhs, h_out, cplx in jobs:
+        n, B = h_rhs.shape
+        es = h_rhs.itemsize
+        dtype = torch.complex128 if cplx else torch.float64
+        cache = getattr(lu, "_pipe", None)
+        if cache is None or cache[0].shape != (n, B) or cache[0].dtype != dtype:
+            cache = (torch.empty((n, B), dtype=dtype, device=dev), torch.empty((n, B), dtype=dtype, device=dev))
+            lu._pipe = cache
+        d_rhs, d_out = cache
+        if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
+            bounds = [(0, B)]
         else:
-            lu.solve_into(d_rhs, d_out, cplx, a, b)
-        ev_c = torch.cuda.Event()
-        ev_c.record(comp)
-        s_out.wait_event(ev_c)
-        with torch.cuda.stream(s_out):
-            check(h.shen_memcpy2d_async(h_out.ctypes.data + a * es, pitch, d_out.data_ptr() + a * es, pitch,
-                                        (b - a) * es, n, 1, s_out.cuda_stream), "D2H slab")
+            nslab = min(_PIPE_MAX_SLABS, B // _PIPE_MIN_SLAB)
+            step = -(-B // nslab)
+            step = -(-step // 128) * 128
+            bounds = [(a, min(a + step, B)) for a in range(0, B, step)]
+        pitch = B * es
+        for a, b in bounds:
+            ev_in = torch.cuda.Event()
+            with torch.cuda.stream(s_in):
+                check(h.shen_memcpy2d_async(d_rhs.data_ptr() + a * es, pitch, h_rhs.ctypes.data + a * es, pitch,
+                                            (b - a) * es, n, 0, s_in.cuda_stream), "H2D slab")
+                ev_in.record(s_in)
+            comp.wait_event(ev_in)
+            if len(bounds) == 1:
+                lu.solve_into(d_rhs, d_out, cplx)
+            else:
+                lu.solve_into(d_rhs, d_out, cplx, a, b)
+            ev_c = torch.cuda.Event()
+            ev_c.record(comp)
+            s_out.wait_event(ev_c)
+            with torch.cuda.stream(s_out):
+                check(h.shen_memcpy2d_async(h_out.ctypes.data + a * es, pitch, d_out.data_ptr() + a * es, pitch,
+                                            (b - a) * es, n, 1, s_out.cuda_stream), "D2H slab")
     s_out.synchronize()
+
+
+def solve_many(jobs):
+    """Solve several (lu, rhs[, out]) at once -- e.g. the Helmholtz and the
+    biharmonic right-hand sides of a time step.  Same results as calling
+    ``lu.solve(rhs, out)`` for each; with host arrays the solves share one
+    copy/compute pipeline (no drain between operators).  Returns the outputs."""
+    host, outs = [], []
+    for job in jobs:
+        lu, rhs = job[0], job[1]
+        out = job[2] if len(job) > 2 else None
+        if dv.is_torch(rhs) and rhs.is_cuda:
+            outs.append(_solve_api(lu, rhs, out))
+            continue
+        _check_rhs_shape(rhs, lu.n_modes, lu.z2_shape)
+        a = rhs.numpy() if dv.is_torch(rhs) else np.asarray(rhs)
+        cplx = np.iscomplexobj(a)
+        a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+        if out is None:
+            out = np.empty(a.shape, dtype=a.dtype)
+        elif out.shape != a.shape or out.dtype != a.dtype or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous {a.dtype} array of shape {a.shape}")
+        outs.append(out)
+        if lu.batch > 0:
+            host.append((lu, a.reshape(lu.n_modes, -1), out.reshape(lu.n_modes, -1), cplx))
+    if host:
+        _host_pipeline_many(host)
+    return outs
 
 
 def _solve_real_via_complex(lu, rhs_dev, out_dev):
