@@ -245,6 +245,10 @@ def run_b200(args):
     ach = ach_b if dom == "biharmonic" else ach_h
     ckpt_bytes_h = 8.0 * hlu._ckpt.numel() if hlu._ckpt is not None else 0.0
     ckpt_bytes_b = 8.0 * blu._ckpt.numel() if blu._ckpt is not None else 0.0
+    # the timed arrays (137 GB at config 4) are done with: free them before the
+    # end-to-end sample allocates its own LU objects and pipeline buffers
+    del fh, fb, xh, xb, hlu, blu
+    torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e and rank == 0:
