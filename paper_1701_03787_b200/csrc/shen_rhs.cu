@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <initializer_list>
 
 #include "shen_common.cuh"
@@ -149,6 +150,12 @@ __global__ void rhs_u_kernel(RhsUArgs a) {
 #define SHEN_RHS_UNROLL 1  // rows per loop trip (measured: unrolling 2-4 is slower)
 #endif
 constexpr int kRhsUnroll = SHEN_RHS_UNROLL;
+#ifndef SHEN_RHS_UPAR_PF
+#define SHEN_RHS_UPAR_PF 0  // measured: 1-3 rows of register prefetch do not help
+#endif
+#ifndef SHEN_RHS_UPAR_MINB
+#define SHEN_RHS_UPAR_MINB 3
+#endif
 #ifndef SHEN_RHS_U_MINB
 #define SHEN_RHS_U_MINB 3  // resident 128-thread blocks per SM the register budget targets
 #endif
@@ -175,20 +182,33 @@ __device__ __forceinline__ C2 term(const RhsBand& m, int q, int k, C2 x) {
 }
 // banded row with the window; the offsets are compile-time (the launcher
 // checks that the matrix has exactly these, in this order)
-template <int Q, int LO, int HI>
-__device__ __forceinline__ void band_terms(const RhsBand&, int, const Win<LO, HI>&, C2&) {}
-template <int Q, int LO, int HI, int D, int... Ds>
-__device__ __forceinline__ void band_terms(const RhsBand& m, int k, const Win<LO, HI>& w, C2& v) {
+template <int Q, typename W>
+__device__ __forceinline__ void band_terms(const RhsBand&, int, const W&, C2&) {}
+template <int Q, typename W, int D, int... Ds>
+__device__ __forceinline__ void band_terms(const RhsBand& m, int k, const W& w, C2& v) {
   constexpr int k0 = D < 0 ? -D : 0;
   if (k >= k0 && k < m.nc - D && k < m.nr) v = add(v, term(m, Q, k, w.at(D)));
-  band_terms<Q + 1, LO, HI, Ds...>(m, k, w, v);
+  band_terms<Q + 1, W, Ds...>(m, k, w, v);
 }
-template <int... Ds, int LO, int HI>
-__device__ __forceinline__ C2 band_win(const RhsBand& m, int k, const Win<LO, HI>& w) {
+template <int... Ds, typename W>
+__device__ __forceinline__ C2 band_win(const RhsBand& m, int k, const W& w) {
   C2 v = {0.0, 0.0};
-  band_terms<0, LO, HI, Ds...>(m, k, w, v);
+  band_terms<0, W, Ds...>(m, k, w, v);
   return v;
 }
+
+// same-parity-step window: values at rows k+LO, k+LO+2, ..., k+HI (LO, HI of
+// one parity); k -> k-2 moves everything one slot up
+template <int LO, int HI>
+struct PWin {
+  C2 v[(HI - LO) / 2 + 1];
+  __device__ __forceinline__ C2 at(int d) const { return v[(d - LO) / 2]; }
+  __device__ __forceinline__ void shift(C2 fresh) {
+#pragma unroll
+    for (int i = (HI - LO) / 2; i > 0; --i) v[i] = v[i - 1];
+    v[0] = fresh;
+  }
+};
 
 __global__ void __launch_bounds__(128) rhs_g_fast_kernel(RhsGArgs a) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,6 +317,121 @@ __global__ void __launch_bounds__(128, SHEN_RHS_U_MINB) rhs_u_fast_kernel(RhsUAr
   }
 }
 
+// ---------------------------------------------------------------- one thread per (line, parity)
+// The operators never mix parities except through odd offsets (read-only), and
+// the tails' suffix sums run within a parity: a thread can own one parity of
+// a line.  Twice the threads of the fast path above, each with half the
+// window registers -- more parallelism for the same (single) pass over HBM.
+__global__ void __launch_bounds__(128) rhs_g_par_kernel(RhsGArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * a.L) return;
+  const int par = t >= a.L ? 1 : 0;
+  const int64_t l = t - (int64_t)par * a.L;
+  const int64_t L = a.L;
+  const int n = a.n_dir;
+  auto ldr = [&](const void* base, int j) -> C2 {
+    return (j >= 0 && j < n) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
+  };
+  const C2 im_m = {__ldg(a.im_m_re + l), __ldg(a.im_m_im + l)}, im_n = {__ldg(a.im_n_re + l), __ldg(a.im_n_im + l)};
+  auto src_row = [&](int j) -> C2 {
+    if (j < 0 || j >= n) return {0.0, 0.0};
+    const C2 hy = sub(rmul(1.5, ldr(a.hcy, j)), rmul(0.5, ldr(a.hpy, j)));
+    const C2 hz = sub(rmul(1.5, ldr(a.hcz, j)), rmul(0.5, ldr(a.hpz, j)));
+    return sub(cmul(im_m, hz), cmul(im_n, hy));
+  };
+  const double cg = __ldg(a.cg + l);
+  const int m = (n - par + 1) / 2;
+  const int ktop = par + 2 * (m - 1);
+  PWin<-2, 2> G, R;  // rows k-2, k, k+2
+#pragma unroll
+  for (int d = -2; d <= 2; d += 2) {
+    G.v[(d + 2) / 2] = ldr(a.g, ktop + d);
+    R.v[(d + 2) / 2] = src_row(ktop + d);
+  }
+  C2 S = {0.0, 0.0};
+  bool have = false;
+  double2* out = static_cast<double2*>(a.out) + l;
+  for (int k = ktop; k >= 0; k -= 2) {
+    C2 st = band_win<0>(a.stiff, k, G);
+    if (k + 2 < n) {  // tail_start == 2: suffix sum over this parity from row k + 2
+      S = have ? add(G.at(2), S) : G.at(2);
+      have = true;
+      st = add(st, rmul(__ldg(a.tail + k), S));
+    }
+    C2 r = rmul(a.c_stiff, st);
+    r = add(r, rmul(cg, band_win<-2, 0, 2>(a.mass, k, G)));
+    r = add(r, rmul(a.dt, band_win<-2, 0, 2>(a.mass, k, R)));
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+    G.shift(ldr(a.g, k - 4));
+    R.shift(src_row(k - 4));
+  }
+}
+
+__global__ void __launch_bounds__(128, SHEN_RHS_UPAR_MINB) rhs_u_par_kernel(RhsUArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 2 * a.L) return;
+  const int par = t >= a.L ? 1 : 0;
+  const int64_t l = t - (int64_t)par * a.L;
+  const int64_t L = a.L;
+  const int n = a.n_bih, nd = a.mixed.nc;
+  auto ldr = [&](const void* base, int j, int rows) -> C2 {
+    return (j >= 0 && j < rows) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
+  };
+  auto hrow = [&](const void* c, const void* p, int j) -> C2 {
+    if (j < 0 || j >= nd) return {0.0, 0.0};
+    return sub(rmul(1.5, ldr(c, j, nd)), rmul(0.5, ldr(p, j, nd)));
+  };
+  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
+  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
+  const int m = (n - par + 1) / 2;
+  const int ktop = par + 2 * (m - 1);
+  // windows extended by PF rows (of this parity step) below what the bands
+  // use: those slots are a prefetch FIFO, a row's loads are issued PF + 1
+  // iterations before the bands read it (ncu: the unextended kernel stalls
+  // on long scoreboard ~6 cycles per issue)
+  constexpr int PF = SHEN_RHS_UPAR_PF;
+  PWin<-4 - 2 * PF, 4> U;    // u rows k-4 .. k+4 (this parity)
+  PWin<-2 - 2 * PF, 4> HX;   // h_x rows k-2 .. k+4 (this parity)
+  PWin<-1 - 2 * PF, 3> HY, HZ;  // h_y, h_z rows k-1, k+1, k+3 (other parity)
+#pragma unroll
+  for (int d = -4 - 2 * PF; d <= 4; d += 2) U.v[(d + 4 + 2 * PF) / 2] = ldr(a.u, ktop + d, n);
+#pragma unroll
+  for (int d = -2 - 2 * PF; d <= 4; d += 2) HX.v[(d + 2 + 2 * PF) / 2] = hrow(a.hcx, a.hpx, ktop + d);
+#pragma unroll
+  for (int d = -1 - 2 * PF; d <= 3; d += 2) {
+    HY.v[(d + 1 + 2 * PF) / 2] = hrow(a.hcy, a.hpy, ktop + d);
+    HZ.v[(d + 1 + 2 * PF) / 2] = hrow(a.hcz, a.hpz, ktop + d);
+  }
+  C2 sq = {0.0, 0.0}, ss = {0.0, 0.0};
+  bool have = false;
+  double2* out = static_cast<double2*>(a.out) + l;
+  for (int k = ktop; k >= 0; k -= 2) {
+    if (k + 2 < n) {  // fold row k + 2 of this parity into the rank-2 tail sums
+      const C2 uj = U.at(2);
+      const C2 qx = rmul(__ldg(a.q + k + 2), uj), sx = rmul(__ldg(a.s + k + 2), uj);
+      sq = have ? add(qx, sq) : qx;
+      ss = have ? add(sx, ss) : sx;
+      have = true;
+    }
+    C2 f = rmul(__ldg(a.d + k), U.at(0));
+    if (k < n - 2) {
+      f = add(f, rmul(__ldg(a.p + k), sq));
+      f = add(f, rmul(__ldg(a.r + k), ss));
+    }
+    C2 r = rmul(a.c_fourth, f);
+    r = sub(r, rmul(cs, band_win<-2, 0, 2>(a.stiff, k, U)));
+    r = add(r, rmul(cm, band_win<-4, -2, 0, 2, 4>(a.mass, k, U)));
+    r = sub(r, rmul(cx, band_win<-2, 0, 2, 4>(a.mixed, k, HX)));
+    r = sub(r, cmul(cy, band_win<-1, 1, 3>(a.deriv, k, HY)));
+    r = sub(r, cmul(cz, band_win<-1, 1, 3>(a.deriv, k, HZ)));
+    out[(int64_t)k * L] = make_double2(r.re, r.im);
+    U.shift(ldr(a.u, k - 6 - 2 * PF, n));
+    HX.shift(hrow(a.hcx, a.hpx, k - 4 - 2 * PF));
+    HY.shift(hrow(a.hcy, a.hpy, k - 3 - 2 * PF));
+    HZ.shift(hrow(a.hcz, a.hpz, k - 3 - 2 * PF));
+  }
+}
+
 static bool offs_are(const RhsBand& m, std::initializer_list<int> o) {
   if (m.n_off != (int)o.size()) return false;
   int i = 0;
@@ -310,7 +445,10 @@ static bool offs_are(const RhsBand& m, std::initializer_list<int> o) {
 cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_dir <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
-  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}))
+  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 2;
+  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant == 2)
+    rhs_g_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
+  else if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant == 1)
     rhs_g_fast_kernel<<<blocks, 128, 0, st>>>(a);
   else
     rhs_g_kernel<<<blocks, 128, 0, st>>>(a);
@@ -320,8 +458,12 @@ cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
 cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_bih <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
-  if (offs_are(a.stiff, {-2, 0, 2}) && offs_are(a.mass, {-4, -2, 0, 2, 4}) && offs_are(a.mixed, {-2, 0, 2, 4}) &&
-      offs_are(a.deriv, {-1, 1, 3}))
+  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 2;
+  const bool fixed = offs_are(a.stiff, {-2, 0, 2}) && offs_are(a.mass, {-4, -2, 0, 2, 4}) &&
+                     offs_are(a.mixed, {-2, 0, 2, 4}) && offs_are(a.deriv, {-1, 1, 3});
+  if (fixed && variant == 2)
+    rhs_u_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
+  else if (fixed && variant == 1)
     rhs_u_fast_kernel<<<blocks, 128, 0, st>>>(a);
   else
     rhs_u_kernel<<<blocks, 128, 0, st>>>(a);
