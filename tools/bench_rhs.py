@@ -24,8 +24,22 @@ L = z2.size
 g = torch.Generator(device="cuda").manual_seed(0)
 
 
+PAD = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # bytes of skew between the arrays (DRAM-partition probe)
+
+
 def rnd(r):
-    return torch.randn((r, rows, n.shape[1]), dtype=torch.complex128, device="cuda", generator=g)
+    if not PAD:
+        return torch.randn((r, rows, n.shape[1]), dtype=torch.complex128, device="cuda", generator=g)
+    cnt = r * rows * n.shape[1]
+    buf = torch.empty(cnt + PAD * (1 + len(_keep)) // 16, dtype=torch.complex128, device="cuda")
+    _keep.append(buf)
+    off = PAD * len(_keep) // 16
+    t = buf[off:off + cnt].view(r, rows, n.shape[1])
+    t.copy_(torch.randn((r, rows, n.shape[1]), dtype=torch.complex128, device="cuda", generator=g))
+    return t
+
+
+_keep = []
 
 
 u, gg = rnd(mats.n_bih), rnd(mats.n_dir)
