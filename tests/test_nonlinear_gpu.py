@@ -33,16 +33,17 @@ def test_nonlinear_vs_reference_golden(golden, fi):
 
 
 @pytest.mark.parametrize("n_x,n_y,n_z", [(64, 16, 12), (128, 32, 32)])
-def test_nonlinear_vs_oracle_larger(n_x, n_y, n_z):
+@pytest.mark.parametrize("fi", [0, 1])
+def test_nonlinear_vs_oracle_larger(n_x, n_y, n_z, fi):
     import torch
 
-    mesh = build_mesh(n_x, n_y, n_z, 2 * np.pi, np.pi)
+    mesh = build_mesh(n_x, n_y, n_z, 2 * np.pi, np.pi, (PointFamily.GAUSS, PointFamily.GAUSS_LOBATTO)[fi])
     gd, gb = wavenumber_grid(mesh, Space.DIRICHLET), wavenumber_grid(mesh, Space.BIHARMONIC)
     m, n = gd.m_scaled[:, None], gd.n_scaled[None, :]
     mi = np.fft.fftfreq(n_y, 1.0 / n_y).astype(int)[:, None]
     ni = np.arange(n_z // 2 + 1)[None, :]
     mask = (np.abs(mi) != n_y // 2) & (ni != n_z // 2) & (np.abs(mi) < max(n_y // 3, 1)) & (ni < max(n_z // 3, 1))
-    mats = assemble(n_x, 0)
+    mats = assemble(n_x, fi)
     rng = np.random.default_rng(n_x)
 
     def c(grid):
@@ -50,7 +51,7 @@ def test_nonlinear_vs_oracle_larger(n_x, n_y, n_z):
         return rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
 
     u, v, w, gg = c(gb), c(gd), c(gd), c(gd)
-    want = O.compute_nonlinear(mats, False, n_y, n_z, m, n, mask, u, v, w, gg)
+    want = O.compute_nonlinear(mats, fi == 1, n_y, n_z, m, n, mask, u, v, w, gg)
     term = NL.NonlinearTerm(mats, mesh, m, n, mask)
     got = term(u, v, w, gg)
     for i in range(3):

@@ -33,13 +33,16 @@ def test_recover_vs_reference_golden(golden, fi):
 
 
 @pytest.mark.parametrize("n_x", [64, 256])
-def test_recover_vs_oracle_larger(n_x):
+@pytest.mark.parametrize("fi", [0, 1])
+def test_recover_vs_oracle_larger(n_x, fi):
     import torch
 
-    mesh = build_mesh(n_x, 24, 16, 2 * np.pi, np.pi)
+    from paper_1701_03787_b200.mesh import PointFamily
+
+    mesh = build_mesh(n_x, 24, 16, 2 * np.pi, np.pi, (PointFamily.GAUSS, PointFamily.GAUSS_LOBATTO)[fi])
     gd = wavenumber_grid(mesh, Space.DIRICHLET)
     m, n, z2 = gd.m_scaled[:, None], gd.n_scaled[None, :], gd.z2()
-    mats = assemble(n_x, 0)
+    mats = assemble(n_x, fi)
     rng = np.random.default_rng(n_x)
     u = rng.standard_normal((mats.n_bih,) + z2.shape) + 1j * rng.standard_normal((mats.n_bih,) + z2.shape)
     gg = rng.standard_normal((mats.n_dir,) + z2.shape) + 1j * rng.standard_normal((mats.n_dir,) + z2.shape)

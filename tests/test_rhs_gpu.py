@@ -28,13 +28,16 @@ def test_rhs_vs_reference_golden(golden, fi):
 
 
 @pytest.mark.parametrize("n_x", [64, 256])
-def test_rhs_vs_oracle_larger(n_x):
+@pytest.mark.parametrize("fi", [0, 1])
+def test_rhs_vs_oracle_larger(n_x, fi):
     import torch
 
-    mesh = build_mesh(n_x, 16, 12, 2 * np.pi, np.pi)
+    from paper_1701_03787_b200.mesh import PointFamily
+
+    mesh = build_mesh(n_x, 16, 12, 2 * np.pi, np.pi, (PointFamily.GAUSS, PointFamily.GAUSS_LOBATTO)[fi])
     grid = wavenumber_grid(mesh, Space.DIRICHLET)
     m, n, z2 = grid.m_scaled[:, None], grid.n_scaled[None, :], grid.z2()
-    mats = assemble(n_x, 0)
+    mats = assemble(n_x, fi)
     rng = np.random.default_rng(n_x)
     shp_d, shp_b = (mats.n_dir,) + z2.shape, (mats.n_bih,) + z2.shape
 
