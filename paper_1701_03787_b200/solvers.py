@@ -55,6 +55,8 @@ __all__ = [
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
 _METHODS = ("chunked", "stream", "stored", "tile")
+
+
 def _env_int(name, default):
     import os
 
@@ -271,12 +273,6 @@ def _check_rhs_shape(rhs, n_modes, z2_shape):
     want = (n_modes,) + tuple(z2_shape)
     if shape != want:
         raise ValueError(f"rhs shape {shape} does not match {want}")
-
-
-def _finish(out_dev, shape, from_numpy):
-    if from_numpy:
-        return out_dev.cpu().numpy().reshape(shape)
-    return out_dev.reshape(shape)
 
 
 # ------------------------------------------------------------------ Helmholtz
