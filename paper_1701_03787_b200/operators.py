@@ -16,7 +16,6 @@ fallback.
 from __future__ import annotations
 
 import ctypes
-from functools import lru_cache
 
 import numpy as np
 
