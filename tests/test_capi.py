@@ -59,3 +59,44 @@ def test_product_fails_loudly_without_device():
 
     with pytest.raises(_lib.ShenBackendError):
         solvers.build_helmholtz(assemble(16, 0), 1e-3, 1e-3, [0.0, 1.0])
+
+
+def test_every_compute_entry_point_validates_arguments():
+    """Bad sizes / NULL pointers are rejected with SHEN_ERR_ARG and a message
+    naming the entry point, before any device work (runs without a GPU)."""
+    import ctypes
+
+    h = _lib.lib()
+    cases = {
+        "shen_helm_solve_stream": (1, 0.0, None, 1, None, None, None, 8, None, None, None, None, 1, 0, 0, 0, -1,
+                                   None),
+        "shen_bih_solve_stream": (1, 0.0, None, None, 1, None, 8, None, None, None, None, 1, 0, 0, 0, -1, None),
+        "shen_helm_solve_tile": (1, 0.0, None, 1, None, None, None, 8, None, None, None, 1, None),
+        "shen_helm_solve_chunked": (1, 0.0, None, 1, None, None, None, 8, None, None, None, 1, None),
+        "shen_bih_factor": (1, 0.0, None, None, 1, None, 8, None, None, 0, None, None),
+        "shen_xform_extend": (3, 5, 1, None, None, None),
+        "shen_xform_fwd_post": (0, 9, 5, 1, 1.0, None, None, None, None),
+        "shen_xform_inv_pre": (0, 1, 9, 5, 1, None, None, None, None, None),
+        "shen_xform_inv_post": (0, 1, 1, None, None, None, None),
+        "shen_xform_mass_solve": (3, 8, 4, 1, None, None, None, None),
+        "shen_apply_banded": (4, 4, 1, 9, None, None, None, None, 1, None),
+        "shen_apply_const_tail": (4, 4, 1, 1, None, None, None, 2, None, None, 1, None),
+        "shen_apply_rank2_tail": (4, 1, None, None, None, None, None, None, None, 1, None),
+        "shen_scale_lines": (2, 2, None, None, None, None, None),
+        "shen_cross": (8, None, None, None),
+        "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
+    }
+    for name, args in cases.items():
+        st = getattr(h, name)(*args)
+        assert st == 1, name
+        assert name.encode() in h.shen_last_error() or b"bad args" in h.shen_last_error(), name
+    for name, cls in (("shen_rhs_g", _lib.ShenRhsGArgs), ("shen_rhs_u", _lib.ShenRhsUArgs),
+                      ("shen_recover_velocity", _lib.ShenRecoverArgs)):
+        a = cls()
+        a.L = 4
+        if hasattr(a, "n_dir"):
+            a.n_dir = 4
+        if hasattr(a, "n_bih"):
+            a.n_bih = 4
+        assert getattr(h, name)(ctypes.byref(a), None) == 1, name
+        assert getattr(h, name)(None, None) == 1, name
