@@ -1,6 +1,9 @@
 /*
  * shen_b200.h -- C ABI of the B200 (sm_100a) Shen-Galerkin wall-normal
- * solvers and transforms (the data-parallel core of arXiv 1701.03787).
+ * solvers and transforms (the data-parallel core of arXiv 1701.03787), plus
+ * the stepper-side pieces around them: structured matrix apply, fused
+ * right-hand-side assembly, velocity recovery and the pointwise parts of the
+ * nonlinear term.
  *
  * Plain C: device pointers, sizes and an opaque CUDA stream handle
  * (cudaStream_t passed as void*, NULL = legacy default stream).  Every call
