@@ -65,6 +65,19 @@ __device__ __forceinline__ void ystore(V* p, V v) {
   if (SHEN_YCKPT_KEEP) st_keep(p, v, policy_evict_last());
   else *p = v;
 }
+// After its single read in the backward sweep a y checkpoint is dead: drop
+// its L2 line without a write-back (discard.global.L2 acts as a weak write of
+// an indeterminate value, ordered after this thread's read of the same
+// address and before its next store there).  One lane per 128-B line.
+#ifndef SHEN_YCKPT_DISCARD
+#define SHEN_YCKPT_DISCARD 1
+#endif
+template <typename V>
+__device__ __forceinline__ void ydiscard(const V* p, int lane) {
+  constexpr int kPer = 128 / (int)sizeof(V);
+  if (SHEN_YCKPT_DISCARD && (lane & (kPer - 1)) == 0 && ((reinterpret_cast<uintptr_t>(p) & 127) == 0))
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -253,6 +266,7 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
         hp_start(q, ckd, cke, ckt);
         yy = ckyv;
       }
+      if (s > 0) ydiscard(ychkj + (s - 1) * kT, lane);
       if (s - 1 > 0) {
         const double* ck = ckj + (int64_t)6 * (s - 1) * B;
         ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
@@ -469,6 +483,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         w2.d = ck[5]; w2.e = ck[6]; w2.f = ck[7]; w2.a = ck[8]; w2.b = ck[9];
         ya = cya;
         yb = cyb;
+        ydiscard(ychkj + (2 * (s - 1)) * kT, lane);
+        ydiscard(ychkj + (2 * (s - 1) + 1) * kT, lane);
         w1.rd = rcp_fast(w1.d);
         w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
       }
