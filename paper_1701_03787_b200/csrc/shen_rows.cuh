@@ -52,16 +52,18 @@ __device__ __forceinline__ double helm_step_exact(HelmState& s, const HelmRow& h
 }
 
 // ---------------------------------------------------------------- fast reciprocal
-// MUFU.RCP64H seed + two Newton steps: ~1 ulp, no slow path (the fast-mode
-// recurrences never see zero, inf or denormal pivots in practice; the
-// exact path keeps IEEE division).  ~56-cycle latency vs ~72 for __drcp_rn.
+// MUFU.RCP64H seed r0, then 1/x = r0 (1 + e + e^2 + ...) with e = 1 - x r0
+// truncated after e^2: the seed's |e| <= 2^-19.9 leaves ~e^3 < 2^-59, i.e.
+// the <= 1 ulp of two Newton steps (measured over 2^30 doubles: max 1 ulp,
+// 99.97% correctly rounded, tools/rcp_check.cu) with two dependent FMAs after
+// the seed instead of four.  No slow path: the
+// fast-mode recurrences never see zero, inf or denormal pivots in practice;
+// the exact path keeps IEEE division.
 __device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = __fma_rn(-x, r, 1.0);
-  r = __fma_rn(r, e, r);
-  e = __fma_rn(-x, r, 1.0);
-  return __fma_rn(r, e, r);
+  double r0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(x));
+  const double e = __fma_rn(-x, r0, 1.0);
+  return __fma_rn(r0, __fma_rn(e, e, e), r0);
 }
 
 // ---------------------------------------------------------------- projective Helmholtz walk
@@ -181,7 +183,7 @@ __host__ __device__ constexpr int bc_src(int col) {  // 18-column source of comp
   return col == BC_Q4 ? B_Q4 : col == BC_S4 ? B_S4 : col == BC_R ? B_R : col == BC_P ? B_P
        : col == BC_ARM2 ? B_ARM2 : col;  // BC_Q0..BC_BB4 coincide with B_Q0..B_BB4
 }
-static_assert(BC_BB4 == B_BB4 && BC_Q0 == B_Q0, "compact columns 0..7 mirror the full table");
+static_assert((int)BC_BB4 == (int)B_BB4 && (int)BC_Q0 == (int)B_Q0, "compact columns 0..7 mirror the full table");
 
 // pos = table position of the row, step = positions between rows k-2 and k
 // (2 in the both-parity table, whose position is k + 4; 1 in a one-parity table)
@@ -265,6 +267,11 @@ __device__ __forceinline__ BihBands bih_bands(double xi0, double xi1, double xi2
 struct BihU {
   double d, e, f, a, b, rd;
 };
+
+// fast-mode reciprocal of a U row's pivot
+__device__ __forceinline__ void bih_set_rcp(BihU& u) { u.rd = rcp_fast(u.d); }
+// zero record ("row before row 0")
+__device__ __forceinline__ void bih_clear_rcp(BihU& u) { u.rd = 0.0; }
 
 // One exact-mode elimination step, rows i-1 (u1) and i-2 (u2) already
 // eliminated (solvers.py:314-346), numpy's evaluation order.  i is the row
@@ -350,7 +357,7 @@ __device__ __forceinline__ void bih_step_fast(BihU& u, const BihU& u1, const Bih
   u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
   u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
   u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
-  u.rd = rcp_fast(u.d);
+  bih_set_rcp(u);
 }
 
 // Row step for consecutive rows of one parity with the products that repeat
@@ -390,7 +397,7 @@ __device__ __forceinline__ void bih_row_fast_carried(BihU& u, const BihU& u1, co
   u.f = __fma_rn(-l2, u24, __fma_rn(-l4, u44, h.hp4));
   u.a = __fma_rn(-l4, u2.a, __fma_rn(-l2, u1.a, c[B_P]));
   u.b = __fma_rn(-l4, u2.b, __fma_rn(-l2, u1.b, c[B_R]));
-  u.rd = rcp_fast(u.d);
+  bih_set_rcp(u);
   pr.u42 = u24;
   pr.x2bb4_prev = pr.x2bb4;
   pr.x2bb4 = x2bb4;

@@ -294,8 +294,9 @@ __global__ void __launch_bounds__(128) bih_chunk_kernel(BihChunkArgs a) {
     if (use_ck) {
       u1.d = ck_n[0]; u1.e = ck_n[1]; u1.f = ck_n[2]; u1.a = ck_n[3]; u1.b = ck_n[4];
       u2.d = ck_n[5]; u2.e = ck_n[6]; u2.f = ck_n[7]; u2.a = ck_n[8]; u2.b = ck_n[9];
-      u1.rd = rcp_fast(u1.d);
-      u2.rd = s0 >= 2 ? rcp_fast(u2.d) : 0.0;
+      bih_set_rcp(u1);
+      if (s0 >= 2) bih_set_rcp(u2);
+      else bih_clear_rcp(u2);
     }
     if (jn < B) {
       prefetch_rows<V, R>(Ybuf + (buf ^ 1) * R * 32, rhs, B, jn, par, s0, nr, lane);

@@ -485,8 +485,9 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
         yb = cyb;
         ydiscard(ychkj + (2 * (s - 1)) * kT, lane);
         ydiscard(ychkj + (2 * (s - 1) + 1) * kT, lane);
-        w1.rd = rcp_fast(w1.d);
-        w2.rd = s * R >= 2 ? rcp_fast(w2.d) : 0.0;
+        bih_set_rcp(w1);
+        if (s * R >= 2) bih_set_rcp(w2);
+        else bih_clear_rcp(w2);
       }
       if (PF && s - 1 > 0) load_ck(s - 1);
       V* cur = consume();
