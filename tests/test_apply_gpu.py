@@ -50,3 +50,16 @@ def test_apply_vs_reference_golden(golden, n_x, fam):
     for name in NAMES:
         x = g[f"nx{n_x}_f{fam}_{name}_x"]
         assert np.array_equal(P.apply(getattr(mats, name), x), g[f"nx{n_x}_f{fam}_{name}_y"]), name
+
+
+@pytest.mark.parametrize("n_x,L", [(256, 1), (256, 9), (1024, 1), (1024, 3), (64, 4096), (256, 5000)])
+def test_apply_bitwise_line_counts(n_x, L):
+    """Both kernels: the staged one (few lines, x and tables in shared memory;
+    lines per block shrink with n_x) and the per-line one (>= 4096 lines)."""
+    mats = assemble(n_x, 0)
+    rng = np.random.default_rng(L)
+    for name in NAMES:
+        M = getattr(mats, name)
+        nc = M.shape[1]
+        for x in (rng.standard_normal((nc, L)) + 1j * rng.standard_normal((nc, L)), rng.standard_normal((nc, L))):
+            assert np.array_equal(P.apply(M, x), M.apply(x)), (name, x.dtype)
