@@ -269,6 +269,17 @@ int shen_recover_velocity(const shen_recover_args* args, void* stream);
 int shen_scale_lines(int64_t rows, int64_t L, const void* x, const double* c_re, const double* c_im, void* y,
                      void* stream);
 int shen_cross(int64_t n, const double* fields, double* h, void* stream);
+/* Paired form (wall-normal points j and N-1-j are mirror images, x -> -x):
+ * every input field is given as [P + Q rows][M points], P = ceil(N/2),
+ * Q = floor(N/2), by parts e (rows 0..P-1) and o (rows P..P+Q-1) with
+ *   f_j = e_j + o_j,  f_{N-1-j} = e_j - o_j  (j < Q),  f_Q = e_Q (centre, P = Q+1);
+ * h is written in the same layout as sums and differences of the two
+ * points' values: rows j < Q: h_j + h_{N-1-j}, row Q: h_Q, rows P + j:
+ * h_j - h_{N-1-j}. */
+int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, void* stream);
+/* shen_scale_lines with row strides (in elements) for x and y. */
+int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
+                    const double* c_im, void* y, int64_t y_row_stride, void* stream);
 
 #ifdef __cplusplus
 }

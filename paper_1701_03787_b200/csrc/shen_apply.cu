@@ -66,46 +66,59 @@ __device__ __forceinline__ double ldt(const double* p) {
   return __ldg(p);
 }
 
-// One line's walk (rows bottom-up).  X(j) reads x row j of this line; the
-// table pointers in `a` point to global memory (SM = false) or to a shared
-// copy (SM = true).
+// row tables of one walk: global memory (SM = false) or a shared copy (SM = true)
+struct Tabs {
+  const double *diag, *tail, *d, *p, *q, *r, *s;
+};
+
+// One line's walk (rows bottom-up).  X(j) reads x row j of this line.  The
+// sizes and offsets come from the kernel parameter `a` (constant bank; no
+// local-memory copy), the tables from `t`.
 template <typename V, bool SM, typename FX>
-__device__ __forceinline__ void apply_walk(const ApplyArgs& a, FX X, V* __restrict__ y, int64_t l) {
+__device__ __forceinline__ void apply_walk(const ApplyArgs& a, const Tabs t, FX X, V* __restrict__ y, int64_t l) {
   using O = A<V>;
   const int64_t L = a.L;
   if (a.kind == 2) {
     // y = diag x; sq/ss = parity suffix sums of q x, s x; y[k] += p sq[k+2]; y[k] += r ss[k+2]
     const int n = a.nr;
-    V sq[2] = {O::zero(), O::zero()}, ss[2] = {O::zero(), O::zero()};
-    bool have[2] = {false, false};
+    // suffix sums of the parity of row k (sq, ss) and of the other parity
+    // (sq_o, ss_o), swapped every row: no dynamically indexed arrays (they
+    // would live in local memory, on the dependency chain)
+    V sq = O::zero(), ss = O::zero(), sq_o = O::zero(), ss_o = O::zero();
+    bool have = false, have_o = false;
     for (int k = n - 1; k >= 0; --k) {
-      const int j = k + 2;  // fold x[j] into its parity's sums before row k uses them
+      const int j = k + 2;  // fold x[j] (same parity as k) into the sums before row k uses them
       if (j < n) {
         const V xj = X(j);
-        const V qx = O::scale(ldt<SM>(a.q + j), xj), sx = O::scale(ldt<SM>(a.s + j), xj);
-        const int pj = j & 1;
-        sq[pj] = have[pj] ? O::add(qx, sq[pj]) : qx;
-        ss[pj] = have[pj] ? O::add(sx, ss[pj]) : sx;
-        have[pj] = true;
+        const V qx = O::scale(ldt<SM>(t.q + j), xj), sx = O::scale(ldt<SM>(t.s + j), xj);
+        sq = have ? O::add(qx, sq) : qx;
+        ss = have ? O::add(sx, ss) : sx;
+        have = true;
       }
-      V v = O::scale(ldt<SM>(a.d + k), X(k));
+      V v = O::scale(ldt<SM>(t.d + k), X(k));
       if (k < n - 2) {
-        v = O::add(v, O::scale(ldt<SM>(a.p + k), sq[k & 1]));
-        v = O::add(v, O::scale(ldt<SM>(a.r + k), ss[k & 1]));
+        v = O::add(v, O::scale(ldt<SM>(t.p + k), sq));
+        v = O::add(v, O::scale(ldt<SM>(t.r + k), ss));
       }
       y[(int64_t)k * L + l] = v;
+      const V tq = sq, ts = ss;  // row k - 1 has the other parity
+      const bool th = have;
+      sq = sq_o; ss = ss_o; have = have_o;
+      sq_o = tq; ss_o = ts; have_o = th;
     }
     return;
   }
-  V S[2] = {O::zero(), O::zero()};
-  bool have[2] = {false, false};
+  V S0 = O::zero(), S1 = O::zero();  // parity suffix sums (even / odd rows)
+  bool have0 = false, have1 = false;
   int next_j = a.nc - 1;  // next x row to fold into the suffix sums
   for (int k = a.nr - 1; k >= 0; --k) {
     V v = O::zero();
-    for (int q = 0; q < a.n_off; ++q) {
+#pragma unroll
+    for (int q = 0; q < kMaxOff; ++q) {  // static indices: a stays in the parameter bank
+      if (q >= a.n_off) break;
       const int dk = a.off[q];
       const int k0 = dk < 0 ? -dk : 0, k1 = min(a.nr, a.nc - dk);
-      if (k >= k0 && k < k1) v = O::add(v, O::scale(ldt<SM>(a.diag + (int64_t)q * a.nr + k), X(k + dk)));
+      if (k >= k0 && k < k1) v = O::add(v, O::scale(ldt<SM>(t.diag + (int64_t)q * a.nr + k), X(k + dk)));
     }
     if (a.kind == 1) {
       const int j = k + a.tail_start;
@@ -113,11 +126,16 @@ __device__ __forceinline__ void apply_walk(const ApplyArgs& a, FX X, V* __restri
         // fold x rows from the bottom down to j (each once, in the
         // reference's s[j] = x[j] + s[j+2] order)
         for (; next_j >= j; --next_j) {
-          const int pj = next_j & 1;
-          S[pj] = have[pj] ? O::add(X(next_j), S[pj]) : X(next_j);
-          have[pj] = true;
+          const V xj = X(next_j);
+          if (next_j & 1) {
+            S1 = have1 ? O::add(xj, S1) : xj;
+            have1 = true;
+          } else {
+            S0 = have0 ? O::add(xj, S0) : xj;
+            have0 = true;
+          }
         }
-        v = O::add(v, O::scale(ldt<SM>(a.tail + k), S[j & 1]));
+        v = O::add(v, O::scale(ldt<SM>(t.tail + k), (j & 1) ? S1 : S0));
       }
     }
     y[(int64_t)k * L + l] = v;
@@ -130,32 +148,37 @@ __global__ void apply_kernel(ApplyArgs a, const V* __restrict__ x, V* __restrict
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= a.L) return;
   const int64_t L = a.L;
-  apply_walk<V, false>(a, [&](int j) { return O::ld(x + (int64_t)j * L + l); }, y, l);
+  const Tabs t{a.diag, a.tail, a.d, a.p, a.q, a.r, a.s};
+  apply_walk<V, false>(a, t, [&](int j) { return O::ld(x + (int64_t)j * L + l); }, y, l);
 }
 
-// Few lines (the stepper's mean-flow vectors, L = 1): one thread per line
-// would wait a global-memory latency per row.  The block first stages its
-// stage_lines (<= 8) lines of x and the row tables in shared memory (all
-// threads, coalesced), then walks them from there -- same operations, same
-// order.
+// Few lines (the stepper's mean-flow vectors, L = 1): a per-line walk is one
+// thread doing ~100 dependent instructions per row.  Here a block takes
+// stage_lines lines: (1) x and the row tables are staged in shared memory,
+// (2) one thread per (line, parity) runs only the parity suffix sums (one
+// add per row on the chain) into shared memory, (3) all threads form the
+// rows in parallel.  Every row gets the same operations in the same order
+// as in apply_walk, so the results are bit-identical.
 constexpr int kStageThreads = 256;
 constexpr int64_t kStagedMaxLines = 4096;  // below this the per-line walk is latency-bound
 
 template <typename V>
 __global__ void __launch_bounds__(kStageThreads) apply_staged_kernel(ApplyArgs a, const V* __restrict__ x,
                                                                      V* __restrict__ y) {
+  using O = A<V>;
   extern __shared__ __align__(16) double sm[];
-  const int LB = a.stage_lines;
+  const int LB = a.stage_lines, nr = a.nr, nc = a.nc;
   const int64_t l0 = (int64_t)blockIdx.x * LB;
   const int nl = (int)min((int64_t)LB, a.L - l0);
-  V* xs = reinterpret_cast<V*>(sm);  // [nc][LB]
-  double* ts = sm + (size_t)a.nc * LB * (sizeof(V) / sizeof(double));
-  for (int idx = threadIdx.x; idx < a.nc * LB; idx += blockDim.x) {
+  V* xs = reinterpret_cast<V*>(sm);                       // [nc][LB]
+  V* s1 = xs + (size_t)nc * LB;                           // kind 1: S [nc][LB]; kind 2: sq [nr][LB]
+  V* s2 = s1 + (size_t)(a.kind == 2 ? nr : 0) * LB;      // kind 2: ss [nr][LB]
+  double* ts = reinterpret_cast<double*>(s2 + (size_t)(a.kind == 2 ? nr : a.kind == 1 ? nc : 0) * LB);
+  for (int idx = threadIdx.x; idx < nc * LB; idx += blockDim.x) {
     const int j = idx / LB, t = idx - j * LB;
-    if (t < nl) xs[idx] = A<V>::ld(x + (int64_t)j * a.L + l0 + t);
+    if (t < nl) xs[idx] = O::ld(x + (int64_t)j * a.L + l0 + t);
   }
-  // tables: the same pointers, rebased to the shared copy
-  ApplyArgs b = a;
+  Tabs tb{a.diag, a.tail, a.d, a.p, a.q, a.r, a.s};
   auto stage = [&](const double* src, int count) -> const double* {
     double* dst = ts;
     for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -163,16 +186,68 @@ __global__ void __launch_bounds__(kStageThreads) apply_staged_kernel(ApplyArgs a
     return dst;
   };
   if (a.kind == 2) {
-    b.d = stage(a.d, a.nr); b.p = stage(a.p, a.nr); b.q = stage(a.q, a.nr);
-    b.r = stage(a.r, a.nr); b.s = stage(a.s, a.nr);
+    tb.d = stage(a.d, nr); tb.p = stage(a.p, nr); tb.q = stage(a.q, nr);
+    tb.r = stage(a.r, nr); tb.s = stage(a.s, nr);
   } else {
-    if (a.n_off > 0) b.diag = stage(a.diag, a.n_off * a.nr);
-    if (a.kind == 1) b.tail = stage(a.tail, a.nr);
+    if (a.n_off > 0) tb.diag = stage(a.diag, a.n_off * nr);
+    if (a.kind == 1) tb.tail = stage(a.tail, nr);
   }
   __syncthreads();
-  const int t = threadIdx.x;
-  if (t >= nl) return;
-  apply_walk<V, true>(b, [&](int j) { return xs[j * LB + t]; }, y, l0 + t);
+  // (2) parity suffix sums, s[j] = v[j] + s[j + 2] from the bottom
+  if (threadIdx.x < 2 * nl && a.kind != 0) {
+    const int t = threadIdx.x >> 1, par = threadIdx.x & 1;
+    if (a.kind == 1) {
+      int j = nc - 1;
+      if ((j & 1) != par) --j;
+      V S = O::zero();
+      for (bool have = false; j >= a.tail_start && j >= 0; j -= 2, have = true) {
+        const V xj = xs[j * LB + t];
+        S = have ? O::add(xj, S) : xj;
+        s1[j * LB + t] = S;
+      }
+    } else {
+      int j = nr - 1;
+      if ((j & 1) != par) --j;
+      V sq = O::zero(), ss = O::zero();
+      for (bool have = false; j >= 2; j -= 2, have = true) {
+        const V xj = xs[j * LB + t];
+        const V qx = O::scale(tb.q[j], xj), sx = O::scale(tb.s[j], xj);
+        sq = have ? O::add(qx, sq) : qx;
+        ss = have ? O::add(sx, ss) : sx;
+        s1[j * LB + t] = sq;
+        s2[j * LB + t] = ss;
+      }
+    }
+  }
+  __syncthreads();
+  // (3) rows in parallel
+  for (int idx = threadIdx.x; idx < nr * LB; idx += blockDim.x) {
+    const int k = idx / LB, t = idx - k * LB;
+    if (t >= nl) continue;
+    auto X = [&](int j) { return xs[j * LB + t]; };
+    V v;
+    if (a.kind == 2) {
+      v = O::scale(tb.d[k], X(k));
+      if (k < nr - 2) {
+        v = O::add(v, O::scale(tb.p[k], s1[(k + 2) * LB + t]));
+        v = O::add(v, O::scale(tb.r[k], s2[(k + 2) * LB + t]));
+      }
+    } else {
+      v = O::zero();
+#pragma unroll
+      for (int q = 0; q < kMaxOff; ++q) {
+        if (q >= a.n_off) break;
+        const int dk = a.off[q];
+        const int k0 = dk < 0 ? -dk : 0, k1 = min(nr, nc - dk);
+        if (k >= k0 && k < k1) v = O::add(v, O::scale(tb.diag[q * nr + k], X(k + dk)));
+      }
+      if (a.kind == 1) {
+        const int j = k + a.tail_start;
+        if (j < nc) v = O::add(v, O::scale(tb.tail[k], s1[j * LB + t]));
+      }
+    }
+    y[(int64_t)k * a.L + l0 + t] = v;
+  }
 }
 
 }  // namespace
@@ -189,12 +264,20 @@ cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const i
   a.d = d; a.p = p; a.q = q; a.r = r; a.s = s;
   if (L < kStagedMaxLines) {
     const size_t tab = kind == 2 ? 5 * (size_t)nr : (size_t)(n_off + (kind == 1)) * nr;
-    const size_t per_line = (size_t)nc * (cplx_data ? 16 : 8), budget = 48 * 1024;
+    const size_t vb = cplx_data ? 16 : 8;
+    const size_t per_line = vb * ((size_t)nc + (kind == 2 ? 2 * (size_t)nr : kind == 1 ? (size_t)nc : 0));
+    const size_t budget = 160 * 1024;  // opt-in above 48 KB
     const int lines = tab * 8 + per_line <= budget ? (int)std::min<size_t>(8, (budget - tab * 8) / per_line) : 0;
     if (lines > 0) {
       a.stage_lines = lines;
       const size_t smem = per_line * lines + tab * 8;
       const unsigned blocks = (unsigned)((L + lines - 1) / lines);
+      if (smem > 48 * 1024) {
+        cudaError_t e = cplx_data
+            ? cudaFuncSetAttribute(apply_staged_kernel<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+            : cudaFuncSetAttribute(apply_staged_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
       if (cplx_data)
         apply_staged_kernel<cplx><<<blocks, kStageThreads, smem, st>>>(a, static_cast<const cplx*>(x),
                                                                        static_cast<cplx*>(y));

@@ -342,6 +342,21 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream) {
   return cuda_check(shen::launch_cross(n, fields, h, S(stream)), "shen_cross");
 }
 
+int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, void* stream) {
+  if (P == 0 || M == 0) return SHEN_OK;
+  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !fields || !h) return fail(SHEN_ERR_ARG, "shen_cross_paired: bad args");
+  return cuda_check(shen::launch_cross_paired(P, Q, M, fields, h, S(stream)), "shen_cross_paired");
+}
+
+int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
+                    const double* c_im, void* y, int64_t y_row_stride, void* stream) {
+  if (rows == 0 || L == 0) return SHEN_OK;
+  if (rows < 0 || L < 0 || x_row_stride < L || y_row_stride < L || !x || !c_re || !c_im || !y)
+    return fail(SHEN_ERR_ARG, "shen_scale_rows: bad args");
+  return cuda_check(shen::launch_scale_rows(rows, L, x, x_row_stride, c_re, c_im, y, y_row_stride, S(stream)),
+                    "shen_scale_rows");
+}
+
 int shen_recover_velocity(const shen_recover_args* r, void* stream) {
   if (!r) return fail(SHEN_ERR_ARG, "shen_recover_velocity: NULL args");
   if (r->L == 0 || r->n_dir == 0) return SHEN_OK;

@@ -84,6 +84,8 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_apply_rank2_tail": (4, 1, None, None, None, None, None, None, None, 1, None),
         "shen_scale_lines": (2, 2, None, None, None, None, None),
         "shen_cross": (8, None, None, None),
+        "shen_cross_paired": (3, 1, 8, None, None, None),
+        "shen_scale_rows": (2, 4, None, 2, None, None, None, 4, None),
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
     }
     for name, args in cases.items():
