@@ -432,6 +432,169 @@ __global__ void __launch_bounds__(128, SHEN_RHS_UPAR_MINB) rhs_u_par_kernel(RhsU
   }
 }
 
+// Same walk as rhs_u_par_kernel, but everything a row step reads arrives
+// through a cp.async ring in shared memory, issued SHEN_RHS_RING - 1 steps
+// ahead: the seven input rows (per thread) and the row's 20 operator entries
+// (per warp: lanes 0..19 copy one each, all lanes read them as broadcasts).
+// ncu on the register-window kernel: 164 registers -> 12 warps per SM and
+// 5.2 long-scoreboard stall cycles per issue, most of them on the operator
+// entries' __ldg latency inside each row's dependency chain (44% of the HBM
+// roofline).  Warps are single-parity (each parity's lines padded to a
+// multiple of 32) so a warp walks one row sequence.  Same operations in the
+// same order -> same bits.
+#ifndef SHEN_RHS_RING
+#define SHEN_RHS_RING 4
+#endif
+constexpr int kRhsRing = SHEN_RHS_RING;
+constexpr int kRhsRingThreads = 128;
+constexpr int kRhsTab = 20;  // stiff 3, mass 5, mixed 4, deriv 3, q s (k+2), d p r (k)
+
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 8 : 0) : "memory");
+}
+
+// banded row with compile-time offsets Ds, entries from tv[0..] (same terms
+// and order as band_win)
+template <typename W>
+__device__ __forceinline__ void band_tab_terms(const RhsBand&, int, const W&, const double*, C2&) {}
+template <typename W, int D, int... Ds>
+__device__ __forceinline__ void band_tab_terms(const RhsBand& m, int k, const W& w, const double* tv, C2& v) {
+  constexpr int k0 = D < 0 ? -D : 0;
+  if (k >= k0 && k < m.nc - D && k < m.nr) v = add(v, rmul(tv[0], w.at(D)));
+  band_tab_terms<W, Ds...>(m, k, w, tv + 1, v);
+}
+template <int... Ds, typename W>
+__device__ __forceinline__ C2 band_tab(const RhsBand& m, int k, const W& w, const double* tv) {
+  C2 v = {0.0, 0.0};
+  band_tab_terms<W, Ds...>(m, k, w, tv, v);
+  return v;
+}
+
+__global__ void __launch_bounds__(kRhsRingThreads, SHEN_RHS_UPAR_MINB) rhs_u_ring_kernel(RhsUArgs a, int64_t Lp) {
+  extern __shared__ __align__(16) double2 rhs_ring_smem[];
+  // rows[slot][stream][thread] (streams u, hcx, hpx, hcy, hpy, hcz, hpz), then tabs[slot][warp][kRhsTab]
+  double2(*rows)[7][kRhsRingThreads] = reinterpret_cast<double2(*)[7][kRhsRingThreads]>(rhs_ring_smem);
+  double(*tabs)[kRhsRingThreads / 32][kRhsTab] =
+      reinterpret_cast<double(*)[kRhsRingThreads / 32][kRhsTab]>(rhs_ring_smem + kRhsRing * 7 * kRhsRingThreads);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int par = t >= Lp ? 1 : 0;
+  const int64_t l_raw = t - (int64_t)par * Lp;
+  const bool live = par < 2 && l_raw < a.L && t < 2 * Lp;
+  const int64_t l = live ? l_raw : 0;
+  const int64_t L = a.L;
+  const int n = a.n_bih, nd = a.mixed.nc;
+  auto ldr = [&](const void* base, int j, int rows_) -> C2 {
+    return (j >= 0 && j < rows_) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
+  };
+  auto hrow = [&](const void* c, const void* p, int j) -> C2 {
+    if (j < 0 || j >= nd) return {0.0, 0.0};
+    return sub(rmul(1.5, ldr(c, j, nd)), rmul(0.5, ldr(p, j, nd)));
+  };
+  const int m = (n - par + 1) / 2;
+  const int ktop = par + 2 * (m - 1);
+  // step i (row k = ktop - 2 i): the row's operator entries, and the rows the
+  // windows shift in after it (u row k - 6, h_x row k - 4, h_y / h_z row k - 3)
+  const void* tsrc = nullptr;  // this lane's operator entry source (row-independent part)
+  int tstride = 0, tadd = 0, tlim = 0;
+  if (lane < kRhsTab) {
+    const RhsBand* b = lane < 3 ? &a.stiff : lane < 8 ? &a.mass : lane < 12 ? &a.mixed : lane < 15 ? &a.deriv : nullptr;
+    const int q = lane < 3 ? lane : lane < 8 ? lane - 3 : lane < 12 ? lane - 8 : lane < 15 ? lane - 12 : 0;
+    if (b) {
+      tsrc = b->diag + (int64_t)q * b->nr;
+      tlim = b->nr;
+    } else {
+      tsrc = lane == 15 ? a.q : lane == 16 ? a.s : lane == 17 ? a.d : lane == 18 ? a.p : a.r;
+      tadd = lane < 17 ? 2 : 0;
+      tlim = n;
+    }
+    tstride = 1;
+  }
+  auto issue = [&](int i) {
+    const int s = i % kRhsRing;
+    const int k = ktop - 2 * i;
+    const bool on = live && i < m;
+    const int ju = k - 6, jx = k - 4, jy = k - 3;
+    const bool ou = on && ju >= 0 && ju < n, ox = on && jx >= 0 && jx < nd, oy = on && jy >= 0 && jy < nd;
+    cp16(&rows[s][0][tid], static_cast<const double2*>(a.u) + (ou ? (int64_t)ju * L + l : 0), ou);
+    cp16(&rows[s][1][tid], static_cast<const double2*>(a.hcx) + (ox ? (int64_t)jx * L + l : 0), ox);
+    cp16(&rows[s][2][tid], static_cast<const double2*>(a.hpx) + (ox ? (int64_t)jx * L + l : 0), ox);
+    cp16(&rows[s][3][tid], static_cast<const double2*>(a.hcy) + (oy ? (int64_t)jy * L + l : 0), oy);
+    cp16(&rows[s][4][tid], static_cast<const double2*>(a.hpy) + (oy ? (int64_t)jy * L + l : 0), oy);
+    cp16(&rows[s][5][tid], static_cast<const double2*>(a.hcz) + (oy ? (int64_t)jy * L + l : 0), oy);
+    cp16(&rows[s][6][tid], static_cast<const double2*>(a.hpz) + (oy ? (int64_t)jy * L + l : 0), oy);
+    if (lane < kRhsTab) {
+      const int kt = k + tadd;
+      const bool ot = i < m && kt >= 0 && kt < tlim;
+      cp8(&tabs[s][wid][lane], static_cast<const double*>(tsrc) + (ot ? kt * tstride : 0), ot);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int i = 0; i < kRhsRing - 1; ++i) issue(i);
+  const bool warp_live = __any_sync(0xffffffffu, live);
+  if (!warp_live) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    return;
+  }
+  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
+  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
+  PWin<-4, 4> U;    // u rows k-4 .. k+4 (this parity)
+  PWin<-2, 4> HX;   // h_x rows k-2 .. k+4 (this parity)
+  PWin<-1, 3> HY, HZ;  // h_y, h_z rows k-1, k+1, k+3 (other parity)
+#pragma unroll
+  for (int d = -4; d <= 4; d += 2) U.v[(d + 4) / 2] = ldr(a.u, ktop + d, n);
+#pragma unroll
+  for (int d = -2; d <= 4; d += 2) HX.v[(d + 2) / 2] = hrow(a.hcx, a.hpx, ktop + d);
+#pragma unroll
+  for (int d = -1; d <= 3; d += 2) {
+    HY.v[(d + 1) / 2] = hrow(a.hcy, a.hpy, ktop + d);
+    HZ.v[(d + 1) / 2] = hrow(a.hcz, a.hpz, ktop + d);
+  }
+  C2 sq = {0.0, 0.0}, ss = {0.0, 0.0};
+  bool have = false;
+  double2* out = static_cast<double2*>(a.out) + l;
+  int i = 0;
+  for (int k = ktop; k >= 0; k -= 2, ++i) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kRhsRing - 2) : "memory");
+    __syncwarp();
+    const int s = i % kRhsRing;
+    const double* tv = tabs[s][wid];
+    if (k + 2 < n) {  // fold row k + 2 of this parity into the rank-2 tail sums
+      const C2 uj = U.at(2);
+      const C2 qx = rmul(tv[15], uj), sx = rmul(tv[16], uj);
+      sq = have ? add(qx, sq) : qx;
+      ss = have ? add(sx, ss) : sx;
+      have = true;
+    }
+    C2 f = rmul(tv[17], U.at(0));
+    if (k < n - 2) {
+      f = add(f, rmul(tv[18], sq));
+      f = add(f, rmul(tv[19], ss));
+    }
+    C2 r = rmul(a.c_fourth, f);
+    r = sub(r, rmul(cs, band_tab<-2, 0, 2>(a.stiff, k, U, tv)));
+    r = add(r, rmul(cm, band_tab<-4, -2, 0, 2, 4>(a.mass, k, U, tv + 3)));
+    r = sub(r, rmul(cx, band_tab<-2, 0, 2, 4>(a.mixed, k, HX, tv + 8)));
+    r = sub(r, cmul(cy, band_tab<-1, 1, 3>(a.deriv, k, HY, tv + 12)));
+    r = sub(r, cmul(cz, band_tab<-1, 1, 3>(a.deriv, k, HZ, tv + 12)));
+    if (live) out[(int64_t)k * L] = make_double2(r.re, r.im);
+    auto g = [&](int q) -> C2 { const double2 v = rows[s][q][tid]; return {v.x, v.y}; };
+    const int jx = k - 4, jy = k - 3;
+    U.shift(g(0));
+    HX.shift(jx >= 0 && jx < nd ? sub(rmul(1.5, g(1)), rmul(0.5, g(2))) : C2{0.0, 0.0});
+    HY.shift(jy >= 0 && jy < nd ? sub(rmul(1.5, g(3)), rmul(0.5, g(4))) : C2{0.0, 0.0});
+    HZ.shift(jy >= 0 && jy < nd ? sub(rmul(1.5, g(5)), rmul(0.5, g(6))) : C2{0.0, 0.0});
+    issue(i + kRhsRing - 1);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 static bool offs_are(const RhsBand& m, std::initializer_list<int> o) {
   if (m.n_off != (int)o.size()) return false;
   int i = 0;
@@ -446,7 +609,7 @@ cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_dir <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
   static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 2;
-  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant == 2)
+  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant >= 2)
     rhs_g_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
   else if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant == 1)
     rhs_g_fast_kernel<<<blocks, 128, 0, st>>>(a);
@@ -458,10 +621,20 @@ cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
 cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_bih <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
-  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 2;
+  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 3;
   const bool fixed = offs_are(a.stiff, {-2, 0, 2}) && offs_are(a.mass, {-4, -2, 0, 2, 4}) &&
                      offs_are(a.mixed, {-2, 0, 2, 4}) && offs_are(a.deriv, {-1, 1, 3});
-  if (fixed && variant == 2)
+  if (fixed && variant == 3) {
+    constexpr int smem = kRhsRing * 7 * kRhsRingThreads * (int)sizeof(double2) +
+                         kRhsRing * (kRhsRingThreads / 32) * kRhsTab * (int)sizeof(double);
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(rhs_u_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    const int64_t Lp = (a.L + 31) / 32 * 32;  // single-parity warps
+    rhs_u_ring_kernel<<<(unsigned)((2 * Lp + kRhsRingThreads - 1) / kRhsRingThreads), kRhsRingThreads, smem, st>>>(
+        a, Lp);
+  }
+  else if (fixed && variant == 2)
     rhs_u_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
   else if (fixed && variant == 1)
     rhs_u_fast_kernel<<<blocks, 128, 0, st>>>(a);
