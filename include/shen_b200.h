@@ -277,6 +277,14 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream);
  * points' values: rows j < Q: h_j + h_{N-1-j}, row Q: h_Q, rows P + j:
  * h_j - h_{N-1-j}. */
 int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, void* stream);
+/* The pairing alone, for the 3-D transforms (x: N = P + Q rows of M doubles;
+ * y: the [P + Q][M] sum / difference form above):
+ * shen_pair_split: y = (x_j + x_{N-1-j}, centre, x_j - x_{N-1-j});
+ * shen_pair_merge: the inverse map with e, o as in the paired form,
+ * x_j = e_j + o_j, x_{N-1-j} = e_j - o_j.  M even, pointers 16-B aligned
+ * (rows of complex128 values), P <= 65535. */
+int shen_pair_split(int64_t P, int64_t Q, int64_t M, const double* x, double* y, void* stream);
+int shen_pair_merge(int64_t P, int64_t Q, int64_t M, const double* y, double* x, void* stream);
 /* shen_scale_lines with row strides (in elements) for x and y. */
 int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
                     const double* c_im, void* y, int64_t y_row_stride, void* stream);

@@ -97,6 +97,8 @@ _SIGS = {
     "shen_scale_lines": (ctypes.c_int, [_c_int64, _c_int64, _vp, _vp, _vp, _vp, _vp]),
     "shen_cross": (ctypes.c_int, [_c_int64, _vp, _vp, _vp]),
     "shen_cross_paired": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
+    "shen_pair_split": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
+    "shen_pair_merge": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
     "shen_scale_rows": (ctypes.c_int, [_c_int64, _c_int64, _vp, _c_int64, _vp, _vp, _vp, _c_int64, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
     "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,

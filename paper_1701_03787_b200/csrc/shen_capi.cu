@@ -348,6 +348,18 @@ int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, dou
   return cuda_check(shen::launch_cross_paired(P, Q, M, fields, h, S(stream)), "shen_cross_paired");
 }
 
+int shen_pair_split(int64_t P, int64_t Q, int64_t M, const double* x, double* y, void* stream) {
+  if (P == 0 || M == 0) return SHEN_OK;
+  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !x || !y) return fail(SHEN_ERR_ARG, "shen_pair_split: bad args");
+  return cuda_check(shen::launch_pair(false, P, Q, M, x, y, S(stream)), "shen_pair_split");
+}
+
+int shen_pair_merge(int64_t P, int64_t Q, int64_t M, const double* y, double* x, void* stream) {
+  if (P == 0 || M == 0) return SHEN_OK;
+  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !x || !y) return fail(SHEN_ERR_ARG, "shen_pair_merge: bad args");
+  return cuda_check(shen::launch_pair(true, P, Q, M, y, x, S(stream)), "shen_pair_merge");
+}
+
 int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
                     const double* c_im, void* y, int64_t y_row_stride, void* stream) {
   if (rows == 0 || L == 0) return SHEN_OK;

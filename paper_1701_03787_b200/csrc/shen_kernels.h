@@ -174,6 +174,8 @@ cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const dou
                                cudaStream_t st);
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
 cudaError_t launch_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, cudaStream_t st);
+cudaError_t launch_pair(bool merge, int64_t P, int64_t Q, int64_t M, const double* src, double* dst,
+                        cudaStream_t st);
 cudaError_t launch_scale_rows(int64_t rows, int64_t L, const void* x, int64_t xs, const double* cre,
                               const double* cim, void* y, int64_t ys, cudaStream_t st);
 

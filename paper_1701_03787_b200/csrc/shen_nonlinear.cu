@@ -16,7 +16,10 @@
 //                     writes h's symmetric / antisymmetric parts -- so both
 //                     wall-normal operators act on half the modes (GEMMs of
 //                     half the flops) with no extra pass;
-//   shen_scale_lines_rows: scale_lines with row strides (the even / odd
+//   shen_pair_split / shen_pair_merge: the same pairing for the 3-D
+//                     transforms (one elementwise pass on each side of the
+//                     half-size operator GEMMs);
+//   shen_scale_rows:  scale_lines with row strides (the even / odd
 //                     coefficient rows of the paired forward operator are
 //                     interleaved while the mask is applied).
 #include <cuda_runtime.h>
@@ -109,6 +112,39 @@ __global__ void scale_rows_kernel(int64_t rows, int64_t L, const double2* x, int
   }
 }
 
+// mirror pairing of wall-normal rows (real view, M doubles per row):
+// split  y[j] = x[j] + x[N-1-j], y[Q] = x[Q] (centre), y[P+j] = x[j] - x[N-1-j]
+// merge  x[j] = y[j] + y[P+j],  x[N-1-j] = y[j] - y[P+j],  x[Q] = y[Q]
+// grid: x over the row's M/2 double2 columns, y = pair row j < P (no index division)
+__global__ void pair_split_kernel(int64_t P, int64_t Q, int64_t M2, const double2* __restrict__ x,
+                                  double2* __restrict__ y) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y, N = P + Q;
+  if (c >= M2) return;
+  const double2 a = __ldg(x + j * M2 + c);
+  if (j < Q) {
+    const double2 b = __ldg(x + (N - 1 - j) * M2 + c);
+    y[j * M2 + c] = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+    y[(P + j) * M2 + c] = make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+  } else {
+    y[j * M2 + c] = a;
+  }
+}
+__global__ void pair_merge_kernel(int64_t P, int64_t Q, int64_t M2, const double2* __restrict__ y,
+                                  double2* __restrict__ x) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = blockIdx.y, N = P + Q;
+  if (c >= M2) return;
+  const double2 e = __ldg(y + j * M2 + c);
+  if (j < Q) {
+    const double2 o = __ldg(y + (P + j) * M2 + c);
+    x[j * M2 + c] = make_double2(__dadd_rn(e.x, o.x), __dadd_rn(e.y, o.y));
+    x[(N - 1 - j) * M2 + c] = make_double2(__dsub_rn(e.x, o.x), __dsub_rn(e.y, o.y));
+  } else {
+    x[j * M2 + c] = e;
+  }
+}
+
 unsigned grid_for(int64_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -122,6 +158,22 @@ unsigned grid_for(int64_t n) {
 cudaError_t launch_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, cudaStream_t st) {
   if (P <= 0 || M <= 0) return cudaSuccess;
   cross_paired_kernel<<<grid_for(P * M), 256, 0, st>>>(P, Q, M, fields, h);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair(bool merge, int64_t P, int64_t Q, int64_t M, const double* src, double* dst,
+                        cudaStream_t st) {
+  if (P <= 0 || M <= 0) return cudaSuccess;
+  if (M % 2 != 0 || P > 65535 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 != 0)
+    return cudaErrorInvalidValue;  // rows of complex values (double2-aligned)
+  const int64_t M2 = M / 2;
+  const dim3 grid((unsigned)((M2 + 255) / 256), (unsigned)P);
+  if (merge)
+    pair_merge_kernel<<<grid, 256, 0, st>>>(P, Q, M2, reinterpret_cast<const double2*>(src),
+                                            reinterpret_cast<double2*>(dst));
+  else
+    pair_split_kernel<<<grid, 256, 0, st>>>(P, Q, M2, reinterpret_cast<const double2*>(src),
+                                            reinterpret_cast<double2*>(dst));
   return cudaGetLastError();
 }
 

@@ -448,6 +448,78 @@ def _apply_operator(M, lines):
     return torch.view_as_complex(out.view(M.shape[0], L, 2))
 
 
+@lru_cache(maxsize=16)
+def _paired_dev(kind: str, n_x: int, fam: int, sp: int, dev_index: int, scale: float = 1.0):
+    """Mirror-paired blocks of an operator, or None if it has no mirror parity.
+
+    x_{N-1-j} = -x_j and every basis function has the parity of its mode, so
+    the inverse E (N x n) satisfies E[N-1-j, k] = (-1)^k E[j, k] and the
+    forward F (n x N) F[k, N-1-j] = (-1)^k F[k, j]: even modes couple only
+    to pair sums (plus the centre point), odd modes only to pair differences.
+    Two GEMMs with the blocks do half the flops of the full operator
+    (nonlinear.py uses the same split)."""
+    import torch
+
+    M = _operator_host(kind, n_x, fam, sp)
+    if scale != 1.0:
+        M = M * scale
+    N = n_x + 1
+    P, Q = (N + 1) // 2, N // 2
+    tol = 1e-12 * np.abs(M).max()
+    if kind == "inv":
+        sign = np.where(np.arange(M.shape[1]) % 2 == 0, 1.0, -1.0)
+        if not np.allclose(M[::-1], M * sign, rtol=0, atol=tol):
+            return None
+        S, A = M[:P, 0::2], M[:Q, 1::2]
+    else:
+        sign = np.where(np.arange(M.shape[0]) % 2 == 0, 1.0, -1.0)[:, None]
+        if not np.allclose(M[:, ::-1], M * sign, rtol=0, atol=tol):
+            return None
+        S, A = M[0::2, :P], M[1::2, :Q]
+    dev = torch.device("cuda", dev_index)
+    return (torch.from_numpy(np.ascontiguousarray(S)).to(dev), torch.from_numpy(np.ascontiguousarray(A)).to(dev),
+            P, Q)
+
+
+PAIRED_MIN_LINES = 512  # below this one full GEMM beats split + two GEMMs + pass
+
+
+def _forward_paired(blocks, lines):
+    """(N, L) lines -> (n, L) coefficients: pair split pass, then the even /
+    odd mode blocks write the interleaved output rows directly (cuBLAS ldc)."""
+    import torch
+
+    S, A, P, Q = blocks
+    N, L = lines.shape
+    y = torch.empty((N, L), dtype=torch.complex128, device=lines.device)
+    _lib.check(_lib.lib().shen_pair_split(P, Q, 2 * L, lines.data_ptr(), y.data_ptr(), stream_handle()),
+               "shen_pair_split")
+    n = S.shape[0] + A.shape[0]
+    out = torch.empty((n, L), dtype=torch.complex128, device=lines.device)
+    outr, yr = torch.view_as_real(out).reshape(n, 2 * L), torch.view_as_real(y).reshape(N, 2 * L)
+    torch.matmul(S, yr[:P], out=outr[0::2])
+    torch.matmul(A, yr[P:], out=outr[1::2])
+    return out
+
+
+def _inverse_paired(blocks, coef):
+    """(n, L) coefficients -> (N, L) lines: the even / odd mode blocks read
+    strided coefficient rows (cuBLAS ldb) into e, o; one merge pass."""
+    import torch
+
+    S, A, P, Q = blocks
+    n, L = coef.shape
+    N = P + Q
+    y = torch.empty((N, L), dtype=torch.complex128, device=coef.device)
+    cr, yr = torch.view_as_real(coef).reshape(n, 2 * L), torch.view_as_real(y).reshape(N, 2 * L)
+    torch.matmul(S, cr[0::2], out=yr[:P])
+    torch.matmul(A, cr[1::2], out=yr[P:])
+    lines = torch.empty((N, L), dtype=torch.complex128, device=coef.device)
+    _lib.check(_lib.lib().shen_pair_merge(P, Q, 2 * L, y.data_ptr(), lines.data_ptr(), stream_handle()),
+               "shen_pair_merge")
+    return lines
+
+
 # ---------------------------------------------------------------- wall-normal stage on lines
 
 def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
@@ -455,6 +527,10 @@ def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
     coefficients (scalar products if ``solve_mass`` is False)."""
     if XFORM_METHOD == "matrix":
         kind = "fwd" if solve_mass else "fsp"
+        if lines.shape[1] >= PAIRED_MIN_LINES:
+            blocks = _paired_dev(kind, n_x, fam, sp, device().index)
+            if blocks is not None:
+                return _forward_paired(blocks, lines.contiguous())
         return _apply_operator(_operator_dev(kind, n_x, fam, sp, device().index), lines)
     scal = _chebyshev_pass(lines, fam, sp)
     if solve_mass and sp != 0:
@@ -467,6 +543,10 @@ def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
     ``norm`` for the following ``irfft2`` (the matrix route folds the
     1/(n_y n_z) of the inverse FFT into its operator)."""
     if XFORM_METHOD == "matrix":
+        if coef.shape[1] >= PAIRED_MIN_LINES:
+            blocks = _paired_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)
+            if blocks is not None:
+                return _inverse_paired(blocks, coef.contiguous()), "forward"
         op = _operator_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)
         return _apply_operator(op, coef), "forward"
     return _expand_pass(coef, sp, n_x, fam), "backward"

@@ -86,6 +86,8 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_cross": (8, None, None, None),
         "shen_cross_paired": (3, 1, 8, None, None, None),
         "shen_scale_rows": (2, 4, None, 2, None, None, None, 4, None),
+        "shen_pair_split": (3, 1, 8, None, None, None),
+        "shen_pair_merge": (2, 3, 8, None, None, None),
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
     }
     for name, args in cases.items():

@@ -101,6 +101,25 @@ def test_transforms_vs_oracle_larger(fi, n_x, xform_method):
 
 
 @pytest.mark.parametrize("fi", [0, 1])
+def test_mirror_paired_route_vs_oracle(fi):
+    """>= PAIRED_MIN_LINES Fourier lines: the matrix route splits each
+    operator into even / odd mode blocks on mirror-paired points (pair
+    split / merge passes + two half-size GEMMs); same gates as above."""
+    mesh = build_mesh(64, 32, 32, 2 * np.pi, np.pi, FAMS[fi])
+    assert mesh.n_y * (mesh.n_z // 2 + 1) >= T.PAIRED_MIN_LINES
+    mats = assemble(64, fi)
+    u = np.random.default_rng(5 + fi).uniform(-1, 1, mesh.shape)
+    for sc, space in enumerate(SPACES):
+        c = T.forward_transform(T.PhysicalField(u, mesh), space)
+        want = O.forward_transform(u, sc, fi == 1, mats)
+        _close(c.data, want)
+        _close(T.forward_scalar_product(T.PhysicalField(u, mesh), space).data,
+               O.forward_scalar_product(u, sc, fi == 1))
+        back = T.inverse_transform(T.SpectralField(want, c.grid, mesh))
+        _close(back.data, O.inverse_transform(want, sc, fi == 1, 64, mesh.n_y, mesh.n_z))
+
+
+@pytest.mark.parametrize("fi", [0, 1])
 def test_real_inputs_stay_real(fi):
     rng = np.random.default_rng(5)
     v = rng.standard_normal((17, 4, 2))
