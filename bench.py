@@ -103,6 +103,9 @@ class ClockSampler:
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
     def __enter__(self):
+        if os.environ.get("SHEN_BENCH_NO_CLOCKS"):  # diagnosis only: the bench line then says "unsampled"
+            self.proc = None
+            return self
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -114,6 +117,17 @@ class ClockSampler:
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        # start timing only once nvidia-smi has initialised NVML and written a
+        # sample: its start-up takes driver locks that can stall CUDA launches
+        # (a host-bound timed region of a few ms would absorb the whole stall)
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 10.0:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.05)
         time.sleep(0.3)
         return self
 
@@ -550,18 +564,26 @@ def run_step(args):
 
     state = FlowState(field(gb), field(gd), field(gd), field(gd), tuple(field(gd) for _ in range(3)),
                       tuple(field(gd) for _ in range(3)), 0.01, 0.0, 0)
+    # warm-up advances the state exactly like the timed loop (same allocation
+    # pattern: each step holds the previous state's nonlinear term)
+    s = state
     for _ in range(max(args.warmup, 3)):
-        stp.step(state)
+        s = stp.step(s)
     torch.cuda.synchronize()
+    # The eager step is ~150 launches from Python, close to host-bound: a host
+    # hiccup inside one short timed block shows up whole.  Time 5 blocks of K
+    # steps and report the median block (all five in "blocks_ms_per_step").
+    blocks = []
     with ClockSampler(local) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        s = state
-        for _ in range(args.steps):
-            s = stp.step(s)
-        e1.record()
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                s = stp.step(s)
+            e1.record()
+            torch.cuda.synchronize()
+            blocks.append(e0.elapsed_time(e1) / args.steps)
+    ms = float(np.median(blocks))
     cpu = None if args.no_cpu else cpu_step(stp, state)
     print(json.dumps({
         "metric": "time steps/s (reference ChannelStepper.step composed of the device kernels)",
@@ -572,6 +594,7 @@ def run_step(args):
                                "dt=1e-4, fixed beta; 8 inverse + 3 forward transforms, 2 RHS, 2 batched solves, "
                                "velocity recovery, mean-flow solve",
                    "l2_policy": "every field 135 MB (> L2)"},
+        "blocks_ms_per_step": blocks, "timing": "median of 5 blocks of `steps` eager steps (CUDA events)",
         "build_s": t_build, "cpu_baseline": cpu, "clocks": clk.summary()}))
 
 
