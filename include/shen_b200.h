@@ -259,8 +259,9 @@ int shen_recover_velocity(const shen_recover_args* args, void* stream);
 /* ---------------------------------------------------------------------
  * Nonlinear term H = u x omega (reference stepper.py:148-185), pointwise
  * pieces; the transforms around them are wall-normal GEMMs + cuFFT.
- * shen_scale_lines: y[r][l] = c_l x[r][l] for rows x L complex128 (numpy
- *   complex product order); c = c_re + i c_im per line (1j m, 1j n, mask).
+ * shen_scale_lines: y[r][l] = c_l x[r][l] for rows x L complex128
+ *   ((c.re x.re - c.im x.im, c.re x.im + c.im x.re), every product rounded);
+ *   c = c_re + i c_im per line (1j m, 1j n, mask: exact either way).
  * shen_cross: fields = 8 real planes-stacked arrays of n points
  *   [u, v, w, om_x, dv_dx, dw_dx, du_dy, du_dz] -> h = 3 arrays
  *   (v om_z - w om_y, w om_x - u om_z, u om_y - v om_x) with

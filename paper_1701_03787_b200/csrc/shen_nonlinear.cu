@@ -2,7 +2,7 @@
 // stepper.py:148-185), SURVEY.md 8(f) rank 3.  The transforms around them are
 // the wall-normal operator GEMMs and cuFFT (nonlinear.py).
 //
-//   shen_scale_lines: y[r, l] = c_l * x[r, l] (complex, numpy product order):
+//   shen_scale_lines: y[r, l] = c_l * x[r, l] (complex, products rounded separately):
 //                     the 1j m / 1j n derivative factors and the dealiasing
 //                     mask, one per Fourier line;
 //   shen_cross:       om_y = du_dz - dw_dx, om_z = dv_dx - du_dy and
