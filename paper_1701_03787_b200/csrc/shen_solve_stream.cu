@@ -626,11 +626,15 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency
   // (a 3-deep ring measured slower at config 4: 29.5 vs 28.6 ms)
+#ifndef SHEN_BIH_RING
+#define SHEN_BIH_RING 2
+#endif
   const size_t ring2 = (size_t)2 * R * 64 * SG * sizeof(V);
+  const size_t ringb = (size_t)SHEN_BIH_RING * R * 64 * SG * sizeof(V);
   const size_t tabb = (size_t)(a.n_bih + 4) * BC_STRIDE * sizeof(double);
   static const bool force_pp = getenv("SHEN_BIH_PP") != nullptr && atoi(getenv("SHEN_BIH_PP")) != 0;
-  if (!force_pp && ring2 + tabb <= 220 * 1024)
-    return bih_stream_launch<V, R, true, 2, SG>(a, scratch, ctas_per_sm, ring2 + tabb, st);
+  if (!force_pp && ringb + tabb <= 220 * 1024)
+    return bih_stream_launch<V, R, true, SHEN_BIH_RING, SG>(a, scratch, ctas_per_sm, ringb + tabb, st);
   const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);  // one parity
   if (ring2 + tabp <= 220 * 1024)
     return bih_stream_launch<V, R, true, 2, SG, true>(a, scratch, ctas_per_sm, ring2 + tabp, st);
