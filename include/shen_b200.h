@@ -135,6 +135,16 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                           void* scratch, int is_complex, int warps_per_sm, int max_ctas, int64_t j_begin,
                           int64_t j_end, void* stream);
+/* Same solve with systems taken in mirror pairs: pairs[0..P) and
+ * pairs[P..2P) are system indices with bitwise-identical z2 (for a channel
+ * grid: wavenumbers (m, n) and (-m, n)); one thread runs the factor
+ * recurrence once for both right-hand sides.  pairs[c] == pairs[P + c] marks
+ * an unpaired system (solved once).  Every system must appear exactly once
+ * over both halves; results are bit-identical to shen_bih_solve_stream. */
+int shen_bih_solve_stream_pairs(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                                const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                                void* scratch, int is_complex, const int64_t* pairs, int64_t n_pairs, int max_ctas,
+                                void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

@@ -201,6 +201,25 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
                     "shen_bih_solve_stream");
 }
 
+int shen_bih_solve_stream_pairs(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                                const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
+                                void* scratch, int is_complex, const int64_t* pairs, int64_t n_pairs, int max_ctas,
+                                void* stream) {
+  if (batch == 0 || n_pairs == 0) return SHEN_OK;
+  if (n_bih < 2 || batch < 0 || n_pairs < 0 || n_pairs > batch || !xi1 || !xi2 || !tab || !rhs || !out || !pairs)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: bad args");
+  const int rows0 = (n_bih + 1) / 2;
+  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: chunk_rows");
+  if (rows0 > chunk_rows && (!ckpt || !scratch)) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: ckpt/scratch");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: rhs must not alias out");
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: max_ctas");
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  return cuda_check(shen::launch_bih_stream(a, scratch, is_complex != 0, 8, S(stream)), "shen_bih_solve_stream_pairs");
+}
+
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream) {

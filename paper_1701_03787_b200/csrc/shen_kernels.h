@@ -101,6 +101,11 @@ struct BihChunkArgs {
   void* out;
   int64_t jb = 0, je = -1;
   int max_ctas = 0;
+  // mirror pairs (stream solve): pairs[0..P) and pairs[P..2P) are two systems
+  // with bitwise-identical z2 (hence identical factors) solved by one thread;
+  // equal entries mark an unpaired system.  nullptr: one system per thread.
+  const int64_t* pairs = nullptr;
+  int64_t n_pairs = 0;
 };
 
 cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);

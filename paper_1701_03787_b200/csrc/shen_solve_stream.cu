@@ -556,6 +556,283 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   cpa_wait<0>();
 }
 
+// ======================================================================= biharmonic, mirror pairs
+// Systems (m, n) and (-m, n) of a channel grid have bitwise-identical z2, so
+// the reference computes bitwise-identical factors for them.  One thread
+// solves such a pair: the factor recurrence (bands, elimination, reciprocal
+// -- ~2/3 of the biharmonic's fp64 work) and the row-table reads run once for
+// two right-hand sides, and the factor checkpoints are read once for two.
+// Every per-system operation is the one bih_stream_kernel performs, so the
+// results are bit-identical to it.  Work items are pairs (P of them; an
+// unpaired system is a pair of itself and is stored once); one parity per
+// CTA with the one-parity compact table (the two RHS streams double the ring).
+template <typename V, int R, int SG>
+__global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V* ychk) {
+  constexpr int kT = 64 * SG;
+  constexpr int SGE = 2 * SG;  // 32-item groups per CTA work item (one parity per CTA)
+  constexpr int RING = 2;
+  using O = VOps<V>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int par = (int)(blockIdx.x & 1), sgi = warp;
+  const int64_t B = a.batch;
+  const int nb = a.n_bih;
+  const int n = (nb - par + 1) / 2;
+  const int nseg = (n + R - 1) / R;
+  // ring slot: rows 0..R-1 of stream 0, then rows 0..R-1 of stream 1
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * 2 * R * 32 + lane;
+  double* stab = smem + (size_t)kT / 32 * RING * 2 * R * 32 * VOps<V>::ndouble;
+  // backward: the next segment's factor checkpoint (10 doubles) and y
+  // checkpoints (4 values) land here by cp.async while the current segment
+  // runs (registers have no room for a prefetch): ckd[q][kT], cky[q][kT]
+  double* ckd = stab + (size_t)(n + 2) * BC_STRIDE;
+  V* cky = reinterpret_cast<V*>(ckd + 10 * kT);
+  for (int q = tid; q < (n + 2) * BC_STRIDE; q += kT) {
+    const int pos = q / BC_STRIDE, col = q - pos * BC_STRIDE, i = pos - 2;
+    double v = 0.0;
+    if (i >= 0 && col < BC_NCOL) {
+      v = __ldg(a.tab + (int64_t)(par + 2 * i) * B_STRIDE + bc_src(col));
+      if (col == BC_P || col == BC_R || col == BC_Q0 || col == BC_T2 || col == BC_T4)
+        v = __dmul_rn(a.xi0, v);  // == bih_fast_prescale
+    } else if (i == -1 && (col == BC_Q4 || col == BC_S4)) {
+      v = __ldg(a.tab + (int64_t)par * B_STRIDE + (col == BC_Q4 ? B_Q2 : B_S2));
+    }
+    stab[q] = v;
+  }
+  __syncthreads();
+  auto tpos = [&](int i) { return i + 2; };
+  constexpr int tstep = 1;
+  auto q4s4 = [&](int i, double& q4, double& s4) {
+    const double2 v = *reinterpret_cast<const double2*>(stab + (int64_t)tpos(i) * BC_STRIDE + BC_Q4);
+    q4 = v.x; s4 = v.y;
+  };
+  const V* rhs = static_cast<const V*>(a.rhs);
+  V* out = static_cast<V*>(a.out);
+  const int64_t P = a.n_pairs;
+  const int64_t* pa = a.pairs;
+  const int64_t* pb = a.pairs + P;
+  const int64_t ngroups = (P + 32 * SGE - 1) / (32 * SGE);
+  const int64_t g0 = blockIdx.x >> 1;
+  const int64_t gstride = (gridDim.x + 1 - par) >> 1;
+  if (g0 >= ngroups) return;
+  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
+  // per-thread segment stream over both systems of the thread's pair
+  auto issue = [&](V* slot, SegRef ref) {
+    if (ref.g < ngroups) {
+      const int64_t c = ref.g * (32 * SGE) + sgi * 32 + lane;
+      const bool cv = c < P;
+      const int64_t cc = cv ? c : P - 1;
+      const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+      const int rows = min(R, n - ref.s * R);
+      const int64_t step = 2 * B;
+      const V* p0 = rhs + (int64_t)(par + 2 * ref.s * R) * B + ja;
+      const V* p1 = rhs + (int64_t)(par + 2 * ref.s * R) * B + jb2;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool ok = cv && r < rows;
+        cpa(slot + r * 32, p0, ok);
+        cpa(slot + (R + r) * 32, p1, ok);
+        if (r + 1 < rows) {
+          p0 += step;
+          p1 += step;
+        }
+      }
+    }
+    cpa_commit();
+  };
+  int64_t qi = 0;
+  SegIt it{g0, 0};
+  for (; qi < RING - 1; ++qi) {
+    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg));
+    else cpa_commit();
+    it.next(nseg, gstride);
+  }
+  int64_t qc = 0;
+  auto consume = [&]() -> V* {
+    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg));
+    else cpa_commit();
+    it.next(nseg, gstride);
+    ++qi;
+    cpa_wait<RING - 1>();
+    V* p = ring + (qc % RING) * 2 * R * 32;
+    ++qc;
+    return p;
+  };
+
+  for (int64_t g = g0; g < ngroups; g += gstride) {
+    const int64_t c = g * (32 * SGE) + sgi * 32 + lane;
+    const bool cv = c < P;
+    const int64_t cc = cv ? c : P - 1;
+    const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+    const bool second = cv && jb2 != ja;  // store the second system (an unpaired one is stored once)
+    const double xi1 = __ldg(a.xi1 + ja), xi2 = __ldg(a.xi2 + ja);
+    V* outa = out + (int64_t)par * B + ja;
+    V* outb = out + (int64_t)par * B + jb2;
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((nb + 1) / 2 + R - 1) / R) * 4 * kT + tid;
+    const double* ckj = a.ckpt + (int64_t)par * 10 * B + ja;
+    using Full = std::integral_constant<bool, true>;
+    using Part = std::integral_constant<bool, false>;
+    // ---------------- forward
+    BihU u{0, 0, 0, 0, 0, 0}, u1{0, 0, 0, 0, 0, 0}, u2{0, 0, 0, 0, 0, 0};
+    V y1 = szero<V>(), y2 = szero<V>(), z1 = szero<V>(), z2 = szero<V>();
+    auto fwd_seg = [&](int s, auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const V* cur = consume();
+      BihCarry cr;
+      BihProd pr;
+      if (FULL) {
+        bih_carry_init(stab, tpos(s * R), tstep, cr);
+        bih_prod_init(xi2, cr, pr);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = s * R + r;
+        const int ic = FULL ? i : min(i, n - 1);
+        double cv_[B_NCOL];
+        double l2, l4;
+        if (FULL) {
+          load_bih_row_carry(stab, tpos(ic), cv_, cr);
+          bih_row_fast_carried(u, u1, u2, cv_, xi1, xi2, pr, r == 0, l2, l4);
+        } else {
+          load_bih_row_compact(stab, tpos(ic), tstep, cv_);
+          const BihBands hb = bih_bands_fast(xi1, xi2, cv_);
+          bih_step_fast(u, u1, u2, hb, cv_, l2, l4);
+        }
+        u2 = u1;
+        u1 = u;
+        const bool valid = FULL || i < n;
+        const V b0 = valid ? cur[r * 32] : szero<V>();
+        const V b1 = valid ? cur[(R + r) * 32] : szero<V>();
+        const V y = sfma(-l4, y2, sfma(-l2, y1, b0));
+        y2 = y1;
+        y1 = y;
+        const V z = sfma(-l4, z2, sfma(-l2, z1, b1));
+        z2 = z1;
+        z1 = z;
+      }
+    };
+    const int nfull = n / R;
+    for (int s = 0; s < nseg; ++s) {
+      if (s < nfull) fwd_seg(s, Full{}); else fwd_seg(s, Part{});
+      if (s + 1 < nseg) {
+        ystore(ychkj + (4 * s) * kT, y1);
+        ystore(ychkj + (4 * s + 1) * kT, y2);
+        ystore(ychkj + (4 * s + 2) * kT, z1);
+        ystore(ychkj + (4 * s + 3) * kT, z2);
+      }
+    }
+    // ---------------- backward
+    V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
+    V w1x = szero<V>(), w2x = szero<V>(), tq = szero<V>(), tv = szero<V>();
+    // checkpoints entering segment s into ckd / cky (own commit group: the
+    // next consume() waits for it -- its ring group is issued after this one)
+    auto ck_issue = [&](int s) {
+      if (s > 0) {
+        const double* cp = ckj + (int64_t)20 * s * B;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) cpa(ckd + q * kT + tid, cp + q * B, true);
+        const V* yk = ychkj + (4 * (s - 1)) * kT;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cpa(cky + q * kT + tid, yk + q * kT, true);
+      }
+      cpa_commit();
+    };
+    auto bwd_seg = [&](int s, auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
+      V ya = szero<V>(), yb = szero<V>(), za = szero<V>(), zb = szero<V>();
+      V* cur = consume();  // also completes ck_issue(s)
+      if (s > 0) {  // factor state and y entering the segment
+        const double* c = ckd + tid;
+        w1.d = c[0]; w1.e = c[kT]; w1.f = c[2 * kT]; w1.a = c[3 * kT]; w1.b = c[4 * kT];
+        w2.d = c[5 * kT]; w2.e = c[6 * kT]; w2.f = c[7 * kT]; w2.a = c[8 * kT]; w2.b = c[9 * kT];
+        const V* yv = cky + tid;
+        ya = yv[0]; yb = yv[kT]; za = yv[2 * kT]; zb = yv[3 * kT];
+        V* yk = ychkj + (4 * (s - 1)) * kT;
+        ydiscard(yk, lane);
+        ydiscard(yk + kT, lane);
+        ydiscard(yk + 2 * kT, lane);
+        ydiscard(yk + 3 * kT, lane);
+        bih_set_rcp(w1);
+        if (s * R >= 2) bih_set_rcp(w2);
+        else bih_clear_rcp(w2);
+      }
+      ck_issue(s - 1);  // the buffer is free again: next segment's checkpoints
+      BihCarry cr;
+      BihProd pr;
+      if (FULL) {
+        bih_carry_init(stab, tpos(s * R), tstep, cr);
+        bih_prod_init(xi2, cr, pr);
+      }
+      double e_[R], f_[R], a_[R], b_[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = s * R + r;
+        const int ic = FULL ? i : min(i, n - 1);
+        double cv_[B_NCOL];
+        double l2, l4;
+        if (FULL) {
+          load_bih_row_carry(stab, tpos(ic), cv_, cr);
+          bih_row_fast_carried(w, w1, w2, cv_, xi1, xi2, pr, r == 0, l2, l4);
+        } else {
+          load_bih_row_compact(stab, tpos(ic), tstep, cv_);
+          const BihBands hb = bih_bands_fast(xi1, xi2, cv_);
+          bih_step_fast(w, w1, w2, hb, cv_, l2, l4);
+        }
+        w2 = w1;
+        w1 = w;
+        const bool valid = FULL || i < n;
+        const V y = sfma(-l4, yb, sfma(-l2, ya, valid ? cur[r * 32] : szero<V>()));
+        yb = ya;
+        ya = y;
+        const V z = sfma(-l4, zb, sfma(-l2, za, valid ? cur[(R + r) * 32] : szero<V>()));
+        zb = za;
+        za = z;
+        const double rd = valid ? w.rd : 0.0;
+        cur[r * 32] = smul(rd, y);
+        cur[(R + r) * 32] = smul(rd, z);
+        e_[r] = rd * w.e;
+        f_[r] = rd * w.f;
+        a_[r] = rd * w.a;
+        b_[r] = rd * w.b;
+      }
+      V* opa = outa + (int64_t)2 * (s * R) * B;
+      V* opb = outb + (int64_t)2 * (s * R) * B;
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        const int i = s * R + r;
+        const bool valid = FULL || i < n;
+        double qn, sn;
+        q4s4(FULL ? i : min(i, n - 1), qn, sn);
+        if (!valid) qn = sn = 0.0;
+        V x = sfma(-e_[r], x1, cur[r * 32]);
+        x = sfma(-f_[r], x2, x);
+        x = sfma(-a_[r], sq, x);
+        x = sfma(-b_[r], sv, x);
+        sq = sfma(qn, x2, sq);
+        sv = sfma(sn, x2, sv);
+        x2 = x1;
+        x1 = x;
+        V xb = sfma(-e_[r], w1x, cur[(R + r) * 32]);
+        xb = sfma(-f_[r], w2x, xb);
+        xb = sfma(-a_[r], tq, xb);
+        xb = sfma(-b_[r], tv, xb);
+        tq = sfma(qn, w2x, tq);
+        tv = sfma(sn, w2x, tv);
+        w2x = w1x;
+        w1x = xb;
+        if (cv && valid) O::st_cs(opa + (int64_t)2 * r * B, x);
+        if (second && valid) O::st_cs(opb + (int64_t)2 * r * B, xb);
+      }
+    };
+    ck_issue(nseg - 1);
+    for (int s = nseg - 1; s >= 0; --s) {
+      if (s < nfull) bwd_seg(s, Full{}); else bwd_seg(s, Part{});
+    }
+  }
+  cpa_wait<0>();
+}
+
 // ======================================================================= launchers
 static int stream_ctas(int ctas_per_sm) {
   int dev = 0, sms = 0;
@@ -622,7 +899,28 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
 }
 
 template <typename V, int R, int SG>
+static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
+  constexpr int kT = 64 * SG;
+  const size_t ring = (size_t)2 * 2 * R * kT * sizeof(V);
+  const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);
+  const size_t ckb = (size_t)kT * (10 * sizeof(double) + 4 * sizeof(V));
+  const size_t smem = ring + tabp + ckb;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = bih_pair_kernel<V, R, SG>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  if (a.n_pairs <= 0) return cudaSuccess;
+  const int64_t groups = 2 * ((a.n_pairs + 32 * 2 * SG - 1) / (32 * 2 * SG));  // one item per parity
+  int64_t cap = stream_ctas(1);
+  if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
+  return cudaGetLastError();
+}
+
+template <typename V, int R, int SG>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
+  if (a.pairs != nullptr) return bih_pair_launch<V, R, SG>(a, scratch, st);
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency
   // (a 3-deep ring measured slower at config 4: 29.5 vs 28.6 ms)

@@ -200,6 +200,38 @@ def solve_many(jobs):
     return outs
 
 
+MIRROR_PAIRS = _env_int("SHEN_PAIRS", 1)  # solve mirror-paired systems together (biharmonic stream)
+
+
+def mirror_pairs(z2):
+    """Pairs of systems with bitwise-identical z2 rows (the channel grid's
+    (m, n) / (-m, n) wavenumbers), as an int64 (2, P) array over the
+    flattened z2, or None.  Rows of a 2-D z2 that are byte-identical are
+    paired up; unpaired rows become self-pairs.  Items of one row pair are
+    consecutive, so a warp's 32 lanes read coalesced row pieces of both
+    systems."""
+    z2 = np.asarray(z2, dtype=float)
+    if z2.ndim != 2 or z2.shape[0] < 2 or z2.shape[1] < 1:
+        return None
+    rows, cols = z2.shape
+    groups = {}
+    for r in range(rows):
+        groups.setdefault(z2[r].tobytes(), []).append(r)
+    pairs_r = []
+    for members in groups.values():
+        for k in range(0, len(members) - 1, 2):
+            pairs_r.append((members[k], members[k + 1]))
+        if len(members) % 2:
+            pairs_r.append((members[-1], members[-1]))
+    if sum(a != b for a, b in pairs_r) * 2 < rows // 2:  # too few pairs to pay
+        return None
+    pairs_r.sort()
+    n = np.arange(cols, dtype=np.int64)
+    a = np.concatenate([r0 * cols + n for r0, _ in pairs_r])
+    b = np.concatenate([r1 * cols + n for _, r1 in pairs_r])
+    return np.stack([a, b])
+
+
 def _solve_real_via_complex(lu, rhs_dev, out_dev):
     """Real RHS whose rows are not 16-B aligned (odd batch): the streaming
     kernel moves 16-B row pieces, so solve the complex system with zero
@@ -527,6 +559,7 @@ class BiharmonicLU:
         self._stored = stored
         self._qs_dev = None
         self._host = None
+        self._pairs = None  # device (2, P) int64 mirror pairs (build_biharmonic), or None
 
     @property
     def n_modes(self) -> int:
@@ -597,6 +630,16 @@ class BiharmonicLU:
                                           ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(), int(is_complex), sh),
                   "shen_bih_solve_stored")
             del keep
+        elif self.method == "stream" and self._pairs is not None and j0 == 0 and j1 in (-1, B):
+            # mirror pairs: one factor recurrence for two systems (bit-identical results)
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
+            P = int(self._pairs.shape[1])
+            check(h.shen_bih_solve_stream_pairs(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
+                                                self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
+                                                out_dev.data_ptr(), scratch, int(is_complex), self._pairs.data_ptr(),
+                                                P, max_ctas, sh),
+                  "shen_bih_solve_stream_pairs")
         elif self.method == "stream":
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
             scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
@@ -659,7 +702,12 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
         del keep
     if B > 0:
         _raise_pivot(pivot.cpu().numpy(), "biharmonic")
-    return BiharmonicLU(mats.n_x, mats.family, np.shape(z2), xi0, x1d, x2d, tab, q, s, R, ckpt, method, stored)
+    lu = BiharmonicLU(mats.n_x, mats.family, np.shape(z2), xi0, x1d, x2d, tab, q, s, R, ckpt, method, stored)
+    if method == "stream" and MIRROR_PAIRS:
+        pr = mirror_pairs(z2)
+        if pr is not None:
+            lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
+    return lu
 
 
 # ------------------------------------------------------------------ host helpers (tests)

@@ -289,3 +289,26 @@ def test_solve_many_matches_single_solves():
     assert xb.dtype == np.float64
     with pytest.raises(ValueError):
         S.solve_many([(hlu, fh[:, :3])])
+
+
+@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64)])
+@pytest.mark.parametrize("cplx", [True, False])
+def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
+    """Mirror-paired systems ((m, n) and (-m, n): identical z2) share one
+    factor recurrence per thread; results must equal the one-system-per-thread
+    solve bit for bit (same per-system operations)."""
+    from paper_1701_03787_b200.mesh import channel_z2
+
+    mats = assemble(n_x, 0)
+    z2 = channel_z2(ny, nz)
+    lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
+    assert lu._pairs is not None
+    rng = np.random.default_rng(n_x + ny)
+    shp = (mats.n_bih,) + z2.shape
+    f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
+    x_pair = lu.solve(f)
+    pairs = lu._pairs
+    lu._pairs = None
+    x_one = lu.solve(f)
+    lu._pairs = pairs
+    assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
