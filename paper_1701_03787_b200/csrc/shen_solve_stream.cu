@@ -49,6 +49,25 @@ __device__ __forceinline__ void cpa(cplx* dst, const cplx* src, bool pred) {
   const int n = pred ? 16 : 0;  // src-size 0 -> zero fill, no global access
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(n) : "memory");
 }
+// streaming RHS rows with an L2 evict-first policy (the pair kernel's y
+// checkpoints, evict-last, then keep more of L2)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cpa_ef(cplx* dst, const cplx* src, bool pred, uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(src), "r"(n), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_ef(double* dst, const double* src, bool pred, uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s), "l"(src), "r"(n), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cpa(double* dst, const double* src, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   const int n = pred ? 8 : 0;
@@ -627,11 +646,20 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
       const int64_t step = 2 * B;
       const V* p0 = rhs + (int64_t)(par + 2 * ref.s * R) * B + ja;
       const V* p1 = rhs + (int64_t)(par + 2 * ref.s * R) * B + jb2;
+#ifndef SHEN_PAIR_EF
+#define SHEN_PAIR_EF 0  // measured: evict-first RHS rows cost more DRAM reads (23.5 vs 22.6 ms)
+#endif
+      const uint64_t pol = policy_evict_first();
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const bool ok = cv && r < rows;
-        cpa(slot + r * 32, p0, ok);
-        cpa(slot + (R + r) * 32, p1, ok);
+        if (SHEN_PAIR_EF) {
+          cpa_ef(slot + r * 32, p0, ok, pol);
+          cpa_ef(slot + (R + r) * 32, p1, ok, pol);
+        } else {
+          cpa(slot + r * 32, p0, ok);
+          cpa(slot + (R + r) * 32, p1, ok);
+        }
         if (r + 1 < rows) {
           p0 += step;
           p1 += step;
@@ -920,7 +948,11 @@ static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStr
 
 template <typename V, int R, int SG>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
-  if (a.pairs != nullptr) return bih_pair_launch<V, R, SG>(a, scratch, st);
+  if (a.pairs != nullptr) {
+    static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
+    if (pw == 6) return bih_pair_launch<V, R, 3>(a, scratch, st);
+    return bih_pair_launch<V, R, 4>(a, scratch, st);
+  }
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency
   // (a 3-deep ring measured slower at config 4: 29.5 vs 28.6 ms)
