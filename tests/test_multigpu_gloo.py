@@ -12,7 +12,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1701_03787_b200.shard import assemble_slabs, kx_slab, slab_of
+from paper_1701_03787_b200.shard import assemble_slabs, kx_rows_folded, kx_slab, slab_of
 
 
 def test_kx_slab_partition():
@@ -25,6 +25,32 @@ def test_kx_slab_partition():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         kx_slab(8, 2, 2)
+
+
+def test_kx_rows_folded_partition_and_pairs():
+    """Folded slabs (bench.py multi-GPU): every kx row on exactly one rank,
+    balanced, and every rank's z2 rows form whole mirror pairs, so the
+    biharmonic pair kernel applies on every rank."""
+    from paper_1701_03787_b200.mesh import channel_z2
+    from paper_1701_03787_b200.solvers import mirror_pairs
+
+    for n_y in (8, 64, 2048):
+        z2 = channel_z2(n_y, 16)
+        for world in (1, 2, 3, 8):
+            parts = [kx_rows_folded(n_y, r, world) for r in range(world)]
+            allr = np.concatenate(parts)
+            assert sorted(allr.tolist()) == list(range(n_y))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 3
+            for rows in parts:
+                if len([r for r in rows if r not in (0, n_y // 2)]) < 2:
+                    continue  # more ranks than pairs: this rank holds no pair
+                pr = mirror_pairs(z2[rows])
+                assert pr is not None
+                zf = z2[rows].reshape(-1)
+                assert np.array_equal(zf[pr[0]], zf[pr[1]])
+                assert sorted(np.concatenate([pr[0], pr[1][pr[1] != pr[0]]]).tolist()) == list(range(zf.size))
+    assert list(kx_rows_folded(7, 0, 1)) == list(range(7))  # odd n_y: plain slab
 
 
 def _free_port():
