@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c4")
     ap.add_argument("--kx-rows", type=int, default=0, help="limit the kx rows per rank (debug)")
+    ap.add_argument("--kx-fold", type=int, default=0,
+                    help="profile subset: the rows of rank 0 of a K-way folded split (keeps mirror pairs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--method", default="stream", choices=["stream", "chunked", "stored", "tile"])
@@ -81,9 +83,7 @@ def measured_peak():
 def measured_traffic(cfg, method, op, unknowns):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
     committed ncu --set full capture (profiles/traffic_c4.json: bytes per
-    unknown measured on a 512-kx-row slab of config 4, scaled to this launch's
-    unknowns -- the kernels stream, so bytes per unknown do not depend on the
-    slab width)."""
+    unknown of the full config-4 launches, scaled to this launch's unknowns)."""
     path = os.path.join(ROOT, "profiles", "traffic_c4.json")
     if cfg != "c4" or method != "stream" or not os.path.exists(path):
         return None, None
@@ -178,6 +178,8 @@ def run_b200(args):
     if args.kx_rows:  # debug slab: contiguous rows
         lo, hi = kx_slab(n_y, rank, world)
         rows = np.arange(lo, min(hi, lo + args.kx_rows))
+    elif args.kx_fold:  # profiling subset with mirror pairs
+        rows = kx_rows_folded(n_y, 0, args.kx_fold)
     else:  # folded slabs: whole (m, -m) pairs per rank (the biharmonic solves them together)
         rows = kx_rows_folded(n_y, rank, world)
     lo, hi = 0, len(rows)

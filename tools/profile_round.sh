@@ -1,13 +1,14 @@
 # Round profiling recipe (run under gpurun, one GPU):
 #   1. the default bench line (no profiler)
 #   2. the ncu launch list of the same command (duration + DRAM bytes per launch)
-#   3. one ncu --set full capture of each streaming kernel on a 512-kx-row slab
+#   3. one ncu --set full capture of each streaming kernel on the full config-4
+#      launch (the first H and B launches of a warm-up step)
 set -e
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_default.csv python bench.py > gpurun_out/bench_under_ncu.log 2>&1
-python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 --kx-rows 512 > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:stream_kernel -c 2 -o gpurun_out/stream_full -f \
-    python bench.py --no-e2e --no-cpu --steps 1 --warmup 3 --kx-rows 512 > gpurun_out/ncu_full.log 2>&1
+python bench.py --no-e2e --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:'stream_kernel|pair_kernel' -c 2 -o gpurun_out/stream_full -f \
+    python bench.py --no-e2e --no-cpu --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1
 ncu -i gpurun_out/stream_full.ncu-rep --page raw --csv > gpurun_out/stream_full_raw.csv
