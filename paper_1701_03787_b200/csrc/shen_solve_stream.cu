@@ -927,12 +927,18 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
 }
 
 template <typename V, int R, int SG>
-static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
+static size_t bih_pair_smem(const BihChunkArgs& a) {
   constexpr int kT = 64 * SG;
   const size_t ring = (size_t)2 * 2 * R * kT * sizeof(V);
   const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);
   const size_t ckb = (size_t)kT * (10 * sizeof(double) + 4 * sizeof(V));
-  const size_t smem = ring + tabp + ckb;
+  return ring + tabp + ckb;
+}
+
+template <typename V, int R, int SG>
+static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
+  constexpr int kT = 64 * SG;
+  const size_t smem = bih_pair_smem<V, R, SG>(a);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = bih_pair_kernel<V, R, SG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -949,9 +955,12 @@ static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStr
 template <typename V, int R, int SG>
 static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_per_sm, cudaStream_t st) {
   if (a.pairs != nullptr) {
+    // the pair kernel needs two RHS rings plus the one-parity table in shared
+    // memory; past n_x ~ 1150 it does not fit and the one-system kernel
+    // solves every system (the pair table lists each exactly once)
     static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
-    if (pw == 6) return bih_pair_launch<V, R, 3>(a, scratch, st);
-    return bih_pair_launch<V, R, 4>(a, scratch, st);
+    if (pw == 6 && bih_pair_smem<V, R, 3>(a) <= 227 * 1024) return bih_pair_launch<V, R, 3>(a, scratch, st);
+    if (bih_pair_smem<V, R, 4>(a) <= 227 * 1024) return bih_pair_launch<V, R, 4>(a, scratch, st);
   }
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency

@@ -291,7 +291,7 @@ def test_solve_many_matches_single_solves():
         S.solve_many([(hlu, fh[:, :3])])
 
 
-@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64)])
+@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32)])
 @pytest.mark.parametrize("cplx", [True, False])
 def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
     """Mirror-paired systems ((m, n) and (-m, n): identical z2) share one
@@ -301,7 +301,11 @@ def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
 
     mats = assemble(n_x, 0)
     z2 = channel_z2(ny, nz)
-    lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
+    S.PAIRS_MIN, saved = 1, S.PAIRS_MIN  # force pairs at test sizes
+    try:
+        lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
+    finally:
+        S.PAIRS_MIN = saved
     assert lu._pairs is not None
     rng = np.random.default_rng(n_x + ny)
     shp = (mats.n_bih,) + z2.shape
