@@ -100,6 +100,16 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
                            int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
+/* Same Helmholtz solve with systems taken in mirror pairs (the layout of
+ * shen_bih_solve_stream_pairs below): one thread runs the factor recurrence
+ * once for both right-hand sides and reads the checkpoints once for two
+ * systems.  warps_per_sm 4 / 6 / 8 selects the CTA size (0: the default).
+ * Results are bit-identical to shen_helm_solve_stream.  Replaces
+ * the reference's HelmholtzLU.solve (solvers.py:100-126) for channel grids. */
+int shen_helm_solve_stream_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                                 const double* st, const double* md, int chunk_rows, const double* ckpt,
+                                 const void* rhs, void* out, void* scratch, int is_complex, const int64_t* pairs,
+                                 int64_t n_pairs, int warps_per_sm, int max_ctas, void* stream);
 /* Tiled chunk-parallel solve: a CTA holds 4 consecutive systems (all rows)
  * in shared memory, warps = (system, parity), lanes = 32 chunks of
  * chunk_rows rows; the RHS is read once.  Same inputs as

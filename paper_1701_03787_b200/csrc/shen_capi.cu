@@ -121,6 +121,28 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                     "shen_helm_solve_stream");
 }
 
+int shen_helm_solve_stream_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
+                                 const double* st, const double* md, int chunk_rows, const double* ckpt,
+                                 const void* rhs, void* out, void* scratch, int is_complex, const int64_t* pairs,
+                                 int64_t n_pairs, int warps_per_sm, int max_ctas, void* stream) {
+  if (batch == 0 || n_pairs == 0) return SHEN_OK;
+  if (n_dir < 2 || batch < 0 || n_pairs < 0 || n_pairs > batch || !cb || !sd || !st || !md || !rhs || !out || !pairs)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: bad args");
+  const int rows0 = (n_dir + 1) / 2;
+  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: chunk_rows");
+  if (rows0 > chunk_rows && (!ckpt || !scratch)) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: ckpt/scratch");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: rhs must not alias out");
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: max_ctas");
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  if (warps_per_sm != 0 && warps_per_sm != 4 && warps_per_sm != 6 && warps_per_sm != 8)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: warps_per_sm");
+  return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
+                    "shen_helm_solve_stream_pairs");
+}
+
 int shen_helm_solve_tile(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
                          const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                          int is_complex, void* stream) {

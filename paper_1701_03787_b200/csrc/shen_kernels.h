@@ -86,6 +86,9 @@ struct HelmChunkArgs {
   void* out;
   int64_t jb = 0, je = -1;  // system range [jb, je) of the streaming solve (je < 0: whole batch)
   int max_ctas = 0;          // streaming solve: cap on persistent CTAs (0: one per SM)
+  // mirror pairs (stream solve, as BihChunkArgs): nullptr = one system per thread
+  const int64_t* pairs = nullptr;
+  int64_t n_pairs = 0;
 };
 
 struct BihChunkArgs {

@@ -113,6 +113,80 @@ template <typename V> __device__ __forceinline__ V szero();
 template <> __device__ __forceinline__ double szero<double>() { return 0.0; }
 template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 
+
+// ---------------------------------------------------------------- tensor memory
+// The biharmonic pair kernel parks the y checkpoints of its first segments
+// (the longest-lived ones: written first in the forward sweep, read last in
+// the backward) in TMEM instead of the L2-resident scratch.  Warp w owns lanes
+// 32 (w % 4) .. +31 (the 32x32b shape: thread = lane) and a column range
+// picked by w / 4.
+#ifndef SHEN_PAIR_TMEM_SEGS
+#define SHEN_PAIR_TMEM_SEGS 16
+#endif
+__device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(slot))
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(base) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t a, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(a), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t a, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(a)
+               : "memory");
+}
+__device__ __forceinline__ void tpack(double x, uint32_t* w) {
+  w[0] = (uint32_t)__double2loint(x);
+  w[1] = (uint32_t)__double2hiint(x);
+}
+__device__ __forceinline__ double tunpack(const uint32_t* w) { return __hiloint2double((int)w[1], (int)w[0]); }
+__device__ __forceinline__ void tpack(cplx x, uint32_t* w) {
+  tpack(x.re, w);
+  tpack(x.im, w + 2);
+}
+template <typename V>
+__device__ __forceinline__ V tunpackv(const uint32_t* w);
+template <>
+__device__ __forceinline__ double tunpackv<double>(const uint32_t* w) { return tunpack(w); }
+template <>
+__device__ __forceinline__ cplx tunpackv<cplx>(const uint32_t* w) { return {tunpack(w), tunpack(w + 2)}; }
+// four values (y1, y2, z1, z2) of one checkpoint: 8 (real) or 16 (complex) columns
+template <typename V>
+__device__ __forceinline__ void tmem_put4(uint32_t a, V v0, V v1, V v2, V v3) {
+  constexpr int W = sizeof(V) / 4;
+  uint32_t w[4 * W];
+  tpack(v0, w);
+  tpack(v1, w + W);
+  tpack(v2, w + 2 * W);
+  tpack(v3, w + 3 * W);
+  tmem_st8(a, w);
+  if (W == 4) tmem_st8(a + 8, w + 8);
+}
+template <typename V>
+__device__ __forceinline__ void tmem_get4(uint32_t a, V& v0, V& v1, V& v2, V& v3) {
+  constexpr int W = sizeof(V) / 4;
+  uint32_t w[4 * W];
+  tmem_ld8(a, w);
+  if (W == 4) tmem_ld8(a + 8, w + 8);
+  tmem_wait_ld();
+  v0 = tunpackv<V>(w);
+  v1 = tunpackv<V>(w + W);
+  v2 = tunpackv<V>(w + 2 * W);
+  v3 = tunpackv<V>(w + 3 * W);
+}
+
 constexpr int kSG = 4;                    // 32-system groups per CTA (128 consecutive systems)
 constexpr int kStreamThreads = 64 * kSG;  // warp w: parity w & 1, system group w >> 1
 
@@ -149,7 +223,8 @@ struct SegIt {
 
 template <typename V, int R, int SG>
 __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int n, int par, int64_t B,
-                                          int64_t ngroups, int64_t jb, int64_t je, int sgi, int lane) {
+                                          int64_t ngroups, int64_t jb, int64_t je, int sgi, int lane,
+                                          uint64_t pol = 0) {
   if (ref.g < ngroups) {
     const int64_t j = jb + ref.g * (32 * SG) + sgi * 32 + lane;
     const bool jv = j < je;
@@ -162,13 +237,15 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
     if (jv && rows == R) {  // every segment but the last: no per-row predicates
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        cpa(slot + r * 32, p, true);
+        if (pol) cpa_ef(slot + r * 32, p, true, pol);
+        else cpa(slot + r * 32, p, true);
         p += step;
       }
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        cpa(slot + r * 32, p, jv && r < rows);
+        if (pol) cpa_ef(slot + r * 32, p, jv && r < rows, pol);
+        else cpa(slot + r * 32, p, jv && r < rows);
         if (r + 1 < rows) p += step;
       }
     }
@@ -182,7 +259,7 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
 // (parity 0 / 1 of the same 32 systems).  HBM traffic per unknown: 2 RHS
 // reads + 1 solution write (+ ~3 B of checkpoints).
 template <typename V, int R, int RING, int SG>
-__global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
+__global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows, int hint) {
   constexpr int kT = 64 * SG;
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
@@ -216,14 +293,18 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
   SegIt it{g0, 0};
+  // L2 policy of the forward (first) and backward (second, last) RHS reads
+  // (hint: 0 none, 1 evict_last / evict_first, 2 - / evict_first, 3 evict_last / -)
+  const uint64_t pfwd = (hint == 1 || hint == 3) ? policy_evict_last() : 0;
+  const uint64_t pbwd = (hint == 1 || hint == 2) ? policy_evict_first() : 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
@@ -317,6 +398,206 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
         S = sadd(x1, S);
         x1 = x;
         if (jv && (full || s * R + r < n)) O::st_cs(outj + (int64_t)2 * (s * R + r) * B, x);
+      }
+    }
+  }
+  cpa_wait<0>();
+}
+
+// ======================================================================= Helmholtz, mirror pairs
+// Systems (m, n) and (-m, n) of a channel grid have bitwise-identical z2, so
+// their factors (cb, hence every d, e, tail) are bitwise identical.  One
+// thread runs the factor recurrence once for both right-hand sides, reads the
+// build's checkpoints once for two systems (3 -> 1.5 B per unknown) and
+// carries two y streams; every per-system operation is the one
+// helm_stream_kernel performs, so the results are bit-identical to it.
+// Warp w: parity w & 1, pair group w >> 1; the ring slot of a segment holds
+// R rows of the first system, then R rows of the second (y replaces b in
+// place in the backward sweep).
+template <typename V, int R, int RING, int SG>
+__global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, V* ychk, int tab_rows, int hint) {
+  constexpr int kT = 64 * SG;
+  using O = VOps<V>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
+  const int64_t B = a.batch;
+  const int n = (a.n_dir - par + 1) / 2;
+  const int nseg = (n + R - 1) / R;
+  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * 2 * R * 32 + lane;
+  const V* rhs = static_cast<const V*>(a.rhs);
+  V* out = static_cast<V*>(a.out);
+  double4* tab = reinterpret_cast<double4*>(smem + (size_t)kT / 32 * RING * 2 * R * 32 * VOps<V>::ndouble);
+  for (int idx = tid; idx < 2 * tab_rows; idx += kT) {
+    const int p = idx / tab_rows, i = idx - p * tab_rows;
+    const int np = (a.n_dir - p + 1) / 2;
+    const int nsp = (a.n_dir - 2 - p + 1) / 2 > 0 ? (a.n_dir - 2 - p + 1) / 2 : 0;
+    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (i < np) {
+      const int k = p + 2 * i;
+      v = make_double4(__ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsp ? 1.0 : 0.0);
+    }
+    tab[idx] = v;
+  }
+  __syncthreads();
+  const double4* mytab = tab + par * tab_rows;
+  const int64_t P = a.n_pairs;
+  const int64_t* pa = a.pairs;
+  const int64_t* pb = a.pairs + P;
+  const int64_t ngroups = (P + 32 * SG - 1) / (32 * SG);
+  const int64_t g0 = blockIdx.x, gstride = gridDim.x;
+  if (g0 >= ngroups) return;
+  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
+  const uint64_t pfwd = (hint == 1 || hint == 3) ? policy_evict_last() : 0;
+  const uint64_t pbwd = (hint == 1 || hint == 2) ? policy_evict_first() : 0;
+  auto issue = [&](V* slot, SegRef ref, uint64_t pol) {
+    if (ref.g < ngroups) {
+      const int64_t c = ref.g * (32 * SG) + sgi * 32 + lane;
+      const bool cv = c < P;
+      const int64_t cc = cv ? c : P - 1;
+      const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+      const int rows = min(R, n - ref.s * R);
+      const int64_t step = 2 * B;
+      const V* p0 = rhs + (int64_t)(par + 2 * ref.s * R) * B + ja;
+      const V* p1 = rhs + (int64_t)(par + 2 * ref.s * R) * B + jb2;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool ok = cv && r < rows;
+        if (pol) {
+          cpa_ef(slot + r * 32, p0, ok, pol);
+          cpa_ef(slot + (R + r) * 32, p1, ok, pol);
+        } else {
+          cpa(slot + r * 32, p0, ok);
+          cpa(slot + (R + r) * 32, p1, ok);
+        }
+        if (r + 1 < rows) {
+          p0 += step;
+          p1 += step;
+        }
+      }
+    }
+    cpa_commit();
+  };
+  int64_t qi = 0;
+  SegIt it{g0, 0};
+  for (; qi < RING - 1; ++qi) {
+    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
+    else cpa_commit();
+    it.next(nseg, gstride);
+  }
+  int64_t qc = 0;
+  auto consume = [&]() -> V* {
+    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
+    else cpa_commit();
+    it.next(nseg, gstride);
+    ++qi;
+    cpa_wait<RING - 1>();
+    V* p = ring + (qc % RING) * 2 * R * 32;
+    ++qc;
+    return p;
+  };
+
+  for (int64_t g = g0; g < ngroups; g += gstride) {
+    const int64_t c = g * (32 * SG) + sgi * 32 + lane;
+    const bool cv = c < P;
+    const int64_t cc = cv ? c : P - 1;
+    const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+    const bool second = cv && jb2 != ja;
+    const double cb = __ldg(a.cb + ja);
+    const double sub = __dmul_rn(cb, -1.5707963267948966);
+    V* outa = out + (int64_t)par * B + ja;
+    V* outb = out + (int64_t)par * B + jb2;
+    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((a.n_dir + 1) / 2 + R - 1) / R) * 2 * kT + tid;
+    const double* ckj = a.ckpt + (int64_t)par * 3 * B + ja;
+    // ---------------- forward: y, z at segment ends only
+    HelmProj pj;
+    hp_origin(pj);
+    V y = szero<V>(), z = szero<V>();
+    double dl = 0.0, el = 0.0, tl = 0.0;
+    for (int s = 0; s < nseg; ++s) {
+      const V* cur = consume();
+      if (s > 0) hp_start(pj, dl, el, tl);
+      const bool full = (s + 1) * R <= n;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = s * R + r;
+        const double4 tv = mytab[i];
+        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
+        if (r > 0 && (r & 7) == 0) hp_rescale(pj);
+        double d, e, t;
+        const double low = hp_step(pj, row, sub, d, e, t);
+        dl = d; el = e; tl = t;
+        const bool valid = full || i < n;
+        y = sfma(-low, y, valid ? cur[r * 32] : szero<V>());
+        z = sfma(-low, z, valid ? cur[(R + r) * 32] : szero<V>());
+      }
+      if (s + 1 < nseg) {
+        ystore(ychkj + (2 * s) * kT, y);
+        ystore(ychkj + (2 * s + 1) * kT, z);
+      }
+    }
+    // ---------------- backward: re-stream each segment (bottom first)
+    V x1 = szero<V>(), S = szero<V>(), w1 = szero<V>(), W = szero<V>();
+    double ckd = 1.0, cke = 0.0, ckt = 0.0;
+    V cky = szero<V>(), ckz = szero<V>();
+    if (nseg - 1 > 0) {
+      const double* ck = ckj + (int64_t)6 * (nseg - 1) * B;
+      ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
+      cky = ychkj[(2 * (nseg - 2)) * kT];
+      ckz = ychkj[(2 * (nseg - 2) + 1) * kT];
+    }
+    for (int s = nseg - 1; s >= 0; --s) {
+      HelmProj q;
+      V yy = szero<V>(), zz = szero<V>();
+      if (s == 0) {
+        hp_origin(q);
+      } else {
+        hp_start(q, ckd, cke, ckt);
+        yy = cky;
+        zz = ckz;
+        ydiscard(ychkj + (2 * (s - 1)) * kT, lane);
+        ydiscard(ychkj + (2 * (s - 1) + 1) * kT, lane);
+      }
+      if (s - 1 > 0) {
+        const double* ck = ckj + (int64_t)6 * (s - 1) * B;
+        ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
+        cky = ychkj[(2 * (s - 2)) * kT];
+        ckz = ychkj[(2 * (s - 2) + 1) * kT];
+      }
+      V* cur = consume();
+      const bool full = (s + 1) * R <= n;
+      double rd_[R], e_[R], t_[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = s * R + r;
+        const double4 tv = mytab[i];
+        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
+        if (r > 0 && (r & 7) == 0) hp_rescale(q);
+        double d, e, t;
+        const double low = hp_step(q, row, sub, d, e, t);
+        const bool valid = full || i < n;
+        yy = sfma(-low, yy, valid ? cur[r * 32] : szero<V>());
+        zz = sfma(-low, zz, valid ? cur[(R + r) * 32] : szero<V>());
+        cur[r * 32] = yy;
+        cur[(R + r) * 32] = zz;
+        rd_[r] = valid ? q.rd : 0.0;
+        e_[r] = valid ? e : 0.0;
+        t_[r] = valid ? t : 0.0;
+      }
+      V* opa = outa + (int64_t)2 * (s * R) * B;
+      V* opb = outb + (int64_t)2 * (s * R) * B;
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        const bool valid = full || s * R + r < n;
+        const V acc = ssub(ssub(cur[r * 32], smul(e_[r], x1)), smul(t_[r], S));
+        const V x = smul(rd_[r], acc);
+        S = sadd(x1, S);
+        x1 = x;
+        const V accb = ssub(ssub(cur[(R + r) * 32], smul(e_[r], w1)), smul(t_[r], W));
+        const V xb = smul(rd_[r], accb);
+        W = sadd(w1, W);
+        w1 = xb;
+        if (cv && valid) O::st_cs(opa + (int64_t)2 * r * B, x);
+        if (second && valid) O::st_cs(opb + (int64_t)2 * r * B, xb);
       }
     }
   }
@@ -635,6 +916,19 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
   const int64_t gstride = (gridDim.x + 1 - par) >> 1;
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
+  // TMEM for the y checkpoints of segments 0 .. KTM-1 (4 values each)
+  constexpr int KTM = (SG == 4 && SHEN_PAIR_TMEM_SEGS > 0) ? SHEN_PAIR_TMEM_SEGS : 0;
+  constexpr int TCOL = (int)sizeof(V);  // columns per checkpoint: 4 values x sizeof(V) / 4 B
+  static_assert(KTM * TCOL <= 256, "two warps share a lane quadrant: 256 columns each");
+  __shared__ uint32_t tmem_slot;
+  uint32_t tbase = 0;
+  if (KTM > 0) {
+    if (warp == 0) tmem_alloc512(&tmem_slot);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
+  }
   // per-thread segment stream over both systems of the thread's pair
   auto issue = [&](V* slot, SegRef ref) {
     if (ref.g < ngroups) {
@@ -743,12 +1037,17 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
     for (int s = 0; s < nseg; ++s) {
       if (s < nfull) fwd_seg(s, Full{}); else fwd_seg(s, Part{});
       if (s + 1 < nseg) {
-        ystore(ychkj + (4 * s) * kT, y1);
-        ystore(ychkj + (4 * s + 1) * kT, y2);
-        ystore(ychkj + (4 * s + 2) * kT, z1);
-        ystore(ychkj + (4 * s + 3) * kT, z2);
+        if (s < KTM) {
+          tmem_put4(tbase + s * TCOL, y1, y2, z1, z2);
+        } else {
+          ystore(ychkj + (4 * s) * kT, y1);
+          ystore(ychkj + (4 * s + 1) * kT, y2);
+          ystore(ychkj + (4 * s + 2) * kT, z1);
+          ystore(ychkj + (4 * s + 3) * kT, z2);
+        }
       }
     }
+    if (KTM > 0) tmem_wait_st();
     // ---------------- backward
     V x1 = szero<V>(), x2 = szero<V>(), sq = szero<V>(), sv = szero<V>();
     V w1x = szero<V>(), w2x = szero<V>(), tq = szero<V>(), tv = szero<V>();
@@ -759,9 +1058,11 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
         const double* cp = ckj + (int64_t)20 * s * B;
 #pragma unroll
         for (int q = 0; q < 10; ++q) cpa(ckd + q * kT + tid, cp + q * B, true);
-        const V* yk = ychkj + (4 * (s - 1)) * kT;
+        if (s - 1 >= KTM) {
+          const V* yk = ychkj + (4 * (s - 1)) * kT;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) cpa(cky + q * kT + tid, yk + q * kT, true);
+          for (int q = 0; q < 4; ++q) cpa(cky + q * kT + tid, yk + q * kT, true);
+        }
       }
       cpa_commit();
     };
@@ -774,13 +1075,17 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
         const double* c = ckd + tid;
         w1.d = c[0]; w1.e = c[kT]; w1.f = c[2 * kT]; w1.a = c[3 * kT]; w1.b = c[4 * kT];
         w2.d = c[5 * kT]; w2.e = c[6 * kT]; w2.f = c[7 * kT]; w2.a = c[8 * kT]; w2.b = c[9 * kT];
-        const V* yv = cky + tid;
-        ya = yv[0]; yb = yv[kT]; za = yv[2 * kT]; zb = yv[3 * kT];
-        V* yk = ychkj + (4 * (s - 1)) * kT;
-        ydiscard(yk, lane);
-        ydiscard(yk + kT, lane);
-        ydiscard(yk + 2 * kT, lane);
-        ydiscard(yk + 3 * kT, lane);
+        if (s - 1 < KTM) {
+          tmem_get4(tbase + (s - 1) * TCOL, ya, yb, za, zb);
+        } else {
+          const V* yv = cky + tid;
+          ya = yv[0]; yb = yv[kT]; za = yv[2 * kT]; zb = yv[3 * kT];
+          V* yk = ychkj + (4 * (s - 1)) * kT;
+          ydiscard(yk, lane);
+          ydiscard(yk + kT, lane);
+          ydiscard(yk + 2 * kT, lane);
+          ydiscard(yk + 3 * kT, lane);
+        }
         bih_set_rcp(w1);
         if (s * R >= 2) bih_set_rcp(w2);
         else bih_clear_rcp(w2);
@@ -859,6 +1164,12 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
     }
   }
   cpa_wait<0>();
+  if (KTM > 0) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc512(tmem_slot);
+  }
 }
 
 // ======================================================================= launchers
@@ -893,7 +1204,8 @@ static cudaError_t helm_stream_RR(const HelmChunkArgs& a, void* scratch, int cta
   int64_t cap = stream_ctas(occ);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
-  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
+  static const int hint = getenv("SHEN_HELM_HINT") ? atoi(getenv("SHEN_HELM_HINT")) : 0;
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows, hint);
   return cudaGetLastError();
 }
 
@@ -902,9 +1214,60 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   // deepest ring that fits next to the row table (bytes in flight per SM)
   const int n0 = (a.n_dir + 1) / 2;
   const size_t tabb = (size_t)2 * (((n0 + R - 1) / R) * R) * sizeof(double4);
+  static const int ring_env = getenv("SHEN_HELM_RING") ? atoi(getenv("SHEN_HELM_RING")) : 0;
+  if (ring_env == 6 && (size_t)6 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
+    return helm_stream_RR<V, R, SG, 6>(a, scratch, ctas_per_sm, st);
+  if (ring_env == 4 && (size_t)4 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
+    return helm_stream_RR<V, R, SG, 4>(a, scratch, ctas_per_sm, st);
   if ((size_t)3 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
     return helm_stream_RR<V, R, SG, 3>(a, scratch, ctas_per_sm, st);
   return helm_stream_RR<V, R, SG, 2>(a, scratch, ctas_per_sm, st);
+}
+
+template <typename V, int R, int SG, int RING>
+static cudaError_t helm_pair_RR(const HelmChunkArgs& a, void* scratch, cudaStream_t st) {
+  constexpr int kT = 64 * SG;
+  const int n0 = (a.n_dir + 1) / 2;
+  const int tab_rows = ((n0 + R - 1) / R) * R;
+  const size_t smem = (size_t)RING * 2 * R * kT * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kern = helm_pair_kernel<V, R, RING, SG>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  if (a.n_pairs <= 0) return cudaSuccess;
+  const int64_t groups = (a.n_pairs + 32 * SG - 1) / (32 * SG);
+  int64_t cap = stream_ctas(1);
+  if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
+  static const int hint = getenv("SHEN_HELM_HINT") ? atoi(getenv("SHEN_HELM_HINT")) : 0;
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows, hint);
+  return cudaGetLastError();
+}
+
+template <typename V, int R, int SG>
+static size_t helm_pair_smem(const HelmChunkArgs& a, int ring) {
+  const int n0 = (a.n_dir + 1) / 2;
+  return (size_t)ring * 2 * R * 64 * SG * sizeof(V) + (size_t)2 * (((n0 + R - 1) / R) * R) * sizeof(double4);
+}
+
+// CTA size (warps_per_sm 4 / 6 / 8) and ring depth (SHEN_HELM_PAIR_RING) of the
+// pair kernel; the default is the one measured best at BASELINE config 4
+template <typename V, int R>
+static cudaError_t helm_pair_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
+  if (w == 0) w = 8;
+  static const int rg = getenv("SHEN_HELM_PAIR_RING") ? atoi(getenv("SHEN_HELM_PAIR_RING")) : 3;
+  if (w == 4) {
+    if (rg >= 4 && helm_pair_smem<V, R, 2>(a, 4) <= 220 * 1024) return helm_pair_RR<V, R, 2, 4>(a, sc, st);
+    if (helm_pair_smem<V, R, 2>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 2, 3>(a, sc, st);
+  } else if (w == 6) {
+    if (rg >= 3 && helm_pair_smem<V, R, 3>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 3, 3>(a, sc, st);
+    if (helm_pair_smem<V, R, 3>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 3, 2>(a, sc, st);
+  } else {
+    if (rg >= 3 && helm_pair_smem<V, R, 4>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 4, 3>(a, sc, st);
+    if (helm_pair_smem<V, R, 4>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 4, 2>(a, sc, st);
+  }
+  if (helm_pair_smem<V, R, 2>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 2, 2>(a, sc, st);
+  return cudaErrorInvalidValue;
 }
 
 template <typename V, int R, bool SMEM_TAB, int RING, int SG, bool PP = false>
@@ -987,10 +1350,20 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
 // can afford to prefetch the segment checkpoints into registers).
 template <typename V>
 static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
+  if (a.pairs != nullptr && a.chunk_rows == 8) {
+    const cudaError_t e = helm_pair_dispatch<V, 8>(a, sc, w, st);
+    if (e != cudaErrorInvalidValue) return e;
+  }
+  // no pairs, or the pair kernel's shared memory does not fit: the
+  // one-system kernel solves the whole batch (a pair table lists every
+  // system exactly once, so this is the same set of solves)
   const bool small = (w == 8);
   switch (a.chunk_rows) {
     case 4: return small ? helm_stream_R<V, 4, 4>(a, sc, 1, st) : helm_stream_R<V, 4, 6>(a, sc, 1, st);
-    case 8: return small ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
+    case 8:
+      if (w == 4) return helm_stream_R<V, 8, 2>(a, sc, 1, st);
+      if (w == 6) return helm_stream_R<V, 8, 3>(a, sc, 1, st);
+      return small ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
     case 16: return helm_stream_R<V, 16, 4>(a, sc, 1, st);
     default: return cudaErrorInvalidValue;
   }

@@ -75,6 +75,14 @@ def stream_warps() -> int:
     return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
 
 
+def helm_pair_warps() -> int:
+    """CTA size of the Helmholtz mirror-pair kernel (4, 6 or 8 warps per SM;
+    0 = the default)."""
+    import os
+
+    return int(os.environ.get("SHEN_HELM_PAIR_WARPS", "0"))
+
+
 # ------------------------------------------------------------------ host <-> device
 
 def _solve_api(lu, rhs, out):
@@ -201,6 +209,7 @@ def solve_many(jobs):
 
 
 MIRROR_PAIRS = _env_int("SHEN_PAIRS", 1)  # solve mirror-paired systems together (biharmonic stream)
+HELM_PAIRS = _env_int("SHEN_HELM_PAIRS", 0)  # the same for the Helmholtz stream solve
 PAIRS_MIN = _env_int("SHEN_PAIRS_MIN", 8192)  # below: one system per thread (c1: 40 vs 33 us; c3 pairs: 0.097 vs 0.120 ms)
 
 
@@ -332,6 +341,7 @@ class HelmholtzLU:
         self._tab = tables_dev
         self.chunk_rows = int(chunk_rows)
         self._ckpt = ckpt
+        self._pairs = None  # device (2, P) int64 mirror pairs (build_helmholtz), or None
         self.method = method
         self._stored = stored  # list of 8 device tensors (exact factors) or None
         self._host = None
@@ -414,6 +424,16 @@ class HelmholtzLU:
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
             del keep
+        elif self.method == "stream" and self._pairs is not None and j0 == 0 and j1 in (-1, B):
+            # mirror pairs: one factor recurrence for two systems (bit-identical results)
+            sd, st, md = self._tab
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
+            check(h.shen_helm_solve_stream_pairs(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
+                                                 md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
+                                                 out_dev.data_ptr(), scratch, int(is_complex), self._pairs.data_ptr(),
+                                                 int(self._pairs.shape[1]), helm_pair_warps(), max_ctas, sh),
+                  "shen_helm_solve_stream_pairs")
         elif self.method == "stream":
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -491,7 +511,12 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
         del keep
     if B > 0:
         _raise_pivot(pivot.cpu().numpy(), "Helmholtz")
-    return HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
+    lu = HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
+    if method == "stream" and HELM_PAIRS and R == 8:
+        pr = mirror_pairs(z2)
+        if pr is not None and pr.shape[1] >= PAIRS_MIN:
+            lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
+    return lu
 
 
 # ------------------------------------------------------------------ biharmonic

@@ -316,3 +316,30 @@ def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
     x_one = lu.solve(f)
     lu._pairs = pairs
     assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
+
+
+@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32)])
+@pytest.mark.parametrize("cplx", [True, False])
+@pytest.mark.parametrize("warps", ["4", "6", "8"])
+def test_helmholtz_mirror_pairs_bitwise(n_x, ny, nz, cplx, warps, monkeypatch):
+    """Helmholtz on mirror pairs (one factor recurrence, two right-hand
+    sides per thread) equals the one-system-per-thread solve bit for bit, for
+    every CTA size of the pair kernel."""
+    from paper_1701_03787_b200.mesh import channel_z2
+
+    monkeypatch.setenv("SHEN_HELM_PAIR_WARPS", warps)
+    mats = assemble(n_x, 0)
+    z2 = channel_z2(ny, nz)
+    monkeypatch.setattr(S, "PAIRS_MIN", 1)
+    monkeypatch.setattr(S, "HELM_PAIRS", 1)
+    lu = S.build_helmholtz(mats, 1 / 2000, 1e-4, z2)
+    assert lu._pairs is not None
+    rng = np.random.default_rng(n_x + ny + 1)
+    shp = (mats.n_dir,) + z2.shape
+    f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
+    x_pair = lu.solve(f)
+    pairs = lu._pairs
+    lu._pairs = None
+    x_one = lu.solve(f)
+    lu._pairs = pairs
+    assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
