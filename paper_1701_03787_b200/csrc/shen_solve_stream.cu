@@ -929,13 +929,21 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
     tmem_fence_after();
     tbase = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
   }
-  // per-thread segment stream over both systems of the thread's pair
+  // per-thread segment stream over both systems of the thread's pair; the
+  // pair's system indices are loaded once per group (a dependent global load
+  // per segment issue was the kernel's largest stall)
+  int64_t ig = -1, ija = 0, ijb = 0;
   auto issue = [&](V* slot, SegRef ref) {
     if (ref.g < ngroups) {
       const int64_t c = ref.g * (32 * SGE) + sgi * 32 + lane;
       const bool cv = c < P;
-      const int64_t cc = cv ? c : P - 1;
-      const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+      if (ref.g != ig) {
+        const int64_t cc = cv ? c : P - 1;
+        ija = __ldg(pa + cc);
+        ijb = __ldg(pb + cc);
+        ig = ref.g;
+      }
+      const int64_t ja = ija, jb2 = ijb;
       const int rows = min(R, n - ref.s * R);
       const int64_t step = 2 * B;
       const V* p0 = rhs + (int64_t)(par + 2 * ref.s * R) * B + ja;
