@@ -292,25 +292,29 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
+  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
   SegIt it{g0, 0};
   // L2 policy of the forward (first) and backward (second, last) RHS reads
   // (hint: 0 none, 1 evict_last / evict_first, 2 - / evict_first, 3 evict_last / -)
   const uint64_t pfwd = (hint == 1 || hint == 3) ? policy_evict_last() : 0;
   const uint64_t pbwd = (hint == 1 || hint == 2) ? policy_evict_first() : 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
+    islot = islot + 1 == RING ? 0 : islot + 1;
   }
   int64_t qc = 0;
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
+    islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
-    const V* p = ring + (qc % RING) * R * 32;
+    const V* p = ring + cslot * R * 32;
     ++qc;
+    cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
 
@@ -478,21 +482,25 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, 
     cpa_commit();
   };
   int64_t qi = 0;
+  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
+    islot = islot + 1 == RING ? 0 : islot + 1;
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
+    islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
-    V* p = ring + (qc % RING) * 2 * R * 32;
+    V* p = ring + cslot * 2 * R * 32;
     ++qc;
+    cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
 
@@ -683,21 +691,25 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
+  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SGE>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SGE>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
+    islot = islot + 1 == RING ? 0 : islot + 1;
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) seg_issue<V, R, SGE>(ring + (qi % RING) * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
+    if (qi < nq) seg_issue<V, R, SGE>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
+    islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
-    V* p = ring + (qc % RING) * R * 32;
+    V* p = ring + cslot * R * 32;
     ++qc;
+    cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
 
@@ -971,21 +983,25 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
     cpa_commit();
   };
   int64_t qi = 0;
+  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg));
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
     else cpa_commit();
     it.next(nseg, gstride);
+    islot = islot + 1 == RING ? 0 : islot + 1;
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) issue(ring + (qi % RING) * 2 * R * 32, it.ref(nseg));
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
+    islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
-    V* p = ring + (qc % RING) * 2 * R * 32;
+    V* p = ring + cslot * 2 * R * 32;
     ++qc;
+    cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
 
