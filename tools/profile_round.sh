@@ -12,3 +12,5 @@ python bench.py --no-e2e --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:'stream_kernel|pair_kernel' -c 2 -o gpurun_out/stream_full -f \
     python bench.py --no-e2e --no-cpu --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1
 ncu -i gpurun_out/stream_full.ncu-rep --page raw --csv > gpurun_out/stream_full_raw.csv
+python tools/full_capture_summary.py gpurun_out/stream_full_raw.csv gpurun_out/r01_ncu_full_stream_c4.csv gpurun_out/traffic_c4.json
+python tools/ncu_summary.py gpurun_out/launches_default.csv --json gpurun_out/launches_default_summary.json > gpurun_out/launches_default_summary.txt
