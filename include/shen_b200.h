@@ -155,6 +155,17 @@ int shen_bih_solve_stream_pairs(int n_bih, double xi0, const double* xi1, const 
                                 const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                                 void* scratch, int is_complex, const int64_t* pairs, int64_t n_pairs, int max_ctas,
                                 void* stream);
+/* Same solve, complex RHS on a channel grid of (grid_ny, grid_nzh)
+ * wavenumbers (batch = grid_ny * grid_nzh), with the pair table warp-aligned:
+ * each run of 32 items holds 32 consecutive kz columns of one (m, -m) row
+ * pair, padding items are -1 in both halves.  The RHS segments are fetched
+ * by TMA (one tensor-map box per warp, system stream and segment) instead of
+ * per-thread cp.async.  Results are bit-identical to
+ * shen_bih_solve_stream_pairs. */
+int shen_bih_solve_stream_pairs_grid(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                                     const double* tab, int chunk_rows, const double* ckpt, const void* rhs,
+                                     void* out, void* scratch, const int64_t* pairs, int64_t n_pairs,
+                                     int64_t grid_ny, int64_t grid_nzh, int max_ctas, void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);

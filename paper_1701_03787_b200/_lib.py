@@ -89,6 +89,9 @@ _SIGS = {
     "shen_bih_solve_stream_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
                                                    ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _c_int64,
                                                    ctypes.c_int, _vp]),
+    "shen_bih_solve_stream_pairs_grid": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
+                                                        ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _c_int64, _c_int64,
+                                                        _c_int64, ctypes.c_int, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
     "shen_apply_banded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int, _vp, _vp, _vp, _vp,

@@ -121,6 +121,29 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                     "shen_helm_solve_stream");
 }
 
+int shen_bih_solve_stream_pairs_grid(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
+                                     const double* tab, int chunk_rows, const double* ckpt, const void* rhs,
+                                     void* out, void* scratch, const int64_t* pairs, int64_t n_pairs,
+                                     int64_t grid_ny, int64_t grid_nzh, int max_ctas, void* stream) {
+  if (batch == 0 || n_pairs == 0) return SHEN_OK;
+  if (n_bih < 2 || batch < 0 || n_pairs < 0 || !xi1 || !xi2 || !tab || !rhs || !out || !pairs || grid_ny < 1 ||
+      grid_nzh < 1 || grid_ny * grid_nzh != batch || n_pairs % 32 != 0)
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: bad args");
+  const int rows0 = (n_bih + 1) / 2;
+  if (chunk_rows != 8) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: chunk_rows");
+  if (rows0 > chunk_rows && (!ckpt || !scratch))
+    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: ckpt/scratch");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: rhs must not alias out");
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: max_ctas");
+  if ((reinterpret_cast<uintptr_t>(rhs) & 15) != 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: rhs alignment");
+  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  a.grid_ny = grid_ny;
+  a.grid_nzh = grid_nzh;
+  return cuda_check(shen::launch_bih_stream(a, scratch, true, 8, S(stream)), "shen_bih_solve_stream_pairs_grid");
+}
+
 int shen_helm_solve_stream_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                                  const double* st, const double* md, int chunk_rows, const double* ckpt,
                                  const void* rhs, void* out, void* scratch, int is_complex, const int64_t* pairs,

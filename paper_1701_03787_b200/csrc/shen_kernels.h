@@ -109,6 +109,9 @@ struct BihChunkArgs {
   // equal entries mark an unpaired system.  nullptr: one system per thread.
   const int64_t* pairs = nullptr;
   int64_t n_pairs = 0;
+  // > 0: pairs is warp-aligned (32 consecutive kz columns of one row pair per
+  // warp, -1 padding) over a (grid_ny, grid_nzh) channel grid -- TMA-fed kernel
+  int64_t grid_ny = 0, grid_nzh = 0;
 };
 
 cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);

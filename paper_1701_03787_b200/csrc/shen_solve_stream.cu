@@ -27,6 +27,10 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda.h>  // CUtensorMap
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+#include <cstring>
+
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
 
@@ -185,6 +189,42 @@ __device__ __forceinline__ void tmem_get4(uint32_t a, V& v0, V& v1, V& v2, V& v3
   v1 = tunpackv<V>(w + W);
   v2 = tunpackv<V>(w + 2 * W);
   v3 = tunpackv<V>(w + 3 * W);
+}
+
+// ---------------------------------------------------------------- TMA + mbarrier
+// The pair kernel's complex RHS segments can come in by tensor-map bulk
+// copies: one 3-D box per warp, stream and segment (32 systems x 8 rows of
+// one parity -- the tensor's row dimension is traversed with element stride
+// 2), landing in the same [row][lane] ring layout the per-thread cp.async
+// path fills, completion tracked by one mbarrier per warp and ring slot.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
+      : "memory");
 }
 
 constexpr int kSG = 4;                    // 32-system groups per CTA (128 consecutive systems)
@@ -878,13 +918,20 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
 // results are bit-identical to it.  Work items are pairs (P of them; an
 // unpaired system is a pair of itself and is stored once); one parity per
 // CTA with the one-parity compact table (the two RHS streams double the ring).
-template <typename V, int R, int SG>
-__global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V* ychk) {
+// TMA = true: RHS segments by tensor-map bulk copies (complex RHS on a 2-D
+// channel grid, pair table padded so a warp's 32 items are 32 consecutive
+// kz columns of one (m, -m) row pair; padding items are -1).
+template <typename V, int R, int SG, bool TMA = false>
+__global__ void __launch_bounds__(64 * SG, 1)
+    bih_pair_kernel(BihChunkArgs a, V* ychk, const __grid_constant__ CUtensorMap tmap) {
   constexpr int kT = 64 * SG;
   constexpr int SGE = 2 * SG;  // 32-item groups per CTA work item (one parity per CTA)
   constexpr int RING = 2;
+  __shared__ __align__(8) uint64_t mbar[TMA ? 2 * SG * RING : 1];
   using O = VOps<V>;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_raw[];
+  // TMA boxes land 128-B aligned: the dynamic window is requested 128 B larger
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (int)(blockIdx.x & 1), sgi = warp;
   const int64_t B = a.batch;
@@ -911,6 +958,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
     }
     stab[q] = v;
   }
+  if (TMA && tid < 2 * SG * RING) mbar_init(&mbar[tid], 1);
+  if (TMA) mbar_fence_init();
   __syncthreads();
   auto tpos = [&](int i) { return i + 2; };
   constexpr int tstep = 1;
@@ -945,6 +994,40 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
   // pair's system indices are loaded once per group (a dependent global load
   // per segment issue was the kernel's largest stall)
   int64_t ig = -1, ija = 0, ijb = 0;
+  // TMA: the warp's box coordinates (kz column of lane 0, the two kx rows), per group
+  const int64_t nzh = a.grid_nzh;
+  int tn0 = -1, tma_ = 0, tmb_ = 0;
+  auto issue_tma = [&](int slot_i, SegRef ref) {
+    if (ref.g != ig) {
+      const int64_t c0 = ref.g * (32 * SGE) + sgi * 32;
+      tn0 = -1;
+      if (c0 < P) {
+        const int64_t ja0 = __ldg(pa + c0), jb0 = __ldg(pb + c0);
+        if (ja0 >= 0) {
+          tma_ = (int)(ja0 / nzh);
+          tn0 = (int)(ja0 - (int64_t)tma_ * nzh);
+          tmb_ = (int)(jb0 / nzh);
+        }
+      }
+      ig = ref.g;
+    }
+    // every lane is done with the slot (its reads and the backward sweep's
+    // in-place y writes) before the async proxy overwrites it
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      uint64_t* bar = &mbar[warp * RING + slot_i];
+      if (tn0 >= 0) {
+        V* dst = reinterpret_cast<V*>(smem) + (size_t)warp * RING * 2 * R * 32 + (size_t)slot_i * 2 * R * 32;
+        mbar_expect_tx(bar, 2 * R * 32 * (uint32_t)sizeof(V));
+        const int row0 = par + 2 * ref.s * R;
+        tma_load_3d(dst, &tmap, 2 * tn0, tma_, row0, bar);
+        tma_load_3d(dst + R * 32, &tmap, 2 * tn0, tmb_, row0, bar);
+      } else {
+        mbar_arrive(bar);  // no valid item in this warp: complete the phase
+      }
+    }
+  };
   auto issue = [&](V* slot, SegRef ref) {
     if (ref.g < ngroups) {
       const int64_t c = ref.g * (32 * SGE) + sgi * 32 + lane;
@@ -985,20 +1068,34 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
   int64_t qi = 0;
   int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
   SegIt it{g0, 0};
+  uint32_t cphase = 0;  // TMA: parity bit of each ring slot's barrier
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
-    else cpa_commit();
+    if (TMA) {
+      if (qi < nq) issue_tma(islot, it.ref(nseg));
+    } else {
+      if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
+      else cpa_commit();
+    }
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
   int64_t qc = 0;
   auto consume = [&]() -> V* {
-    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
-    else cpa_commit();
+    if (TMA) {
+      if (qi < nq) issue_tma(islot, it.ref(nseg));
+    } else {
+      if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
+      else cpa_commit();
+    }
     it.next(nseg, gstride);
     ++qi;
     islot = islot + 1 == RING ? 0 : islot + 1;
-    cpa_wait<RING - 1>();
+    if (TMA) {
+      mbar_wait(&mbar[warp * RING + cslot], (cphase >> cslot) & 1u);
+      cphase ^= 1u << cslot;
+    } else {
+      cpa_wait<RING - 1>();
+    }
     V* p = ring + cslot * 2 * R * 32;
     ++qc;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
@@ -1007,9 +1104,13 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
     const int64_t c = g * (32 * SGE) + sgi * 32 + lane;
-    const bool cv = c < P;
+    bool cv = c < P;
     const int64_t cc = cv ? c : P - 1;
-    const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+    int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
+    if (TMA) {  // padding items (-1): solve system 0 for nothing, store nothing
+      cv = cv && ja >= 0;
+      if (ja < 0) ja = jb2 = 0;
+    }
     const bool second = cv && jb2 != ja;  // store the second system (an unpaired one is stored once)
     const double xi1 = __ldg(a.xi1 + ja), xi2 = __ldg(a.xi2 + ja);
     V* outa = out + (int64_t)par * B + ja;
@@ -1094,7 +1195,8 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V*
       constexpr bool FULL = decltype(full_tag)::value;
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>(), za = szero<V>(), zb = szero<V>();
-      V* cur = consume();  // also completes ck_issue(s)
+      V* cur = consume();  // also completes ck_issue(s) (cp.async path)
+      if (TMA) cpa_wait<0>();  // the checkpoint group (the only cp.async traffic)
       if (s > 0) {  // factor state and y entering the segment
         const double* c = ckd + tid;
         w1.d = c[0]; w1.e = c[kT]; w1.f = c[2 * kT]; w1.a = c[3 * kT]; w1.b = c[4 * kT];
@@ -1319,15 +1421,54 @@ static size_t bih_pair_smem(const BihChunkArgs& a) {
   const size_t ring = (size_t)2 * 2 * R * kT * sizeof(V);
   const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);
   const size_t ckb = (size_t)kT * (10 * sizeof(double) + 4 * sizeof(V));
-  return ring + tabp + ckb;
+  return ring + tabp + ckb + 128;  // + alignment slack of the TMA ring
 }
 
-template <typename V, int R, int SG>
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// the complex RHS (n_bih, ny, nzh) as a 3-D tensor of doubles: dim 0 = 2 nzh
+// (contiguous), dim 1 = kx row, dim 2 = mode row traversed with stride 2 (one
+// parity); box = 32 complex x 1 kx row x R rows of one parity
+template <int R>
+static bool rhs_tensor_map(CUtensorMap* tm, const BihChunkArgs& a) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * a.grid_nzh), (cuuint64_t)a.grid_ny, (cuuint64_t)a.n_bih};
+  const cuuint64_t strides[2] = {(cuuint64_t)(2 * a.grid_nzh * 8), (cuuint64_t)(a.grid_ny * 2 * a.grid_nzh * 8)};
+  const cuuint32_t box[3] = {64, 1, 2 * R};
+  const cuuint32_t estr[3] = {1, 1, 2};
+  // no L2 promotion: the box rows start 16 B past a 128-B line (a kx row is
+  // 1025 x 16 B), and promoting to 256-B granules read 1.5x the box bytes
+  static const int promo = getenv("SHEN_TMA_PROMO") ? atoi(getenv("SHEN_TMA_PROMO")) : 0;
+  const CUtensorMapL2promotion pr = promo == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(a.rhs), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <typename V, int R, int SG, bool TMA = false>
 static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
   constexpr int kT = 64 * SG;
   const size_t smem = bih_pair_smem<V, R, SG>(a);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = bih_pair_kernel<V, R, SG>;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (TMA && !rhs_tensor_map<R>(&tm, a)) return cudaErrorNotSupported;
+  auto kern = bih_pair_kernel<V, R, SG, TMA>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   if (a.n_pairs <= 0) return cudaSuccess;
@@ -1335,7 +1476,7 @@ static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStr
   int64_t cap = stream_ctas(1);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
-  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tm);
   return cudaGetLastError();
 }
 
@@ -1346,6 +1487,11 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
     // memory; past n_x ~ 1150 it does not fit and the one-system kernel
     // solves every system (the pair table lists each exactly once)
     static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
+    if (a.grid_nzh > 0) {  // warp-aligned pair table of a channel grid: TMA-fed pair kernel
+      if (!std::is_same<V, cplx>::value || R != 8 || bih_pair_smem<V, R, 4>(a) > 227 * 1024)
+        return cudaErrorInvalidValue;
+      return bih_pair_launch<V, R, 4, std::is_same<V, cplx>::value && R == 8>(a, scratch, st);
+    }
     if (pw == 6 && bih_pair_smem<V, R, 3>(a) <= 227 * 1024) return bih_pair_launch<V, R, 3>(a, scratch, st);
     if (bih_pair_smem<V, R, 4>(a) <= 227 * 1024) return bih_pair_launch<V, R, 4>(a, scratch, st);
   }

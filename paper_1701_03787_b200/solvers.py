@@ -242,6 +242,30 @@ def mirror_pairs(z2):
     return np.stack([a, b])
 
 
+# complex biharmonic pairs: TMA-fed kernel on a warp-aligned table (bit-identical;
+# measured slower at config 4: 27.8 vs 20.9 ms, DRAM reads +20%; off by default)
+PAIR_TMA = _env_int("SHEN_PAIR_TMA", 0)
+
+
+def mirror_pairs_grid(z2):
+    """The mirror pairs of a 2-D z2 grid in warp-aligned form for the TMA-fed
+    biharmonic kernel: for every row pair, its kz columns padded to a multiple
+    of 32 (padding items -1), so 32 consecutive items are 32 consecutive
+    columns of one row pair.  Returns ((2, P) int64, (ny, nzh)) or None."""
+    pr = mirror_pairs(z2)
+    if pr is None:
+        return None
+    ny, nzh = np.shape(z2)
+    npad = -(-nzh // 32) * 32
+    r0 = pr[0, ::nzh] // nzh  # one entry per row pair (items of a row pair are consecutive)
+    r1 = pr[1, ::nzh] // nzh
+    col = np.arange(npad, dtype=np.int64)
+    ok = col < nzh
+    a = np.where(ok[None, :], r0[:, None] * nzh + col[None, :], -1).reshape(-1)
+    b = np.where(ok[None, :], r1[:, None] * nzh + col[None, :], -1).reshape(-1)
+    return np.stack([a, b]), (int(ny), int(nzh))
+
+
 def _solve_real_via_complex(lu, rhs_dev, out_dev):
     """Real RHS whose rows are not 16-B aligned (odd batch): the streaming
     kernel moves 16-B row pieces, so solve the complex system with zero
@@ -586,6 +610,7 @@ class BiharmonicLU:
         self._qs_dev = None
         self._host = None
         self._pairs = None  # device (2, P) int64 mirror pairs (build_biharmonic), or None
+        self._pairs_grid = None  # (device warp-aligned (2, P) pairs, (ny, nzh)) for complex RHS, or None
 
     @property
     def n_modes(self) -> int:
@@ -656,6 +681,17 @@ class BiharmonicLU:
                                           ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(), int(is_complex), sh),
                   "shen_bih_solve_stored")
             del keep
+        elif (self.method == "stream" and self._pairs_grid is not None and is_complex and j0 == 0
+              and j1 in (-1, B) and rhs_dev.data_ptr() % 16 == 0):
+            # mirror pairs, RHS segments fetched by TMA (bit-identical results)
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
+            pg, (ny, nzh) = self._pairs_grid
+            check(h.shen_bih_solve_stream_pairs_grid(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
+                                                     self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
+                                                     out_dev.data_ptr(), scratch, pg.data_ptr(), int(pg.shape[1]),
+                                                     ny, nzh, max_ctas, sh),
+                  "shen_bih_solve_stream_pairs_grid")
         elif self.method == "stream" and self._pairs is not None and j0 == 0 and j1 in (-1, B):
             # mirror pairs: one factor recurrence for two systems (bit-identical results)
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -736,6 +772,11 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
         # (config 1, 1.1k pairs: 44 vs 39 us; config 3, 16.6k pairs: 0.097 vs 0.120 ms)
         if pr is not None and pr.shape[1] >= PAIRS_MIN:
             lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
+            # the TMA-fed kernel needs the 8-row checkpoints and a pair kernel that fits
+            # shared memory (n_x <= ~1150, as the cp.async pair kernel)
+            pg = mirror_pairs_grid(z2) if PAIR_TMA and R == 8 and mats.n_x <= 1100 else None
+            if pg is not None:
+                lu._pairs_grid = (torch.from_numpy(np.ascontiguousarray(pg[0])).to(dev), pg[1])
     return lu
 
 

@@ -75,6 +75,8 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_helm_solve_chunked": (1, 0.0, None, 1, None, None, None, 8, None, None, None, 1, None),
         "shen_bih_factor": (1, 0.0, None, None, 1, None, 8, None, None, 0, None, None),
         "shen_bih_solve_stream_pairs": (1, 0.0, None, None, 1, None, 8, None, None, None, None, 1, None, 1, 0, None),
+        "shen_bih_solve_stream_pairs_grid": (1, 0.0, None, None, 1, None, 8, None, None, None, None, None, 32, 1, 1,
+                                             0, None),
         "shen_helm_solve_stream_pairs": (1, 0.0, None, 1, None, None, None, 8, None, None, None, None, 1, None, 1, 0, 0,
                                          None),
         "shen_xform_extend": (3, 5, 1, None, None, None),

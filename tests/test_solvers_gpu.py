@@ -291,7 +291,7 @@ def test_solve_many_matches_single_solves():
         S.solve_many([(hlu, fh[:, :3])])
 
 
-@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32)])
+@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32), (64, 12, 66)])
 @pytest.mark.parametrize("cplx", [True, False])
 def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
     """Mirror-paired systems ((m, n) and (-m, n): identical z2) share one
@@ -302,20 +302,27 @@ def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
     mats = assemble(n_x, 0)
     z2 = channel_z2(ny, nz)
     S.PAIRS_MIN, saved = 1, S.PAIRS_MIN  # force pairs at test sizes
+    S.PAIR_TMA, saved_tma = 1, S.PAIR_TMA  # and the TMA-fed variant for complex RHS
     try:
         lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
     finally:
         S.PAIRS_MIN = saved
+        S.PAIR_TMA = saved_tma
     assert lu._pairs is not None
     rng = np.random.default_rng(n_x + ny)
     shp = (mats.n_bih,) + z2.shape
     f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
-    x_pair = lu.solve(f)
-    pairs = lu._pairs
+    x_pair = lu.solve(f)  # complex on a grid that fits: the TMA-fed pair kernel
+    if cplx and n_x <= 1100:
+        assert lu._pairs_grid is not None
+    pairs, grid = lu._pairs, lu._pairs_grid
+    lu._pairs_grid = None
+    x_pair_cp = lu.solve(f)  # cp.async-fed pair kernel
     lu._pairs = None
     x_one = lu.solve(f)
-    lu._pairs = pairs
+    lu._pairs, lu._pairs_grid = pairs, grid
     assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
+    assert np.array_equal(x_pair_cp, x_one)
 
 
 @pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32)])
