@@ -15,7 +15,10 @@ import threading
 __all__ = ["ShenBackendError", "lib", "lib_path", "require_device", "check", "declared_symbols"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libshen_b200.so")
+# SHEN_LIB_VARIANT=<tag> loads libshen_b200_<tag>.so from the same directory
+# (A/B timing of kernel variants built by tools/ab_build.sh; default: the product library)
+_variant = os.environ.get("SHEN_LIB_VARIANT", "")
+lib_path = os.path.join(_HERE, f"libshen_b200_{_variant}.so" if _variant else "libshen_b200.so")
 
 
 class ShenBackendError(RuntimeError):

@@ -124,6 +124,9 @@ template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 // the backward) in TMEM instead of the L2-resident scratch.  Warp w owns lanes
 // 32 (w % 4) .. +31 (the 32x32b shape: thread = lane) and a column range
 // picked by w / 4.
+#ifndef SHEN_PAIR_ALIGN_GENERIC
+#define SHEN_PAIR_ALIGN_GENERIC 0
+#endif
 #ifndef SHEN_PAIR_TMEM_SEGS
 #define SHEN_PAIR_TMEM_SEGS 16
 #endif
@@ -931,7 +934,14 @@ __global__ void __launch_bounds__(64 * SG, 1)
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem_raw[];
   // TMA boxes land 128-B aligned: the dynamic window is requested 128 B larger
+  // (pointer arithmetic on the shared array itself, so the compiler keeps
+  // the shared address space: LDS/STS, not generic loads)
+#if SHEN_PAIR_ALIGN_GENERIC  // A/B: the generic-pointer variant (generic loads)
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+#else
+  const uint32_t sbase = smem_u32(smem_raw);
+  double* smem = smem_raw + ((((sbase + 127u) & ~127u) - sbase) >> 3);
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (int)(blockIdx.x & 1), sgi = warp;
   const int64_t B = a.batch;
