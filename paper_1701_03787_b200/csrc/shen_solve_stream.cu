@@ -23,6 +23,12 @@
 // biharmonic) -- DESIGN.md section 4.2 has the measured numbers.  Latency is
 // hidden by a per-thread cp.async ring that prefetches segments continuously
 // across both sweeps and across system groups.
+//
+// Kernels: helm_stream_kernel / bih_stream_kernel (one system per thread);
+// bih_pair_kernel (default for channel grids: mirror pairs (m, n) / (-m, n)
+// share one factor recurrence, y checkpoints of the first 16 segments parked
+// in tensor memory; an optional TMA-fed variant); helm_pair_kernel (mirror
+// pairs for the Helmholtz, measured slower, off by default).
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
-  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
+  int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
   // L2 policy of the forward (first) and backward (second, last) RHS reads
   // (hint: 0 none, 1 evict_last / evict_first, 2 - / evict_first, 3 evict_last / -)
@@ -347,7 +353,6 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
-  int64_t qc = 0;
   auto consume = [&]() -> const V* {
     if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
@@ -356,7 +361,6 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
     islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
     const V* p = ring + cslot * R * 32;
-    ++qc;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, 
     cpa_commit();
   };
   int64_t qi = 0;
-  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
+  int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
     if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
@@ -533,7 +537,6 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, 
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
-  int64_t qc = 0;
   auto consume = [&]() -> V* {
     if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
     else cpa_commit();
@@ -542,7 +545,6 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, 
     islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
     V* p = ring + cslot * 2 * R * 32;
-    ++qc;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
@@ -734,7 +736,7 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
   if (g0 >= ngroups) return;
   const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
   int64_t qi = 0;
-  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
+  int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
   for (; qi < RING - 1; ++qi) {
     if (qi < nq) seg_issue<V, R, SGE>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
@@ -742,7 +744,6 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
-  int64_t qc = 0;
   auto consume = [&]() -> V* {
     if (qi < nq) seg_issue<V, R, SGE>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
@@ -751,7 +752,6 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
     islot = islot + 1 == RING ? 0 : islot + 1;
     cpa_wait<RING - 1>();
     V* p = ring + cslot * R * 32;
-    ++qc;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(64 * SG, 1)
     cpa_commit();
   };
   int64_t qi = 0;
-  int islot = 0, cslot = 0;  // ring slots of qi / qc (no 64-bit modulo)
+  int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
   uint32_t cphase = 0;  // TMA: parity bit of each ring slot's barrier
   for (; qi < RING - 1; ++qi) {
@@ -1089,7 +1089,6 @@ __global__ void __launch_bounds__(64 * SG, 1)
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
-  int64_t qc = 0;
   auto consume = [&]() -> V* {
     if (TMA) {
       if (qi < nq) issue_tma(islot, it.ref(nseg));
@@ -1107,7 +1106,6 @@ __global__ void __launch_bounds__(64 * SG, 1)
       cpa_wait<RING - 1>();
     }
     V* p = ring + cslot * 2 * R * 32;
-    ++qc;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
   };
