@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--kx-fold", type=int, default=0,
                     help="profile subset: the rows of rank 0 of a K-way folded split (keeps mirror pairs)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the multi-rank launch: gloo ranks, folded slabs, max-over-ranks "
+                         "timing, oracle solves instead of the device (no GPU needed; not a bench number)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--method", default="stream", choices=["stream", "chunked", "stored", "tile"])
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -295,8 +298,11 @@ def run_b200(args):
     torch.cuda.empty_cache()
 
     e2e = None
-    if not args.no_e2e and rank == 0:
-        e2e = run_e2e(S, mats, nu, dt, z2_full, n_y, args)
+    if not args.no_e2e:
+        # every rank streams its own sample through the public API (its own
+        # PCIe link); the value is the sum of the ranks' unknowns over the
+        # slowest rank's time
+        e2e = run_e2e(S, mats, nu, dt, z2_full[rows], args, world)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_baseline(mats, nu, dt, z2_full)
@@ -367,16 +373,19 @@ def spot_parity(mats, nu, dt, z2, fh, xh, fb, xb):
             "biharmonic_residual_max": resid, "reference_residual_max_same_systems": resid_ref}
 
 
-def run_e2e(S, mats, nu, dt, z2_full, n_y, args):
+def run_e2e(S, mats, nu, dt, z2_rank, args, world=1):
     """Same metric through the public API with HOST buffers: page-locked numpy
     arrays in and out (the application's own buffers), so every step copies
     the RHS host->device and the solution device->host; the API pipelines the
-    copies against the solve in column slabs.  Bounded sample: 256 kx rows
-    (262,400 systems; 4.3 GB per operator RHS)."""
+    copies against the solve in column slabs.  Bounded sample per rank: the
+    first 256 of the rank's kx rows (262,400 systems; 4.3 GB per operator
+    RHS).  With N ranks each rank runs its own sample concurrently (one PCIe
+    link per GPU); timing is max over ranks after a barrier, unknowns summed."""
     import torch
+    import torch.distributed as dist
 
-    rows = min(256, n_y)
-    z2 = np.ascontiguousarray(z2_full[:rows])
+    rows = min(256, z2_rank.shape[0])
+    z2 = np.ascontiguousarray(z2_rank[:rows])
     hlu = S.build_helmholtz(mats, nu, dt, z2, method=args.method)
     blu = S.build_biharmonic(mats, nu, dt, z2, method=args.method)
 
@@ -392,15 +401,26 @@ def run_e2e(S, mats, nu, dt, z2_full, n_y, args):
     for _ in range(2):
         S.solve_many(jobs)
     steps = 3
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         S.solve_many(jobs)  # both operators through one host<->device pipeline
     dt_s = (time.perf_counter() - t0) / steps
     unk = (mats.n_dir + mats.n_bih) * z2.size
-    return {"value": unk / dt_s, "unit": "unknowns/s", "h2d_bytes_per_step": int(fh.nbytes + fb.nbytes),
-            "d2h_bytes_per_step": int(xh.nbytes + xb.nbytes),
-            "sample": f"{rows} kx rows x {z2.shape[1]} systems, page-locked numpy in/out",
-            "path": "solvers.solve_many([(hlu, fh, xh), (blu, fb, xb)]) (host wall clock incl. copies)"}
+    h2d, d2h = int(fh.nbytes + fb.nbytes), int(xh.nbytes + xb.nbytes)
+    if world > 1:
+        t = torch.tensor([dt_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c = torch.tensor([unk, h2d, d2h], dtype=torch.int64, device="cuda")
+        dist.all_reduce(c)
+        dt_s = float(t.item())
+        unk, h2d, d2h = (int(v) for v in c.tolist())
+    return {"value": unk / dt_s, "unit": "unknowns/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "sample": f"{world} rank(s) x {rows} kx rows x {z2.shape[1]} systems, page-locked numpy in/out",
+            "ranks": world,
+            "path": "solvers.solve_many([(hlu, fh, xh), (blu, fb, xb)]) (host wall clock incl. copies, "
+                    "max over ranks)"}
 
 
 def cpu_baseline(mats, nu, dt, z2_full):
@@ -423,6 +443,49 @@ def cpu_baseline(mats, nu, dt, z2_full):
     return {"value": unk / t, "unit": "unknowns/s", "cores": 1, "kind": "port",
             "sample": f"{z2.shape[0]} kx rows x {z2.shape[1]} systems of the same plane, solve only (LU prebuilt), "
                       "1 thread"}
+
+
+def run_dry(args):
+    """The launcher and reduction logic of run_b200 on CPU: gloo process
+    group, each rank's folded kx rows, the oracle's solves as the per-rank
+    work, barrier + max-over-ranks time, summed systems; prints the same kind
+    of JSON line (marked dry_run).  Used by tests/test_bench_launch.py."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import shen_oracle as O
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import channel_z2
+    from paper_1701_03787_b200.shard import kx_rows_folded
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    name, n_x, n_y, n_z, nu, dt = workload(args.config)
+    rows = kx_rows_folded(n_y, rank, world)
+    z2 = np.ascontiguousarray(channel_z2(n_y, n_z)[rows])
+    mats = assemble(n_x, 0)
+    rng = np.random.default_rng(1234 + rank)
+    fh = rng.standard_normal((mats.n_dir,) + z2.shape) + 0j
+    hf = O.helmholtz_factor(mats, nu, dt, z2)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.helmholtz_solve(hf, fh)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    b = torch.tensor([z2.size], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(b)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "config": {"workload": name, "systems_total": int(b.item()), "kx_rows_rank0": len(rows),
+                                     "parallelism": f"kx-slab x{world} (folded: (m, -m) pairs per rank)"},
+                          "ms_per_step": 1e3 * float(t.item()) / args.steps}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ======================================================================= config 3
@@ -699,9 +762,39 @@ def run_reference(args):
     }))
 
 
+def spawn_ranks(n: int) -> int:
+    """``bench.py --gpus N`` without torchrun: start one process per GPU
+    (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR=127.0.0.1 / MASTER_PORT in
+    the environment, NCCL_DEBUG=INFO unless set, so the NCCL init lines on
+    stderr show nranks), rank 0 prints the JSON line.  Returns the worst exit
+    code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    codes = [p.wait() for p in procs]
+    return max(abs(c) for c in codes)
+
+
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl != "reference":
+        sys.exit(spawn_ranks(a.gpus))
+    if "WORLD_SIZE" in os.environ and a.gpus != int(os.environ["WORLD_SIZE"]):
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}; using WORLD_SIZE",
+              file=sys.stderr)
+    if a.dry_run:
+        run_dry(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.config == "c3":
         run_c3(a)

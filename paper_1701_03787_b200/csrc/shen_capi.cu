@@ -101,6 +101,24 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
   return cuda_check(shen::launch_helm_chunk(a, is_complex != 0, S(stream)), "shen_helm_solve_chunked");
 }
 
+int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
+                       const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out, int max_ctas,
+                       void* stream) {
+  if (batch == 0) return SHEN_OK;
+  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: bad args");
+  const int rows0 = (n_dir + 1) / 2;
+  if (chunk_rows <= 0 || chunk_rows > 16 || (chunk_rows & (chunk_rows - 1)) || 32LL * chunk_rows < rows0)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: chunk_rows");
+  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: ckpt required");
+  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs must not alias out");
+  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: max_ctas");
+  if ((reinterpret_cast<uintptr_t>(rhs) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs/out must be 16-B aligned");
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
+  return cuda_check(shen::launch_helm_cr(a, S(stream)), "shen_helm_solve_cr");
+}
+
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
                            void* out, void* scratch, int is_complex, int warps_per_sm, int max_ctas,

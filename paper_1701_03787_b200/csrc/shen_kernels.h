@@ -126,6 +126,8 @@ cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool compl
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
                               cudaStream_t st);
 int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
+// column-resident solves (shen_solve_cr.cu): complex RHS, RHS read once; ckpt made with chunk_rows = R
+cudaError_t launch_helm_cr(const HelmChunkArgs& a, cudaStream_t st);
 
 // tiled chunk-parallel Helmholtz solve (shen_solve_tile.cu); ckpt made with chunk_rows = R, 32 R >= rows_p0
 cudaError_t launch_helm_tile(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);

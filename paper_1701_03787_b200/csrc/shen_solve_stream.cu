@@ -104,7 +104,11 @@ __device__ __forceinline__ void ystore(V* p, V v) {
 template <typename V>
 __device__ __forceinline__ void ydiscard(const V* p, int lane) {
   constexpr int kPer = 128 / (int)sizeof(V);
-  if (SHEN_YCKPT_DISCARD && (lane & (kPer - 1)) == 0 && ((reinterpret_cast<uintptr_t>(p) & 127) == 0))
+  if (!SHEN_YCKPT_DISCARD) return;
+  // the line also holds the checkpoints the other lanes of the warp read by
+  // their own loads: order those reads before the discard explicitly
+  __syncwarp(__activemask());
+  if ((lane & (kPer - 1)) == 0 && ((reinterpret_cast<uintptr_t>(p) & 127) == 0))
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -1418,6 +1422,7 @@ static cudaError_t bih_stream_launch(const BihChunkArgs& a, void* scratch, int c
   const int64_t groups = (PP ? 2 : 1) * ((nsys + 32 * SGE - 1) / (32 * SGE));  // PP: one item per parity
   int64_t cap = stream_ctas(occ);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  if (PP) cap = std::max<int64_t>(cap, 2);  // the CTA's parity is blockIdx.x & 1: both must exist
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
   kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
@@ -1483,6 +1488,7 @@ static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStr
   const int64_t groups = 2 * ((a.n_pairs + 32 * 2 * SG - 1) / (32 * 2 * SG));  // one item per parity
   int64_t cap = stream_ctas(1);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
+  cap = std::max<int64_t>(cap, 2);  // the CTA's parity is blockIdx.x & 1: both must exist
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
   kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tm);
   return cudaGetLastError();

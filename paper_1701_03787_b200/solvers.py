@@ -92,7 +92,13 @@ def _solve_api(lu, rhs, out):
     if dv.is_torch(rhs) and rhs.is_cuda:
         r, cplx, _ = dv.as_rhs(rhs)
         flat = r.reshape(lu.n_modes, -1)
-        res = torch.empty_like(flat) if out is None else out.reshape(lu.n_modes, -1)
+        if out is not None:
+            # the kernels write n_modes x batch elements of r's dtype into out's storage
+            if not (dv.is_torch(out) and out.is_cuda and out.device == r.device and out.dtype == r.dtype
+                    and tuple(out.shape) == tuple(rhs.shape) and out.is_contiguous()):
+                raise ValueError(f"out must be a contiguous CUDA tensor on {r.device} of dtype {r.dtype} "
+                                 f"and shape {tuple(rhs.shape)}")
+        res = torch.empty_like(flat) if out is None else out.view(lu.n_modes, -1)
         lu.solve_into(flat, res, cplx)
         return res.reshape(tuple(rhs.shape))
     a = rhs.numpy() if dv.is_torch(rhs) else np.asarray(rhs)

@@ -218,7 +218,49 @@ def rhs_fixture():
     np.savez_compressed(os.path.join(OUT, "rhs.npz"), **out)
 
 
+def big_fixture():
+    """Headline-size pins: sha256 of every assemble() table at n_x = 1024 and
+    2048 (config 4 / config 5's largest N), and the reference's 3-D forward
+    and inverse transforms at n_x = 512 and 1024 (Gauss and Lobatto) on a thin
+    (n_y, n_z) = (4, 2) plane, where the biharmonic forward map is most
+    ill-conditioned."""
+    tables = {}
+    for n_x in (1024, 2048):
+        for fi, fam in enumerate(FAMS):
+            m = RM.assemble(n_x, fam)
+            key = f"nx{n_x}_f{fi}"
+            tables[key + "_mass_cheb"] = sha(m.mass_cheb)
+            for name in ("mass_dir", "mass_bih", "mixed_mass", "stiff_bih", "deriv_dir_to_bih", "deriv_bih_to_dir"):
+                mat = getattr(m, name)
+                for off, dg in zip(mat.offsets, mat.diagonals):
+                    tables[f"{key}_{name}_{off}"] = sha(dg)
+            for name in ("stiff_dir", "deriv_dir_to_cheb"):
+                mat = getattr(m, name)
+                for off, dg in zip(mat.banded.offsets, mat.banded.diagonals):
+                    tables[f"{key}_{name}_{off}"] = sha(dg)
+                tables[f"{key}_{name}_tail"] = sha(mat.tail)
+            tables[key + "_fourth_bih_diag"] = sha(m.fourth_bih.diag)
+    out = {}
+    for n_x in (512, 1024):
+        for fi, fam in enumerate(FAMS):
+            mesh = build_mesh(n_x, 4, 2, 2 * np.pi, np.pi, fam)
+            u = np.random.default_rng(n_x + fi).uniform(-1, 1, mesh.shape)
+            key = f"nx{n_x}_f{fi}"
+            out[key + "_u"] = u
+            for space in (Space.DIRICHLET, Space.BIHARMONIC):
+                sc = list(Space).index(space)
+                c = RT.forward_transform(RT.PhysicalField(u, mesh), space)
+                out[f"{key}_s{sc}_fwd"] = c.data
+                out[f"{key}_s{sc}_inv"] = RT.inverse_transform(c).data
+    np.savez_compressed(os.path.join(OUT, "big_transforms.npz"), **out)
+    with open(os.path.join(OUT, "big_tables.json"), "w") as fh:
+        json.dump(tables, fh, indent=0, sort_keys=True)
+
+
 if __name__ == "__main__":
+    if "--big-only" in sys.argv:
+        big_fixture()
+        sys.exit(0)
     if "--apply-only" in sys.argv:
         apply_fixture()
         sys.exit(0)
@@ -231,6 +273,7 @@ if __name__ == "__main__":
     transforms_fixture()
     apply_fixture()
     rhs_fixture()
+    big_fixture()
     with open(os.path.join(OUT, "golden_meta.json"), "w") as fh:
         json.dump({"solver_cases": meta, "baseline": base,
                    "generator": "tests/golden/make_golden.py from /root/reference/pkg/src (chebchan 0.1.0)",

@@ -89,3 +89,35 @@ def test_host_apply_vs_reference_golden(golden, n_x, fam):
                  "deriv_bih_to_dir", "deriv_dir_to_cheb"):
         x = g[f"nx{n_x}_f{fam}_{name}_x"]
         assert np.array_equal(getattr(mats, name).apply(x), g[f"nx{n_x}_f{fam}_{name}_y"]), name
+
+
+@pytest.mark.parametrize("n_x", [1024, 2048])
+@pytest.mark.parametrize("fi", [0, 1])
+def test_assemble_headline_sizes_sha(n_x, fi):
+    """assemble() at the headline sizes (config 4 n_x = 1024, config 5's
+    largest N = 2049): every table equals the reference's byte for byte
+    (sha256 pinned by tests/golden/make_golden.py big_fixture)."""
+    import hashlib
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "big_tables.json")) as fh:
+        want = json.load(fh)
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+    m = assemble(n_x, fi)
+    key = f"nx{n_x}_f{fi}"
+    got = {key + "_mass_cheb": sha(m.mass_cheb), key + "_fourth_bih_diag": sha(m.fourth_bih.diag)}
+    for name in ("mass_dir", "mass_bih", "mixed_mass", "stiff_bih", "deriv_dir_to_bih", "deriv_bih_to_dir"):
+        mat = getattr(m, name)
+        for off, dg in zip(mat.offsets, mat.diagonals):
+            got[f"{key}_{name}_{off}"] = sha(dg)
+    for name in ("stiff_dir", "deriv_dir_to_cheb"):
+        mat = getattr(m, name)
+        for off, dg in zip(mat.banded.offsets, mat.banded.diagonals):
+            got[f"{key}_{name}_{off}"] = sha(dg)
+        got[f"{key}_{name}_tail"] = sha(mat.tail)
+    ref = {k: v for k, v in want.items() if k.startswith(key + "_")}
+    assert got == ref

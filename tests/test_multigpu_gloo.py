@@ -112,29 +112,36 @@ def test_plane_slab_partition():
 def _exchange_worker(rank, world, port, out_dir):
     import torch
 
-    from paper_1701_03787_b200.distributed import kx_to_planes, plane_slab, planes_to_kx
+    from paper_1701_03787_b200.distributed import kx_rows, kx_to_planes, plane_slab, planes_to_kx
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n_planes, n_y, K = 9, 7, 5  # uneven splits on both axes
-    g = torch.Generator().manual_seed(4)
-    full = torch.complex(torch.randn(n_planes, n_y, K, generator=g, dtype=torch.float64),
-                         torch.randn(n_planes, n_y, K, generator=g, dtype=torch.float64))
-    lo, hi = plane_slab(n_planes, rank, world)
-    cols = planes_to_kx(full[lo:hi].clone(), n_planes)
-    a, b = kx_slab(n_y, rank, world)
-    ok1 = torch.equal(cols, full[:, a:b, :])
-    back = kx_to_planes(cols, n_y)
-    ok2 = torch.equal(back, full[lo:hi])
-    np.save(os.path.join(out_dir, f"ex{rank}.npy"), np.array([ok1, ok2]))
+    oks = []
+    # folded rows (the default: the solver's row set, whole (m, -m) pairs) and
+    # contiguous slabs; uneven splits on both axes
+    for n_planes, n_y, K, rows_of in ((9, 12, 5, None), (9, 7, 5, None),
+                                      (9, 7, 5, lambda n, r, w: np.arange(*kx_slab(n, r, w)))):
+        g = torch.Generator().manual_seed(4)
+        full = torch.complex(torch.randn(n_planes, n_y, K, generator=g, dtype=torch.float64),
+                             torch.randn(n_planes, n_y, K, generator=g, dtype=torch.float64))
+        lo, hi = plane_slab(n_planes, rank, world)
+        cols = planes_to_kx(full[lo:hi].clone(), n_planes, rows_of=rows_of)
+        rows = kx_rows(n_y, rank, world, rows_of)
+        if rows_of is None:
+            oks.append(np.array_equal(rows, kx_rows_folded(n_y, rank, world)))
+        oks.append(torch.equal(cols, full[:, torch.from_numpy(rows), :]))
+        back = kx_to_planes(cols, n_y, rows_of=rows_of)
+        oks.append(torch.equal(back, full[lo:hi]))
+    np.save(os.path.join(out_dir, f"ex{rank}.npy"), np.array(oks))
     dist.destroy_process_group()
 
 
 def test_transform_exchange_gloo(tmp_path):
     """The all-to-all of the slab-decomposed transforms (distributed.py):
-    x-planes -> kx slabs -> x-planes reproduces the global transpose exactly
-    on uneven splits (world size 2, gloo; NCCL over NVLink on GPUs)."""
+    x-planes -> kx rows -> x-planes reproduces the global transpose exactly on
+    uneven splits, for the folded rows the solver slabs use (the default) and
+    for contiguous slabs (world size 2, gloo; NCCL over NVLink on GPUs)."""
     world = 2
     mp.spawn(_exchange_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     for r in range(world):

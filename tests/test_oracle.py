@@ -148,3 +148,18 @@ def test_oracle_nonlinear_and_recovery_bitwise(golden, fi):
         assert np.array_equal(nl[i], g[f"{k}_nl{i}"])
     v, w = O.recover_velocity(mats, g[k + "_z2"], g[k + "_m"], g[k + "_n"], g[k + "_u"], g[k + "_g"])
     assert np.array_equal(v, g[k + "_vrec"]) and np.array_equal(w, g[k + "_wrec"])
+
+
+@pytest.mark.parametrize("n_x", [512, 1024])
+@pytest.mark.parametrize("fi", [0, 1])
+def test_oracle_big_transforms_bitwise(golden, n_x, fi):
+    """The oracle's 3-D transforms at n_x = 512 / 1024 (where the biharmonic
+    forward map is most ill-conditioned) reproduce the reference's bytes."""
+    g = golden("big_transforms.npz")
+    mats = assemble(n_x, fi)
+    key = f"nx{n_x}_f{fi}"
+    u = g[key + "_u"]
+    for sc in (1, 2):
+        c = O.forward_transform(u, sc, fi == 1, mats)
+        assert np.array_equal(c, g[f"{key}_s{sc}_fwd"])
+        assert np.array_equal(O.inverse_transform(c, sc, fi == 1, n_x, 4, 2), g[f"{key}_s{sc}_inv"])
