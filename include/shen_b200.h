@@ -106,11 +106,13 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
  * chunk_rows rows per (system, parity) are solved in parallel and coupled by
  * warp scans.  ckpt from shen_helm_factor(exact = 0) with the same
  * chunk_rows (a power of two <= 16 with 32 * chunk_rows >= rows of parity 0).
- * rhs/out 16-B aligned, not aliased.  max_ctas > 0 caps the persistent grid.
+ * rhs/out 16-B aligned, not aliased.  max_ctas > 0 caps the persistent grid;
+ * [j_begin, j_end) restricts the solve to a range of systems (j_end < 0: the
+ * whole batch; row pitch stays `batch`) for pipelined host copies.
  * Replaces HelmholtzLU.solve (solvers.py:100-126). */
 int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
                        const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out, int max_ctas,
-                       void* stream);
+                       int64_t j_begin, int64_t j_end, void* stream);
 /* Same Helmholtz solve with systems taken in mirror pairs (the layout of
  * shen_bih_solve_stream_pairs below): one thread runs the factor recurrence
  * once for both right-hand sides and reads the checkpoints once for two

@@ -79,6 +79,8 @@ _SIGS = {
     "shen_helm_solve_stream_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                                     ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _c_int64,
                                                     ctypes.c_int, ctypes.c_int, _vp]),
+    "shen_helm_solve_cr": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
+                                          ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_helm_solve_tile": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                             ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),

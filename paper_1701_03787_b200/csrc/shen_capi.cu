@@ -103,7 +103,7 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
 
 int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
                        const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out, int max_ctas,
-                       void* stream) {
+                       int64_t j_begin, int64_t j_end, void* stream) {
   if (batch == 0) return SHEN_OK;
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: bad args");
@@ -113,9 +113,11 @@ int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, co
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs must not alias out");
   if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: max_ctas");
+  if (j_end < 0) j_end = batch;
+  if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: range");
   if ((reinterpret_cast<uintptr_t>(rhs) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs/out must be 16-B aligned");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
+  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end, max_ctas};
   return cuda_check(shen::launch_helm_cr(a, S(stream)), "shen_helm_solve_cr");
 }
 

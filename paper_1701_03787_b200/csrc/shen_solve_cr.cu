@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(kNT, 1)
     helm_cr_kernel(HelmChunkArgs a, const __grid_constant__ CUtensorMap in0, const __grid_constant__ CUtensorMap in1,
                    const __grid_constant__ CUtensorMap out0, const __grid_constant__ CUtensorMap out1, int box_rows,
                    int rows_slot) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[NSLOT];
+  // dynamic window only (no static shared memory in front of it), base
+  // rounded up to 1024 B in the kernel: TMA boxes land 128-B aligned
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = tid & 7, c = (warp << 2) | (lane >> 3);
   const int par = (int)(blockIdx.x & 1);
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kNT, 1)
   cplx* slots = reinterpret_cast<cplx*>(smem);
   double* tab = reinterpret_cast<double*>(smem + (size_t)NSLOT * slot_elems * sizeof(cplx));
   double* xch = tab + R * 4 * 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xch + kXq * kS * kXs);
   auto X = [&](int q, int ss, int cc) -> double& { return xch[(q * kS + ss) * kXs + cc]; };
   for (int idx = tid; idx < R * 32; idx += kNT) {
     const int r = idx >> 5, cc = idx & 31, i = cc * R + r;
@@ -123,7 +126,8 @@ __global__ void __launch_bounds__(kNT, 1)
   const int s0 = c * R;
   const int nr = max(0, min(R, n - s0));
   const bool use_ck = s0 > 0 && nr > 0;
-  const int64_t ntiles = (B + kS - 1) / kS;
+  const int64_t jb = a.jb, je = a.je < 0 ? B : a.je;  // systems [jb, je); columns >= je are clipped by TMA
+  const int64_t ntiles = (je - jb + kS - 1) / kS;
   const int64_t tfirst = blockIdx.x >> 1;
   const int64_t tstride = (gridDim.x + 1 - par) >> 1;
   if (tfirst >= ntiles) return;
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(kNT, 1)
   auto issue_load = [&](int64_t t, int sl) {
     mb_expect(bars + sl, tile_bytes);
     for (int b = 0; b < nbox; ++b)
-      tma_load_2d(slots + sl * slot_elems + (size_t)b * box_rows * kS, mi, (int)(t * kS * 2), b * box_rows, bars + sl);
+      tma_load_2d(slots + sl * slot_elems + (size_t)b * box_rows * kS, mi, (int)((jb + t * kS) * 2), b * box_rows,
+                  bars + sl);
   };
   int64_t t_ld = tfirst;
   if (tid == 0)
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(kNT, 1)
   // per-system scalars, loaded one tile ahead
   double cb_n = 1.0, ckd_n = 1.0, cke_n = 0.0, ckt_n = 0.0;
   auto load_scalars = [&](int64_t t) {
-    const int64_t j = min(t * kS + s, B - 1);
+    const int64_t j = min(jb + t * kS + s, je - 1);
     cb_n = __ldg(a.cb + j);
     if (use_ck) {
       const double* ck = a.ckpt + ((int64_t)(c * 2 + par) * 3) * B + j;
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kNT, 1)
     if (tid == 0) {
       const cplx* base = slots + slot * slot_elems;
       for (int b = 0; b < nbox; ++b)
-        tma_store_2d(mo, (int)(t * kS * 2), b * box_rows, base + (size_t)b * box_rows * kS);
+        tma_store_2d(mo, (int)((jb + t * kS) * 2), b * box_rows, base + (size_t)b * box_rows * kS);
       bulk_commit();
     }
     slot = slot + 1 == NSLOT ? 0 : slot + 1;
@@ -334,7 +339,7 @@ size_t helm_cr_smem(int n_dir, int chunk_rows, int nslot) {
   const int br = cr_box_rows(n0);
   const int rows_slot = ((n0 + br - 1) / br) * br;
   return (size_t)nslot * rows_slot * kS * sizeof(cplx) + (size_t)chunk_rows * 4 * 32 * sizeof(double) +
-         (size_t)kXq * kS * kXs * sizeof(double);
+         (size_t)kXq * kS * kXs * sizeof(double) + (size_t)nslot * sizeof(uint64_t) + 1024;  // + base alignment
 }
 
 template <int R, int NSLOT>
@@ -345,13 +350,16 @@ static cudaError_t helm_cr_RR(const HelmChunkArgs& a, cudaStream_t st) {
   const size_t smem = helm_cr_smem(a.n_dir, R, NSLOT);
   CUtensorMap m[4];
   const uint64_t pitch = (uint64_t)a.batch * sizeof(cplx);
+  const int64_t je = a.je < 0 ? a.batch : a.je;
+  if (je <= a.jb) return cudaSuccess;
   const char* rin = static_cast<const char*>(a.rhs);
   const char* rout = static_cast<const char*>(a.out);
   // parity p: rows p, p + 2, ... -> a 2-D tensor (2 batch doubles, rows_p) with a 2-row stride
-  if (!encode_tiled_2d(m + 0, rin, 2 * a.batch, n0, 2 * pitch, 2 * kS, br) ||
-      (n1 > 0 && !encode_tiled_2d(m + 1, rin + pitch, 2 * a.batch, n1, 2 * pitch, 2 * kS, br)) ||
-      !encode_tiled_2d(m + 2, rout, 2 * a.batch, n0, 2 * pitch, 2 * kS, br) ||
-      (n1 > 0 && !encode_tiled_2d(m + 3, rout + pitch, 2 * a.batch, n1, 2 * pitch, 2 * kS, br)))
+  // (the tensor ends at column je: a partial last tile is zero-filled on load and clipped on store)
+  if (!encode_tiled_2d(m + 0, rin, 2 * je, n0, 2 * pitch, 2 * kS, br) ||
+      (n1 > 0 && !encode_tiled_2d(m + 1, rin + pitch, 2 * je, n1, 2 * pitch, 2 * kS, br)) ||
+      !encode_tiled_2d(m + 2, rout, 2 * je, n0, 2 * pitch, 2 * kS, br) ||
+      (n1 > 0 && !encode_tiled_2d(m + 3, rout + pitch, 2 * je, n1, 2 * pitch, 2 * kS, br)))
     return cudaErrorNotSupported;
   if (n1 == 0) {
     m[1] = m[0];
@@ -363,7 +371,7 @@ static cudaError_t helm_cr_RR(const HelmChunkArgs& a, cudaStream_t st) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t ntiles = (a.batch + kS - 1) / kS;
+  const int64_t ntiles = (je - a.jb + kS - 1) / kS;
   int64_t grid = std::min<int64_t>((int64_t)sms, 2 * ntiles);
   if (a.max_ctas > 0) grid = std::min<int64_t>(grid, a.max_ctas);
   grid = std::max<int64_t>(grid, n1 > 0 ? 2 : 1);  // parity = blockIdx.x & 1: both must exist

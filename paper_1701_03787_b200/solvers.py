@@ -54,7 +54,7 @@ __all__ = [
 
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
-_METHODS = ("chunked", "stream", "stored", "tile")
+_METHODS = ("cr", "chunked", "stream", "stored", "tile")
 
 
 def _env_int(name, default):
@@ -158,7 +158,7 @@ def _host_pipeline_many(jobs):
             cache = (torch.empty((n, B), dtype=dtype, device=dev), torch.empty((n, B), dtype=dtype, device=dev))
             lu._pipe = cache
         d_rhs, d_out = cache
-        if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
+        if lu.method not in ("stream", "cr") or B < 2 * _PIPE_MIN_SLAB:
             bounds = [(0, B)]
         else:
             nslab = min(_PIPE_MAX_SLABS, B // _PIPE_MIN_SLAB)
@@ -272,17 +272,22 @@ def mirror_pairs_grid(z2):
     return np.stack([a, b]), (int(ny), int(nzh))
 
 
-def _solve_real_via_complex(lu, rhs_dev, out_dev):
-    """Real RHS whose rows are not 16-B aligned (odd batch): the streaming
-    kernel moves 16-B row pieces, so solve the complex system with zero
+def _solve_real_via_complex(lu, rhs_dev, out_dev, j0=0, j1=-1):
+    """Real RHS (or a complex one on misaligned storage): the tile kernels move
+    16-B row pieces of complex values, so solve the complex system with zero
     imaginary part -- every coefficient is real, so the real part is the same
     arithmetic as the real solve."""
     import torch
 
-    z = torch.complex(rhs_dev, torch.zeros_like(rhs_dev)).contiguous()
+    if rhs_dev.is_complex():
+        z = rhs_dev.clone()
+    else:
+        z = torch.complex(rhs_dev, torch.zeros_like(rhs_dev)).contiguous()
     xz = torch.empty_like(z)
-    lu.solve_into(z, xz, True)
-    out_dev.copy_(xz.real)
+    lu.solve_into(z, xz, True, j0, j1)
+    hi = xz.shape[1] if j1 < 0 else j1
+    src = xz[:, j0:hi]
+    out_dev[:, j0:hi].copy_(src if out_dev.is_complex() else src.real)
     return out_dev
 
 
@@ -447,9 +452,17 @@ class HelmholtzLU:
             return out_dev
         if self.method == "stream" and not is_complex and (B % 2 or rhs_dev.data_ptr() % 16):
             return _solve_real_via_complex(self, rhs_dev, out_dev)
+        if self.method == "cr" and (not is_complex or rhs_dev.data_ptr() % 16 or out_dev.data_ptr() % 16):
+            return _solve_real_via_complex(self, rhs_dev, out_dev, j0, j1)
         h = lib()
         sh = dv.stream_handle()
-        if self.method == "stored":
+        if self.method == "cr":
+            sd, st, md = self._tab
+            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
+            check(h.shen_helm_solve_cr(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
+                                       md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(), out_dev.data_ptr(),
+                                       max_ctas, j0, j1, sh), "shen_helm_solve_cr")
+        elif self.method == "stored":
             ptrs, keep = ptr_array([b.data_ptr() for b in self._stored])
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
@@ -513,16 +526,16 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
     tabs = tuple(torch.from_numpy(t).to(dev) for t in _helm_tables(mats))
     cb_dev = torch.from_numpy(np.ascontiguousarray(cb_flat)).to(dev)
     B = cb_flat.size
-    if method == "tile" and chunk_rows_for(nd) > 16:
-        method = "stream"  # the tile kernel keeps at most 32 x 16 rows per parity in a warp
-    R = chunk_rows_for(nd) if method in ("chunked", "tile") else STREAM_ROWS_H
+    if method in ("tile", "cr") and chunk_rows_for(nd) > 16:
+        method = "stream"  # the tile kernels keep at most 32 x 16 rows per parity
+    R = chunk_rows_for(nd) if method in ("chunked", "tile", "cr") else STREAM_ROWS_H
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method in ("chunked", "stream", "tile"):
+    if method in ("chunked", "stream", "tile", "cr"):
         C = _n_chunks(nd, R)
         ckpt = torch.empty((C, 2, 3, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_helm_factor(nd, float(ca), cb_dev.data_ptr(), B, tabs[0].data_ptr(), tabs[1].data_ptr(),
@@ -743,8 +756,8 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
     x1d = torch.from_numpy(x1).to(dev)
     x2d = torch.from_numpy(x2).to(dev)
     B = x1.size
-    if method == "tile":
-        method = "stream"  # no tiled biharmonic variant (its chunk state does not fit a tile CTA)
+    if method in ("tile", "cr"):
+        method = "stream"  # no tiled biharmonic variant yet: the streaming pair kernel
     R = chunk_rows_for(nb) if method == "chunked" else STREAM_ROWS_B
     h = lib()
     sh = dv.stream_handle()

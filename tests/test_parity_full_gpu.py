@@ -54,14 +54,14 @@ def _gather(t, idx):
     return t.index_select(1, torch.from_numpy(idx).to(t.device)).cpu().numpy()
 
 
-@pytest.mark.parametrize("op", ["h", "b"])
-def test_config4_full_plane_sampled(op):
+@pytest.mark.parametrize("op,method", [("h", "stream"), ("h", "cr"), ("b", "stream")])
+def test_config4_full_plane_sampled(op, method):
     import torch
 
     mats = assemble(1024, 0)
     z2 = channel_z2(2048, 2048)
     build = S.build_helmholtz if op == "h" else S.build_biharmonic
-    lu = build(mats, NU4, DT4, z2)
+    lu = build(mats, NU4, DT4, z2, method=method)
     nm, B = lu.n_modes, z2.size
     gen = torch.Generator(device="cuda").manual_seed(99 if op == "h" else 98)
     f = torch.randn((nm, B), dtype=torch.complex128, device="cuda", generator=gen)
@@ -91,8 +91,8 @@ def test_config4_full_plane_sampled(op):
 
 
 @pytest.mark.parametrize("N", [129, 257, 513, 1025, 2049])
-@pytest.mark.parametrize("op", ["h", "b"])
-def test_config5_batch(N, op):
+@pytest.mark.parametrize("op,method", [("h", "stream"), ("h", "cr"), ("b", "stream")])
+def test_config5_batch(N, op, method):
     """Config 5 (512 x 257 wavenumbers): the whole batch for N <= 513, 4,096
     random systems plus the special rows above."""
     import torch
@@ -100,7 +100,7 @@ def test_config5_batch(N, op):
     mats = assemble(N - 1, 0)
     z2 = channel_z2(512, 512)
     build = S.build_helmholtz if op == "h" else S.build_biharmonic
-    lu = build(mats, NU4, DT4, z2)
+    lu = build(mats, NU4, DT4, z2, method=method)
     nm, B = lu.n_modes, z2.size
     gen = torch.Generator(device="cuda").manual_seed(N)
     f = torch.randn((nm, B), dtype=torch.complex128, device="cuda", generator=gen)

@@ -40,11 +40,12 @@ template <int S, int NSLOT, int NT, int BOX>
 __global__ void __launch_bounds__(NT, 1) cr_copy(const __grid_constant__ CUtensorMap in0, const __grid_constant__ CUtensorMap in1,
                                                const __grid_constant__ CUtensorMap out0, const __grid_constant__ CUtensorMap out1,
                                                int np0, int np1, int64_t ntiles) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bars[NSLOT];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   constexpr int ROWB = S * 16;
   const int npmax = np0;
   const size_t slot_bytes = (size_t)npmax * ROWB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSLOT * slot_bytes);
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int k = 0; k < NSLOT; ++k) mb_init(bars + k, 1);
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(NT, 1) cr_copy(const __grid_constant__ CUtenso
   auto issue_load = [&](int64_t t, int slot) {
     const int par = (int)(t & 1), np = par ? np1 : np0;
     const CUtensorMap* m = par ? &in1 : &in0;
-    mb_expect(bars + slot, (unsigned)(np * ROWB));
+    mb_expect(bars + slot, (unsigned)(((np + BOX - 1) / BOX) * BOX * ROWB));  // full boxes (OOB rows zero-filled)
     for (int r = 0; r < np; r += BOX) tma_load(smem + slot * slot_bytes + (size_t)r * ROWB, m, (int)((t >> 1) * S * 2), r, bars + slot);
   };
   int64_t t_ld = blockIdx.x;
@@ -96,6 +97,71 @@ __global__ void __launch_bounds__(NT, 1) cr_copy(const __grid_constant__ CUtenso
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Row-blocked tiles (the cluster variant's per-CTA share): tile t = (system
+// block sb, parity, row block rb of RB rows); consecutive t are the row blocks
+// of one (sb, parity), i.e. the CTAs of one cluster run side by side.
+template <int S, int NSLOT, int NT, int RB>
+__global__ void __launch_bounds__(NT, 1) cr_copy_rb(const __grid_constant__ CUtensorMap in0, const __grid_constant__ CUtensorMap in1,
+                                                  const __grid_constant__ CUtensorMap out0, const __grid_constant__ CUtensorMap out1,
+                                                  int np0, int np1, int64_t ntiles, int nrb) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  constexpr int ROWB = S * 16;
+  const size_t slot_bytes = (size_t)RB * ROWB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSLOT * slot_bytes);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int k = 0; k < NSLOT; ++k) mb_init(bars + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto coords = [&](int64_t t, int& par, int& c0, int& r0) {
+    const int64_t sb = t / (2 * nrb);
+    par = (int)((t / nrb) & 1);
+    r0 = (int)(t % nrb) * RB;
+    c0 = (int)(sb * S * 2);
+  };
+  auto issue_load = [&](int64_t t, int slot) {
+    int par, c0, r0;
+    coords(t, par, c0, r0);
+    mb_expect(bars + slot, (unsigned)(RB * ROWB));
+    tma_load(smem + slot * slot_bytes, par ? &in1 : &in0, c0, r0, bars + slot);
+  };
+  int64_t t_ld = blockIdx.x;
+  if (tid == 0)
+    for (int k = 0; k < NSLOT - 1 && t_ld < ntiles; ++k, t_ld += gridDim.x) issue_load(t_ld, k);
+  unsigned phase = 0;
+  int slot = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (tid == 0 && t_ld < ntiles) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue_load(t_ld, (slot + NSLOT - 1) % NSLOT);
+      t_ld += gridDim.x;
+    }
+    mb_wait(bars + slot, (phase >> slot) & 1);
+    phase ^= 1u << slot;
+    double2* tile = reinterpret_cast<double2*>(smem + slot * slot_bytes);
+    constexpr int NCH = NT / S;
+    const int s = tid % S, c = tid / S;
+    constexpr int rpc = (RB + NCH - 1) / NCH;
+    for (int r = c * rpc; r < min(RB, (c + 1) * rpc); ++r) {
+      double2 v = tile[r * S + s];
+      v.x += 1.0;
+      tile[r * S + s] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      int par, c0, r0;
+      coords(t, par, c0, r0);
+      tma_store(par ? &out1 : &out0, c0, r0, smem + slot * slot_bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    slot = (slot + 1) % NSLOT;
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -119,7 +185,7 @@ static int run(EncodeFn enc, double* in, double* out, int n_rows, int64_t B, int
     printf("encode failed\n");
     return 1;
   }
-  const size_t smem = (size_t)NSLOT * np0 * S * 16;
+  const size_t smem = (size_t)NSLOT * np0 * S * 16 + 64 + 1024;
   auto k = cr_copy<S, NSLOT, NT, BOX>;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t ntiles = 2 * (B / S);
@@ -139,6 +205,42 @@ static int run(EncodeFn enc, double* in, double* out, int n_rows, int64_t B, int
   }
   printf("S=%2d NSLOT=%d NT=%3d BOX=%3d ctas/SM=%d promo=%s smem=%3zu KB: %.2f ms  %.0f GB/s\n", S, NSLOT, NT, BOX,
          ctas_per_sm, prn, smem / 1024, best, 2.0 * n_rows * (double)(B / S * S) * 16 / (best * 1e6));
+  fflush(stdout);
+  return 0;
+}
+
+template <int S, int NSLOT, int NT, int RB>
+static int run_rb(EncodeFn enc, double* in, double* out, int n_rows, int64_t B, int sms) {
+  const int np0 = (n_rows + 1) / 2, np1 = n_rows / 2;
+  const auto pr = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  CUtensorMap m[4];
+  if (make_map(enc, m + 0, in, B, np0, S, RB, pr) || make_map(enc, m + 1, in + 2 * B, B, np1, S, RB, pr) ||
+      make_map(enc, m + 2, out, B, np0, S, RB, pr) || make_map(enc, m + 3, out + 2 * B, B, np1, S, RB, pr)) {
+    printf("encode failed\n");
+    return 1;
+  }
+  const int nrb = (np0 + RB - 1) / RB;
+  const size_t smem = (size_t)NSLOT * RB * S * 16 + 64 + 1024;
+  auto k = cr_copy_rb<S, NSLOT, NT, RB>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t ntiles = 2 * (B / S) * nrb;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0);
+    k<<<sms, NT, smem>>>(m[0], m[1], m[2], m[3], np0, np1, ntiles, nrb);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  printf("rowblock S=%2d RB=%3d NSLOT=%d NT=%3d smem=%3zu KB: %.2f ms  %.0f GB/s\n", S, RB, NSLOT, NT, smem / 1024, best,
+         2.0 * n_rows * (double)(B / S * S) * 16 / (best * 1e6));
+  fflush(stdout);
   return 0;
 }
 
@@ -154,16 +256,15 @@ int main() {
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const auto P0 = CU_TENSOR_MAP_L2_PROMOTION_NONE, P2 = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  run<8, 3, 256, 256>(enc, in, out, n_rows, B, sms, 1, P0, "none");
-  run<8, 3, 256, 256>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
-  run<8, 3, 256, 64>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
-  run<8, 2, 256, 256>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
-  run<8, 1, 256, 256>(enc, in, out, n_rows, B, sms, 3, P2, "256B");
+  const auto P2 = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   run<16, 1, 512, 256>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
-  run<4, 3, 128, 256>(enc, in, out, n_rows, B, sms, 2, P2, "256B");
-  run<4, 6, 256, 256>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
-  // mirror-pair friendly: 8 systems, both parities handled as separate tiles
-  run<8, 3, 512, 256>(enc, in, out, n_rows, B, sms, 1, P2, "256B");
+  run_rb<16, 3, 256, 256>(enc, in, out, n_rows, B, sms);
+  run_rb<16, 3, 256, 128>(enc, in, out, n_rows, B, sms);
+  run_rb<16, 6, 256, 128>(enc, in, out, n_rows, B, sms);
+  run_rb<32, 3, 256, 128>(enc, in, out, n_rows, B, sms);
+  run_rb<32, 6, 256, 64>(enc, in, out, n_rows, B, sms);
+  run_rb<32, 3, 256, 64>(enc, in, out, n_rows, B, sms);
+  run_rb<64, 3, 256, 64>(enc, in, out, n_rows, B, sms);
+  run_rb<16, 12, 256, 64>(enc, in, out, n_rows, B, sms);
   return 0;
 }
