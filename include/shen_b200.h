@@ -220,6 +220,35 @@ int shen_xform_mass_solve(int nband, int n, int mmax, int64_t L, const double* f
                           void* stream);
 
 /* ---------------------------------------------------------------------
+ * Fused wall-normal transform (one kernel per direction, reference
+ * transforms.py:81-205): on a tile of Fourier lines held in shared memory,
+ *   forward  DCT (type 2 Gauss / type 1 Gauss-Lobatto) -> Chebyshev scaling
+ *            -> Shen stencil -> optional per-parity banded Cholesky mass
+ *            solve (forward_transform / forward_scalar_product /
+ *            shen_scalar / chebyshev_scalar);
+ *   inverse  shen_expand -> Chebyshev evaluation on the points, times
+ *            `scale` (inverse_transform's wall-normal stage, chebyshev_evaluate).
+ * The DFT behind the DCT is a power-of-two FFT, Rader's algorithm (prime
+ * length with a power-of-two predecessor: N = 257) or Bluestein's, all in
+ * shared memory.  The plan (tables, all device pointers) is built by the
+ * host layer (paper_1701_03787_b200/wall.py); `in` and `out` are (rows, L)
+ * complex128, lines contiguous, not aliased. */
+typedef struct shen_wall_plan {
+  int direction, family, space, mass, N, n_out, n_in, kind, Ld, M, nstage;
+  int radix[4];
+  int log2_lines, rows_smem;
+  double scale;
+  int nband, mmax;
+  const void *tw, *ker_f, *ker_i, *chirp_f, *chirp_i; /* complex128 tables */
+  const int *gin_f, *gin_i, *gout, *pinv;
+  const void* mk;                                     /* complex128 */
+  const double *c2, *c4, *mfac;
+} shen_wall_plan;
+int shen_wall_transform(const shen_wall_plan* plan, int64_t L, const void* in, void* out, void* stream);
+/* shared-memory bytes per CTA of a plan (host-side plan checks) */
+int64_t shen_wall_smem_bytes(const shen_wall_plan* plan);
+
+/* ---------------------------------------------------------------------
  * Structured matrix-vector products y = M x along the rows of (rows, L)
  * arrays (reference matrices.py:62-71, 109-117, 145-152; the
  * _parity_suffix_sum of :84-90), bit-identical to the reference's.

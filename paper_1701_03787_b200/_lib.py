@@ -62,6 +62,17 @@ class ShenRecoverArgs(ctypes.Structure):
                 ("u", ctypes.c_void_p), ("g", ctypes.c_void_p), ("v", ctypes.c_void_p), ("w", ctypes.c_void_p)]
 
 
+class ShenWallPlan(ctypes.Structure):
+    _fields_ = [("direction", ctypes.c_int), ("family", ctypes.c_int), ("space", ctypes.c_int), ("mass", ctypes.c_int),
+                ("N", ctypes.c_int), ("n_out", ctypes.c_int), ("n_in", ctypes.c_int), ("kind", ctypes.c_int),
+                ("Ld", ctypes.c_int), ("M", ctypes.c_int), ("nstage", ctypes.c_int), ("radix", ctypes.c_int * 4),
+                ("log2_lines", ctypes.c_int), ("rows_smem", ctypes.c_int), ("scale", ctypes.c_double),
+                ("nband", ctypes.c_int), ("mmax", ctypes.c_int),
+                ("tw", _vp), ("ker_f", _vp), ("ker_i", _vp), ("chirp_f", _vp), ("chirp_i", _vp),
+                ("gin_f", _vp), ("gin_i", _vp), ("gout", _vp), ("pinv", _vp), ("mk", _vp),
+                ("c2", _vp), ("c4", _vp), ("mfac", _vp)]
+
+
 _SIGS = {
     "shen_version": (ctypes.c_char_p, []),
     "shen_last_error": (ctypes.c_char_p, []),
@@ -79,6 +90,8 @@ _SIGS = {
     "shen_helm_solve_stream_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                                     ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _c_int64,
                                                     ctypes.c_int, ctypes.c_int, _vp]),
+    "shen_wall_transform": (ctypes.c_int, [ctypes.POINTER(ShenWallPlan), _c_int64, _vp, _vp, _vp]),
+    "shen_wall_smem_bytes": (ctypes.c_int64, [ctypes.POINTER(ShenWallPlan)]),
     "shen_helm_solve_cr": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                           ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),

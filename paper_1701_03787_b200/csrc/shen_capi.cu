@@ -10,6 +10,7 @@
 #include "shen_rows.cuh"
 
 static_assert(SHEN_BIH_NCOL == shen::B_STRIDE, "table pitch mismatch");
+static_assert(sizeof(shen_wall_plan) == sizeof(shen::WallPlan), "wall plan layout mismatch");
 
 namespace {
 thread_local std::string g_err;
@@ -99,6 +100,25 @@ int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batc
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: rhs must not alias out");
   shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
   return cuda_check(shen::launch_helm_chunk(a, is_complex != 0, S(stream)), "shen_helm_solve_chunked");
+}
+
+int shen_wall_transform(const shen_wall_plan* plan, int64_t L, const void* in, void* out, void* stream) {
+  if (!plan) return fail(SHEN_ERR_ARG, "shen_wall_transform: plan");
+  if (L == 0) return SHEN_OK;
+  const shen::WallPlan& p = *reinterpret_cast<const shen::WallPlan*>(plan);
+  if (L < 0 || !in || !out || in == out || p.N < 2 || p.M < 2 || (p.M & (p.M - 1)) || p.nstage < 1 || p.nstage > 4 ||
+      !p.tw || p.log2_lines < 0 || p.log2_lines > 4 || p.rows_smem < p.N || p.rows_smem < p.M)
+    return fail(SHEN_ERR_ARG, "shen_wall_transform: bad args");
+  if ((p.kind == 1 && (!p.ker_f || !p.ker_i || !p.gin_f || !p.gin_i || !p.gout)) ||
+      (p.kind == 2 && (!p.ker_f || !p.ker_i || !p.chirp_f || !p.chirp_i)) || (p.kind == 0 && !p.pinv) ||
+      (p.family == 0 && !p.mk) || (p.space == 2 && (!p.c2 || !p.c4)) || (p.mass && !p.mfac))
+    return fail(SHEN_ERR_ARG, "shen_wall_transform: missing table");
+  return cuda_check(shen::launch_wall(p, L, in, out, S(stream)), "shen_wall_transform");
+}
+
+int64_t shen_wall_smem_bytes(const shen_wall_plan* plan) {
+  if (!plan) return -1;
+  return (int64_t)shen::wall_smem_bytes(*reinterpret_cast<const shen::WallPlan*>(plan));
 }
 
 int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,

@@ -192,6 +192,40 @@ cudaError_t launch_pair(bool merge, int64_t P, int64_t Q, int64_t M, const doubl
 cudaError_t launch_scale_rows(int64_t rows, int64_t L, const void* x, int64_t xs, const double* cre,
                               const double* cim, void* y, int64_t ys, cudaStream_t st);
 
+// fused wall-normal transforms (shen_wall.cu); tables built on the host (wall.py)
+struct WallPlan {
+  int direction;   // 0 forward (points -> coefficients), 1 inverse
+  int family;      // 0 Gauss, 1 Gauss-Lobatto
+  int space;       // 0 Chebyshev, 1 Dirichlet, 2 biharmonic, 3 raw scalar products (forward only)
+  int mass;        // forward: 1 = banded mass solve after the stencil
+  int N;           // points (n_x + 1)
+  int n_out;       // forward output rows
+  int n_in;        // inverse input rows
+  int kind;        // DFT: 0 power of two, 1 Rader, 2 Bluestein
+  int Ld, M;       // DFT length, FFT size (power of two)
+  int nstage;
+  int radix[4];    // radix of each DIF pass, first to last (product = M)
+  int log2_lines;  // lines per CTA = 1 << log2_lines
+  int rows_smem;   // shared-memory rows of the tile (>= max(N, M))
+  double scale;    // forward: Chebyshev scaling pi/(2N) or pi/(2 n_x); inverse: 1/(n_y n_z)
+  int nband, mmax;
+  const double2* tw;       // [M] exp(-2 pi i k / M)
+  const double2* ker_f;    // [M] convolution kernel spectrum (digit-reversed, / M), forward DFT
+  const double2* ker_i;    // [M] same for the inverse DFT
+  const double2* chirp_f;  // [Ld] Bluestein chirp, forward
+  const double2* chirp_i;  // [Ld] Bluestein chirp, inverse
+  const int* gin_f;        // [M] Rader gather rows, forward (sigma(g^p))
+  const int* gin_i;        // [M] Rader gather rows, inverse (g^p)
+  const int* gout;         // [M] Rader output index g^{-q} mod N
+  const int* pinv;         // [M] power of two: position of frequency k
+  const double2* mk;       // [N] exp(-i pi k / 2N) (Gauss)
+  const double* c2;        // [n_bih] biharmonic stencil 2(k+2)/(k+3)
+  const double* c4;        // [n_bih] (k+1)/(k+3)
+  const double* mfac;      // [2][3][mmax] 1/U_ii, U_{i-1,i}, U_{i-2,i} per parity
+};
+size_t wall_smem_bytes(const WallPlan& p);
+cudaError_t launch_wall(const WallPlan& p, int64_t L, const void* in, void* out, cudaStream_t st);
+
 // transforms (shen_transform.cu)
 cudaError_t launch_xf_extend(int kind, int N, int64_t L, const void* x, void* e, cudaStream_t st);
 cudaError_t launch_xf_fwd_post(int gl, int space, int N, int64_t L, double scale, const void* tw, const void* Y,

@@ -162,6 +162,23 @@ def _fam(family) -> int:
     return family_code(family)  # 0 = Gauss, 1 = Gauss-Lobatto
 
 
+def _wall_run(plan, x, rows_out):
+    """shen_wall_transform of (rows_in, L) complex128 lines -> (rows_out, L)."""
+    import ctypes
+
+    import torch
+
+    L = x.shape[1]
+    out = torch.empty((rows_out, L), dtype=torch.complex128, device=x.device)
+    _lib.check(_lib.lib().shen_wall_transform(ctypes.byref(plan.struct), L, x.data_ptr(), out.data_ptr(),
+                                              stream_handle()), "shen_wall_transform")
+    return out
+
+
+def _cheb_scale(N: int, fam: int) -> float:
+    return np.pi / (2 * N) if fam == 0 else np.pi / (2 * (N - 1))  # transforms.py:84-86
+
+
 def _chebyshev_pass(x, fam: int, space: int):
     """x: (N, L) complex128 device -> fwd_post output (n_modes(space), L)."""
     import torch
@@ -169,6 +186,12 @@ def _chebyshev_pass(x, fam: int, space: int):
     N, L = x.shape
     if N < 2:
         raise ValueError("need at least 2 points along axis 0")
+    if XFORM_METHOD == "wall" and N >= 3:
+        from .wall import wall_plan
+
+        plan = wall_plan(N - 1, fam, space, 0, False, _cheb_scale(N, fam))
+        if plan is not None:
+            return _wall_run(plan, x.contiguous(), plan.struct.n_out)
     M = 2 * N if fam == 0 else 2 * N - 2
     e = torch.empty((M, L), dtype=torch.complex128, device=x.device)
     lib = _lib.lib()
@@ -193,6 +216,12 @@ def _expand_pass(c, space: int, n_x: int, fam: int):
 
     n, L = c.shape
     N = n_x + 1
+    if fam != 2 and XFORM_METHOD == "wall" and N >= 3:
+        from .wall import wall_plan
+
+        plan = wall_plan(n_x, fam, space, 1, False, 1.0)
+        if plan is not None and plan.struct.n_in == n:
+            return _wall_run(plan, c.contiguous(), N)
     lib = _lib.lib()
     st = stream_handle()
     tw = _twiddles(N)
@@ -331,7 +360,7 @@ def mass_solve(scalar, space, n_x: int, family):
 # 80-bit arithmetic and rounded to float64.  SHEN_XFORM=fft selects the
 # kernel/cuFFT pipeline above instead (used by the 1-D building blocks).
 
-XFORM_METHOD = __import__("os").environ.get("SHEN_XFORM", "matrix")
+XFORM_METHOD = __import__("os").environ.get("SHEN_XFORM", "wall")
 
 
 def _ld_pi():
@@ -525,6 +554,12 @@ def _inverse_paired(blocks, coef):
 def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
     """(N, L) complex128 Fourier lines on the device -> (n_modes, L) Shen
     coefficients (scalar products if ``solve_mass`` is False)."""
+    if XFORM_METHOD == "wall" and n_x >= 2:
+        from .wall import wall_plan
+
+        plan = wall_plan(n_x, fam, sp, 0, solve_mass, _cheb_scale(n_x + 1, fam))
+        if plan is not None:
+            return _wall_run(plan, lines.contiguous(), plan.struct.n_out)
     if XFORM_METHOD == "matrix":
         kind = "fwd" if solve_mass else "fsp"
         if lines.shape[1] >= PAIRED_MIN_LINES:
@@ -542,6 +577,12 @@ def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
     """(n, L) coefficients -> (N, L) values on the Chebyshev points, and the
     ``norm`` for the following ``irfft2`` (the matrix route folds the
     1/(n_y n_z) of the inverse FFT into its operator)."""
+    if XFORM_METHOD == "wall" and n_x >= 2:
+        from .wall import wall_plan
+
+        plan = wall_plan(n_x, fam, sp, 1, False, 1.0 / yz_points)
+        if plan is not None and plan.struct.n_in == coef.shape[0]:
+            return _wall_run(plan, coef.contiguous(), n_x + 1), "forward"
     if XFORM_METHOD == "matrix":
         if coef.shape[1] >= PAIRED_MIN_LINES:
             blocks = _paired_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)

@@ -71,7 +71,7 @@ def test_mass_factors_match_oracle(fi):
             assert np.array_equal(mine[p], want[p])
 
 
-@pytest.fixture(params=["matrix", "fft"])
+@pytest.fixture(params=["wall", "matrix", "fft"])
 def xform_method(request, monkeypatch):
     monkeypatch.setattr(T, "XFORM_METHOD", request.param)
     return request.param
