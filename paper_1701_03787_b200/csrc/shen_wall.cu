@@ -258,10 +258,7 @@ __device__ __forceinline__ void pass_dit_inv_scatter(cd* T, int TLs, int M, cons
     dft<R, true>(v);
   }
   __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) st(n1 + q * k, l, v[k]);
-  }
+  if (act) st(n1, q, l, v);  // outputs n1 + q k, k < R (v by reference: stays in registers)
 }
 
 template <class LD>
@@ -396,13 +393,32 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   if (p.kind == 0) {  // power of two: Lobatto even extension z (Ld = M = 2 n_x)
     const int nx = N - 1;
     wall_dft(p, T, TLs, nullptr, nullptr,
-             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, cd) {});
+             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, int, auto&) {});
   } else if (p.kind == 1) {  // Rader (Gauss, N prime, M = N - 1)
     if (tid < TL) side[tid] = T[tid];  // v_0 = x_0
+    const double scl = p.scale;
     wall_dft(p, T, TLs, p.ker_f, side + TL,
              [&](int i, int l) { return T[(__ldg(p.gin_f + i) << TLs) + l]; },
-             [&](int q, int l, cd v) { T[(__ldg(p.gout + q) << TLs) + l] = cadd(side[l], v); });
-    if (tid < TL) T[tid] = cadd(side[tid], side[TL + tid]);  // V_0 = v_0 + A(0)
+             [&](int n1, int q, int l, auto& v) {
+               // V_k = x_0 + conv_q at k = g^{-q}; its partner N - k is R/2
+               // outputs later in the same butterfly (g^{(N-1)/2} = -1), so
+               // the DCT-II post step (w_k, w_{N-k}) happens here in registers
+               constexpr int R = sizeof(v) / sizeof(cd);
+               const cd x0 = side[l];
+#pragma unroll
+               for (int kk = 0; kk < R / 2; ++kk) {
+                 const int qa = n1 + q * kk, qb = qa + q * (R / 2);
+                 const int ka = __ldg(p.gout + qa), kb = __ldg(p.gout + qb);
+                 const cd Va = cadd(x0, v[kk]), Vb = cadd(x0, v[kk + R / 2]);
+                 const cd mka = __ldg(p.mk + ka), mkb = __ldg(p.mk + kb);
+                 const cd sa = cmul(mka, cadd(Va, cconj(Vb))), da = cmul(mka, csub(Va, cconj(Vb)));
+                 const cd sb = cmul(mkb, cadd(Vb, cconj(Va))), db = cmul(mkb, csub(Vb, cconj(Va)));
+                 T[(ka << TLs) + l] = make_double2(sa.x * scl, da.y * scl);
+                 T[(kb << TLs) + l] = make_double2(sb.x * scl, db.y * scl);
+               }
+             });
+    // w_0 = 2 V_0 (scaled), V_0 = x_0 + A(0)
+    if (tid < TL) T[tid] = cscale(2.0 * scl, cadd(side[tid], side[TL + tid]));
     __syncthreads();
   } else {  // Bluestein
     const int Ld = p.Ld, nx = N - 1;
@@ -412,14 +428,21 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
                const int src = gauss ? sigma(i, N) : (i <= nx ? i : Ld - i);
                return cmul(T[(src << TLs) + l], __ldg(p.chirp_f + i));
              },
-             [&](int q, int l, cd v) {
-               if (q < Ld) T[(q << TLs) + l] = cmul(v, __ldg(p.chirp_f + q));
+             [&](int n1, int q, int l, auto& v) {
+               constexpr int R = sizeof(v) / sizeof(cd);
+#pragma unroll
+               for (int kk = 0; kk < R; ++kk) {
+                 const int qq = n1 + q * kk;
+                 if (qq < Ld) T[(qq << TLs) + l] = cmul(v[kk], __ldg(p.chirp_f + qq));
+               }
              });
   }
   // ---- Chebyshev scalar products w_k (k < N), in place
   const int n = p.n_out, sp = p.space, nx = N - 1;
   const double scl = p.scale;
-  if (gauss) {
+  if (p.kind == 1) {
+    // already w (fused into the last FFT pass)
+  } else if (gauss) {
     // DCT-II from V_k and V_{N-k}: one thread owns both rows of a pair
     const int npair = N / 2 + 1;  // k = 0 .. N/2, partner (N - k) mod N
     for (int e = tid; e < npair * TL; e += kWallThreads) {
@@ -558,7 +581,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
   // (transforms.py:113-126), in place: chunks walked downwards in k, the 4
   // rows below the chunk read before anyone writes
   const int sp = p.space;
-  if (sp == 1 || sp == 2) {
+  if (!gauss && (sp == 1 || sp == 2)) {  // (Gauss: expanded on the fly in the FFT's gather)
     const int per_line = kWallThreads >> TLs;
     const int R = (N + per_line - 1) / per_line;
     const int l = tid & (TL - 1), k0 = (tid >> TLs) * R, k1 = min(N, k0 + R);
@@ -586,21 +609,8 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     __syncthreads();
   }
   if (gauss) {
-    // V_k = e^{i pi k / 2N} (y_k - i y_{N-k}) / 2 with y_0 = 2 c_0, y_k = c_k,
-    // y_N = 0: one thread owns both rows of a pair (k, N - k)
-    const int npair = N / 2 + 1;
-    for (int e = tid; e < npair * TL; e += kWallThreads) {
-      const int k = e >> TLs, l = e & (TL - 1), k2 = k == 0 ? 0 : N - k;
-      const cd ck = T[(k << TLs) + l], ck2 = T[(k2 << TLs) + l];
-      const cd yk = k == 0 ? cscale(2.0, ck) : ck;
-      const cd yn = k == 0 ? make_double2(0.0, 0.0) : ck2;
-      const cd t = make_double2(0.5 * (yk.x + yn.y), 0.5 * (yk.y - yn.x));
-      if (k2 != k) {
-        const cd t2 = make_double2(0.5 * (ck2.x + ck.y), 0.5 * (ck2.y - ck.x));  // y_{k2} = c_{k2}, y_{N-k2} = c_k
-        T[(k2 << TLs) + l] = cmulc(t2, __ldg(p.mk + k2));
-      }
-      T[(k << TLs) + l] = cmulc(t, __ldg(p.mk + k));
-    }
+    // shen_expand and the DCT-III pre-twiddle are evaluated on the fly in the
+    // FFT's gather from the untouched coefficient tile (below)
   } else {
     // even sequence with doubled ends: its DFT is twice the point values
     if (tid < TL) {
@@ -610,9 +620,25 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
   }
   __syncthreads();
   const double sc = p.scale;
+  // Chebyshev coefficient c_k of the expansion (reference order) from the
+  // coefficient tile (rows >= n are zero), and the Makhoul pre-twiddled
+  // V_m = e^{i pi m / 2N} (y_m - i y_{N-m}) / 2, y_m = c_m (1 <= m < N)
+  auto cheb = [&](int k, int l) -> cd {
+    cd c = T[(k << TLs) + l];
+    if (sp == 1 && k >= 2) c = csub(c, T[((k - 2) << TLs) + l]);
+    if (sp == 2) {
+      if (k >= 2) c = csub(c, cscale(__ldg(p.c2 + k - 2), T[((k - 2) << TLs) + l]));
+      if (k >= 4) c = cadd(c, cscale(__ldg(p.c4 + k - 4), T[((k - 4) << TLs) + l]));
+    }
+    return c;
+  };
+  auto vgauss = [&](int m, int l) -> cd {
+    const cd ym = cheb(m, l), yn = cheb(N - m, l);
+    return cmulc(make_double2(0.5 * (ym.x + yn.y), 0.5 * (ym.y - yn.x)), __ldg(p.mk + m));
+  };
   if (p.kind == 0) {  // Lobatto, power of two: f_j = DFT(even extension)_j / 2
     wall_dft(p, T, TLs, nullptr, nullptr,
-             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, cd) {});
+             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, int, auto&) {});
     const int items = N * TL;
     cd wv[KMAX];
 #pragma unroll
@@ -631,12 +657,16 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     }
     __syncthreads();
   } else if (p.kind == 1) {  // Rader, inverse sign: X'_k = V_0 + conv; rows sigma(k)
-    if (tid < TL) side[tid] = T[tid];
-    wall_dft(p, T, TLs, p.ker_i, side + TL,
-             [&](int i, int l) { return T[(__ldg(p.gin_i + i) << TLs) + l]; },
-             [&](int q, int l, cd v) {
-               const int k = __ldg(p.gout + q);
-               T[(sigma(k, N) << TLs) + l] = cscale(sc, cadd(side[l], v));
+    if (tid < TL) side[tid] = T[tid];  // V_0 = c_0 = coefficient 0
+    wall_dft(p, T, TLs, p.ker_i, side + TL, [&](int i, int l) { return vgauss(__ldg(p.gin_i + i), l); },
+             [&](int n1, int q, int l, auto& v) {
+               constexpr int R = sizeof(v) / sizeof(cd);
+               const cd v0 = side[l];
+#pragma unroll
+               for (int kk = 0; kk < R; ++kk) {
+                 const int k = __ldg(p.gout + n1 + q * kk);
+                 T[(sigma(k, N) << TLs) + l] = cscale(sc, cadd(v0, v[kk]));
+               }
              });
     if (tid < TL) T[tid] = cscale(sc, cadd(side[tid], side[TL + tid]));  // row sigma(0) = 0
     __syncthreads();
@@ -645,14 +675,18 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     wall_dft(p, T, TLs, p.ker_i, nullptr,
              [&](int i, int l) {
                if (i >= Ld) return make_double2(0.0, 0.0);
-               const int src = gauss ? i : (i <= nx ? i : Ld - i);
-               return cmul(T[(src << TLs) + l], __ldg(p.chirp_i + i));
+               const cd v = gauss ? (i == 0 ? T[l] : vgauss(i, l)) : T[((i <= nx ? i : Ld - i) << TLs) + l];
+               return cmul(v, __ldg(p.chirp_i + i));
              },
-             [&](int q, int l, cd v) {
-               if (q >= (gauss ? N : N)) return;
-               const cd x = cmul(v, __ldg(p.chirp_i + q));
-               const int row = gauss ? sigma(q, N) : q;
-               T[(row << TLs) + l] = cscale(gauss ? sc : 0.5 * sc, x);
+             [&](int n1, int q, int l, auto& v) {
+               constexpr int R = sizeof(v) / sizeof(cd);
+#pragma unroll
+               for (int kk = 0; kk < R; ++kk) {
+                 const int qq = n1 + q * kk;
+                 if (qq >= N) continue;
+                 const cd x = cmul(v[kk], __ldg(p.chirp_i + qq));
+                 T[((gauss ? sigma(qq, N) : qq) << TLs) + l] = cscale(gauss ? sc : 0.5 * sc, x);
+               }
              });
   }
   wall_store(T, &tout, N, box_out, TL, l0);

@@ -75,13 +75,19 @@ def primitive_root(p: int) -> int:
 
 
 def stages_for(M: int) -> list:
-    """Radix of each pass (largest first), at most 4 bits per pass, balanced."""
+    """Radix of each pass: radix 16 first (the first and last passes bound
+    the lines a CTA can take: M / R1 butterflies per line), the remaining
+    bits in balanced passes of at most 4 bits."""
     m = M.bit_length() - 1
     if m == 0:
         return [1]
-    nst = -(-m // 4)
-    base, extra = divmod(m, nst)
-    return [2 ** (base + 1)] * extra + [2 ** base] * (nst - extra)
+    first = min(4, m)
+    rest = m - first
+    if rest == 0:
+        return [2 ** first]
+    nst = -(-rest // 4)
+    base, extra = divmod(rest, nst)
+    return [2 ** first] + [2 ** (base + 1)] * extra + [2 ** base] * (nst - extra)
 
 
 def digit_reversal(radices) -> np.ndarray:
