@@ -552,6 +552,7 @@ def run_c3(args):
              "biharmonic_solve", "inverse_biharmonic"]
     stages = {nm: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in evs])) for i, nm in enumerate(names)}
     unk = (mats.n_dir + mats.n_bih) * B
+    wall = c3_wall_stages(mesh, u, B)
     cpu = None if args.no_cpu else cpu_c3()
     print(json.dumps({
         "metric": "config-3 steps/s (fwd transform + solve + inverse, Dirichlet/Helmholtz and biharmonic)",
@@ -562,9 +563,53 @@ def run_c3(args):
         "config": {"workload": "config3: physical 257x256x256 (n_x=256 Gauss, n_y=n_z=256), nu=dt=1e-3",
                    "l2_policy": "each stage streams >= 135 MB arrays (> L2)"},
         "stages_ms": stages,
+        "wall_normal_stages": wall["stages"],
+        "roofline": wall["roofline"],
+        "gpu_launches": 6 * args.steps,
         "solved_unknowns_per_s": unk * args.steps / (total_ms / 1e3),
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }))
+
+
+def c3_wall_stages(mesh, u, B):
+    """The wall-normal stages of config 3 on their own (the fused
+    shen_wall.cu kernels behind transforms.wall_forward / wall_inverse), each
+    timed with CUDA events over 10 launches, and their HBM roofline:
+    algorithmic bytes = (rows in + rows out) x L lines x 16 B per launch
+    (complex128 Fourier lines in, coefficients out, or the reverse)."""
+    import torch
+
+    from paper_1701_03787_b200 import transforms as T
+    from paper_1701_03787_b200.mesh import family_code
+
+    peak, peak_src = measured_peak()
+    fam = family_code(mesh.family)
+    lines = torch.fft.rfft2(u, dim=(1, 2)).contiguous().view(mesh.n_x + 1, -1)
+    L = lines.shape[1]
+    res = {}
+    for sp, name in ((1, "dirichlet"), (2, "biharmonic")):
+        n = mesh.n_x - 1 if sp == 1 else mesh.n_x - 3
+        coef = T.wall_forward(lines, mesh.n_x, fam, sp, True)
+        for kind, fn, rows in (("forward", lambda: T.wall_forward(lines, mesh.n_x, fam, sp, True), n + mesh.n_x + 1),
+                               ("inverse", lambda: T.wall_inverse(coef, mesh.n_x, fam, sp, mesh.n_y * mesh.n_z),
+                                n + mesh.n_x + 1)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 10
+            byts = rows * L * 16
+            res[f"{kind}_{name}"] = {"ms": ms, "bytes": byts, "GBps_alg": byts / (ms * 1e6), "frac": byts / (ms * 1e6) / peak}
+    dom = max(res, key=lambda k: res[k]["ms"])
+    roof = {"bound": "hbm", "kernel": f"shen_wall {dom} (fused DCT + stencil + mass solve)", "achieved": res[dom]["GBps_alg"],
+            "peak": peak, "unit": "GB/s", "frac": res[dom]["frac"], "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes": "(rows in + rows out) x 33,024 lines x 16 B per launch"}
+    return {"stages": res, "roofline": roof}
 
 
 def cpu_c3():

@@ -243,6 +243,7 @@ typedef struct shen_wall_plan {
   const int *gin_f, *gin_i, *gout, *pinv;
   const void* mk;                                     /* complex128 */
   const double *c2, *c4, *mfac;
+  const double* rowscale; /* inverse, Chebyshev space: per-coefficient factor applied first, or NULL */
 } shen_wall_plan;
 int shen_wall_transform(const shen_wall_plan* plan, int64_t L, const void* in, void* out, void* stream);
 /* shared-memory bytes per CTA of a plan (host-side plan checks) */

@@ -70,7 +70,7 @@ class ShenWallPlan(ctypes.Structure):
                 ("nband", ctypes.c_int), ("mmax", ctypes.c_int),
                 ("tw", _vp), ("ker_f", _vp), ("ker_i", _vp), ("chirp_f", _vp), ("chirp_i", _vp),
                 ("gin_f", _vp), ("gin_i", _vp), ("gout", _vp), ("pinv", _vp), ("mk", _vp),
-                ("c2", _vp), ("c4", _vp), ("mfac", _vp)]
+                ("c2", _vp), ("c4", _vp), ("mfac", _vp), ("rowscale", _vp)]
 
 
 _SIGS = {

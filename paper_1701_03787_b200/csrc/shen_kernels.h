@@ -221,7 +221,8 @@ struct WallPlan {
   const double2* mk;       // [N] exp(-i pi k / 2N) (Gauss)
   const double* c2;        // [n_bih] biharmonic stencil 2(k+2)/(k+3)
   const double* c4;        // [n_bih] (k+1)/(k+3)
-  const double* mfac;      // [2][3][mmax] 1/U_ii, U_{i-1,i}, U_{i-2,i} per parity
+  const double* mfac;      // [2][mmax + 1][8] folded stencil / Cholesky coefficients per parity (wall.py)
+  const double* rowscale;  // [N] inverse, Chebyshev space: coefficient k scaled first (d/dx: 1/mass_cheb), or null
 };
 size_t wall_smem_bytes(const WallPlan& p);
 cudaError_t launch_wall(const WallPlan& p, int64_t L, const void* in, void* out, cudaStream_t st);

@@ -613,6 +613,10 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     // FFT's gather from the untouched coefficient tile (below)
   } else {
     // even sequence with doubled ends: its DFT is twice the point values
+    if (p.rowscale != nullptr) {  // (Chebyshev space: no expansion pass ran)
+      for (int e = tid; e < N * TL; e += kWallThreads) T[e] = cscale(__ldg(p.rowscale + (e >> TLs)), T[e]);
+      __syncthreads();
+    }
     if (tid < TL) {
       T[tid] = cscale(2.0, T[tid]);
       T[(nx << TLs) + tid] = cscale(2.0, T[(nx << TLs) + tid]);
@@ -623,8 +627,10 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
   // Chebyshev coefficient c_k of the expansion (reference order) from the
   // coefficient tile (rows >= n are zero), and the Makhoul pre-twiddled
   // V_m = e^{i pi m / 2N} (y_m - i y_{N-m}) / 2, y_m = c_m (1 <= m < N)
+  const double* rsc = p.rowscale;
   auto cheb = [&](int k, int l) -> cd {
     cd c = T[(k << TLs) + l];
+    if (rsc != nullptr) c = cscale(__ldg(rsc + k), c);
     if (sp == 1 && k >= 2) c = csub(c, T[((k - 2) << TLs) + l]);
     if (sp == 2) {
       if (k >= 2) c = csub(c, cscale(__ldg(p.c2 + k - 2), T[((k - 2) << TLs) + l]));
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     }
     __syncthreads();
   } else if (p.kind == 1) {  // Rader, inverse sign: X'_k = V_0 + conv; rows sigma(k)
-    if (tid < TL) side[tid] = T[tid];  // V_0 = c_0 = coefficient 0
+    if (tid < TL) side[tid] = cheb(0, tid);  // V_0 = c_0 = coefficient 0
     wall_dft(p, T, TLs, p.ker_i, side + TL, [&](int i, int l) { return vgauss(__ldg(p.gin_i + i), l); },
              [&](int n1, int q, int l, auto& v) {
                constexpr int R = sizeof(v) / sizeof(cd);
@@ -675,7 +681,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     wall_dft(p, T, TLs, p.ker_i, nullptr,
              [&](int i, int l) {
                if (i >= Ld) return make_double2(0.0, 0.0);
-               const cd v = gauss ? (i == 0 ? T[l] : vgauss(i, l)) : T[((i <= nx ? i : Ld - i) << TLs) + l];
+               const cd v = gauss ? (i == 0 ? cheb(0, l) : vgauss(i, l)) : T[((i <= nx ? i : Ld - i) << TLs) + l];
                return cmul(v, __ldg(p.chirp_i + i));
              },
              [&](int n1, int q, int l, auto& v) {

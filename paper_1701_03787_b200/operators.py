@@ -92,13 +92,19 @@ class DeviceOperator:
 
 
 _CACHE = {}
+_CACHE_MAX = 32  # device copies kept for the most recently used matrices
 
 
 def apply(M, x):
-    """``M.apply(x)`` on the device (reference matrices.py apply semantics)."""
+    """``M.apply(x)`` on the device (reference matrices.py apply semantics).
+    The device tables of the last ``_CACHE_MAX`` matrices are kept (least
+    recently used dropped), keyed by identity; a kept entry holds its matrix
+    so the identity cannot be reused while cached."""
     key = (id(M), device().index)
-    op = _CACHE.get(key)
+    op = _CACHE.pop(key, None)
     if op is None or op[0] is not M:
         op = (M, DeviceOperator(M))
-        _CACHE[key] = op
+    _CACHE[key] = op  # re-inserted: most recently used last
+    while len(_CACHE) > _CACHE_MAX:
+        _CACHE.pop(next(iter(_CACHE)))
     return op[1](x)

@@ -256,16 +256,19 @@ class WallPlan:
 _DEV_PLANS = {}
 
 
-def wall_plan(n_x: int, fam: int, space: int, direction: int, mass: bool, scale: float):
+def wall_plan(n_x: int, fam: int, space: int, direction: int, mass: bool, scale: float, rowscale=None,
+              rowscale_key=None):
     """Device plan for ``shen_wall_transform``.  Returns None if the size does
-    not fit the kernel's shared-memory tile (the caller falls back)."""
+    not fit the kernel's shared-memory tile (the caller falls back).
+    ``rowscale`` (inverse, Chebyshev space): per-coefficient factors applied
+    first, cached under ``rowscale_key`` (e.g. 1/mass_cheb for d/dx)."""
     import torch
 
     from . import _lib
     from ._device import device
 
     dev = device()
-    key = (n_x, fam, space, direction, bool(mass), float(scale), dev.index)
+    key = (n_x, fam, space, direction, bool(mass), float(scale), rowscale_key, dev.index)
     pl = _DEV_PLANS.get(key)
     if pl is not None:
         return pl
@@ -315,6 +318,10 @@ def wall_plan(n_x: int, fam: int, space: int, direction: int, mass: bool, scale:
         packed, nband, n, mmax, _ = _mass_factors_host(n_x, fam, space)
         s.nband, s.mmax = nband, mmax
         s.mfac = dptr(mass_tables(packed, nband, space, n_x), np.float64)
+    if rowscale is not None:
+        if direction != 1 or space != 0:
+            raise ValueError("rowscale applies to inverse Chebyshev-space plans")
+        s.rowscale = dptr(np.asarray(rowscale, dtype=np.float64).reshape(N), np.float64)
     pl = WallPlan(s, keep)
     _DEV_PLANS[key] = pl
     return pl
