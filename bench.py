@@ -48,7 +48,7 @@ def parse():
                     help="CPU check of the multi-rank launch: gloo ranks, folded slabs, max-over-ranks "
                          "timing, oracle solves instead of the device (no GPU needed; not a bench number)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--method", default="stream", choices=["stream", "cr", "chunked", "stored", "tile"])
+    ap.add_argument("--method", default="stream", choices=["stream", "stored"])
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the timed step from a CUDA graph (auto: launch-bound sizes only)")
     return ap.parse_args()

@@ -67,17 +67,16 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  * shen_helm_factor: sequential unpivoted elimination per (system, parity).
  *   exact != 0 -> reference evaluation order and IEEE division (bit-equal
  *   factors); exact == 0 -> reciprocal/FMA arithmetic shared with the
- *   chunked solve.  Outputs are optional (NULL to skip):
+ *   streaming solve.  Outputs are optional (NULL to skip):
  *     factors[8] = {low_p0, low_p1, d_p0, d_p1, e_p0, e_p1, tail_p0, tail_p1}
  *                  device arrays (rows_p - 1 or rows_p, batch);
  *     ckpt       = [C][2][3][batch] factor state entering each chunk of
  *                  chunk_rows rows (C = ceil(rows_p0 / chunk_rows));
  *     pivot_dev  = int[2]; atomic-min of the first row (within parity) whose
  *                  pivot has |d| < 1e-300 (reset it first).
- * shen_helm_solve_chunked: fused factor+solve from the checkpoints
- *   (requires 32 * chunk_rows >= rows_p0; ckpt made with exact == 0).
- * shen_helm_solve_stream: same inputs as the chunked solve (chunk_rows in
- *   {4, 8, 16}); one thread per system with coalesced row access; y is
+ * shen_helm_solve_stream: fused factor+solve from the checkpoints (ckpt made
+ *   with exact == 0, chunk_rows in {4, 8, 16}); one thread per (system,
+ *   parity) with coalesced row access; y is
  *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
  *   bytes) and recomputed in the backward sweep; warps_per_sm selects the
  *   persistent CTA size (8 or 12 warps per SM; 0 = the per-operator default,
@@ -93,44 +92,10 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
 int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
                      const double* md, int chunk_rows, double* ckpt, double* const* factors, int exact,
                      int* pivot_dev, void* stream);
-int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                            const double* st, const double* md, int chunk_rows, const double* ckpt,
-                            const void* rhs, void* out, int is_complex, void* stream);
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
                            int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
-/* Column-resident Helmholtz solve (complex RHS): tiles of 8 consecutive
- * systems x all rows of one parity staged in shared memory by TMA, so the
- * RHS is read from HBM once and the solution written once; 32 chunks of
- * chunk_rows rows per (system, parity) are solved in parallel and coupled by
- * warp scans.  ckpt from shen_helm_factor(exact = 0) with the same
- * chunk_rows (a power of two <= 16 with 32 * chunk_rows >= rows of parity 0).
- * rhs/out 16-B aligned, not aliased.  max_ctas > 0 caps the persistent grid;
- * [j_begin, j_end) restricts the solve to a range of systems (j_end < 0: the
- * whole batch; row pitch stays `batch`) for pipelined host copies.
- * Replaces HelmholtzLU.solve (solvers.py:100-126). */
-int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                       const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out, int max_ctas,
-                       int64_t j_begin, int64_t j_end, void* stream);
-/* Same Helmholtz solve with systems taken in mirror pairs (the layout of
- * shen_bih_solve_stream_pairs below): one thread runs the factor recurrence
- * once for both right-hand sides and reads the checkpoints once for two
- * systems.  warps_per_sm 4 / 6 / 8 selects the CTA size (0: the default).
- * Results are bit-identical to shen_helm_solve_stream.  Replaces
- * the reference's HelmholtzLU.solve (solvers.py:100-126) for channel grids. */
-int shen_helm_solve_stream_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                                 const double* st, const double* md, int chunk_rows, const double* ckpt,
-                                 const void* rhs, void* out, void* scratch, int is_complex, const int64_t* pairs,
-                                 int64_t n_pairs, int warps_per_sm, int max_ctas, void* stream);
-/* Tiled chunk-parallel solve: a CTA holds 4 consecutive systems (all rows)
- * in shared memory, warps = (system, parity), lanes = 32 chunks of
- * chunk_rows rows; the RHS is read once.  Same inputs as
- * shen_helm_solve_chunked (ckpt from shen_helm_factor with the same
- * chunk_rows, exact == 0); chunk_rows <= 16. */
-int shen_helm_solve_tile(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                         const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                         int is_complex, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 
@@ -151,9 +116,6 @@ int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factor
 int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                     const double* tab, int chunk_rows, double* ckpt, double* const* factors, int exact,
                     int* pivot_dev, void* stream);
-int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
-                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                           int is_complex, void* stream);
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                           void* scratch, int is_complex, int warps_per_sm, int max_ctas, int64_t j_begin,
@@ -168,17 +130,6 @@ int shen_bih_solve_stream_pairs(int n_bih, double xi0, const double* xi1, const 
                                 const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
                                 void* scratch, int is_complex, const int64_t* pairs, int64_t n_pairs, int max_ctas,
                                 void* stream);
-/* Same solve, complex RHS on a channel grid of (grid_ny, grid_nzh)
- * wavenumbers (batch = grid_ny * grid_nzh), with the pair table warp-aligned:
- * each run of 32 items holds 32 consecutive kz columns of one (m, -m) row
- * pair, padding items are -1 in both halves.  The RHS segments are fetched
- * by TMA (one tensor-map box per warp, system stream and segment) instead of
- * per-thread cp.async.  Results are bit-identical to
- * shen_bih_solve_stream_pairs. */
-int shen_bih_solve_stream_pairs_grid(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
-                                     const double* tab, int chunk_rows, const double* ckpt, const void* rhs,
-                                     void* out, void* scratch, const int64_t* pairs, int64_t n_pairs,
-                                     int64_t grid_ny, int64_t grid_nzh, int max_ctas, void* stream);
 int shen_bih_solve_stored(int n_bih, int64_t batch, double xi0, const double* q, const double* s,
                           const double* const* factors, const void* rhs, void* out, int is_complex,
                           void* stream);
@@ -332,7 +283,7 @@ int shen_recover_velocity(const shen_recover_args* args, void* stream);
 
 /* ---------------------------------------------------------------------
  * Nonlinear term H = u x omega (reference stepper.py:148-185), pointwise
- * pieces; the transforms around them are wall-normal GEMMs + cuFFT.
+ * pieces; the transforms around them are shen_wall_transform + cuFFT.
  * shen_scale_lines: y[r][l] = c_l x[r][l] for rows x L complex128
  *   ((c.re x.re - c.im x.im, c.re x.im + c.im x.re), every product rounded);
  *   c = c_re + i c_im per line (1j m, 1j n, mask: exact either way).
@@ -344,25 +295,6 @@ int shen_recover_velocity(const shen_recover_args* args, void* stream);
 int shen_scale_lines(int64_t rows, int64_t L, const void* x, const double* c_re, const double* c_im, void* y,
                      void* stream);
 int shen_cross(int64_t n, const double* fields, double* h, void* stream);
-/* Paired form (wall-normal points j and N-1-j are mirror images, x -> -x):
- * every input field is given as [P + Q rows][M points], P = ceil(N/2),
- * Q = floor(N/2), by parts e (rows 0..P-1) and o (rows P..P+Q-1) with
- *   f_j = e_j + o_j,  f_{N-1-j} = e_j - o_j  (j < Q),  f_Q = e_Q (centre, P = Q+1);
- * h is written in the same layout as sums and differences of the two
- * points' values: rows j < Q: h_j + h_{N-1-j}, row Q: h_Q, rows P + j:
- * h_j - h_{N-1-j}. */
-int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, void* stream);
-/* The pairing alone, for the 3-D transforms (x: N = P + Q rows of M doubles;
- * y: the [P + Q][M] sum / difference form above):
- * shen_pair_split: y = (x_j + x_{N-1-j}, centre, x_j - x_{N-1-j});
- * shen_pair_merge: the inverse map with e, o as in the paired form,
- * x_j = e_j + o_j, x_{N-1-j} = e_j - o_j.  M even, pointers 16-B aligned
- * (rows of complex128 values), P <= 65535. */
-int shen_pair_split(int64_t P, int64_t Q, int64_t M, const double* x, double* y, void* stream);
-int shen_pair_merge(int64_t P, int64_t Q, int64_t M, const double* y, double* x, void* stream);
-/* shen_scale_lines with row strides (in elements) for x and y. */
-int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
-                    const double* c_im, void* y, int64_t y_row_stride, void* stream);
 
 #ifdef __cplusplus
 }

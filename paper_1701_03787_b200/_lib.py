@@ -82,34 +82,20 @@ _SIGS = {
     "shen_stream_scratch_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int]),
     "shen_helm_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                         ctypes.c_int, _vp, _pp, ctypes.c_int, _vp, _vp]),
-    "shen_helm_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                               ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_helm_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
                                               ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_int, _c_int64, _c_int64, _vp]),
-    "shen_helm_solve_stream_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                                    ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _c_int64,
-                                                    ctypes.c_int, ctypes.c_int, _vp]),
     "shen_wall_transform": (ctypes.c_int, [ctypes.POINTER(ShenWallPlan), _c_int64, _vp, _vp, _vp]),
     "shen_wall_smem_bytes": (ctypes.c_int64, [ctypes.POINTER(ShenWallPlan)]),
-    "shen_helm_solve_cr": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                          ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
-    "shen_helm_solve_tile": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                            ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp, ctypes.c_int,
                                        _vp, _pp, ctypes.c_int, _vp, _vp]),
-    "shen_bih_solve_chunked": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
-                                              ctypes.c_int, _vp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_solve_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
                                              ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_bih_solve_stream_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
                                                    ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, _c_int64,
                                                    ctypes.c_int, _vp]),
-    "shen_bih_solve_stream_pairs_grid": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp,
-                                                        ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _c_int64, _c_int64,
-                                                        _c_int64, ctypes.c_int, _vp]),
     "shen_bih_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, ctypes.c_double, _vp, _vp, _pp, _vp, _vp,
                                              ctypes.c_int, _vp]),
     "shen_apply_banded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_int, _vp, _vp, _vp, _vp,
@@ -123,10 +109,6 @@ _SIGS = {
     "shen_recover_velocity": (ctypes.c_int, [ctypes.POINTER(ShenRecoverArgs), _vp]),
     "shen_scale_lines": (ctypes.c_int, [_c_int64, _c_int64, _vp, _vp, _vp, _vp, _vp]),
     "shen_cross": (ctypes.c_int, [_c_int64, _vp, _vp, _vp]),
-    "shen_cross_paired": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
-    "shen_pair_split": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
-    "shen_pair_merge": (ctypes.c_int, [_c_int64, _c_int64, _c_int64, _vp, _vp, _vp]),
-    "shen_scale_rows": (ctypes.c_int, [_c_int64, _c_int64, _vp, _c_int64, _vp, _vp, _vp, _c_int64, _vp]),
     "shen_xform_extend": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _c_int64, _vp, _vp, _vp]),
     "shen_xform_fwd_post": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_int64, ctypes.c_double,
                                            _vp, _vp, _vp, _vp]),

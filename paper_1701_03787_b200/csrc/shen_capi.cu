@@ -88,20 +88,6 @@ int shen_helm_factor(int n_dir, double ca, const double* cb, int64_t batch, cons
   return cuda_check(shen::launch_helm_factor(a, exact != 0, S(stream)), "shen_helm_factor");
 }
 
-int shen_helm_solve_chunked(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                            const double* st, const double* md, int chunk_rows, const double* ckpt,
-                            const void* rhs, void* out, int is_complex, void* stream) {
-  if (batch == 0) return SHEN_OK;
-  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: bad args");
-  const int rows0 = (n_dir + 1) / 2;
-  if (chunk_rows <= 0 || 32LL * chunk_rows < rows0) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: chunk_rows");
-  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: ckpt required");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_chunked: rhs must not alias out");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
-  return cuda_check(shen::launch_helm_chunk(a, is_complex != 0, S(stream)), "shen_helm_solve_chunked");
-}
-
 int shen_wall_transform(const shen_wall_plan* plan, int64_t L, const void* in, void* out, void* stream) {
   if (!plan) return fail(SHEN_ERR_ARG, "shen_wall_transform: plan");
   if (L == 0) return SHEN_OK;
@@ -119,26 +105,6 @@ int shen_wall_transform(const shen_wall_plan* plan, int64_t L, const void* in, v
 int64_t shen_wall_smem_bytes(const shen_wall_plan* plan) {
   if (!plan) return -1;
   return (int64_t)shen::wall_smem_bytes(*reinterpret_cast<const shen::WallPlan*>(plan));
-}
-
-int shen_helm_solve_cr(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                       const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out, int max_ctas,
-                       int64_t j_begin, int64_t j_end, void* stream) {
-  if (batch == 0) return SHEN_OK;
-  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: bad args");
-  const int rows0 = (n_dir + 1) / 2;
-  if (chunk_rows <= 0 || chunk_rows > 16 || (chunk_rows & (chunk_rows - 1)) || 32LL * chunk_rows < rows0)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: chunk_rows");
-  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: ckpt required");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs must not alias out");
-  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: max_ctas");
-  if (j_end < 0) j_end = batch;
-  if (j_begin < 0 || j_begin > j_end || j_end > batch) return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: range");
-  if ((reinterpret_cast<uintptr_t>(rhs) | reinterpret_cast<uintptr_t>(out)) & 15)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_cr: rhs/out must be 16-B aligned");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end, max_ctas};
-  return cuda_check(shen::launch_helm_cr(a, S(stream)), "shen_helm_solve_cr");
 }
 
 int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
@@ -159,64 +125,6 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
   shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, j_begin, j_end, max_ctas};
   return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
                     "shen_helm_solve_stream");
-}
-
-int shen_bih_solve_stream_pairs_grid(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
-                                     const double* tab, int chunk_rows, const double* ckpt, const void* rhs,
-                                     void* out, void* scratch, const int64_t* pairs, int64_t n_pairs,
-                                     int64_t grid_ny, int64_t grid_nzh, int max_ctas, void* stream) {
-  if (batch == 0 || n_pairs == 0) return SHEN_OK;
-  if (n_bih < 2 || batch < 0 || n_pairs < 0 || !xi1 || !xi2 || !tab || !rhs || !out || !pairs || grid_ny < 1 ||
-      grid_nzh < 1 || grid_ny * grid_nzh != batch || n_pairs % 32 != 0)
-    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: bad args");
-  const int rows0 = (n_bih + 1) / 2;
-  if (chunk_rows != 8) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: chunk_rows");
-  if (rows0 > chunk_rows && (!ckpt || !scratch))
-    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: ckpt/scratch");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: rhs must not alias out");
-  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: max_ctas");
-  if ((reinterpret_cast<uintptr_t>(rhs) & 15) != 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs_grid: rhs alignment");
-  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
-  a.pairs = pairs;
-  a.n_pairs = n_pairs;
-  a.grid_ny = grid_ny;
-  a.grid_nzh = grid_nzh;
-  return cuda_check(shen::launch_bih_stream(a, scratch, true, 8, S(stream)), "shen_bih_solve_stream_pairs_grid");
-}
-
-int shen_helm_solve_stream_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                                 const double* st, const double* md, int chunk_rows, const double* ckpt,
-                                 const void* rhs, void* out, void* scratch, int is_complex, const int64_t* pairs,
-                                 int64_t n_pairs, int warps_per_sm, int max_ctas, void* stream) {
-  if (batch == 0 || n_pairs == 0) return SHEN_OK;
-  if (n_dir < 2 || batch < 0 || n_pairs < 0 || n_pairs > batch || !cb || !sd || !st || !md || !rhs || !out || !pairs)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: bad args");
-  const int rows0 = (n_dir + 1) / 2;
-  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: chunk_rows");
-  if (rows0 > chunk_rows && (!ckpt || !scratch)) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: ckpt/scratch");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: rhs must not alias out");
-  if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: max_ctas");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out, 0, -1, max_ctas};
-  a.pairs = pairs;
-  a.n_pairs = n_pairs;
-  if (warps_per_sm != 0 && warps_per_sm != 4 && warps_per_sm != 6 && warps_per_sm != 8)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_stream_pairs: warps_per_sm");
-  return cuda_check(shen::launch_helm_stream(a, scratch, is_complex != 0, warps_per_sm, S(stream)),
-                    "shen_helm_solve_stream_pairs");
-}
-
-int shen_helm_solve_tile(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                         const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                         int is_complex, void* stream) {
-  if (batch == 0) return SHEN_OK;
-  if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out || chunk_rows <= 0 || chunk_rows > 16 ||
-      32 * chunk_rows < (n_dir + 1) / 2 || (!ckpt && (n_dir + 1) / 2 > chunk_rows))
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_tile: bad args (needs 32 * chunk_rows >= rows of parity 0, chunk_rows <= 16)");
-  shen::HelmChunkArgs a{};
-  a.n_dir = n_dir; a.ca = ca; a.cb = cb; a.batch = batch; a.sd = sd; a.st = st; a.md = md;
-  a.chunk_rows = chunk_rows; a.ckpt = ckpt; a.rhs = rhs; a.out = out;
-  return cuda_check(shen::launch_helm_tile(a, is_complex != 0, S(stream)), "shen_helm_solve_tile");
 }
 
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
@@ -250,20 +158,6 @@ int shen_bih_factor(int n_bih, double xi0, const double* xi1, const double* xi2,
     a.b[p] = factors ? factors[12 + p] : nullptr;
   }
   return cuda_check(shen::launch_bih_factor(a, exact != 0, S(stream)), "shen_bih_factor");
-}
-
-int shen_bih_solve_chunked(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
-                           const double* tab, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                           int is_complex, void* stream) {
-  if (batch == 0) return SHEN_OK;
-  if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
-    return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: bad args");
-  const int rows0 = (n_bih + 1) / 2;
-  if (chunk_rows <= 0 || 32LL * chunk_rows < rows0) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: chunk_rows");
-  if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: ckpt required");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_chunked: rhs must not alias out");
-  shen::BihChunkArgs a{n_bih, xi0, xi1, xi2, batch, tab, chunk_rows, ckpt, rhs, out};
-  return cuda_check(shen::launch_bih_chunk(a, is_complex != 0, S(stream)), "shen_bih_solve_chunked");
 }
 
 int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double* xi2, int64_t batch,
@@ -444,33 +338,6 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream) {
   if (n == 0) return SHEN_OK;
   if (n < 0 || !fields || !h) return fail(SHEN_ERR_ARG, "shen_cross: bad args");
   return cuda_check(shen::launch_cross(n, fields, h, S(stream)), "shen_cross");
-}
-
-int shen_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, void* stream) {
-  if (P == 0 || M == 0) return SHEN_OK;
-  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !fields || !h) return fail(SHEN_ERR_ARG, "shen_cross_paired: bad args");
-  return cuda_check(shen::launch_cross_paired(P, Q, M, fields, h, S(stream)), "shen_cross_paired");
-}
-
-int shen_pair_split(int64_t P, int64_t Q, int64_t M, const double* x, double* y, void* stream) {
-  if (P == 0 || M == 0) return SHEN_OK;
-  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !x || !y) return fail(SHEN_ERR_ARG, "shen_pair_split: bad args");
-  return cuda_check(shen::launch_pair(false, P, Q, M, x, y, S(stream)), "shen_pair_split");
-}
-
-int shen_pair_merge(int64_t P, int64_t Q, int64_t M, const double* y, double* x, void* stream) {
-  if (P == 0 || M == 0) return SHEN_OK;
-  if (P < 0 || M < 0 || Q < 0 || Q > P || P - Q > 1 || !x || !y) return fail(SHEN_ERR_ARG, "shen_pair_merge: bad args");
-  return cuda_check(shen::launch_pair(true, P, Q, M, y, x, S(stream)), "shen_pair_merge");
-}
-
-int shen_scale_rows(int64_t rows, int64_t L, const void* x, int64_t x_row_stride, const double* c_re,
-                    const double* c_im, void* y, int64_t y_row_stride, void* stream) {
-  if (rows == 0 || L == 0) return SHEN_OK;
-  if (rows < 0 || L < 0 || x_row_stride < L || y_row_stride < L || !x || !c_re || !c_im || !y)
-    return fail(SHEN_ERR_ARG, "shen_scale_rows: bad args");
-  return cuda_check(shen::launch_scale_rows(rows, L, x, x_row_stride, c_re, c_im, y, y_row_stride, S(stream)),
-                    "shen_scale_rows");
 }
 
 int shen_recover_velocity(const shen_recover_args* r, void* stream) {

@@ -71,7 +71,7 @@ struct BihSeqArgs {
   void* out;
 };
 
-// Chunk-parallel fused solve: factors recomputed from checkpoints.
+// Streaming fused solve: factors recomputed from checkpoints.
 struct HelmChunkArgs {
   int n_dir;
   double ca;
@@ -86,9 +86,6 @@ struct HelmChunkArgs {
   void* out;
   int64_t jb = 0, je = -1;  // system range [jb, je) of the streaming solve (je < 0: whole batch)
   int max_ctas = 0;          // streaming solve: cap on persistent CTAs (0: one per SM)
-  // mirror pairs (stream solve, as BihChunkArgs): nullptr = one system per thread
-  const int64_t* pairs = nullptr;
-  int64_t n_pairs = 0;
 };
 
 struct BihChunkArgs {
@@ -109,29 +106,18 @@ struct BihChunkArgs {
   // equal entries mark an unpaired system.  nullptr: one system per thread.
   const int64_t* pairs = nullptr;
   int64_t n_pairs = 0;
-  // > 0: pairs is warp-aligned (32 consecutive kz columns of one row pair per
-  // warp, -1 padding) over a (grid_ny, grid_nzh) channel grid -- TMA-fed kernel
-  int64_t grid_ny = 0, grid_nzh = 0;
 };
 
 cudaError_t launch_helm_factor(const HelmFactorArgs& a, bool exact, cudaStream_t st);
 cudaError_t launch_bih_factor(const BihFactorArgs& a, bool exact, cudaStream_t st);
 cudaError_t launch_helm_seq(const HelmSeqArgs& a, bool complex_rhs, cudaStream_t st);
 cudaError_t launch_bih_seq(const BihSeqArgs& a, bool complex_rhs, cudaStream_t st);
-cudaError_t launch_helm_chunk(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
-cudaError_t launch_bih_chunk(const BihChunkArgs& a, bool complex_rhs, cudaStream_t st);
 // streaming sequential solve (lanes = systems); warps_per_sm bounds the systems in flight
 cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
                                cudaStream_t st);
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
                               cudaStream_t st);
 int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
-// column-resident solves (shen_solve_cr.cu): complex RHS, RHS read once; ckpt made with chunk_rows = R
-cudaError_t launch_helm_cr(const HelmChunkArgs& a, cudaStream_t st);
-
-// tiled chunk-parallel Helmholtz solve (shen_solve_tile.cu); ckpt made with chunk_rows = R, 32 R >= rows_p0
-cudaError_t launch_helm_tile(const HelmChunkArgs& a, bool complex_rhs, cudaStream_t st);
-
 // structured apply along the rows (shen_apply.cu): kind 0 banded, 1 constant tail, 2 rank-2 tail
 cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const int* offs, const double* diag,
                          const double* tail, int tail_start, const double* d, const double* p, const double* q,
@@ -186,11 +172,6 @@ cudaError_t launch_recover(const RecoverArgs& a, cudaStream_t st);
 cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const double* cre, const double* cim, void* y,
                                cudaStream_t st);
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
-cudaError_t launch_cross_paired(int64_t P, int64_t Q, int64_t M, const double* fields, double* h, cudaStream_t st);
-cudaError_t launch_pair(bool merge, int64_t P, int64_t Q, int64_t M, const double* src, double* dst,
-                        cudaStream_t st);
-cudaError_t launch_scale_rows(int64_t rows, int64_t L, const void* x, int64_t xs, const double* cre,
-                              const double* cim, void* y, int64_t ys, cudaStream_t st);
 
 // fused wall-normal transforms (shen_wall.cu); tables built on the host (wall.py)
 struct WallPlan {

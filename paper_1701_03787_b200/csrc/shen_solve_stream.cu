@@ -27,15 +27,13 @@
 // Kernels: helm_stream_kernel / bih_stream_kernel (one system per thread);
 // bih_pair_kernel (default for channel grids: mirror pairs (m, n) / (-m, n)
 // share one factor recurrence, y checkpoints of the first 16 segments parked
-// in tensor memory; an optional TMA-fed variant); helm_pair_kernel (mirror
-// pairs for the Helmholtz, measured slower, off by default).
+// in tensor memory).  Variants measured slower (Helmholtz mirror pairs, a
+// bulk-tensor-fed pair kernel) were removed from the product; DESIGN.md
+// section 4.2 has their numbers.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
-#include <cuda.h>  // CUtensorMap
-#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
-#include <cstring>
 
 #include "shen_rows.cuh"
 #include "shen_kernels.h"
@@ -134,9 +132,6 @@ template <> __device__ __forceinline__ cplx szero<cplx>() { return {0.0, 0.0}; }
 // the backward) in TMEM instead of the L2-resident scratch.  Warp w owns lanes
 // 32 (w % 4) .. +31 (the 32x32b shape: thread = lane) and a column range
 // picked by w / 4.
-#ifndef SHEN_PAIR_ALIGN_GENERIC
-#define SHEN_PAIR_ALIGN_GENERIC 0
-#endif
 #ifndef SHEN_PAIR_TMEM_SEGS
 #define SHEN_PAIR_TMEM_SEGS 16
 #endif
@@ -204,41 +199,7 @@ __device__ __forceinline__ void tmem_get4(uint32_t a, V& v0, V& v1, V& v2, V& v3
   v3 = tunpackv<V>(w + 3 * W);
 }
 
-// ---------------------------------------------------------------- TMA + mbarrier
-// The pair kernel's complex RHS segments can come in by tensor-map bulk
-// copies: one 3-D box per warp, stream and segment (32 systems x 8 rows of
-// one parity -- the tensor's row dimension is traversed with element stride
-// 2), landing in the same [row][lane] ring layout the per-thread cp.async
-// path fills, completion tracked by one mbarrier per warp and ring slot.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
-      : "memory");
-}
 
 constexpr int kSG = 4;                    // 32-system groups per CTA (128 consecutive systems)
 constexpr int kStreamThreads = 64 * kSG;  // warp w: parity w & 1, system group w >> 1
@@ -312,7 +273,7 @@ __device__ __forceinline__ void seg_issue(V* slot, const V* rhs, SegRef ref, int
 // (parity 0 / 1 of the same 32 systems).  HBM traffic per unknown: 2 RHS
 // reads + 1 solution write (+ ~3 B of checkpoints).
 template <typename V, int R, int RING, int SG>
-__global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows, int hint) {
+__global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a, V* ychk, int tab_rows) {
   constexpr int kT = 64 * SG;
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem[];
@@ -347,18 +308,14 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
   int64_t qi = 0;
   int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
-  // L2 policy of the forward (first) and backward (second, last) RHS reads
-  // (hint: 0 none, 1 evict_last / evict_first, 2 - / evict_first, 3 evict_last / -)
-  const uint64_t pfwd = (hint == 1 || hint == 3) ? policy_evict_last() : 0;
-  const uint64_t pbwd = (hint == 1 || hint == 2) ? policy_evict_first() : 0;
   for (; qi < RING - 1; ++qi) {
-    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
   auto consume = [&]() -> const V* {
-    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane, it.k < nseg ? pfwd : pbwd);
+    if (qi < nq) seg_issue<V, R, SG>(ring + islot * R * 32, rhs, it.ref(nseg), n, par, B, ngroups, jb, je, sgi, lane);
     else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
@@ -453,208 +410,6 @@ __global__ void __launch_bounds__(64 * SG, 1) helm_stream_kernel(HelmChunkArgs a
         S = sadd(x1, S);
         x1 = x;
         if (jv && (full || s * R + r < n)) O::st_cs(outj + (int64_t)2 * (s * R + r) * B, x);
-      }
-    }
-  }
-  cpa_wait<0>();
-}
-
-// ======================================================================= Helmholtz, mirror pairs
-// Systems (m, n) and (-m, n) of a channel grid have bitwise-identical z2, so
-// their factors (cb, hence every d, e, tail) are bitwise identical.  One
-// thread runs the factor recurrence once for both right-hand sides, reads the
-// build's checkpoints once for two systems (3 -> 1.5 B per unknown) and
-// carries two y streams; every per-system operation is the one
-// helm_stream_kernel performs, so the results are bit-identical to it.
-// Warp w: parity w & 1, pair group w >> 1; the ring slot of a segment holds
-// R rows of the first system, then R rows of the second (y replaces b in
-// place in the backward sweep).
-template <typename V, int R, int RING, int SG>
-__global__ void __launch_bounds__(64 * SG, 1) helm_pair_kernel(HelmChunkArgs a, V* ychk, int tab_rows, int hint) {
-  constexpr int kT = 64 * SG;
-  using O = VOps<V>;
-  extern __shared__ __align__(16) double smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, par = warp & 1, sgi = warp >> 1;
-  const int64_t B = a.batch;
-  const int n = (a.n_dir - par + 1) / 2;
-  const int nseg = (n + R - 1) / R;
-  V* ring = reinterpret_cast<V*>(smem) + (size_t)warp * RING * 2 * R * 32 + lane;
-  const V* rhs = static_cast<const V*>(a.rhs);
-  V* out = static_cast<V*>(a.out);
-  double4* tab = reinterpret_cast<double4*>(smem + (size_t)kT / 32 * RING * 2 * R * 32 * VOps<V>::ndouble);
-  for (int idx = tid; idx < 2 * tab_rows; idx += kT) {
-    const int p = idx / tab_rows, i = idx - p * tab_rows;
-    const int np = (a.n_dir - p + 1) / 2;
-    const int nsp = (a.n_dir - 2 - p + 1) / 2 > 0 ? (a.n_dir - 2 - p + 1) / 2 : 0;
-    double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (i < np) {
-      const int k = p + 2 * i;
-      v = make_double4(__ldg(a.sd + k), __ldg(a.st + k), __ldg(a.md + k), i < nsp ? 1.0 : 0.0);
-    }
-    tab[idx] = v;
-  }
-  __syncthreads();
-  const double4* mytab = tab + par * tab_rows;
-  const int64_t P = a.n_pairs;
-  const int64_t* pa = a.pairs;
-  const int64_t* pb = a.pairs + P;
-  const int64_t ngroups = (P + 32 * SG - 1) / (32 * SG);
-  const int64_t g0 = blockIdx.x, gstride = gridDim.x;
-  if (g0 >= ngroups) return;
-  const int64_t nq = ((ngroups - g0 + gstride - 1) / gstride) * 2 * nseg;
-  const uint64_t pfwd = (hint == 1 || hint == 3) ? policy_evict_last() : 0;
-  const uint64_t pbwd = (hint == 1 || hint == 2) ? policy_evict_first() : 0;
-  auto issue = [&](V* slot, SegRef ref, uint64_t pol) {
-    if (ref.g < ngroups) {
-      const int64_t c = ref.g * (32 * SG) + sgi * 32 + lane;
-      const bool cv = c < P;
-      const int64_t cc = cv ? c : P - 1;
-      const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
-      const int rows = min(R, n - ref.s * R);
-      const int64_t step = 2 * B;
-      const V* p0 = rhs + (int64_t)(par + 2 * ref.s * R) * B + ja;
-      const V* p1 = rhs + (int64_t)(par + 2 * ref.s * R) * B + jb2;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const bool ok = cv && r < rows;
-        if (pol) {
-          cpa_ef(slot + r * 32, p0, ok, pol);
-          cpa_ef(slot + (R + r) * 32, p1, ok, pol);
-        } else {
-          cpa(slot + r * 32, p0, ok);
-          cpa(slot + (R + r) * 32, p1, ok);
-        }
-        if (r + 1 < rows) {
-          p0 += step;
-          p1 += step;
-        }
-      }
-    }
-    cpa_commit();
-  };
-  int64_t qi = 0;
-  int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
-  SegIt it{g0, 0};
-  for (; qi < RING - 1; ++qi) {
-    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
-    else cpa_commit();
-    it.next(nseg, gstride);
-    islot = islot + 1 == RING ? 0 : islot + 1;
-  }
-  auto consume = [&]() -> V* {
-    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg), it.k < nseg ? pfwd : pbwd);
-    else cpa_commit();
-    it.next(nseg, gstride);
-    ++qi;
-    islot = islot + 1 == RING ? 0 : islot + 1;
-    cpa_wait<RING - 1>();
-    V* p = ring + cslot * 2 * R * 32;
-    cslot = cslot + 1 == RING ? 0 : cslot + 1;
-    return p;
-  };
-
-  for (int64_t g = g0; g < ngroups; g += gstride) {
-    const int64_t c = g * (32 * SG) + sgi * 32 + lane;
-    const bool cv = c < P;
-    const int64_t cc = cv ? c : P - 1;
-    const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
-    const bool second = cv && jb2 != ja;
-    const double cb = __ldg(a.cb + ja);
-    const double sub = __dmul_rn(cb, -1.5707963267948966);
-    V* outa = out + (int64_t)par * B + ja;
-    V* outb = out + (int64_t)par * B + jb2;
-    V* ychkj = ychk + (int64_t)blockIdx.x * (int64_t)(((a.n_dir + 1) / 2 + R - 1) / R) * 2 * kT + tid;
-    const double* ckj = a.ckpt + (int64_t)par * 3 * B + ja;
-    // ---------------- forward: y, z at segment ends only
-    HelmProj pj;
-    hp_origin(pj);
-    V y = szero<V>(), z = szero<V>();
-    double dl = 0.0, el = 0.0, tl = 0.0;
-    for (int s = 0; s < nseg; ++s) {
-      const V* cur = consume();
-      if (s > 0) hp_start(pj, dl, el, tl);
-      const bool full = (s + 1) * R <= n;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        const double4 tv = mytab[i];
-        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
-        if (r > 0 && (r & 7) == 0) hp_rescale(pj);
-        double d, e, t;
-        const double low = hp_step(pj, row, sub, d, e, t);
-        dl = d; el = e; tl = t;
-        const bool valid = full || i < n;
-        y = sfma(-low, y, valid ? cur[r * 32] : szero<V>());
-        z = sfma(-low, z, valid ? cur[(R + r) * 32] : szero<V>());
-      }
-      if (s + 1 < nseg) {
-        ystore(ychkj + (2 * s) * kT, y);
-        ystore(ychkj + (2 * s + 1) * kT, z);
-      }
-    }
-    // ---------------- backward: re-stream each segment (bottom first)
-    V x1 = szero<V>(), S = szero<V>(), w1 = szero<V>(), W = szero<V>();
-    double ckd = 1.0, cke = 0.0, ckt = 0.0;
-    V cky = szero<V>(), ckz = szero<V>();
-    if (nseg - 1 > 0) {
-      const double* ck = ckj + (int64_t)6 * (nseg - 1) * B;
-      ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-      cky = ychkj[(2 * (nseg - 2)) * kT];
-      ckz = ychkj[(2 * (nseg - 2) + 1) * kT];
-    }
-    for (int s = nseg - 1; s >= 0; --s) {
-      HelmProj q;
-      V yy = szero<V>(), zz = szero<V>();
-      if (s == 0) {
-        hp_origin(q);
-      } else {
-        hp_start(q, ckd, cke, ckt);
-        yy = cky;
-        zz = ckz;
-        ydiscard(ychkj + (2 * (s - 1)) * kT, lane);
-        ydiscard(ychkj + (2 * (s - 1) + 1) * kT, lane);
-      }
-      if (s - 1 > 0) {
-        const double* ck = ckj + (int64_t)6 * (s - 1) * B;
-        ckd = __ldg(ck); cke = __ldg(ck + B); ckt = __ldg(ck + 2 * B);
-        cky = ychkj[(2 * (s - 2)) * kT];
-        ckz = ychkj[(2 * (s - 2) + 1) * kT];
-      }
-      V* cur = consume();
-      const bool full = (s + 1) * R <= n;
-      double rd_[R], e_[R], t_[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = s * R + r;
-        const double4 tv = mytab[i];
-        const HelmRow row = helm_row(a.ca, cb, sub, tv.x, tv.y, tv.z, tv.w != 0.0);
-        if (r > 0 && (r & 7) == 0) hp_rescale(q);
-        double d, e, t;
-        const double low = hp_step(q, row, sub, d, e, t);
-        const bool valid = full || i < n;
-        yy = sfma(-low, yy, valid ? cur[r * 32] : szero<V>());
-        zz = sfma(-low, zz, valid ? cur[(R + r) * 32] : szero<V>());
-        cur[r * 32] = yy;
-        cur[(R + r) * 32] = zz;
-        rd_[r] = valid ? q.rd : 0.0;
-        e_[r] = valid ? e : 0.0;
-        t_[r] = valid ? t : 0.0;
-      }
-      V* opa = outa + (int64_t)2 * (s * R) * B;
-      V* opb = outb + (int64_t)2 * (s * R) * B;
-#pragma unroll
-      for (int r = R - 1; r >= 0; --r) {
-        const bool valid = full || s * R + r < n;
-        const V acc = ssub(ssub(cur[r * 32], smul(e_[r], x1)), smul(t_[r], S));
-        const V x = smul(rd_[r], acc);
-        S = sadd(x1, S);
-        x1 = x;
-        const V accb = ssub(ssub(cur[(R + r) * 32], smul(e_[r], w1)), smul(t_[r], W));
-        const V xb = smul(rd_[r], accb);
-        W = sadd(w1, W);
-        w1 = xb;
-        if (cv && valid) O::st_cs(opa + (int64_t)2 * r * B, x);
-        if (second && valid) O::st_cs(opb + (int64_t)2 * r * B, xb);
       }
     }
   }
@@ -925,27 +680,18 @@ __global__ void __launch_bounds__(64 * SG, 1) bih_stream_kernel(BihChunkArgs a, 
 // results are bit-identical to it.  Work items are pairs (P of them; an
 // unpaired system is a pair of itself and is stored once); one parity per
 // CTA with the one-parity compact table (the two RHS streams double the ring).
-// TMA = true: RHS segments by tensor-map bulk copies (complex RHS on a 2-D
-// channel grid, pair table padded so a warp's 32 items are 32 consecutive
-// kz columns of one (m, -m) row pair; padding items are -1).
-template <typename V, int R, int SG, bool TMA = false>
-__global__ void __launch_bounds__(64 * SG, 1)
-    bih_pair_kernel(BihChunkArgs a, V* ychk, const __grid_constant__ CUtensorMap tmap) {
+template <typename V, int R, int SG>
+__global__ void __launch_bounds__(64 * SG, 1) bih_pair_kernel(BihChunkArgs a, V* ychk) {
   constexpr int kT = 64 * SG;
   constexpr int SGE = 2 * SG;  // 32-item groups per CTA work item (one parity per CTA)
   constexpr int RING = 2;
-  __shared__ __align__(8) uint64_t mbar[TMA ? 2 * SG * RING : 1];
   using O = VOps<V>;
   extern __shared__ __align__(16) double smem_raw[];
-  // TMA boxes land 128-B aligned: the dynamic window is requested 128 B larger
+  // ring rows 128-B aligned: the dynamic window is requested 128 B larger
   // (pointer arithmetic on the shared array itself, so the compiler keeps
   // the shared address space: LDS/STS, not generic loads)
-#if SHEN_PAIR_ALIGN_GENERIC  // A/B: the generic-pointer variant (generic loads)
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-#else
   const uint32_t sbase = smem_u32(smem_raw);
   double* smem = smem_raw + ((((sbase + 127u) & ~127u) - sbase) >> 3);
-#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (int)(blockIdx.x & 1), sgi = warp;
   const int64_t B = a.batch;
@@ -972,8 +718,6 @@ __global__ void __launch_bounds__(64 * SG, 1)
     }
     stab[q] = v;
   }
-  if (TMA && tid < 2 * SG * RING) mbar_init(&mbar[tid], 1);
-  if (TMA) mbar_fence_init();
   __syncthreads();
   auto tpos = [&](int i) { return i + 2; };
   constexpr int tstep = 1;
@@ -1008,40 +752,6 @@ __global__ void __launch_bounds__(64 * SG, 1)
   // pair's system indices are loaded once per group (a dependent global load
   // per segment issue was the kernel's largest stall)
   int64_t ig = -1, ija = 0, ijb = 0;
-  // TMA: the warp's box coordinates (kz column of lane 0, the two kx rows), per group
-  const int64_t nzh = a.grid_nzh;
-  int tn0 = -1, tma_ = 0, tmb_ = 0;
-  auto issue_tma = [&](int slot_i, SegRef ref) {
-    if (ref.g != ig) {
-      const int64_t c0 = ref.g * (32 * SGE) + sgi * 32;
-      tn0 = -1;
-      if (c0 < P) {
-        const int64_t ja0 = __ldg(pa + c0), jb0 = __ldg(pb + c0);
-        if (ja0 >= 0) {
-          tma_ = (int)(ja0 / nzh);
-          tn0 = (int)(ja0 - (int64_t)tma_ * nzh);
-          tmb_ = (int)(jb0 / nzh);
-        }
-      }
-      ig = ref.g;
-    }
-    // every lane is done with the slot (its reads and the backward sweep's
-    // in-place y writes) before the async proxy overwrites it
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      uint64_t* bar = &mbar[warp * RING + slot_i];
-      if (tn0 >= 0) {
-        V* dst = reinterpret_cast<V*>(smem) + (size_t)warp * RING * 2 * R * 32 + (size_t)slot_i * 2 * R * 32;
-        mbar_expect_tx(bar, 2 * R * 32 * (uint32_t)sizeof(V));
-        const int row0 = par + 2 * ref.s * R;
-        tma_load_3d(dst, &tmap, 2 * tn0, tma_, row0, bar);
-        tma_load_3d(dst + R * 32, &tmap, 2 * tn0, tmb_, row0, bar);
-      } else {
-        mbar_arrive(bar);  // no valid item in this warp: complete the phase
-      }
-    }
-  };
   auto issue = [&](V* slot, SegRef ref) {
     if (ref.g < ngroups) {
       const int64_t c = ref.g * (32 * SGE) + sgi * 32 + lane;
@@ -1082,33 +792,19 @@ __global__ void __launch_bounds__(64 * SG, 1)
   int64_t qi = 0;
   int islot = 0, cslot = 0;  // ring slots being issued / consumed (no 64-bit modulo)
   SegIt it{g0, 0};
-  uint32_t cphase = 0;  // TMA: parity bit of each ring slot's barrier
   for (; qi < RING - 1; ++qi) {
-    if (TMA) {
-      if (qi < nq) issue_tma(islot, it.ref(nseg));
-    } else {
-      if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
-      else cpa_commit();
-    }
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
+    else cpa_commit();
     it.next(nseg, gstride);
     islot = islot + 1 == RING ? 0 : islot + 1;
   }
   auto consume = [&]() -> V* {
-    if (TMA) {
-      if (qi < nq) issue_tma(islot, it.ref(nseg));
-    } else {
-      if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
-      else cpa_commit();
-    }
+    if (qi < nq) issue(ring + islot * 2 * R * 32, it.ref(nseg));
+    else cpa_commit();
     it.next(nseg, gstride);
     ++qi;
     islot = islot + 1 == RING ? 0 : islot + 1;
-    if (TMA) {
-      mbar_wait(&mbar[warp * RING + cslot], (cphase >> cslot) & 1u);
-      cphase ^= 1u << cslot;
-    } else {
-      cpa_wait<RING - 1>();
-    }
+    cpa_wait<RING - 1>();
     V* p = ring + cslot * 2 * R * 32;
     cslot = cslot + 1 == RING ? 0 : cslot + 1;
     return p;
@@ -1116,13 +812,9 @@ __global__ void __launch_bounds__(64 * SG, 1)
 
   for (int64_t g = g0; g < ngroups; g += gstride) {
     const int64_t c = g * (32 * SGE) + sgi * 32 + lane;
-    bool cv = c < P;
+    const bool cv = c < P;
     const int64_t cc = cv ? c : P - 1;
-    int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
-    if (TMA) {  // padding items (-1): solve system 0 for nothing, store nothing
-      cv = cv && ja >= 0;
-      if (ja < 0) ja = jb2 = 0;
-    }
+    const int64_t ja = __ldg(pa + cc), jb2 = __ldg(pb + cc);
     const bool second = cv && jb2 != ja;  // store the second system (an unpaired one is stored once)
     const double xi1 = __ldg(a.xi1 + ja), xi2 = __ldg(a.xi2 + ja);
     V* outa = out + (int64_t)par * B + ja;
@@ -1208,7 +900,6 @@ __global__ void __launch_bounds__(64 * SG, 1)
       BihU w{0, 0, 0, 0, 0, 0}, w1{0, 0, 0, 0, 0, 0}, w2{0, 0, 0, 0, 0, 0};
       V ya = szero<V>(), yb = szero<V>(), za = szero<V>(), zb = szero<V>();
       V* cur = consume();  // also completes ck_issue(s) (cp.async path)
-      if (TMA) cpa_wait<0>();  // the checkpoint group (the only cp.async traffic)
       if (s > 0) {  // factor state and y entering the segment
         const double* c = ckd + tid;
         w1.d = c[0]; w1.e = c[kT]; w1.f = c[2 * kT]; w1.a = c[3 * kT]; w1.b = c[4 * kT];
@@ -1342,8 +1033,7 @@ static cudaError_t helm_stream_RR(const HelmChunkArgs& a, void* scratch, int cta
   int64_t cap = stream_ctas(occ);
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
-  static const int hint = getenv("SHEN_HELM_HINT") ? atoi(getenv("SHEN_HELM_HINT")) : 0;
-  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows, hint);
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows);
   return cudaGetLastError();
 }
 
@@ -1360,52 +1050,6 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   if ((size_t)3 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
     return helm_stream_RR<V, R, SG, 3>(a, scratch, ctas_per_sm, st);
   return helm_stream_RR<V, R, SG, 2>(a, scratch, ctas_per_sm, st);
-}
-
-template <typename V, int R, int SG, int RING>
-static cudaError_t helm_pair_RR(const HelmChunkArgs& a, void* scratch, cudaStream_t st) {
-  constexpr int kT = 64 * SG;
-  const int n0 = (a.n_dir + 1) / 2;
-  const int tab_rows = ((n0 + R - 1) / R) * R;
-  const size_t smem = (size_t)RING * 2 * R * kT * sizeof(V) + (size_t)2 * tab_rows * sizeof(double4);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  auto kern = helm_pair_kernel<V, R, RING, SG>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  if (a.n_pairs <= 0) return cudaSuccess;
-  const int64_t groups = (a.n_pairs + 32 * SG - 1) / (32 * SG);
-  int64_t cap = stream_ctas(1);
-  if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
-  const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
-  static const int hint = getenv("SHEN_HELM_HINT") ? atoi(getenv("SHEN_HELM_HINT")) : 0;
-  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tab_rows, hint);
-  return cudaGetLastError();
-}
-
-template <typename V, int R, int SG>
-static size_t helm_pair_smem(const HelmChunkArgs& a, int ring) {
-  const int n0 = (a.n_dir + 1) / 2;
-  return (size_t)ring * 2 * R * 64 * SG * sizeof(V) + (size_t)2 * (((n0 + R - 1) / R) * R) * sizeof(double4);
-}
-
-// CTA size (warps_per_sm 4 / 6 / 8) and ring depth (SHEN_HELM_PAIR_RING) of the
-// pair kernel; the default is the one measured best at BASELINE config 4
-template <typename V, int R>
-static cudaError_t helm_pair_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
-  if (w == 0) w = 8;
-  static const int rg = getenv("SHEN_HELM_PAIR_RING") ? atoi(getenv("SHEN_HELM_PAIR_RING")) : 3;
-  if (w == 4) {
-    if (rg >= 4 && helm_pair_smem<V, R, 2>(a, 4) <= 220 * 1024) return helm_pair_RR<V, R, 2, 4>(a, sc, st);
-    if (helm_pair_smem<V, R, 2>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 2, 3>(a, sc, st);
-  } else if (w == 6) {
-    if (rg >= 3 && helm_pair_smem<V, R, 3>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 3, 3>(a, sc, st);
-    if (helm_pair_smem<V, R, 3>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 3, 2>(a, sc, st);
-  } else {
-    if (rg >= 3 && helm_pair_smem<V, R, 4>(a, 3) <= 220 * 1024) return helm_pair_RR<V, R, 4, 3>(a, sc, st);
-    if (helm_pair_smem<V, R, 4>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 4, 2>(a, sc, st);
-  }
-  if (helm_pair_smem<V, R, 2>(a, 2) <= 220 * 1024) return helm_pair_RR<V, R, 2, 2>(a, sc, st);
-  return cudaErrorInvalidValue;
 }
 
 template <typename V, int R, bool SMEM_TAB, int RING, int SG, bool PP = false>
@@ -1434,54 +1078,15 @@ static size_t bih_pair_smem(const BihChunkArgs& a) {
   const size_t ring = (size_t)2 * 2 * R * kT * sizeof(V);
   const size_t tabp = (size_t)((a.n_bih + 1) / 2 + 2) * BC_STRIDE * sizeof(double);
   const size_t ckb = (size_t)kT * (10 * sizeof(double) + 4 * sizeof(V));
-  return ring + tabp + ckb + 128;  // + alignment slack of the TMA ring
+  return ring + tabp + ckb + 128;  // + alignment slack of the ring
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// the complex RHS (n_bih, ny, nzh) as a 3-D tensor of doubles: dim 0 = 2 nzh
-// (contiguous), dim 1 = kx row, dim 2 = mode row traversed with stride 2 (one
-// parity); box = 32 complex x 1 kx row x R rows of one parity
-template <int R>
-static bool rhs_tensor_map(CUtensorMap* tm, const BihChunkArgs& a) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)(2 * a.grid_nzh), (cuuint64_t)a.grid_ny, (cuuint64_t)a.n_bih};
-  const cuuint64_t strides[2] = {(cuuint64_t)(2 * a.grid_nzh * 8), (cuuint64_t)(a.grid_ny * 2 * a.grid_nzh * 8)};
-  const cuuint32_t box[3] = {64, 1, 2 * R};
-  const cuuint32_t estr[3] = {1, 1, 2};
-  // no L2 promotion: the box rows start 16 B past a 128-B line (a kx row is
-  // 1025 x 16 B), and promoting to 256-B granules read 1.5x the box bytes
-  static const int promo = getenv("SHEN_TMA_PROMO") ? atoi(getenv("SHEN_TMA_PROMO")) : 0;
-  const CUtensorMapL2promotion pr = promo == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                    : promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(a.rhs), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
-
-template <typename V, int R, int SG, bool TMA = false>
+template <typename V, int R, int SG>
 static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
   constexpr int kT = 64 * SG;
   const size_t smem = bih_pair_smem<V, R, SG>(a);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  CUtensorMap tm;
-  memset(&tm, 0, sizeof(tm));
-  if (TMA && !rhs_tensor_map<R>(&tm, a)) return cudaErrorNotSupported;
-  auto kern = bih_pair_kernel<V, R, SG, TMA>;
+  auto kern = bih_pair_kernel<V, R, SG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   if (a.n_pairs <= 0) return cudaSuccess;
@@ -1490,7 +1095,7 @@ static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStr
   if (a.max_ctas > 0) cap = std::min<int64_t>(cap, a.max_ctas);
   cap = std::max<int64_t>(cap, 2);  // the CTA's parity is blockIdx.x & 1: both must exist
   const unsigned grid = (unsigned)std::min<int64_t>(groups, cap);
-  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch), tm);
+  kern<<<grid, kT, smem, st>>>(a, static_cast<V*>(scratch));
   return cudaGetLastError();
 }
 
@@ -1501,11 +1106,6 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
     // memory; past n_x ~ 1150 it does not fit and the one-system kernel
     // solves every system (the pair table lists each exactly once)
     static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
-    if (a.grid_nzh > 0) {  // warp-aligned pair table of a channel grid: TMA-fed pair kernel
-      if (!std::is_same<V, cplx>::value || R != 8 || bih_pair_smem<V, R, 4>(a) > 227 * 1024)
-        return cudaErrorInvalidValue;
-      return bih_pair_launch<V, R, 4, std::is_same<V, cplx>::value && R == 8>(a, scratch, st);
-    }
     if (pw == 6 && bih_pair_smem<V, R, 3>(a) <= 227 * 1024) return bih_pair_launch<V, R, 3>(a, scratch, st);
     if (bih_pair_smem<V, R, 4>(a) <= 227 * 1024) return bih_pair_launch<V, R, 4>(a, scratch, st);
   }
@@ -1534,13 +1134,6 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
 // can afford to prefetch the segment checkpoints into registers).
 template <typename V>
 static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
-  if (a.pairs != nullptr && a.chunk_rows == 8) {
-    const cudaError_t e = helm_pair_dispatch<V, 8>(a, sc, w, st);
-    if (e != cudaErrorInvalidValue) return e;
-  }
-  // no pairs, or the pair kernel's shared memory does not fit: the
-  // one-system kernel solves the whole batch (a pair table lists every
-  // system exactly once, so this is the same set of solves)
   const bool small = (w == 8);
   switch (a.chunk_rows) {
     case 4: return small ? helm_stream_R<V, 4, 4>(a, sc, 1, st) : helm_stream_R<V, 4, 6>(a, sc, 1, st);

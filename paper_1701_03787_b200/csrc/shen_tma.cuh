@@ -1,6 +1,6 @@
-// TMA (cp.async.bulk.tensor) and mbarrier helpers shared by the
-// column-resident kernels (sm_100a).  Tensor maps are encoded on the host
-// through the runtime's driver entry point (no -lcuda).
+// TMA (cp.async.bulk.tensor) and mbarrier helpers of the wall-normal
+// transform kernels (sm_100a).  Tensor maps are encoded on the host through
+// the runtime's driver entry point (shen_tma.cu, no -lcuda).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>

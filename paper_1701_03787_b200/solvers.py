@@ -16,8 +16,7 @@ What changes is where and how the work happens:
 * ``solve`` (default ``method="stream"``) is the streaming fused
   factor+solve kernel (``csrc/shen_solve_stream.cu``): one thread per
   (system, parity), coalesced row pieces, the factors recomputed from the
-  checkpoints in both sweeps; ``method="chunked"`` is the chunk-parallel
-  variant (lanes = row chunks, ``csrc/shen_solve_chunk.cu``);
+  checkpoints in both sweeps (the biharmonic on mirror pairs of systems);
 * the full factors ``low``/``d``/``e``/``tail`` (and ``low2`` ... ``b``) are
   materialised lazily, bit-identical to the reference, only when accessed;
 * ``method="stored"`` keeps full reference-exact factors on the device and
@@ -54,7 +53,7 @@ __all__ = [
 
 PIVOT_FLOOR = 1e-300  # reference solvers.py:54
 _INT_MAX = 2**31 - 1
-_METHODS = ("cr", "chunked", "stream", "stored", "tile")
+_METHODS = ("stream", "stored")
 
 
 def _env_int(name, default):
@@ -73,14 +72,6 @@ def stream_warps() -> int:
     import os
 
     return int(os.environ.get("SHEN_STREAM_WARPS", "0"))
-
-
-def helm_pair_warps() -> int:
-    """CTA size of the Helmholtz mirror-pair kernel (4, 6 or 8 warps per SM;
-    0 = the default)."""
-    import os
-
-    return int(os.environ.get("SHEN_HELM_PAIR_WARPS", "0"))
 
 
 # ------------------------------------------------------------------ host <-> device
@@ -138,7 +129,7 @@ def _pipe_streams(dev):
 def _host_pipeline_many(jobs):
     """Column-slab pipeline over one or several solves: the H2D copy of slab
     k+1 and the D2H copy of slab k-1 run on their own streams while slab k is
-    solved (stream method; the other methods solve each batch after one copy).
+    solved (stream method; the stored method solves each batch after one copy).
     Consecutive jobs share the pipeline, so the next operator's first copy-in
     overlaps the previous one's last copy-out.  Page-locked host arrays make
     the copies asynchronous; pageable ones still work (staged)."""
@@ -158,7 +149,7 @@ def _host_pipeline_many(jobs):
             cache = (torch.empty((n, B), dtype=dtype, device=dev), torch.empty((n, B), dtype=dtype, device=dev))
             lu._pipe = cache
         d_rhs, d_out = cache
-        if lu.method not in ("stream", "cr") or B < 2 * _PIPE_MIN_SLAB:
+        if lu.method != "stream" or B < 2 * _PIPE_MIN_SLAB:
             bounds = [(0, B)]
         else:
             nslab = min(_PIPE_MAX_SLABS, B // _PIPE_MIN_SLAB)
@@ -215,7 +206,6 @@ def solve_many(jobs):
 
 
 MIRROR_PAIRS = _env_int("SHEN_PAIRS", 1)  # solve mirror-paired systems together (biharmonic stream)
-HELM_PAIRS = _env_int("SHEN_HELM_PAIRS", 0)  # the same for the Helmholtz stream solve
 PAIRS_MIN = _env_int("SHEN_PAIRS_MIN", 8192)  # below: one system per thread (c1: 40 vs 33 us; c3 pairs: 0.097 vs 0.120 ms)
 
 
@@ -248,33 +238,9 @@ def mirror_pairs(z2):
     return np.stack([a, b])
 
 
-# complex biharmonic pairs: TMA-fed kernel on a warp-aligned table (bit-identical;
-# measured slower at config 4: 27.8 vs 20.9 ms, DRAM reads +20%; off by default)
-PAIR_TMA = _env_int("SHEN_PAIR_TMA", 0)
-
-
-def mirror_pairs_grid(z2):
-    """The mirror pairs of a 2-D z2 grid in warp-aligned form for the TMA-fed
-    biharmonic kernel: for every row pair, its kz columns padded to a multiple
-    of 32 (padding items -1), so 32 consecutive items are 32 consecutive
-    columns of one row pair.  Returns ((2, P) int64, (ny, nzh)) or None."""
-    pr = mirror_pairs(z2)
-    if pr is None:
-        return None
-    ny, nzh = np.shape(z2)
-    npad = -(-nzh // 32) * 32
-    r0 = pr[0, ::nzh] // nzh  # one entry per row pair (items of a row pair are consecutive)
-    r1 = pr[1, ::nzh] // nzh
-    col = np.arange(npad, dtype=np.int64)
-    ok = col < nzh
-    a = np.where(ok[None, :], r0[:, None] * nzh + col[None, :], -1).reshape(-1)
-    b = np.where(ok[None, :], r1[:, None] * nzh + col[None, :], -1).reshape(-1)
-    return np.stack([a, b]), (int(ny), int(nzh))
-
-
 def _solve_real_via_complex(lu, rhs_dev, out_dev, j0=0, j1=-1):
-    """Real RHS (or a complex one on misaligned storage): the tile kernels move
-    16-B row pieces of complex values, so solve the complex system with zero
+    """Real RHS with an odd batch or misaligned storage: the streaming kernels
+    move 16-B row pieces, so solve the complex system with zero
     imaginary part -- every coefficient is real, so the real part is the same
     arithmetic as the real solve."""
     import torch
@@ -376,7 +342,6 @@ class HelmholtzLU:
         self._tab = tables_dev
         self.chunk_rows = int(chunk_rows)
         self._ckpt = ckpt
-        self._pairs = None  # device (2, P) int64 mirror pairs (build_helmholtz), or None
         self.method = method
         self._stored = stored  # list of 8 device tensors (exact factors) or None
         self._host = None
@@ -452,32 +417,14 @@ class HelmholtzLU:
             return out_dev
         if self.method == "stream" and not is_complex and (B % 2 or rhs_dev.data_ptr() % 16):
             return _solve_real_via_complex(self, rhs_dev, out_dev)
-        if self.method == "cr" and (not is_complex or rhs_dev.data_ptr() % 16 or out_dev.data_ptr() % 16):
-            return _solve_real_via_complex(self, rhs_dev, out_dev, j0, j1)
         h = lib()
         sh = dv.stream_handle()
-        if self.method == "cr":
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_helm_solve_cr(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                       md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(), out_dev.data_ptr(),
-                                       max_ctas, j0, j1, sh), "shen_helm_solve_cr")
-        elif self.method == "stored":
+        if self.method == "stored":
             ptrs, keep = ptr_array([b.data_ptr() for b in self._stored])
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
             del keep
-        elif self.method == "stream" and self._pairs is not None and j0 == 0 and j1 in (-1, B):
-            # mirror pairs: one factor recurrence for two systems (bit-identical results)
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
-            check(h.shen_helm_solve_stream_pairs(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                                 md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                                 out_dev.data_ptr(), scratch, int(is_complex), self._pairs.data_ptr(),
-                                                 int(self._pairs.shape[1]), helm_pair_warps(), max_ctas, sh),
-                  "shen_helm_solve_stream_pairs")
-        elif self.method == "stream":
+        else:
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
             scratch = _scratch(self, 0, nd, B, is_complex, out_dev.device)
@@ -486,19 +433,6 @@ class HelmholtzLU:
                                            out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), max_ctas,
                                            j0, j1, sh),
                   "shen_helm_solve_stream")
-        elif self.method == "tile":
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_helm_solve_tile(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                         md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(), out_dev.data_ptr(),
-                                         int(is_complex), sh), "shen_helm_solve_tile")
-        else:
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_helm_solve_chunked(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                            md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                            out_dev.data_ptr(), int(is_complex), sh),
-                  "shen_helm_solve_chunked")
         return out_dev
 
 
@@ -507,9 +441,6 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
 
     ``method="stream"`` (default): checkpoints every 8 rows for the streaming
     fused solve (one thread per system, coalesced rows).
-    ``method="chunked"``: checkpoints for the warp-per-system chunked solve.
-    ``method="tile"``: the same checkpoints for the tiled chunk-parallel
-    solve (RHS read once; rows of parity 0 <= 512, else the stream solve).
     ``method="stored"``: full reference-exact factors kept on the device.
     Raises ``ZeroPivotError`` exactly like the reference."""
     import torch
@@ -526,16 +457,14 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
     tabs = tuple(torch.from_numpy(t).to(dev) for t in _helm_tables(mats))
     cb_dev = torch.from_numpy(np.ascontiguousarray(cb_flat)).to(dev)
     B = cb_flat.size
-    if method in ("tile", "cr") and chunk_rows_for(nd) > 16:
-        method = "stream"  # the tile kernels keep at most 32 x 16 rows per parity
-    R = chunk_rows_for(nd) if method in ("chunked", "tile", "cr") else STREAM_ROWS_H
+    R = STREAM_ROWS_H
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method in ("chunked", "stream", "tile", "cr"):
+    if method == "stream":
         C = _n_chunks(nd, R)
         ckpt = torch.empty((C, 2, 3, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_helm_factor(nd, float(ca), cb_dev.data_ptr(), B, tabs[0].data_ptr(), tabs[1].data_ptr(),
@@ -554,12 +483,7 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
         del keep
     if B > 0:
         _raise_pivot(pivot.cpu().numpy(), "Helmholtz")
-    lu = HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
-    if method == "stream" and HELM_PAIRS and R == 8:
-        pr = mirror_pairs(z2)
-        if pr is not None and pr.shape[1] >= PAIRS_MIN:
-            lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
-    return lu
+    return HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
 
 
 # ------------------------------------------------------------------ biharmonic
@@ -629,7 +553,6 @@ class BiharmonicLU:
         self._qs_dev = None
         self._host = None
         self._pairs = None  # device (2, P) int64 mirror pairs (build_biharmonic), or None
-        self._pairs_grid = None  # (device warp-aligned (2, P) pairs, (ny, nzh)) for complex RHS, or None
 
     @property
     def n_modes(self) -> int:
@@ -700,17 +623,6 @@ class BiharmonicLU:
                                           ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(), int(is_complex), sh),
                   "shen_bih_solve_stored")
             del keep
-        elif (self.method == "stream" and self._pairs_grid is not None and is_complex and j0 == 0
-              and j1 in (-1, B) and rhs_dev.data_ptr() % 16 == 0):
-            # mirror pairs, RHS segments fetched by TMA (bit-identical results)
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
-            pg, (ny, nzh) = self._pairs_grid
-            check(h.shen_bih_solve_stream_pairs_grid(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
-                                                     self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                                     out_dev.data_ptr(), scratch, pg.data_ptr(), int(pg.shape[1]),
-                                                     ny, nzh, max_ctas, sh),
-                  "shen_bih_solve_stream_pairs_grid")
         elif self.method == "stream" and self._pairs is not None and j0 == 0 and j1 in (-1, B):
             # mirror pairs: one factor recurrence for two systems (bit-identical results)
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -721,7 +633,7 @@ class BiharmonicLU:
                                                 out_dev.data_ptr(), scratch, int(is_complex), self._pairs.data_ptr(),
                                                 P, max_ctas, sh),
                   "shen_bih_solve_stream_pairs")
-        elif self.method == "stream":
+        else:
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
             scratch = _scratch(self, 1, nb, B, is_complex, out_dev.device)
             check(h.shen_bih_solve_stream(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
@@ -729,11 +641,6 @@ class BiharmonicLU:
                                           out_dev.data_ptr(), scratch, int(is_complex), stream_warps(), max_ctas,
                                           j0, j1, sh),
                   "shen_bih_solve_stream")
-        else:
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_bih_solve_chunked(nb, self.xi0, self._xi1.data_ptr(), self._xi2.data_ptr(), B,
-                                           self._tab.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                           out_dev.data_ptr(), int(is_complex), sh), "shen_bih_solve_chunked")
         return out_dev
 
 
@@ -756,16 +663,14 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
     x1d = torch.from_numpy(x1).to(dev)
     x2d = torch.from_numpy(x2).to(dev)
     B = x1.size
-    if method in ("tile", "cr"):
-        method = "stream"  # no tiled biharmonic variant yet: the streaming pair kernel
-    R = chunk_rows_for(nb) if method == "chunked" else STREAM_ROWS_B
+    R = STREAM_ROWS_B
     h = lib()
     sh = dv.stream_handle()
     pivot = torch.empty(2, dtype=torch.int32, device=dev)
     check(h.shen_pivot_reset(pivot.data_ptr(), sh), "shen_pivot_reset")
     ckpt = None
     stored = None
-    if method in ("chunked", "stream"):
+    if method == "stream":
         C = _n_chunks(nb, R)
         ckpt = torch.empty((C, 2, 10, B), dtype=torch.float64, device=dev) if C > 1 else None
         check(h.shen_bih_factor(nb, float(xi0), x1d.data_ptr(), x2d.data_ptr(), B, tab.data_ptr(), R,
@@ -791,11 +696,6 @@ def build_biharmonic(mats: MatrixSet, nu: float, dt: float, z2, method: str = "s
         # (config 1, 1.1k pairs: 44 vs 39 us; config 3, 16.6k pairs: 0.097 vs 0.120 ms)
         if pr is not None and pr.shape[1] >= PAIRS_MIN:
             lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
-            # the TMA-fed kernel needs the 8-row checkpoints and a pair kernel that fits
-            # shared memory (n_x <= ~1150, as the cp.async pair kernel)
-            pg = mirror_pairs_grid(z2) if PAIR_TMA and R == 8 and mats.n_x <= 1100 else None
-            if pg is not None:
-                lu._pairs_grid = (torch.from_numpy(np.ascontiguousarray(pg[0])).to(dev), pg[1])
     return lu
 
 

@@ -17,14 +17,17 @@ Device pipeline.  Everything runs on the GPU with axis 0
 contiguous lane index:
 
 * periodic y/z: ``torch.fft.rfft2`` / ``irfft2`` (cuFFT, library);
-* wall-normal DCT: our ``shen_xform_extend`` / ``shen_xform_inv_pre`` kernels
-  build the extended sequence, cuFFT does one FFT along the rows, our
-  ``shen_xform_fwd_post`` / ``shen_xform_inv_post`` kernels apply the twiddle,
-  the Chebyshev scaling and the Shen stencil in the same pass;
-* mass solve: our ``shen_xform_mass_solve`` kernel, one thread per
-  (line, parity), with the host's LAPACK banded Cholesky factors of the 1-D
-  mass matrix (the very factors the reference computes,
-  transforms.py:143-160).
+* wall-normal stage (default): one fused kernel per direction
+  (``shen_wall_transform``, csrc/shen_wall.cu) on tiles of Fourier lines in
+  shared memory -- the DCT as an on-chip FFT (power-of-two, Rader or
+  Bluestein), the Chebyshev scaling, the Shen stencil and the per-parity
+  banded Cholesky mass solve with the reference's own LAPACK factors
+  (transforms.py:143-160), one HBM read and one write per line;
+* alternative route (``SHEN_XFORM=fft``, and the 1-D blocks below N = 3):
+  our ``shen_xform_extend`` / ``shen_xform_inv_pre`` kernels build the
+  extended sequence, cuFFT does one FFT along the rows, our post kernels
+  apply twiddle, scaling and stencil, ``shen_xform_mass_solve`` the mass
+  solve.
 
 numpy inputs are copied to the device and the result copied back (numpy out);
 torch CUDA tensors stay on the device (torch out).  There is no CPU fallback:
@@ -348,205 +351,14 @@ def mass_solve(scalar, space, n_x: int, family):
     return ln.give_back(_mass_pass(ln.t, sp, int(n_x), _fam(family), out=out))
 
 
-# ---------------------------------------------------------------- wall-normal operators
+# ---------------------------------------------------------------- wall-normal route
 #
-# For the 3-D transforms the whole wall-normal map is one linear operator per
-# (n_x, family, space): forward = B^-1 S W (Chebyshev scalar products W, Shen
-# stencil S, mass solve B^-1), scalar product = S W, inverse = C X (Shen ->
-# Chebyshev expansion X, evaluation at the points C).  At N = 257 (config 3)
-# the FFT route needs a Bluestein FFT (N prime) and several HBM passes; one
-# fp64 GEMM over all Fourier lines (cuBLAS) is about 4x faster, reads the
-# spectrum once and writes the result once.  The operators are built once in
-# 80-bit arithmetic and rounded to float64.  SHEN_XFORM=fft selects the
-# kernel/cuFFT pipeline above instead (used by the 1-D building blocks).
+# Default (SHEN_XFORM=wall): the fused wall-normal kernel (csrc/shen_wall.cu,
+# plans built in wall.py) does the whole axis-0 stage of a transform in one
+# pass over the lines.  SHEN_XFORM=fft selects the extension / cuFFT / post
+# pipeline above instead (also the route of the 1-D blocks when N < 3).
 
 XFORM_METHOD = __import__("os").environ.get("SHEN_XFORM", "wall")
-
-
-def _ld_pi():
-    return np.arccos(np.longdouble(-1))
-
-
-def _scalar_matrix_ld(N: int, fam: int):
-    """W (N x N): chebyshev_scalar as a matrix (transforms.py:81-86)."""
-    pi = _ld_pi()
-    k = np.arange(N, dtype=np.longdouble)[:, None]
-    n = np.arange(N, dtype=np.longdouble)[None, :]
-    if fam == 0:
-        return (pi / N) * np.cos(pi * k * (2 * n + 1) / (2 * N))
-    nx = N - 1
-    W = (pi / nx) * np.cos(pi * k * n / nx)
-    W[:, 0] *= 0.5
-    W[:, nx] *= 0.5
-    return W
-
-
-def _stencil_ld(sp: int, N: int, fam: int):
-    """S (n x N): shen_scalar applied to the Chebyshev scalar products (transforms.py:89-110)."""
-    n_x = N - 1
-    if sp == 0:
-        S = np.eye(N, dtype=np.longdouble) * (2 / _ld_pi())
-        S[0, 0] /= 2
-        if fam == 1:
-            S[n_x, n_x] /= 2
-        return S
-    if sp == 1:
-        n = n_x - 1
-        S = np.zeros((n, N), dtype=np.longdouble)
-        r = np.arange(n)
-        S[r, r] = 1
-        S[r, r + 2] = -1
-        return S
-    n = n_x - 3
-    S = np.zeros((n, N), dtype=np.longdouble)
-    r = np.arange(n)
-    k = r.astype(np.longdouble)
-    S[r, r] = 1
-    S[r, r + 2] = -2 * (k + 2) / (k + 3)
-    S[r, r + 4] = (k + 1) / (k + 3)
-    return S
-
-
-def _banded_solve_ld(Bd, R):
-    """Solve B Y = R in long double (B banded SPD, no pivoting needed)."""
-    A = Bd.astype(np.longdouble).copy()
-    Y = R.copy()
-    n = A.shape[0]
-    bw = 4
-    for i in range(n):
-        hi = min(n, i + bw + 1)
-        for r in range(i + 1, hi):
-            if A[r, i] != 0:
-                f = A[r, i] / A[i, i]
-                A[r, i:hi] -= f * A[i, i:hi]
-                Y[r] -= f * Y[i]
-    for i in range(n - 1, -1, -1):
-        hi = min(n, i + bw + 1)
-        Y[i] = (Y[i] - A[i, i + 1:hi] @ Y[i + 1:hi]) / A[i, i]
-    return Y
-
-
-@lru_cache(maxsize=16)
-def _operator_host(kind: str, n_x: int, fam: int, sp: int):
-    N = n_x + 1
-    if kind in ("fwd", "fsp"):
-        M = _stencil_ld(sp, N, fam) @ _scalar_matrix_ld(N, fam)
-        if kind == "fwd" and sp != 0:
-            mats = assemble(n_x, as_family(fam))
-            Bd = (mats.mass_dir if sp == 1 else mats.mass_bih).dense()
-            M = _banded_solve_ld(Bd, M)
-        return np.ascontiguousarray(M.astype(np.float64))
-    # inverse: C (N x N) evaluation at the points times the expansion X (N x n)
-    pi = _ld_pi()
-    j = np.arange(N, dtype=np.longdouble)[:, None]
-    m = np.arange(N, dtype=np.longdouble)[None, :]
-    theta = pi * (2 * j + 1) / (2 * N) if fam == 0 else pi * j / n_x
-    C = np.cos(m * theta)
-    n = N - (0, 2, 4)[sp]
-    X = np.zeros((N, n), dtype=np.longdouble)
-    c = np.arange(n)
-    k = c.astype(np.longdouble)
-    X[c, c] = 1
-    if sp == 1:
-        X[c + 2, c] = -1
-    elif sp == 2:
-        X[c + 2, c] = -2 * (k + 2) / (k + 3)
-        X[c + 4, c] = (k + 1) / (k + 3)
-    return np.ascontiguousarray((C @ X).astype(np.float64))
-
-
-@lru_cache(maxsize=16)
-def _operator_dev(kind: str, n_x: int, fam: int, sp: int, dev_index: int, scale: float = 1.0):
-    """Device copy; ``scale`` folds a constant factor into the operator (the
-    inverse folds irfft2's 1/(n_y n_z) so no separate scaling pass runs)."""
-    import torch
-
-    M = _operator_host(kind, n_x, fam, sp)
-    if scale != 1.0:
-        M = M * scale
-    return torch.from_numpy(np.ascontiguousarray(M)).to(torch.device("cuda", dev_index))
-
-
-def _apply_operator(M, lines):
-    """(n x N) float64 operator applied to (N, L) complex128 lines -> (n, L)."""
-    import torch
-
-    N, L = lines.shape
-    xr = torch.view_as_real(lines).reshape(N, 2 * L)
-    out = torch.matmul(M, xr)
-    return torch.view_as_complex(out.view(M.shape[0], L, 2))
-
-
-@lru_cache(maxsize=16)
-def _paired_dev(kind: str, n_x: int, fam: int, sp: int, dev_index: int, scale: float = 1.0):
-    """Mirror-paired blocks of an operator, or None if it has no mirror parity.
-
-    x_{N-1-j} = -x_j and every basis function has the parity of its mode, so
-    the inverse E (N x n) satisfies E[N-1-j, k] = (-1)^k E[j, k] and the
-    forward F (n x N) F[k, N-1-j] = (-1)^k F[k, j]: even modes couple only
-    to pair sums (plus the centre point), odd modes only to pair differences.
-    Two GEMMs with the blocks do half the flops of the full operator
-    (nonlinear.py uses the same split)."""
-    import torch
-
-    M = _operator_host(kind, n_x, fam, sp)
-    if scale != 1.0:
-        M = M * scale
-    N = n_x + 1
-    P, Q = (N + 1) // 2, N // 2
-    tol = 1e-12 * np.abs(M).max()
-    if kind == "inv":
-        sign = np.where(np.arange(M.shape[1]) % 2 == 0, 1.0, -1.0)
-        if not np.allclose(M[::-1], M * sign, rtol=0, atol=tol):
-            return None
-        S, A = M[:P, 0::2], M[:Q, 1::2]
-    else:
-        sign = np.where(np.arange(M.shape[0]) % 2 == 0, 1.0, -1.0)[:, None]
-        if not np.allclose(M[:, ::-1], M * sign, rtol=0, atol=tol):
-            return None
-        S, A = M[0::2, :P], M[1::2, :Q]
-    dev = torch.device("cuda", dev_index)
-    return (torch.from_numpy(np.ascontiguousarray(S)).to(dev), torch.from_numpy(np.ascontiguousarray(A)).to(dev),
-            P, Q)
-
-
-PAIRED_MIN_LINES = 512  # below this one full GEMM beats split + two GEMMs + pass
-
-
-def _forward_paired(blocks, lines):
-    """(N, L) lines -> (n, L) coefficients: pair split pass, then the even /
-    odd mode blocks write the interleaved output rows directly (cuBLAS ldc)."""
-    import torch
-
-    S, A, P, Q = blocks
-    N, L = lines.shape
-    y = torch.empty((N, L), dtype=torch.complex128, device=lines.device)
-    _lib.check(_lib.lib().shen_pair_split(P, Q, 2 * L, lines.data_ptr(), y.data_ptr(), stream_handle()),
-               "shen_pair_split")
-    n = S.shape[0] + A.shape[0]
-    out = torch.empty((n, L), dtype=torch.complex128, device=lines.device)
-    outr, yr = torch.view_as_real(out).reshape(n, 2 * L), torch.view_as_real(y).reshape(N, 2 * L)
-    torch.matmul(S, yr[:P], out=outr[0::2])
-    torch.matmul(A, yr[P:], out=outr[1::2])
-    return out
-
-
-def _inverse_paired(blocks, coef):
-    """(n, L) coefficients -> (N, L) lines: the even / odd mode blocks read
-    strided coefficient rows (cuBLAS ldb) into e, o; one merge pass."""
-    import torch
-
-    S, A, P, Q = blocks
-    n, L = coef.shape
-    N = P + Q
-    y = torch.empty((N, L), dtype=torch.complex128, device=coef.device)
-    cr, yr = torch.view_as_real(coef).reshape(n, 2 * L), torch.view_as_real(y).reshape(N, 2 * L)
-    torch.matmul(S, cr[0::2], out=yr[:P])
-    torch.matmul(A, cr[1::2], out=yr[P:])
-    lines = torch.empty((N, L), dtype=torch.complex128, device=coef.device)
-    _lib.check(_lib.lib().shen_pair_merge(P, Q, 2 * L, y.data_ptr(), lines.data_ptr(), stream_handle()),
-               "shen_pair_merge")
-    return lines
 
 
 # ---------------------------------------------------------------- wall-normal stage on lines
@@ -560,13 +372,6 @@ def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
         plan = wall_plan(n_x, fam, sp, 0, solve_mass, _cheb_scale(n_x + 1, fam))
         if plan is not None:
             return _wall_run(plan, lines.contiguous(), plan.struct.n_out)
-    if XFORM_METHOD == "matrix":
-        kind = "fwd" if solve_mass else "fsp"
-        if lines.shape[1] >= PAIRED_MIN_LINES:
-            blocks = _paired_dev(kind, n_x, fam, sp, device().index)
-            if blocks is not None:
-                return _forward_paired(blocks, lines.contiguous())
-        return _apply_operator(_operator_dev(kind, n_x, fam, sp, device().index), lines)
     scal = _chebyshev_pass(lines, fam, sp)
     if solve_mass and sp != 0:
         scal = _mass_pass(scal, sp, n_x, fam)
@@ -575,21 +380,14 @@ def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
 
 def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
     """(n, L) coefficients -> (N, L) values on the Chebyshev points, and the
-    ``norm`` for the following ``irfft2`` (the matrix route folds the
-    1/(n_y n_z) of the inverse FFT into its operator)."""
+    ``norm`` for the following ``irfft2`` (the wall kernel folds the
+    1/(n_y n_z) of the inverse FFT into its output scale)."""
     if XFORM_METHOD == "wall" and n_x >= 2:
         from .wall import wall_plan
 
         plan = wall_plan(n_x, fam, sp, 1, False, 1.0 / yz_points)
         if plan is not None and plan.struct.n_in == coef.shape[0]:
             return _wall_run(plan, coef.contiguous(), n_x + 1), "forward"
-    if XFORM_METHOD == "matrix":
-        if coef.shape[1] >= PAIRED_MIN_LINES:
-            blocks = _paired_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)
-            if blocks is not None:
-                return _inverse_paired(blocks, coef.contiguous()), "forward"
-        op = _operator_dev("inv", n_x, fam, sp, device().index, 1.0 / yz_points)
-        return _apply_operator(op, coef), "forward"
     return _expand_pass(coef, sp, n_x, fam), "backward"
 
 

@@ -71,14 +71,8 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_helm_solve_stream": (1, 0.0, None, 1, None, None, None, 8, None, None, None, None, 1, 0, 0, 0, -1,
                                    None),
         "shen_bih_solve_stream": (1, 0.0, None, None, 1, None, 8, None, None, None, None, 1, 0, 0, 0, -1, None),
-        "shen_helm_solve_tile": (1, 0.0, None, 1, None, None, None, 8, None, None, None, 1, None),
-        "shen_helm_solve_chunked": (1, 0.0, None, 1, None, None, None, 8, None, None, None, 1, None),
         "shen_bih_factor": (1, 0.0, None, None, 1, None, 8, None, None, 0, None, None),
         "shen_bih_solve_stream_pairs": (1, 0.0, None, None, 1, None, 8, None, None, None, None, 1, None, 1, 0, None),
-        "shen_bih_solve_stream_pairs_grid": (1, 0.0, None, None, 1, None, 8, None, None, None, None, None, 32, 1, 1,
-                                             0, None),
-        "shen_helm_solve_stream_pairs": (1, 0.0, None, 1, None, None, None, 8, None, None, None, None, 1, None, 1, 0, 0,
-                                         None),
         "shen_xform_extend": (3, 5, 1, None, None, None),
         "shen_xform_fwd_post": (0, 9, 5, 1, 1.0, None, None, None, None),
         "shen_xform_inv_pre": (0, 1, 9, 5, 1, None, None, None, None, None),
@@ -89,10 +83,6 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_apply_rank2_tail": (4, 1, None, None, None, None, None, None, None, 1, None),
         "shen_scale_lines": (2, 2, None, None, None, None, None),
         "shen_cross": (8, None, None, None),
-        "shen_cross_paired": (3, 1, 8, None, None, None),
-        "shen_scale_rows": (2, 4, None, 2, None, None, None, 4, None),
-        "shen_pair_split": (3, 1, 8, None, None, None),
-        "shen_pair_merge": (2, 3, 8, None, None, None),
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
     }
     for name, args in cases.items():

@@ -29,7 +29,7 @@ def _sha(a):
 
 
 @pytest.mark.parametrize("case", range(8))
-@pytest.mark.parametrize("method", ["stored", "chunked"])
+@pytest.mark.parametrize("method", ["stored", "stream"])
 def test_factors_bitwise_vs_reference(golden, golden_meta, case, method):
     """Materialised factors (lazy attributes) equal the reference's bit for bit."""
     g = golden("solvers.npz")
@@ -65,7 +65,7 @@ def test_stored_solve_bitwise_vs_reference(golden, golden_meta, case):
 
 
 @pytest.mark.parametrize("case", range(8))
-@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
+@pytest.mark.parametrize("method", ["stream"])
 def test_fused_solve_parity(golden, golden_meta, case, method):
     g = golden("solvers.npz")
     meta = golden_meta["solver_cases"][case]
@@ -186,7 +186,7 @@ def _degenerate(n_x, rows):
 
 
 @pytest.mark.parametrize("rows,want", [([0], 0), ([1], 1), ([0, 1], 0)])
-@pytest.mark.parametrize("method", ["stream", "chunked", "stored", "tile"])
+@pytest.mark.parametrize("method", ["stream", "stored"])
 def test_zero_pivot_raises(rows, want, method):
     with pytest.raises(S.ZeroPivotError, match=f"Helmholtz factorization hit a near-zero pivot at row {want}$"):
         S.build_helmholtz(_degenerate(16, rows), 0.0, 1.0, np.array([0.0, 1.0]), method=method)
@@ -203,7 +203,7 @@ def _corner_systems(n_y, n_z):
 
 
 @pytest.mark.parametrize("op", ["h", "b"])
-@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
+@pytest.mark.parametrize("method", ["stream"])
 def test_config4_corners_residual(op, method):
     """BASELINE config 4 parameters (n_x = 1024, nu = 1/2000, dt = 1e-4) on
     32 systems including the largest z^2 of the 2048 x 1025 plane."""
@@ -230,7 +230,7 @@ def test_config4_corners_residual(op, method):
 
 
 @pytest.mark.parametrize("N", [129, 257, 513, 1025, 2049])
-@pytest.mark.parametrize("method", ["chunked", "stream", "tile"])
+@pytest.mark.parametrize("method", ["stream"])
 def test_config5_sizes(N, method):
     """BASELINE config 5 wall-normal sweep, 24 systems of the 512 x 257 plane."""
     mats = assemble(N - 1, 0)
@@ -302,47 +302,13 @@ def test_biharmonic_mirror_pairs_bitwise(n_x, ny, nz, cplx):
     mats = assemble(n_x, 0)
     z2 = channel_z2(ny, nz)
     S.PAIRS_MIN, saved = 1, S.PAIRS_MIN  # force pairs at test sizes
-    S.PAIR_TMA, saved_tma = 1, S.PAIR_TMA  # and the TMA-fed variant for complex RHS
     try:
         lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
     finally:
         S.PAIRS_MIN = saved
-        S.PAIR_TMA = saved_tma
     assert lu._pairs is not None
     rng = np.random.default_rng(n_x + ny)
     shp = (mats.n_bih,) + z2.shape
-    f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
-    x_pair = lu.solve(f)  # complex on a grid that fits: the TMA-fed pair kernel
-    if cplx and n_x <= 1100:
-        assert lu._pairs_grid is not None
-    pairs, grid = lu._pairs, lu._pairs_grid
-    lu._pairs_grid = None
-    x_pair_cp = lu.solve(f)  # cp.async-fed pair kernel
-    lu._pairs = None
-    x_one = lu.solve(f)
-    lu._pairs, lu._pairs_grid = pairs, grid
-    assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
-    assert np.array_equal(x_pair_cp, x_one)
-
-
-@pytest.mark.parametrize("n_x,ny,nz", [(32, 16, 16), (256, 64, 30), (1024, 8, 64), (2048, 4, 32)])
-@pytest.mark.parametrize("cplx", [True, False])
-@pytest.mark.parametrize("warps", ["4", "6", "8"])
-def test_helmholtz_mirror_pairs_bitwise(n_x, ny, nz, cplx, warps, monkeypatch):
-    """Helmholtz on mirror pairs (one factor recurrence, two right-hand
-    sides per thread) equals the one-system-per-thread solve bit for bit, for
-    every CTA size of the pair kernel."""
-    from paper_1701_03787_b200.mesh import channel_z2
-
-    monkeypatch.setenv("SHEN_HELM_PAIR_WARPS", warps)
-    mats = assemble(n_x, 0)
-    z2 = channel_z2(ny, nz)
-    monkeypatch.setattr(S, "PAIRS_MIN", 1)
-    monkeypatch.setattr(S, "HELM_PAIRS", 1)
-    lu = S.build_helmholtz(mats, 1 / 2000, 1e-4, z2)
-    assert lu._pairs is not None
-    rng = np.random.default_rng(n_x + ny + 1)
-    shp = (mats.n_dir,) + z2.shape
     f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
     x_pair = lu.solve(f)
     pairs = lu._pairs
@@ -350,3 +316,77 @@ def test_helmholtz_mirror_pairs_bitwise(n_x, ny, nz, cplx, warps, monkeypatch):
     x_one = lu.solve(f)
     lu._pairs = pairs
     assert x_pair.dtype == x_one.dtype and np.array_equal(x_pair, x_one)
+
+
+def _degenerate_bih(n_x, rows):
+    """stiff_bih with a zeroed main diagonal on `rows`: with nu*dt = 0 and
+    z2 = 0 the biharmonic operator is -stiff_bih, whose pivot d vanishes on
+    the first zeroed row (reference solvers.py:314-346 pivot check)."""
+    import dataclasses
+
+    m = assemble(n_x, 0)
+    sb = m.stiff_bih
+    d0 = sb.diagonal(0).copy()
+    d0[list(rows)] = 0.0
+    nb = BandedMatrix(sb.shape, sb.offsets, tuple(d0 if o == 0 else dg for o, dg in zip(sb.offsets, sb.diagonals)))
+    return dataclasses.replace(m, stiff_bih=nb)
+
+
+@pytest.mark.parametrize("rows,want", [([0], 0), ([1], 1), ([0, 1], 0)])
+@pytest.mark.parametrize("method", ["stream", "stored"])
+def test_biharmonic_zero_pivot_raises(rows, want, method):
+    """The device pivot flag of the biharmonic factor raises the reference's
+    error at build, first bad row in parity-0-then-parity-1 order; the oracle
+    (the reference's arithmetic) agrees on the row."""
+    mats = _degenerate_bih(16, rows)
+    msg = f"biharmonic factorization hit a near-zero pivot at row {want}$"
+    with pytest.raises(S.ZeroPivotError, match=msg):
+        S.build_biharmonic(mats, 0.0, 1.0, np.array([0.0, 0.0]), method=method)
+    with pytest.raises(ArithmeticError, match=msg):
+        O.biharmonic_factor(mats, 0.0, 1.0, np.array([0.0, 0.0]))
+
+
+@pytest.mark.parametrize("cplx", [True, False])
+@pytest.mark.parametrize("max_ctas", [1, 2, 3])
+def test_biharmonic_pair_grid_caps(max_ctas, cplx):
+    """The pair kernel takes its parity from blockIdx.x & 1: a CTA cap of 1
+    or an odd cap must still solve both parities of every system (advisor
+    round 1), bit-identical to the uncapped launch."""
+    import torch
+
+    mats = assemble(64, 0)
+    z2 = channel_z2(32, 64)
+    S.PAIRS_MIN, saved = 1, S.PAIRS_MIN
+    try:
+        lu = S.build_biharmonic(mats, 1 / 2000, 1e-4, z2)
+    finally:
+        S.PAIRS_MIN = saved
+    assert lu._pairs is not None
+    rng = np.random.default_rng(max_ctas)
+    shp = (mats.n_bih, z2.size)
+    f = rng.standard_normal(shp) + 1j * rng.standard_normal(shp) if cplx else rng.standard_normal(shp)
+    fd = torch.from_numpy(f).cuda()
+    want = torch.empty_like(fd)
+    lu.solve_into(fd, want, cplx)
+    got = torch.full_like(fd, float("nan"))
+    lu.solve_into(fd, got, cplx, max_ctas=max_ctas)
+    assert torch.equal(got, want)
+
+
+def test_solve_field_wraps_solve():
+    """solve_field (reference solvers.py:387-392): the SpectralField's data
+    solved per wavenumber, grid and mesh carried over."""
+    from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
+    from paper_1701_03787_b200.transforms import SpectralField
+
+    mesh = build_mesh(32, 16, 16, 2 * np.pi, np.pi)
+    mats = assemble(32, 0)
+    for space, build in ((Space.DIRICHLET, S.build_helmholtz), (Space.BIHARMONIC, S.build_biharmonic)):
+        grid = wavenumber_grid(mesh, space)
+        lu = build(mats, NU, DT, grid.z2())
+        rng = np.random.default_rng(5)
+        shp = (grid.n_modes,) + tuple(mesh.spectral_shape_yz)
+        field = SpectralField(rng.standard_normal(shp) + 1j * rng.standard_normal(shp), grid, mesh)
+        out = S.solve_field(lu, field)
+        assert isinstance(out, SpectralField) and out.grid is grid and out.mesh is mesh
+        assert np.array_equal(out.data, lu.solve(field.data))

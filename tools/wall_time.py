@@ -14,7 +14,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 lines = torch.complex(torch.randn((N, L), generator=g, device="cuda", dtype=torch.float64),
                       torch.randn((N, L), generator=g, device="cuda", dtype=torch.float64))
 res = {}
-for method in sys.argv[1:] or ["wall", "matrix"]:
+for method in sys.argv[1:] or ["wall", "fft"]:
     T.XFORM_METHOD = method
     for fam in (0, 1):
         for sp in (1, 2):
