@@ -44,6 +44,27 @@ namespace {
 using cd = double2;
 constexpr int kWallThreads = 256;
 
+// per-CTA phase timestamps (A/B variant builds with -DSHEN_WALL_TIMING only;
+// tools/wall_phases.py reads them)
+#ifdef SHEN_WALL_TIMING
+__device__ long long g_wall_ts[1 << 16][6];
+#define WALL_TS(k)                                                \
+  do {                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {             \
+      g_wall_ts[blockIdx.x][k] = clock64();                       \
+      if ((k) == 0) {                                             \
+        unsigned smid;                                            \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));         \
+        g_wall_ts[blockIdx.x][5] = smid;                          \
+      }                                                           \
+    }                                                             \
+  } while (0)
+#else
+#define WALL_TS(k) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ cd cadd(cd a, cd b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ cd csub(cd a, cd b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ cd cmul(cd a, cd b) {
@@ -381,6 +402,11 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   double* mf = reinterpret_cast<double*>(bar + 2);
   const int64_t l0 = (int64_t)blockIdx.x * TL;
   const int N = p.N, tid = threadIdx.x;
+#ifdef SHEN_WALL_POISON
+  for (int e = threadIdx.x; e < (p.rows_smem + 2) * TL; e += kWallThreads) T[e] = make_double2(__longlong_as_double(0x7ff8dead00000000LL), 0.0);
+  __syncthreads();
+#endif
+  WALL_TS(0);
   wall_load(T, bar, &tin, N, box_in, TL, l0);
   const bool do_mass = p.mass && (p.space == 1 || p.space == 2);
   if (do_mass)
@@ -388,6 +414,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   if (tid < TL) side[tid] = make_double2(0.0, 0.0);
   mb_wait(bar, 0);
   __syncthreads();
+  WALL_TS(1);
   const bool gauss = p.family == 0;
   // ---- DFT of the gathered sequence
   if (p.kind == 0) {  // power of two: Lobatto even extension z (Ld = M = 2 n_x)
@@ -475,6 +502,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
     for (int e = tid; e < N * TL; e += kWallThreads) T[e] = cscale(scl, T[e]);
   }
   __syncthreads();
+  WALL_TS(2);
   // ---- Shen stencil (shen_scalar, transforms.py:89-110) and mass solve
   if (do_mass) {
     // the stencil rides the forward sweep: s_k needs w_k, w_{k+2}, w_{k+4}
@@ -495,34 +523,50 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
       const double2* F = reinterpret_cast<const double2*>(mf) + (size_t)par * (p.mmax + 1) * 4;  // [m][4] double2
       cd* col = T + (par << TLs) + l;  // row par + 2 i at col[i << (TLs + 1)]
       const int rs = 1 << (TLs + 1);
-      cd wa = col[0], wb = col[rs];                 // w_k, w_{k+2}
+      // w rows i, i+1, i+2 (w_k, w_{k+2}, w_{k+4}) in a register queue; row
+      // i+3 is loaded one iteration before its use (issued before the store
+      // of row i, so it need not wait behind it), as are the next row's
+      // coefficients
+      cd q0 = col[0], q1 = col[rs], q2 = col[2 * rs];
       cd y1 = make_double2(0.0, 0.0), y2 = y1;
       double2 F0 = F[0], F1 = F[1], F2 = F[2];
+#pragma unroll 2
       for (int i = 0; i < m; ++i) {
-        const cd wc = sp == 2 ? col[(i + 2) * rs] : make_double2(0.0, 0.0);  // w_{k+4}
+        const cd q3 = col[min(i + 3, m + 1) * rs];  // (rows past i + 2 = m + 1 are never used)
         const double2 G0 = F[4 * (i + 1)], G1 = F[4 * (i + 1) + 1], G2 = F[4 * (i + 1) + 2];  // next row
+        const cd wc = sp == 2 ? q2 : make_double2(0.0, 0.0);
         // t = a0 w_k - a2 w_{k+2} + a4 w_{k+4} - f2 y_{i-2};  y = t - f1 y_{i-1}
-        cd t = make_double2(fma(F0.x, wa.x, fma(-F0.y, wb.x, fma(F1.x, wc.x, -F2.x * y2.x))),
-                            fma(F0.x, wa.y, fma(-F0.y, wb.y, fma(F1.x, wc.y, -F2.x * y2.y))));
+        cd t = make_double2(fma(F0.x, q0.x, fma(-F0.y, q1.x, fma(F1.x, wc.x, -F2.x * y2.x))),
+                            fma(F0.x, q0.y, fma(-F0.y, q1.y, fma(F1.x, wc.y, -F2.x * y2.y))));
         const cd y = make_double2(fma(-F1.y, y1.x, t.x), fma(-F1.y, y1.y, t.y));
         col[i * rs] = y;
         y2 = y1;
         y1 = y;
-        wa = wb;
-        wb = sp == 2 ? wc : col[(i + 2) * rs];
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
         F0 = G0;
         F1 = G1;
         F2 = G2;
       }
       cd x1 = make_double2(0.0, 0.0), x2 = x1;
+      const int il = m > 0 ? m - 1 : 0;
+      cd yn = col[il * rs];
+      double2 Fa = F[4 * il], Fc = F[4 * il + 2], Fd = F[4 * il + 3];
+#pragma unroll 2
       for (int i = m - 1; i >= 0; --i) {
-        const cd yk = col[i * rs];
-        const double2 Fa = F[4 * i], Fc = F[4 * i + 2], Fd = F[4 * i + 3];  // a0 | f2 g1 | g2 -
+        const cd yk = yn;
+        const int ip = i > 0 ? i - 1 : 0;  // next (upper) row, loaded one iteration ahead
+        yn = col[ip * rs];
+        const double2 Ha = F[4 * ip], Hc = F[4 * ip + 2], Hd = F[4 * ip + 3];  // a0 | f2 g1 | g2 -
         const cd t = make_double2(fma(Fa.x, yk.x, -Fd.x * x2.x), fma(Fa.x, yk.y, -Fd.x * x2.y));
         const cd x = make_double2(fma(-Fc.y, x1.x, t.x), fma(-Fc.y, x1.y, t.y));
         col[i * rs] = x;
         x2 = x1;
         x1 = x;
+        Fa = Ha;
+        Fc = Hc;
+        Fd = Hd;
       }
     }
   } else if (sp != 3) {
@@ -553,7 +597,9 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
       T[(k << TLs) + l] = sk;
     }
   }
+  WALL_TS(3);
   wall_store(T, &tout, n, box_out, TL, l0);
+  WALL_TS(4);
 }
 
 // ------------------------------------------------------------------ inverse
@@ -570,6 +616,10 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
   const int64_t l0 = (int64_t)blockIdx.x * TL;
   const int N = p.N, n = p.n_in, tid = threadIdx.x, nx = N - 1;
   const bool gauss = p.family == 0;
+#ifdef SHEN_WALL_POISON  // debug variant: every tile row starts as NaN (reads of unwritten rows show up)
+  for (int e = threadIdx.x; e < (p.rows_smem + 2) * TL; e += kWallThreads) T[e] = make_double2(__longlong_as_double(0x7ff8dead00000000LL), 0.0);
+  __syncthreads();
+#endif
   wall_load(T, bar, &tin, n, box_in, TL, l0);
   {  // rows the boxes do not cover, up to N: zero (the expansion reads them)
     const int covered = ((n + box_in - 1) / box_in) * box_in;
@@ -632,9 +682,9 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     cd c = T[(k << TLs) + l];
     if (rsc != nullptr) c = cscale(__ldg(rsc + k), c);
     if (sp == 1 && k >= 2) c = csub(c, T[((k - 2) << TLs) + l]);
-    if (sp == 2) {
-      if (k >= 2) c = csub(c, cscale(__ldg(p.c2 + k - 2), T[((k - 2) << TLs) + l]));
-      if (k >= 4) c = cadd(c, cscale(__ldg(p.c4 + k - 4), T[((k - 4) << TLs) + l]));
+    if (sp == 2) {  // coefficient rows >= n are zero: the stencil tables (n entries) stop there
+      if (k >= 2 && k - 2 < n) c = csub(c, cscale(__ldg(p.c2 + k - 2), T[((k - 2) << TLs) + l]));
+      if (k >= 4 && k - 4 < n) c = cadd(c, cscale(__ldg(p.c4 + k - 4), T[((k - 4) << TLs) + l]));
     }
     return c;
   };
@@ -745,3 +795,9 @@ cudaError_t launch_wall(const WallPlan& p, int64_t L, const void* in, void* out,
 }
 
 }  // namespace shen
+
+#ifdef SHEN_WALL_TIMING
+extern "C" int shen_wall_ts_read(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, shen::g_wall_ts, bytes);
+}
+#endif

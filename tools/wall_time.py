@@ -14,13 +14,13 @@ g = torch.Generator(device="cuda").manual_seed(0)
 lines = torch.complex(torch.randn((N, L), generator=g, device="cuda", dtype=torch.float64),
                       torch.randn((N, L), generator=g, device="cuda", dtype=torch.float64))
 res = {}
-for method in sys.argv[1:] or ["wall", "fft"]:
+for method in [a for a in sys.argv[1:] if not a.startswith("--")] or ["wall"]:
     T.XFORM_METHOD = method
     for fam in (0, 1):
         for sp in (1, 2):
-            for kind in ("fwd", "inv"):
-                if kind == "fwd":
-                    fn = lambda: T.wall_forward(lines, 256, fam, sp, True)  # noqa: E731
+            for kind in ("fwd", "fsp", "inv"):
+                if kind in ("fwd", "fsp"):
+                    fn = lambda: T.wall_forward(lines, 256, fam, sp, kind == "fwd")  # noqa: E731
                     nin, nout = N, 256 - 1 if sp == 1 else 256 - 3
                 else:
                     coef = lines[: (255 if sp == 1 else 253)].contiguous()
@@ -39,4 +39,6 @@ for method in sys.argv[1:] or ["wall", "fft"]:
                 gbs = (nin + nout) * L * 16 / (ms * 1e6)
                 res[f"{method}_f{fam}_s{sp}_{kind}"] = {"ms": ms, "GBps_alg": gbs}
                 print(method, fam, sp, kind, f"{ms*1e3:.1f} us  {gbs:.0f} GB/s", flush=True)
-json.dump(res, open("gpurun_out/wall_time.json", "w"), indent=1)
+import os
+tag = os.environ.get("SHEN_LIB_VARIANT", "") or "product"
+json.dump(res, open(f"gpurun_out/wall_time_{tag}.json", "w"), indent=1)
