@@ -606,9 +606,21 @@ def c3_wall_stages(mesh, u, B):
             byts = rows * L * 16
             res[f"{kind}_{name}"] = {"ms": ms, "bytes": byts, "GBps_alg": byts / (ms * 1e6), "frac": byts / (ms * 1e6) / peak}
     dom = max(res, key=lambda k: res[k]["ms"])
+    # DRAM bytes per launch of that kernel from the committed ncu launch list
+    # (profiles/r02/c3_launches_summary.json, cold-cache serialised launches)
+    traffic, tsrc = None, None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "r02", "c3_launches_summary.json")))
+        want = "wall_forward_kernel" if dom.startswith("forward") else "wall_inverse_kernel"
+        ent = [e for e in summ if want in e["kernel"]]
+        if ent:
+            traffic = float(ent[0]["dram_bytes_per_launch"])
+            tsrc = f"ncu launch list, profiles/r02/c3_launches_summary.json ({want}, mean over the step's launches)"
+    except Exception:
+        pass
     roof = {"bound": "hbm", "kernel": f"shen_wall {dom} (fused DCT + stencil + mass solve)", "achieved": res[dom]["GBps_alg"],
-            "peak": peak, "unit": "GB/s", "frac": res[dom]["frac"], "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes": "(rows in + rows out) x 33,024 lines x 16 B per launch"}
+            "peak": peak, "unit": "GB/s", "frac": res[dom]["frac"], "traffic": traffic, "traffic_source": tsrc,
+            "peak_source": peak_src, "algorithmic_bytes": "(rows in + rows out) x 33,024 lines x 16 B per launch"}
     return {"stages": res, "roofline": roof}
 
 

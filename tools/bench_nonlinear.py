@@ -46,5 +46,14 @@ ms = e0.elapsed_time(e1) / 5
 t0 = time.perf_counter()
 O.compute_nonlinear(mats, False, n_y, n_z, m, n, mask, *host)
 cpu = time.perf_counter() - t0
+# roofline: the call's compulsory HBM traffic is its 4 spectral inputs and 3
+# spectral outputs (complex128); every transform stage in between is
+# intermediate traffic the fused pipeline still pays
+field = 16 * (n_x + 1) * n_y * (n_z // 2 + 1)
+alg = 16 * sum(x.size for x in host) + 3 * 16 * gd.n_modes * n_y * (n_z // 2 + 1)
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if __import__("os").path.exists("MEASURED_PEAKS.json") else 6548.2
 print(json.dumps({"workload": "compute_nonlinear, config-3 mesh 257x256x256 (8 inverse + 3 forward transforms)",
-                  "device_ms": ms, "cpu_oracle_s_1core": cpu, "speedup": cpu / (ms / 1e3)}))
+                  "device_ms": ms, "cpu_oracle_s_1core": cpu, "speedup": cpu / (ms / 1e3),
+                  "roofline": {"bound": "hbm", "algorithmic_bytes": alg, "achieved_GBps": alg / (ms * 1e6),
+                               "peak_GBps": peak, "frac": alg / (ms * 1e6) / peak,
+                               "note": "compulsory traffic only (4 fields in, 3 out)"}}))
