@@ -96,16 +96,6 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
                            int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
-/* Chunk-split streaming Helmholtz solve, complex RHS: groups of 16
- * consecutive systems, each (system, parity) column split into 16 chunks
- * solved by 16 threads (chunk-local sweeps joined by two scans), so the
- * backward sweep re-reads the RHS from L2 instead of HBM.  Same inputs as
- * shen_helm_solve_stream with chunk_rows = 8 (checkpoints every 8 rows);
- * supports rows_p0 <= 512 (n_x <= 1024), otherwise SHEN_ERR_ARG.  rhs/out
- * 16-B aligned, not aliased.  Replaces HelmholtzLU.solve (solvers.py:100-126). */
-int shen_helm_solve_split(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                          const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 

@@ -127,24 +127,6 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                     "shen_helm_solve_stream");
 }
 
-int shen_helm_solve_split(int n_dir, double ca, const double* cb, int64_t batch, const double* sd, const double* st,
-                          const double* md, int chunk_rows, const double* ckpt, const void* rhs, void* out,
-                          int max_ctas, int64_t j_begin, int64_t j_end, void* stream) {
-  if (n_dir < 1 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out || chunk_rows != 8 || max_ctas < 0)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_split: bad args");
-  if ((n_dir + 1) / 2 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_split: ckpt");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_split: rhs must not alias out");
-  if (j_begin < 0 || (j_end >= 0 && (j_end > batch || j_end < j_begin)))
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_split: system range");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
-  a.jb = j_begin;
-  a.je = j_end;
-  a.max_ctas = max_ctas;
-  const cudaError_t e = shen::launch_helm_split(a, S(stream));
-  if (e == cudaErrorNotSupported) return fail(SHEN_ERR_ARG, "shen_helm_solve_split: shape not supported (n_x > 1024)");
-  return cuda_check(e, "shen_helm_solve_split");
-}
-
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream) {
   if (batch == 0) return SHEN_OK;

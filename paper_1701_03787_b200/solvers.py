@@ -206,15 +206,6 @@ def solve_many(jobs):
 
 
 MIRROR_PAIRS = _env_int("SHEN_PAIRS", 1)  # solve mirror-paired systems together (biharmonic stream)
-# Helmholtz, complex RHS: chunk-split streaming kernel (RHS re-read from L2, csrc/shen_solve_split.cu)
-HELM_SPLIT = _env_int("SHEN_HELM_SPLIT", 0)
-
-
-def helm_split_ok(n_modes: int, R: int) -> bool:
-    """Shapes the chunk-split kernel takes: 8-row checkpoints, 2..4 segments
-    of the 16 chunks per parity column (n_x <= 1024)."""
-    nseg0 = -(-((n_modes + 1) // 2) // 8)
-    return R == 8 and 2 <= nseg0 and -(-nseg0 // 16) <= 4
 PAIRS_MIN = _env_int("SHEN_PAIRS_MIN", 8192)  # below: one system per thread (c1: 40 vs 33 us; c3 pairs: 0.097 vs 0.120 ms)
 
 
@@ -433,13 +424,6 @@ class HelmholtzLU:
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
             del keep
-        elif (HELM_SPLIT and is_complex and helm_split_ok(nd, self.chunk_rows)
-              and rhs_dev.data_ptr() % 16 == 0 and out_dev.data_ptr() % 16 == 0):
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_helm_solve_split(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                          md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(), out_dev.data_ptr(),
-                                          max_ctas, j0, j1, sh), "shen_helm_solve_split")
         else:
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
