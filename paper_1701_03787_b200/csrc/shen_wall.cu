@@ -144,6 +144,32 @@ struct Stage {
   int R, Ls;
 };
 
+// Compile-time plan shape: the DFT kind, radix sequence and lines per tile of
+// the hot configurations (BASELINE config 3, n_x = 256: Gauss = Rader over
+// 16 x 16, Lobatto = powers of two 16 x 8 x 4) are template constants, so
+// every radix switch folds and the tile index math is constant shifts; any
+// other plan runs the dynamic instantiation (WDyn) of the same code.
+template <int K_, int S_, int R0_, int R1_, int R2_, int TLS_>
+struct WShape {
+  static constexpr int K = K_, S = S_, R0 = R0_, R1 = R1_, R2 = R2_, TLS = TLS_;
+};
+using WDyn = WShape<-1, 0, 0, 0, 0, -1>;
+template <class SH>
+__device__ __forceinline__ int sh_kind(const WallPlan& p) { return SH::K >= 0 ? SH::K : p.kind; }
+template <class SH>
+__device__ __forceinline__ int sh_nst(const WallPlan& p) { return SH::S > 0 ? SH::S : p.nstage; }
+template <class SH>
+__device__ __forceinline__ int sh_rad(const WallPlan& p, int s) {
+  if (SH::S > 0) return s == 0 ? SH::R0 : s == 1 ? SH::R1 : s == 2 ? SH::R2 : 1;
+  return p.radix[s];
+}
+template <class SH>
+__device__ __forceinline__ int sh_M(const WallPlan& p) {
+  return SH::S > 0 ? SH::R0 * (SH::S > 1 ? SH::R1 : 1) * (SH::S > 2 ? SH::R2 : 1) : p.M;
+}
+template <class SH>
+__device__ __forceinline__ int sh_tls(const WallPlan& p) { return SH::TLS >= 0 ? SH::TLS : p.log2_lines; }
+
 // one decimation-in-frequency pass (forward sign) in place: butterflies of
 // radix R over sub-FFTs of size Ls (q = Ls / R apart), twiddle after
 template <int R>
@@ -305,18 +331,20 @@ __device__ __forceinline__ void scatter_last(int R, cd* T, int TLs, int M, const
 // (digit-reversed result left in T) or, with a kernel, the cyclic
 // convolution of the gathered sequence with it (natural order, handed to
 // the scatter).  a0 receives the DC term of the forward FFT (Rader).
-template <class LD, class ST>
+template <class SH, class LD, class ST>
 __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, const cd* ker, cd* a0, LD ld,
                                          ST st) {
-  const int M = p.M, S = p.nstage;
+  const int M = sh_M<SH>(p), S = sh_nst<SH>(p);
   int Ls = M;
-  gather_first(p.radix[0], T, TLs, M, p.tw, ld);
+  gather_first(sh_rad<SH>(p, 0), T, TLs, M, p.tw, ld);
   __syncthreads();
   if (ker == nullptr) {
-    Ls /= p.radix[0];
-    for (int s = 1; s < S; ++s) {
-      run_dif(p.radix[s], T, TLs, M, Ls, p.tw);
-      Ls /= p.radix[s];
+    Ls /= sh_rad<SH>(p, 0);
+#pragma unroll
+    for (int s = 1; s < 4; ++s) {
+      if (s >= S) break;
+      run_dif(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
+      Ls /= sh_rad<SH>(p, s);
       __syncthreads();
     }
     return;
@@ -330,25 +358,31 @@ __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, cons
       T[(i << TLs) + l] = cmul(T[(i << TLs) + l], __ldg(ker + i));
     }
     __syncthreads();
-    scatter_last(p.radix[0], T, TLs, M, p.tw, st);
+    scatter_last(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
     __syncthreads();
     return;
   }
-  Ls /= p.radix[0];
-  for (int s = 1; s < S - 1; ++s) {
-    run_dif(p.radix[s], T, TLs, M, Ls, p.tw);
-    Ls /= p.radix[s];
+  Ls /= sh_rad<SH>(p, 0);
+#pragma unroll
+  for (int s = 1; s < 3; ++s) {
+    if (s >= S - 1) break;
+    run_dif(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
+    Ls /= sh_rad<SH>(p, s);
     __syncthreads();
   }
-  run_conv(p.radix[S - 1], T, TLs, M, ker, a0);  // Ls == radix[S-1]
+  // S - 1 = 1..3: the last stage's convolution pass
+  const int RL = S == 2 ? sh_rad<SH>(p, 1) : S == 3 ? sh_rad<SH>(p, 2) : sh_rad<SH>(p, 3);
+  run_conv(RL, T, TLs, M, ker, a0);  // Ls == radix[S-1]
   __syncthreads();
-  Ls = p.radix[S - 1];
-  for (int s = S - 2; s >= 1; --s) {
-    Ls *= p.radix[s];
-    run_dit_inv(p.radix[s], T, TLs, M, Ls, p.tw);
+  Ls = RL;
+#pragma unroll
+  for (int s = 2; s >= 1; --s) {
+    if (s > S - 2) continue;
+    Ls *= sh_rad<SH>(p, s);
+    run_dit_inv(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
     __syncthreads();
   }
-  scatter_last(p.radix[0], T, TLs, M, p.tw, st);
+  scatter_last(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
   __syncthreads();
 }
 
@@ -389,13 +423,14 @@ __device__ __forceinline__ void wall_store(cd* T, const CUtensorMap* tout, int r
   }
 }
 
-template <int KMAX>
+template <int KMAX, class SH>
 __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const WallPlan p, int64_t L,
                                                                        const __grid_constant__ CUtensorMap tin,
                                                                        const __grid_constant__ CUtensorMap tout,
                                                                        int box_in, int box_out) {
   extern __shared__ __align__(1024) unsigned char wsm_raw[];
-  const int TLs = p.log2_lines, TL = 1 << TLs;
+  const int TLs = sh_tls<SH>(p), TL = 1 << TLs;
+  const int kind = sh_kind<SH>(p), Mv = sh_M<SH>(p);
   cd* T = reinterpret_cast<cd*>(wall_smem_base(wsm_raw));
   cd* side = T + (size_t)p.rows_smem * TL;  // [2][TL]: x0, A(0)
   uint64_t* bar = reinterpret_cast<uint64_t*>(side + 2 * TL);
@@ -417,14 +452,14 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   WALL_TS(1);
   const bool gauss = p.family == 0;
   // ---- DFT of the gathered sequence
-  if (p.kind == 0) {  // power of two: Lobatto even extension z (Ld = M = 2 n_x)
+  if (kind == 0) {  // power of two: Lobatto even extension z (Ld = M = 2 n_x)
     const int nx = N - 1;
-    wall_dft(p, T, TLs, nullptr, nullptr,
-             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, int, auto&) {});
-  } else if (p.kind == 1) {  // Rader (Gauss, N prime, M = N - 1)
+    wall_dft<SH>(p, T, TLs, nullptr, nullptr,
+             [&](int i, int l) { return T[((i <= nx ? i : Mv - i) << TLs) + l]; }, [](int, int, int, auto&) {});
+  } else if (kind == 1) {  // Rader (Gauss, N prime, M = N - 1)
     if (tid < TL) side[tid] = T[tid];  // v_0 = x_0
     const double scl = p.scale;
-    wall_dft(p, T, TLs, p.ker_f, side + TL,
+    wall_dft<SH>(p, T, TLs, p.ker_f, side + TL,
              [&](int i, int l) { return T[(__ldg(p.gin_f + i) << TLs) + l]; },
              [&](int n1, int q, int l, auto& v) {
                // V_k = x_0 + conv_q at k = g^{-q}; its partner N - k is R/2
@@ -449,7 +484,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
     __syncthreads();
   } else {  // Bluestein
     const int Ld = p.Ld, nx = N - 1;
-    wall_dft(p, T, TLs, p.ker_f, nullptr,
+    wall_dft<SH>(p, T, TLs, p.ker_f, nullptr,
              [&](int i, int l) {
                if (i >= Ld) return make_double2(0.0, 0.0);
                const int src = gauss ? sigma(i, N) : (i <= nx ? i : Ld - i);
@@ -467,7 +502,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   // ---- Chebyshev scalar products w_k (k < N), in place
   const int n = p.n_out, sp = p.space, nx = N - 1;
   const double scl = p.scale;
-  if (p.kind == 1) {
+  if (kind == 1) {
     // already w (fused into the last FFT pass)
   } else if (gauss) {
     // DCT-II from V_k and V_{N-k}: one thread owns both rows of a pair
@@ -484,7 +519,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
       }
       T[(k << TLs) + l] = make_double2(sa.x * scl, da.y * scl);
     }
-  } else if (p.kind == 0) {
+  } else if (kind == 0) {
     // DCT-I read in digit-reversed order: gather, then store
     cd wv[KMAX];
 #pragma unroll
@@ -603,13 +638,14 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
 }
 
 // ------------------------------------------------------------------ inverse
-template <int KMAX>
+template <int KMAX, class SH>
 __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const WallPlan p, int64_t L,
                                                                        const __grid_constant__ CUtensorMap tin,
                                                                        const __grid_constant__ CUtensorMap tout,
                                                                        int box_in, int box_out) {
   extern __shared__ __align__(1024) unsigned char wsm_raw[];
-  const int TLs = p.log2_lines, TL = 1 << TLs;
+  const int TLs = sh_tls<SH>(p), TL = 1 << TLs;
+  const int kind = sh_kind<SH>(p), Mv = sh_M<SH>(p);
   cd* T = reinterpret_cast<cd*>(wall_smem_base(wsm_raw));
   cd* side = T + (size_t)p.rows_smem * TL;
   uint64_t* bar = reinterpret_cast<uint64_t*>(side + 2 * TL);
@@ -692,9 +728,9 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     const cd ym = cheb(m, l), yn = cheb(N - m, l);
     return cmulc(make_double2(0.5 * (ym.x + yn.y), 0.5 * (ym.y - yn.x)), __ldg(p.mk + m));
   };
-  if (p.kind == 0) {  // Lobatto, power of two: f_j = DFT(even extension)_j / 2
-    wall_dft(p, T, TLs, nullptr, nullptr,
-             [&](int i, int l) { return T[((i <= nx ? i : p.M - i) << TLs) + l]; }, [](int, int, int, auto&) {});
+  if (kind == 0) {  // Lobatto, power of two: f_j = DFT(even extension)_j / 2
+    wall_dft<SH>(p, T, TLs, nullptr, nullptr,
+             [&](int i, int l) { return T[((i <= nx ? i : Mv - i) << TLs) + l]; }, [](int, int, int, auto&) {});
     const int items = N * TL;
     cd wv[KMAX];
 #pragma unroll
@@ -712,9 +748,9 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
       if (e < items) T[e] = wv[it];
     }
     __syncthreads();
-  } else if (p.kind == 1) {  // Rader, inverse sign: X'_k = V_0 + conv; rows sigma(k)
+  } else if (kind == 1) {  // Rader, inverse sign: X'_k = V_0 + conv; rows sigma(k)
     if (tid < TL) side[tid] = cheb(0, tid);  // V_0 = c_0 = coefficient 0
-    wall_dft(p, T, TLs, p.ker_i, side + TL, [&](int i, int l) { return vgauss(__ldg(p.gin_i + i), l); },
+    wall_dft<SH>(p, T, TLs, p.ker_i, side + TL, [&](int i, int l) { return vgauss(__ldg(p.gin_i + i), l); },
              [&](int n1, int q, int l, auto& v) {
                constexpr int R = sizeof(v) / sizeof(cd);
                const cd v0 = side[l];
@@ -728,7 +764,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_inverse_kernel(const Wal
     __syncthreads();
   } else {  // Bluestein
     const int Ld = p.Ld;
-    wall_dft(p, T, TLs, p.ker_i, nullptr,
+    wall_dft<SH>(p, T, TLs, p.ker_i, nullptr,
              [&](int i, int l) {
                if (i >= Ld) return make_double2(0.0, 0.0);
                const cd v = gauss ? (i == 0 ? cheb(0, l) : vgauss(i, l)) : T[((i <= nx ? i : Ld - i) << TLs) + l];
@@ -760,7 +796,7 @@ int wall_box_rows(int rows) {  // fewest boxes of <= 256 rows; 8-row multiples k
   return (((rows + nb - 1) / nb) + 7) & ~7;
 }
 
-template <int KMAX>
+template <int KMAX, class SH = WDyn>
 static cudaError_t launch_wall_k(const WallPlan& p, int64_t L, const void* in, void* out, cudaStream_t st) {
   const int TL = 1 << p.log2_lines;
   const int rows_in = p.direction == 0 ? p.N : p.n_in;
@@ -773,7 +809,7 @@ static cudaError_t launch_wall_k(const WallPlan& p, int64_t L, const void* in, v
       !encode_tiled_2d(&tout, out, 2 * (uint64_t)L, rows_out, (uint64_t)L * sizeof(double2), 2 * TL, bo))
     return cudaErrorNotSupported;
   const size_t smem = wall_smem_bytes(p);
-  auto kern = p.direction == 0 ? wall_forward_kernel<KMAX> : wall_inverse_kernel<KMAX>;
+  auto kern = p.direction == 0 ? wall_forward_kernel<KMAX, SH> : wall_inverse_kernel<KMAX, SH>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const unsigned grid = (unsigned)((L + TL - 1) / TL);
@@ -787,6 +823,12 @@ cudaError_t launch_wall(const WallPlan& p, int64_t L, const void* in, void* out,
   const int TL = 1 << p.log2_lines;
   const int items = (p.N * TL + kWallThreads - 1) / kWallThreads;  // register-staged rows per thread
   if (p.M / p.radix[0] * TL > kWallThreads) return cudaErrorInvalidValue;
+  // the config-3 shapes (n_x = 256) run their compile-time instantiations
+  if (p.kind == 1 && p.nstage == 2 && p.radix[0] == 16 && p.radix[1] == 16 && p.log2_lines == 4 && items <= 17)
+    return launch_wall_k<17, WShape<1, 2, 16, 16, 0, 4>>(p, L, in, out, st);
+  if (p.kind == 0 && p.nstage == 3 && p.radix[0] == 16 && p.radix[1] == 8 && p.radix[2] == 4 && p.log2_lines == 3 &&
+      items <= 9)
+    return launch_wall_k<9, WShape<0, 3, 16, 8, 4, 3>>(p, L, in, out, st);
   if (items <= 5) return launch_wall_k<5>(p, L, in, out, st);
   if (items <= 9) return launch_wall_k<9>(p, L, in, out, st);
   if (items <= 17) return launch_wall_k<17>(p, L, in, out, st);
