@@ -45,6 +45,20 @@ def _world(group):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
+def _all_to_all(recv, send, recv_sizes, send_sizes, group):
+    """all_to_all_single; with a gloo group, device tensors go through host
+    buffers (gloo has no CUDA all-to-all) -- the multi-rank path then also
+    runs with several ranks on one GPU (tests) or on CPU-only hosts."""
+    import torch.distributed as dist
+
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        r = recv.cpu()
+        dist.all_to_all_single(r, send.cpu(), recv_sizes, send_sizes, group=group)
+        recv.copy_(r)
+    else:
+        dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+
+
 def kx_rows(n_y: int, rank: int, world: int, rows_of=None):
     """The kx rows (ascending int64 array) rank `rank` holds after the exchange."""
     import numpy as np
@@ -77,7 +91,7 @@ def planes_to_kx(x, n_planes: int, group=None, rows_of=None):
     recv_sizes = [(plane_slab(n_planes, q, world)[1] - plane_slab(n_planes, q, world)[0]) * m * K
                   for q in range(world)]
     recv = torch.empty(sum(recv_sizes), dtype=x.dtype, device=x.device)
-    dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+    _all_to_all(recv, send, recv_sizes, send_sizes, group)
     # blocks arrive in rank order = plane order: already (n_planes, rows_r, K)
     return recv.view(n_planes, m, K)
 
@@ -101,7 +115,7 @@ def kx_to_planes(y, n_y: int, group=None, rows_of=None):
     rows = [kx_rows(n_y, q, world, rows_of) for q in range(world)]
     recv_sizes = [p * len(r) * K for r in rows]
     recv = torch.empty(sum(recv_sizes), dtype=y.dtype, device=y.device)
-    dist.all_to_all_single(recv, y.view(-1), recv_sizes, send_sizes, group=group)
+    _all_to_all(recv, y.view(-1), recv_sizes, send_sizes, group)
     out = torch.empty((p, n_y, K), dtype=y.dtype, device=y.device)
     for part, r in zip(torch.split(recv, recv_sizes), rows):
         out.index_copy_(1, torch.from_numpy(r).to(y.device), part.view(p, len(r), K))
