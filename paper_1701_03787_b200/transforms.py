@@ -193,7 +193,7 @@ def _chebyshev_pass(x, fam: int, space: int):
         from .wall import wall_plan
 
         plan = wall_plan(N - 1, fam, space, 0, False, _cheb_scale(N, fam))
-        if plan is not None:
+        if plan is not None and not (fam == 0 and plan.struct.log2_lines == 0):  # (route choice: wall_forward)
             return _wall_run(plan, x.contiguous(), plan.struct.n_out)
     M = 2 * N if fam == 0 else 2 * N - 2
     e = torch.empty((M, L), dtype=torch.complex128, device=x.device)
@@ -223,7 +223,7 @@ def _expand_pass(c, space: int, n_x: int, fam: int):
         from .wall import wall_plan
 
         plan = wall_plan(n_x, fam, space, 1, False, 1.0)
-        if plan is not None and plan.struct.n_in == n:
+        if plan is not None and plan.struct.n_in == n and not (fam == 0 and plan.struct.log2_lines == 0):
             return _wall_run(plan, c.contiguous(), N)
     lib = _lib.lib()
     st = stream_handle()
@@ -363,6 +363,22 @@ XFORM_METHOD = __import__("os").environ.get("SHEN_XFORM", "wall")
 
 # ---------------------------------------------------------------- wall-normal stage on lines
 
+# Route choice for large n_x (tools/wall_split_mass.py, 8192 and 33,024 lines):
+# the fused kernel's mass solve runs 2 TL serial chains per CTA, so with few
+# lines per tile the fused scalar product followed by the standalone
+# mass-solve kernel (one thread per (line, parity) over all lines) is faster:
+# TL <= 2 always (n_x = 1024 Lobatto, 33k lines: 4.59 -> 1.58 ms), TL = 4
+# once there are enough lines to fill the GPU with chains (n_x = 512
+# Lobatto: 0.76 -> 0.66 ms at 33k lines, but 0.20 -> 0.32 ms at 8192).  With
+# one line per tile (Gauss n_x >= 1024, Bluestein over M = 4096) the cuFFT
+# route is faster in both directions (3.5 vs 4.5 ms forward, 0.72 vs 0.98 ms
+# inverse at 8192 lines).
+
+
+def _split_mass(log2_lines: int, n_lines: int) -> bool:
+    return log2_lines <= 1 or (log2_lines == 2 and n_lines >= 16384)
+
+
 def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
     """(N, L) complex128 Fourier lines on the device -> (n_modes, L) Shen
     coefficients (scalar products if ``solve_mass`` is False)."""
@@ -370,7 +386,12 @@ def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
         from .wall import wall_plan
 
         plan = wall_plan(n_x, fam, sp, 0, solve_mass, _cheb_scale(n_x + 1, fam))
-        if plan is not None:
+        tls = plan.struct.log2_lines if plan is not None else -1
+        if plan is not None and not (fam == 0 and tls == 0):
+            if solve_mass and sp != 0 and _split_mass(tls, lines.shape[1]):
+                fsp = wall_plan(n_x, fam, sp, 0, False, _cheb_scale(n_x + 1, fam))
+                scal = _wall_run(fsp, lines.contiguous(), fsp.struct.n_out)
+                return _mass_pass(scal, sp, n_x, fam)
             return _wall_run(plan, lines.contiguous(), plan.struct.n_out)
     scal = _chebyshev_pass(lines, fam, sp)
     if solve_mass and sp != 0:
@@ -386,7 +407,7 @@ def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
         from .wall import wall_plan
 
         plan = wall_plan(n_x, fam, sp, 1, False, 1.0 / yz_points)
-        if plan is not None and plan.struct.n_in == coef.shape[0]:
+        if plan is not None and plan.struct.n_in == coef.shape[0] and not (fam == 0 and plan.struct.log2_lines == 0):
             return _wall_run(plan, coef.contiguous(), n_x + 1), "forward"
     return _expand_pass(coef, sp, n_x, fam), "backward"
 
