@@ -175,37 +175,98 @@ __global__ void xf_inv_post_kernel(int gl, int N, int64_t L, const double2* __re
 // Per parity p, the banded SPD system U^T U x = s (upper Cholesky factor U of
 // bandwidth nb = 1 or 2, LAPACK band storage rows (nb+1) x m per parity):
 // forward U^T y = s, backward U x = y (zpbtrs).  fac layout: [2][nb+1][mmax].
-__global__ void xf_mass_kernel(int nband, int n, int mmax, int64_t L, const double* __restrict__ fac,
-                               const double2* __restrict__ s, double2* __restrict__ x) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * L) return;
-  const int par = (int)(t / L);
-  const int64_t l = t - (int64_t)par * L;
+// Per CTA: the rows' reciprocal pivots and off-diagonal factor entries of
+// both parities are staged in shared memory once ([2][mmax + 1] each of
+// 1/U_ii, U_{i-1,i}, U_{i-2,i}); one thread per (line, parity), a warp =
+// 32 consecutive lines of one parity (coalesced 512-B row pieces); each sweep
+// keeps the next kQ rows' loads in flight in a register queue (the loads are
+// independent of the recurrence), so the sweep is bound by its FMA chain and
+// HBM rather than by load latency.  Arithmetic: y = (s - u1 y1 - u2 y2) / U_ii
+// and x = (y - U_{i,i+1} x1 - U_{i,i+2} x2) / U_ii with the division as a
+// product by the reciprocal, as before.
+constexpr int kMassQ = 4;
+
+// (s and x may be the same array: the in-place solve of transforms._mass_pass)
+__global__ void __launch_bounds__(256) xf_mass_kernel(int nband, int n, int mmax, int64_t L,
+                                                      const double* __restrict__ fac, const double2* s, double2* x) {
+  extern __shared__ double msm[];
+  double* rdg = msm;                       // [2][mmax + 1] 1 / U_ii
+  double* u1 = msm + 2 * (mmax + 1);       // [2][mmax + 1] U_{i-1,i} (0 for i = 0)
+  double* u2 = msm + 4 * (mmax + 1);       // [2][mmax + 1] U_{i-2,i} (0 for i < 2 or nband = 1)
+  for (int e = threadIdx.x; e < 2 * (mmax + 1); e += blockDim.x) {
+    const int p = e / (mmax + 1), i = e - p * (mmax + 1);
+    const int m = (n - p + 1) / 2;
+    const double* ab = fac + (int64_t)p * (nband + 1) * mmax;
+    double r = 0.0, a = 0.0, b = 0.0;
+    if (i < m) {
+      r = 1.0 / __ldg(ab + (int64_t)nband * mmax + i);
+      if (i >= 1) a = __ldg(ab + (int64_t)(nband - 1) * mmax + i);
+      if (nband == 2 && i >= 2) b = __ldg(ab + i);
+    }
+    rdg[e] = r;
+    u1[e] = a;
+    u2[e] = b;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nw = ((L + 31) / 32) * 2;  // warps of work: (32-line group, parity)
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (w >= nw) return;
+  const int par = (int)(w & 1);
+  const int64_t l = (w >> 1) * 32 + lane;
+  if (l >= L) return;
   const int m = (n - par + 1) / 2;
-  const double* ab = fac + (int64_t)par * (nband + 1) * mmax;
-  auto U = [&](int i, int j) -> double {  // U[i][j], j - i in [0, nband]
-    return __ldg(ab + (int64_t)(nband - (j - i)) * mmax + j);
-  };
-  auto row = [&](int i) -> int64_t { return (int64_t)(par + 2 * i) * L + l; };
+  const double* R = rdg + par * (mmax + 1);
+  const double* A = u1 + par * (mmax + 1);
+  const double* Bq = u2 + par * (mmax + 1);
+  const int64_t rs = 2 * L;
+  const double2* sp = s + (int64_t)par * L + l;
+  double2* xp = x + (int64_t)par * L + l;
+  // forward U^T y = s
+  c2 q[kMassQ];
+#pragma unroll
+  for (int k = 0; k < kMassQ; ++k) q[k] = k < m ? ld2(sp + k * rs) : c2{0.0, 0.0};
   c2 y1 = {0, 0}, y2 = {0, 0};
-  for (int i = 0; i < m; ++i) {
-    c2 acc = ld2(s + row(i));
-    if (i >= 1) acc = csub(acc, cscale(U(i - 1, i), y1));
-    if (nband == 2 && i >= 2) acc = csub(acc, cscale(U(i - 2, i), y2));
-    const c2 y = cscale(1.0 / U(i, i), acc);
-    st2(x + row(i), y);
-    y2 = y1;
-    y1 = y;
+  for (int i0 = 0; i0 < m; i0 += kMassQ) {
+#pragma unroll
+    for (int k = 0; k < kMassQ; ++k) {
+      const int i = i0 + k;
+      if (i < m) {
+        c2 acc = q[k];
+        const int inext = i + kMassQ;
+        q[k] = inext < m ? ld2(sp + inext * rs) : c2{0.0, 0.0};
+        acc = csub(acc, cscale(A[i], y1));
+        if (nband == 2) acc = csub(acc, cscale(Bq[i], y2));
+        const c2 y = cscale(R[i], acc);
+        st2(xp + i * rs, y);
+        y2 = y1;
+        y1 = y;
+      }
+    }
+  }
+  // backward U x = y (y read back from x, the queue refilled bottom-up)
+#pragma unroll
+  for (int k = 0; k < kMassQ; ++k) {
+    const int i = m - 1 - k;
+    q[k] = i >= 0 ? c2{xp[i * rs].x, xp[i * rs].y} : c2{0.0, 0.0};
   }
   c2 x1 = {0, 0}, x2 = {0, 0};
-  for (int i = m - 1; i >= 0; --i) {
-    c2 acc = {x[row(i)].x, x[row(i)].y};
-    if (i + 1 < m) acc = csub(acc, cscale(U(i, i + 1), x1));
-    if (nband == 2 && i + 2 < m) acc = csub(acc, cscale(U(i, i + 2), x2));
-    const c2 v = cscale(1.0 / U(i, i), acc);
-    st2(x + row(i), v);
-    x2 = x1;
-    x1 = v;
+  for (int i0 = m - 1; i0 >= 0; i0 -= kMassQ) {
+#pragma unroll
+    for (int k = 0; k < kMassQ; ++k) {
+      const int i = i0 - k;
+      if (i >= 0) {
+        c2 acc = q[k];
+        const int inext = i - kMassQ;
+        q[k] = inext >= 0 ? c2{xp[inext * rs].x, xp[inext * rs].y} : c2{0.0, 0.0};
+        if (i + 1 < m) acc = csub(acc, cscale(A[i + 1], x1));
+        if (nband == 2 && i + 2 < m) acc = csub(acc, cscale(Bq[i + 2], x2));
+        const c2 v = cscale(R[i], acc);
+        st2(xp + i * rs, v);
+        x2 = x1;
+        x1 = v;
+      }
+    }
   }
 }
 
@@ -241,8 +302,14 @@ cudaError_t launch_xf_inv_post(int gl, int N, int64_t L, const void* F, const vo
 cudaError_t launch_xf_mass(int nband, int n, int mmax, int64_t L, const double* fac, const void* s, void* x,
                            cudaStream_t st) {
   if (L <= 0) return cudaSuccess;
-  xf_mass_kernel<<<blocks_for(2 * L), 256, 0, st>>>(nband, n, mmax, L, fac, static_cast<const double2*>(s),
-                                                    static_cast<double2*>(x));
+  const int64_t warps = ((L + 31) / 32) * 2;
+  const size_t smem = (size_t)6 * (mmax + 1) * sizeof(double);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(xf_mass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  xf_mass_kernel<<<(unsigned)((warps + 7) / 8), 256, smem, st>>>(nband, n, mmax, L, fac, static_cast<const double2*>(s),
+                                                                 static_cast<double2*>(x));
   return cudaGetLastError();
 }
 
