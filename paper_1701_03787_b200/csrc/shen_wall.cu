@@ -34,6 +34,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "shen_common.cuh"
 #include "shen_kernels.h"
 #include "shen_tma.cuh"
@@ -149,11 +152,24 @@ struct Stage {
 // 16 x 16, Lobatto = powers of two 16 x 8 x 4) are template constants, so
 // every radix switch folds and the tile index math is constant shifts; any
 // other plan runs the dynamic instantiation (WDyn) of the same code.
-template <int K_, int S_, int R0_, int R1_, int R2_, int TLS_>
+template <int K_, int S_, int R0_, int R1_, int R2_, int TLS_, bool PIPE_ = false>
 struct WShape {
   static constexpr int K = K_, S = S_, R0 = R0_, R1 = R1_, R2 = R2_, TLS = TLS_;
+  // PIPE: barriers span the 256 DFT threads only (named barrier 1), for a
+  // kernel whose extra warps work on another tile meanwhile; a pipelined
+  // forward kernel built on it (8 DFT warps + 1 mass-sweep warp, two tile
+  // buffers, 1 CTA per SM) measured slower than two one-tile CTAs per SM
+  // (190 vs 149 us at C3): the DFT passes need the second CTA's warps
+  static constexpr bool PIPE = PIPE_;
 };
 using WDyn = WShape<-1, 0, 0, 0, 0, -1>;
+// barrier of the threads that run the DFT passes (all of them, or warps 0-7
+// of the pipelined kernel, whose ninth warp runs the mass sweeps meanwhile)
+template <class SH>
+__device__ __forceinline__ void wsync() {
+  if (SH::PIPE) asm volatile("bar.sync 1, 256;" ::: "memory");
+  else __syncthreads();
+}
 template <class SH>
 __device__ __forceinline__ int sh_kind(const WallPlan& p) { return SH::K >= 0 ? SH::K : p.kind; }
 template <class SH>
@@ -263,7 +279,7 @@ __device__ __forceinline__ void run_conv(int R, cd* T, int TLs, int M, const cd*
 // first DIF pass with a gather: position i of line l takes ld(i, l); every
 // thread loads all of its butterflies' inputs before any thread stores
 // (requires nb * TL <= threads), so the gather may read the rows it overwrites
-template <int R, class LD>
+template <class SH, int R, class LD>
 __device__ __forceinline__ void pass_dif_gather(cd* T, int TLs, int M, const cd* __restrict__ tw, LD ld) {
   const int Ls = M, q = M / R, nb = M / R, TL = 1 << TLs, tstep = 1;
   const int w = threadIdx.x;
@@ -274,7 +290,7 @@ __device__ __forceinline__ void pass_dif_gather(cd* T, int TLs, int M, const cd*
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = ld(n1 + q * j, l);
   }
-  __syncthreads();
+  wsync<SH>();
   if (act) {
     dft<R, false>(v);
     if (q > 1) {
@@ -288,7 +304,7 @@ __device__ __forceinline__ void pass_dif_gather(cd* T, int TLs, int M, const cd*
 }
 // last inverse DIT pass (Ls = M) with a scatter: natural output index i of
 // line l goes to st(i, l, value); loads all before any store (same condition)
-template <int R, class ST>
+template <class SH, int R, class ST>
 __device__ __forceinline__ void pass_dit_inv_scatter(cd* T, int TLs, int M, const cd* __restrict__ tw, ST st) {
   const int q = M / R, nb = M / R, TL = 1 << TLs;
   const int w = threadIdx.x;
@@ -304,26 +320,26 @@ __device__ __forceinline__ void pass_dit_inv_scatter(cd* T, int TLs, int M, cons
     }
     dft<R, true>(v);
   }
-  __syncthreads();
+  wsync<SH>();
   if (act) st(n1, q, l, v);  // outputs n1 + q k, k < R (v by reference: stays in registers)
 }
 
-template <class LD>
+template <class SH, class LD>
 __device__ __forceinline__ void gather_first(int R, cd* T, int TLs, int M, const cd* tw, LD ld) {
   switch (R) {
-    case 16: pass_dif_gather<16>(T, TLs, M, tw, ld); break;
-    case 8: pass_dif_gather<8>(T, TLs, M, tw, ld); break;
-    case 4: pass_dif_gather<4>(T, TLs, M, tw, ld); break;
-    default: pass_dif_gather<2>(T, TLs, M, tw, ld); break;
+    case 16: pass_dif_gather<SH, 16>(T, TLs, M, tw, ld); break;
+    case 8: pass_dif_gather<SH, 8>(T, TLs, M, tw, ld); break;
+    case 4: pass_dif_gather<SH, 4>(T, TLs, M, tw, ld); break;
+    default: pass_dif_gather<SH, 2>(T, TLs, M, tw, ld); break;
   }
 }
-template <class ST>
+template <class SH, class ST>
 __device__ __forceinline__ void scatter_last(int R, cd* T, int TLs, int M, const cd* tw, ST st) {
   switch (R) {
-    case 16: pass_dit_inv_scatter<16>(T, TLs, M, tw, st); break;
-    case 8: pass_dit_inv_scatter<8>(T, TLs, M, tw, st); break;
-    case 4: pass_dit_inv_scatter<4>(T, TLs, M, tw, st); break;
-    default: pass_dit_inv_scatter<2>(T, TLs, M, tw, st); break;
+    case 16: pass_dit_inv_scatter<SH, 16>(T, TLs, M, tw, st); break;
+    case 8: pass_dit_inv_scatter<SH, 8>(T, TLs, M, tw, st); break;
+    case 4: pass_dit_inv_scatter<SH, 4>(T, TLs, M, tw, st); break;
+    default: pass_dit_inv_scatter<SH, 2>(T, TLs, M, tw, st); break;
   }
 }
 
@@ -336,8 +352,8 @@ __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, cons
                                          ST st) {
   const int M = sh_M<SH>(p), S = sh_nst<SH>(p);
   int Ls = M;
-  gather_first(sh_rad<SH>(p, 0), T, TLs, M, p.tw, ld);
-  __syncthreads();
+  gather_first<SH>(sh_rad<SH>(p, 0), T, TLs, M, p.tw, ld);
+  wsync<SH>();
   if (ker == nullptr) {
     Ls /= sh_rad<SH>(p, 0);
 #pragma unroll
@@ -345,7 +361,7 @@ __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, cons
       if (s >= S) break;
       run_dif(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
       Ls /= sh_rad<SH>(p, s);
-      __syncthreads();
+      wsync<SH>();
     }
     return;
   }
@@ -357,9 +373,9 @@ __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, cons
       if (i == 0 && a0 != nullptr) a0[l] = T[l];
       T[(i << TLs) + l] = cmul(T[(i << TLs) + l], __ldg(ker + i));
     }
-    __syncthreads();
-    scatter_last(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
-    __syncthreads();
+    wsync<SH>();
+    scatter_last<SH>(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
+    wsync<SH>();
     return;
   }
   Ls /= sh_rad<SH>(p, 0);
@@ -368,22 +384,22 @@ __device__ __forceinline__ void wall_dft(const WallPlan& p, cd* T, int TLs, cons
     if (s >= S - 1) break;
     run_dif(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
     Ls /= sh_rad<SH>(p, s);
-    __syncthreads();
+    wsync<SH>();
   }
   // S - 1 = 1..3: the last stage's convolution pass
   const int RL = S == 2 ? sh_rad<SH>(p, 1) : S == 3 ? sh_rad<SH>(p, 2) : sh_rad<SH>(p, 3);
   run_conv(RL, T, TLs, M, ker, a0);  // Ls == radix[S-1]
-  __syncthreads();
+  wsync<SH>();
   Ls = RL;
 #pragma unroll
   for (int s = 2; s >= 1; --s) {
     if (s > S - 2) continue;
     Ls *= sh_rad<SH>(p, s);
     run_dit_inv(sh_rad<SH>(p, s), T, TLs, M, Ls, p.tw);
-    __syncthreads();
+    wsync<SH>();
   }
-  scatter_last(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
-  __syncthreads();
+  scatter_last<SH>(sh_rad<SH>(p, 0), T, TLs, M, p.tw, st);
+  wsync<SH>();
 }
 
 __device__ __forceinline__ int sigma(int i, int N) {  // Makhoul: v_i = x_sigma(i)
@@ -423,33 +439,13 @@ __device__ __forceinline__ void wall_store(cd* T, const CUtensorMap* tout, int r
   }
 }
 
+// DFT of a tile's lines and the Chebyshev scaling (everything of the
+// forward kernel before the stencil / mass solve); the 256 DFT threads.
 template <int KMAX, class SH>
-__global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const WallPlan p, int64_t L,
-                                                                       const __grid_constant__ CUtensorMap tin,
-                                                                       const __grid_constant__ CUtensorMap tout,
-                                                                       int box_in, int box_out) {
-  extern __shared__ __align__(1024) unsigned char wsm_raw[];
+__device__ __forceinline__ void fwd_dft_post(const WallPlan& p, cd* T, cd* side, int tid) {
   const int TLs = sh_tls<SH>(p), TL = 1 << TLs;
   const int kind = sh_kind<SH>(p), Mv = sh_M<SH>(p);
-  cd* T = reinterpret_cast<cd*>(wall_smem_base(wsm_raw));
-  cd* side = T + (size_t)p.rows_smem * TL;  // [2][TL]: x0, A(0)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(side + 2 * TL);
-  double* mf = reinterpret_cast<double*>(bar + 2);
-  const int64_t l0 = (int64_t)blockIdx.x * TL;
-  const int N = p.N, tid = threadIdx.x;
-#ifdef SHEN_WALL_POISON
-  for (int e = threadIdx.x; e < (p.rows_smem + 2) * TL; e += kWallThreads) T[e] = make_double2(__longlong_as_double(0x7ff8dead00000000LL), 0.0);
-  __syncthreads();
-#endif
-  WALL_TS(0);
-  wall_load(T, bar, &tin, N, box_in, TL, l0);
-  const bool do_mass = p.mass && (p.space == 1 || p.space == 2);
-  if (do_mass)
-    for (int e = tid; e < 16 * (p.mmax + 1); e += kWallThreads) mf[e] = __ldg(p.mfac + e);
-  if (tid < TL) side[tid] = make_double2(0.0, 0.0);
-  mb_wait(bar, 0);
-  __syncthreads();
-  WALL_TS(1);
+  const int N = p.N;
   const bool gauss = p.family == 0;
   // ---- DFT of the gathered sequence
   if (kind == 0) {  // power of two: Lobatto even extension z (Ld = M = 2 n_x)
@@ -481,7 +477,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
              });
     // w_0 = 2 V_0 (scaled), V_0 = x_0 + A(0)
     if (tid < TL) T[tid] = cscale(2.0 * scl, cadd(side[tid], side[TL + tid]));
-    __syncthreads();
+    wsync<SH>();
   } else {  // Bluestein
     const int Ld = p.Ld, nx = N - 1;
     wall_dft<SH>(p, T, TLs, p.ker_f, nullptr,
@@ -527,7 +523,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
       const int e = tid + it * kWallThreads;
       if (e < N * TL) wv[it] = cscale(scl, T[(__ldg(p.pinv + (e >> TLs)) << TLs) + (e & (TL - 1))]);
     }
-    __syncthreads();
+    wsync<SH>();
 #pragma unroll
     for (int it = 0; it < KMAX; ++it) {
       const int e = tid + it * kWallThreads;
@@ -536,24 +532,14 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
   } else {
     for (int e = tid; e < N * TL; e += kWallThreads) T[e] = cscale(scl, T[e]);
   }
-  __syncthreads();
-  WALL_TS(2);
-  // ---- Shen stencil (shen_scalar, transforms.py:89-110) and mass solve
-  if (do_mass) {
-    // the stencil rides the forward sweep: s_k needs w_k, w_{k+2}, w_{k+4}
-    // of the same parity, all at or ahead of the sweep, so y overwrites w in
-    // place.  U^T y = s then U x = y (the reference's zpbtrs, transforms.py:
-    // 173) in LAPACK's row order, one thread per (line, parity) -- a chunked
-    // (scan) split measured less accurate on the biharmonic mass matrix,
-    // whose recurrence is only marginally stable (roots near -0.98).  The
-    // host folds the stencil and the reciprocal pivots into per-row
-    // coefficients ([m][8]: a0 = 1/U_ii, a2 = c2/U_ii, a4 = c4/U_ii,
-    // f1 = U_{i-1,i}/U_ii, f2 = U_{i-2,i}/U_ii, g1 = U_{i,i+1}/U_ii,
-    // g2 = U_{i,i+2}/U_ii): one FMA per row on the dependency chain, the
-    // w window slides in registers and the next row's coefficients are
-    // loaded one row ahead.
-    if (tid < 2 * TL) {
-      const int l = tid & (TL - 1), par = tid >> TLs;
+}
+
+// Stencil + U^T y = s + U x = y for the (line, parity) system t < 2 TL of
+// the tile (the mass-solve block of the forward kernel, see below).
+__device__ __forceinline__ void fwd_mass_system(const WallPlan& p, cd* T, const double* mf, int TLs, int t) {
+  const int TL = 1 << TLs, n = p.n_out, sp = p.space;
+  {
+      const int l = t & (TL - 1), par = t >> TLs;
       const int m = (n - par + 1) / 2;
       const double2* F = reinterpret_cast<const double2*>(mf) + (size_t)par * (p.mmax + 1) * 4;  // [m][4] double2
       cd* col = T + (par << TLs) + l;  // row par + 2 i at col[i << (TLs + 1)]
@@ -603,7 +589,56 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
         Fc = Hc;
         Fd = Hd;
       }
-    }
+  }
+}
+
+template <int KMAX, class SH>
+__global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const WallPlan p, int64_t L,
+                                                                       const __grid_constant__ CUtensorMap tin,
+                                                                       const __grid_constant__ CUtensorMap tout,
+                                                                       int box_in, int box_out) {
+  extern __shared__ __align__(1024) unsigned char wsm_raw[];
+  const int TLs = sh_tls<SH>(p), TL = 1 << TLs;
+  const int kind = sh_kind<SH>(p), Mv = sh_M<SH>(p);
+  cd* T = reinterpret_cast<cd*>(wall_smem_base(wsm_raw));
+  cd* side = T + (size_t)p.rows_smem * TL;  // [2][TL]: x0, A(0)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(side + 2 * TL);
+  double* mf = reinterpret_cast<double*>(bar + 2);
+  const int64_t l0 = (int64_t)blockIdx.x * TL;
+  const int N = p.N, tid = threadIdx.x;
+#ifdef SHEN_WALL_POISON
+  for (int e = threadIdx.x; e < (p.rows_smem + 2) * TL; e += kWallThreads) T[e] = make_double2(__longlong_as_double(0x7ff8dead00000000LL), 0.0);
+  __syncthreads();
+#endif
+  WALL_TS(0);
+  wall_load(T, bar, &tin, N, box_in, TL, l0);
+  const bool do_mass = p.mass && (p.space == 1 || p.space == 2);
+  if (do_mass)
+    for (int e = tid; e < 16 * (p.mmax + 1); e += kWallThreads) mf[e] = __ldg(p.mfac + e);
+  if (tid < TL) side[tid] = make_double2(0.0, 0.0);
+  mb_wait(bar, 0);
+  __syncthreads();
+  WALL_TS(1);
+  const bool gauss = p.family == 0;
+  fwd_dft_post<KMAX, SH>(p, T, side, tid);
+  const int n = p.n_out, sp = p.space, nx = N - 1;
+  __syncthreads();
+  WALL_TS(2);
+  // ---- Shen stencil (shen_scalar, transforms.py:89-110) and mass solve
+  if (do_mass) {
+    // the stencil rides the forward sweep: s_k needs w_k, w_{k+2}, w_{k+4}
+    // of the same parity, all at or ahead of the sweep, so y overwrites w in
+    // place.  U^T y = s then U x = y (the reference's zpbtrs, transforms.py:
+    // 173) in LAPACK's row order, one thread per (line, parity) -- a chunked
+    // (scan) split measured less accurate on the biharmonic mass matrix,
+    // whose recurrence is only marginally stable (roots near -0.98).  The
+    // host folds the stencil and the reciprocal pivots into per-row
+    // coefficients ([m][8]: a0 = 1/U_ii, a2 = c2/U_ii, a4 = c4/U_ii,
+    // f1 = U_{i-1,i}/U_ii, f2 = U_{i-2,i}/U_ii, g1 = U_{i,i+1}/U_ii,
+    // g2 = U_{i,i+2}/U_ii): one FMA per row on the dependency chain, the
+    // w window slides in registers and the next row's coefficients are
+    // loaded one row ahead.
+    if (tid < 2 * TL) fwd_mass_system(p, T, mf, TLs, tid);
   } else if (sp != 3) {
     // stencil alone, in place: chunks of R rows per thread walked upwards in
     // k, the 4 rows past the chunk read before anyone writes
