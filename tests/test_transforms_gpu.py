@@ -204,3 +204,27 @@ def test_slab_transforms_single_rank(space):
     assert torch.equal(c, want)
     back = D.inverse_transform_slab(c, mesh, space)
     assert torch.equal(back, T.inverse_transform(T.SpectralField(want, wavenumber_grid(mesh, space), mesh)).data)
+
+
+@pytest.mark.parametrize("n_x,fi,L", [(512, 1, 17000), (512, 0, 2048), (1024, 0, 1024), (1024, 1, 1024)])
+def test_large_nx_routes_vs_oracle(n_x, fi, L):
+    """The large-n_x routes of wall_forward / wall_inverse (transforms._split_mass:
+    fused scalar product + standalone mass-solve kernel when tiles hold few
+    lines; the cuFFT route for one-line Gauss tiles) against the oracle."""
+    from paper_1701_03787_b200.wall import wall_plan
+
+    N = n_x + 1
+    plan = wall_plan(n_x, fi, 1, 0, True, T._cheb_scale(N, fi))
+    assert plan is not None and plan.struct.log2_lines <= 2
+    rng = np.random.default_rng(n_x + fi)
+    x = rng.standard_normal((N, L)) + 1j * rng.standard_normal((N, L))
+    mats = assemble(n_x, fi)
+    import torch
+
+    xd = torch.from_numpy(x).cuda()
+    for sc in (1, 2):
+        c = T.wall_forward(xd, n_x, fi, sc, True).cpu().numpy()
+        want = O.mass_solve(O.shen_scalar(x, fi == 1, sc), sc, mats)
+        _close(c, want, 1e-10 if sc == 2 else TOL)
+        back, _ = T.wall_inverse(torch.from_numpy(want).cuda(), n_x, fi, sc, 1)
+        _close(back.cpu().numpy(), O.chebyshev_evaluate(O.shen_expand(want, sc, n_x), fi == 1))
