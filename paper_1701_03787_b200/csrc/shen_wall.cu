@@ -496,7 +496,6 @@ __device__ __forceinline__ void fwd_dft_post(const WallPlan& p, cd* T, cd* side,
              });
   }
   // ---- Chebyshev scalar products w_k (k < N), in place
-  const int n = p.n_out, sp = p.space, nx = N - 1;
   const double scl = p.scale;
   if (kind == 1) {
     // already w (fused into the last FFT pass)
@@ -599,7 +598,6 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
                                                                        int box_in, int box_out) {
   extern __shared__ __align__(1024) unsigned char wsm_raw[];
   const int TLs = sh_tls<SH>(p), TL = 1 << TLs;
-  const int kind = sh_kind<SH>(p), Mv = sh_M<SH>(p);
   cd* T = reinterpret_cast<cd*>(wall_smem_base(wsm_raw));
   cd* side = T + (size_t)p.rows_smem * TL;  // [2][TL]: x0, A(0)
   uint64_t* bar = reinterpret_cast<uint64_t*>(side + 2 * TL);
