@@ -152,6 +152,78 @@ __global__ void apply_kernel(ApplyArgs a, const V* __restrict__ x, V* __restrict
   apply_walk<V, false>(a, t, [&](int j) { return O::ld(x + (int64_t)j * L + l); }, y, l);
 }
 
+// Many lines, parity-separable operator (every matrix of the set: all band
+// offsets and the tail start of one parity, so rows of parity p read only x
+// rows of parity (p + off) mod 2): one thread per (line, row parity) walks
+// its rows bottom-up -- twice the threads, half the chain of apply_kernel --
+// with the next rows' x loads issued ahead of the recurrence.  Each row gets
+// the operations of apply_walk in the same order (banded terms in offset
+// order onto zero, then the tail with its parity's suffix sum folded
+// bottom-up), so the results stay bit-identical.
+template <typename V>
+__global__ void __launch_bounds__(128) apply_par_kernel(ApplyArgs a, const V* __restrict__ x, V* __restrict__ y) {
+  using O = A<V>;
+  const int64_t L = a.L;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // (32-line group, parity)
+  const int par = (int)(w & 1);
+  const int64_t l = (w >> 1) * 32 + (threadIdx.x & 31);
+  if (l >= L) return;
+  auto X = [&](int j) { return O::ld(x + (int64_t)j * L + l); };
+  int k = a.nr - 1;
+  if ((k & 1) != par) --k;
+  if (a.kind == 2) {
+    // y = d x; sq/ss: suffix sums of q x, s x over rows of parity par from k + 2 down
+    V sq = O::zero(), ss = O::zero();
+    bool have = false;
+    for (; k >= 0; k -= 2) {
+      const int j = k + 2;
+      if (j < a.nr) {
+        const V xj = X(j);
+        const V qx = O::scale(__ldg(a.q + j), xj), sx = O::scale(__ldg(a.s + j), xj);
+        sq = have ? O::add(qx, sq) : qx;
+        ss = have ? O::add(sx, ss) : sx;
+        have = true;
+      }
+      V v = O::scale(__ldg(a.d + k), X(k));
+      if (k < a.nr - 2) {
+        v = O::add(v, O::scale(__ldg(a.p + k), sq));
+        v = O::add(v, O::scale(__ldg(a.r + k), ss));
+      }
+      y[(int64_t)k * L + l] = v;
+    }
+    return;
+  }
+  V S = O::zero();
+  bool have = false;
+  int next_j = -1;  // next x row of the tail parity to fold
+  if (a.kind == 1) {
+    next_j = a.nc - 1;
+    if ((next_j & 1) != ((par + a.tail_start) & 1)) --next_j;
+  }
+  for (; k >= 0; k -= 2) {
+    V v = O::zero();
+#pragma unroll
+    for (int q = 0; q < kMaxOff; ++q) {
+      if (q >= a.n_off) break;
+      const int dk = a.off[q];
+      const int k0 = dk < 0 ? -dk : 0, k1 = min(a.nr, a.nc - dk);
+      if (k >= k0 && k < k1) v = O::add(v, O::scale(__ldg(a.diag + (int64_t)q * a.nr + k), X(k + dk)));
+    }
+    if (a.kind == 1) {
+      const int j = k + a.tail_start;
+      if (j < a.nc) {
+        for (; next_j >= j; next_j -= 2) {
+          const V xj = X(next_j);
+          S = have ? O::add(xj, S) : xj;
+          have = true;
+        }
+        v = O::add(v, O::scale(__ldg(a.tail + k), S));
+      }
+    }
+    y[(int64_t)k * L + l] = v;
+  }
+}
+
 // Few lines (the stepper's mean-flow vectors, L = 1): a per-line walk is one
 // thread doing ~100 dependent instructions per row.  Here a block takes
 // stage_lines lines: (1) x and the row tables are staged in shared memory,
@@ -286,6 +358,18 @@ cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const i
                                                                          static_cast<double*>(y));
       return cudaGetLastError();
     }
+  }
+  bool separable = true;  // every band offset (and the tail start) of one parity
+  for (int i = 0; i < n_off; ++i) separable = separable && (((offs[i] - offs[0]) & 1) == 0);
+  if (kind == 1 && n_off > 0) separable = separable && (((tail_start - offs[0]) & 1) == 0);
+  if (separable) {
+    const int64_t warps = ((L + 31) / 32) * 2;
+    const unsigned pb = (unsigned)((warps + 3) / 4);
+    if (cplx_data)
+      apply_par_kernel<cplx><<<pb, 128, 0, st>>>(a, static_cast<const cplx*>(x), static_cast<cplx*>(y));
+    else
+      apply_par_kernel<double><<<pb, 128, 0, st>>>(a, static_cast<const double*>(x), static_cast<double*>(y));
+    return cudaGetLastError();
   }
   const unsigned blocks = (unsigned)((L + 127) / 128);
   if (cplx_data)

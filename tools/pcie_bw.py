@@ -1,7 +1,10 @@
 """Pinned host <-> device copy bandwidth on this box: 1-D copies one way and
 both ways concurrently, and the 2-D column-slab copies the pipelined solve
 uses (bytes per direction / s)."""
+import sys
 import time
+
+sys.path.insert(0, ".")
 
 import torch
 
