@@ -93,7 +93,7 @@ def _wall(plan, L, xin, rows_out):
 
 @pytest.mark.parametrize("fi", [0, 1])
 @pytest.mark.parametrize("sp", [0, 1, 2])
-@pytest.mark.parametrize("n_x,L", [(16, 37), (256, 1000), (24, 3), (63, 17)])
+@pytest.mark.parametrize("n_x,L", [(16, 37), (256, 1000), (24, 3), (63, 17), (100, 50), (127, 40), (300, 33)])
 def test_wall_transform_guards(fi, sp, n_x, L):
     """The fused wall-normal kernels (TMA boxes clipped at the array edges,
     partial line tiles) forward with the mass solve and inverse."""
