@@ -1108,6 +1108,11 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
     static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
     if (pw == 6 && bih_pair_smem<V, R, 3>(a) <= 227 * 1024) return bih_pair_launch<V, R, 3>(a, scratch, st);
     if (bih_pair_smem<V, R, 4>(a) <= 227 * 1024) return bih_pair_launch<V, R, 4>(a, scratch, st);
+    // larger n_x (the one-parity table alone is ~115 KB at n_x = 2048): a
+    // 4-warp pair CTA still fits (SHEN_PAIR_SMALL=0 falls through to the
+    // one-system kernel)
+    static const int small = getenv("SHEN_PAIR_SMALL") ? atoi(getenv("SHEN_PAIR_SMALL")) : 1;
+    if (small && bih_pair_smem<V, R, 2>(a) <= 227 * 1024) return bih_pair_launch<V, R, 2>(a, scratch, st);
   }
   // the table in shared memory beats a deeper ring: the biharmonic rows are
   // slow enough that one segment of prefetch covers HBM latency
