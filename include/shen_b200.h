@@ -96,16 +96,6 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                            const double* st, const double* md, int chunk_rows, const double* ckpt,
                            const void* rhs, void* out, void* scratch, int is_complex, int warps_per_sm,
                            int max_ctas, int64_t j_begin, int64_t j_end, void* stream);
-/* Chunk-split Helmholtz solve on mirror pairs, complex RHS: groups of 16
- * pairs (the layout of shen_bih_solve_stream_pairs), each parity column split
- * into 16 chunks solved in parallel and joined by two scans, so the backward
- * sweep re-reads the RHS from L2 instead of HBM and the factor recurrence
- * runs once per pair.  Same inputs as shen_helm_solve_stream with
- * chunk_rows = 8; rows_p0 <= 512 (n_x <= 1024), otherwise SHEN_ERR_ARG.
- * Replaces HelmholtzLU.solve (solvers.py:100-126). */
-int shen_helm_solve_split_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                                const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
-                                void* out, const int64_t* pairs, int64_t n_pairs, int max_ctas, void* stream);
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream);
 

@@ -87,8 +87,6 @@ _SIGS = {
                                               ctypes.c_int, _c_int64, _c_int64, _vp]),
     "shen_wall_transform": (ctypes.c_int, [ctypes.POINTER(ShenWallPlan), _c_int64, _vp, _vp, _vp]),
     "shen_wall_smem_bytes": (ctypes.c_int64, [ctypes.POINTER(ShenWallPlan)]),
-    "shen_helm_solve_split_pairs": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _c_int64, _vp, _vp, _vp,
-                                                   ctypes.c_int, _vp, _vp, _vp, _vp, _c_int64, ctypes.c_int, _vp]),
     "shen_helm_solve_stored": (ctypes.c_int, [ctypes.c_int, _c_int64, _pp, _vp, _vp, ctypes.c_int, _vp]),
     "shen_bih_factor": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, _vp, _vp, _c_int64, _vp, ctypes.c_int,
                                        _vp, _pp, ctypes.c_int, _vp, _vp]),

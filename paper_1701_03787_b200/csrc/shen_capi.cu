@@ -127,23 +127,6 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
                     "shen_helm_solve_stream");
 }
 
-int shen_helm_solve_split_pairs(int n_dir, double ca, const double* cb, int64_t batch, const double* sd,
-                                const double* st, const double* md, int chunk_rows, const double* ckpt, const void* rhs,
-                                void* out, const int64_t* pairs, int64_t n_pairs, int max_ctas, void* stream) {
-  if (n_dir < 1 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out || chunk_rows != 8 || max_ctas < 0 ||
-      !pairs || n_pairs < 0)
-    return fail(SHEN_ERR_ARG, "shen_helm_solve_split_pairs: bad args");
-  if ((n_dir + 1) / 2 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_split_pairs: ckpt");
-  if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_split_pairs: rhs must not alias out");
-  shen::HelmChunkArgs a{n_dir, ca, cb, batch, sd, st, md, chunk_rows, ckpt, rhs, out};
-  a.max_ctas = max_ctas;
-  a.pairs = pairs;
-  a.n_pairs = n_pairs;
-  const cudaError_t e = shen::launch_helm_split_pairs(a, S(stream));
-  if (e == cudaErrorNotSupported) return fail(SHEN_ERR_ARG, "shen_helm_solve_split_pairs: shape not supported");
-  return cuda_check(e, "shen_helm_solve_split_pairs");
-}
-
 int shen_helm_solve_stored(int n_dir, int64_t batch, const double* const* factors, const void* rhs, void* out,
                            int is_complex, void* stream) {
   if (batch == 0) return SHEN_OK;

@@ -86,9 +86,6 @@ struct HelmChunkArgs {
   void* out;
   int64_t jb = 0, je = -1;  // system range [jb, je) of the streaming solve (je < 0: whole batch)
   int max_ctas = 0;          // streaming solve: cap on persistent CTAs (0: one per SM)
-  // mirror pairs (chunk-split solve): pairs[0..P) and pairs[P..2P) share z2
-  const int64_t* pairs = nullptr;
-  int64_t n_pairs = 0;
 };
 
 struct BihChunkArgs {
@@ -121,8 +118,6 @@ cudaError_t launch_helm_stream(const HelmChunkArgs& a, void* scratch, bool compl
 cudaError_t launch_bih_stream(const BihChunkArgs& a, void* scratch, bool complex_rhs, int warps_per_sm,
                               cudaStream_t st);
 int64_t stream_scratch_bytes(int op, int n_modes, int chunk_rows, bool complex_rhs);
-// chunk-split Helmholtz solve on mirror pairs (shen_solve_split.cu): complex RHS, RHS read once from HBM
-cudaError_t launch_helm_split_pairs(const HelmChunkArgs& a, cudaStream_t st);
 // structured apply along the rows (shen_apply.cu): kind 0 banded, 1 constant tail, 2 rank-2 tail
 cudaError_t launch_apply(int kind, int nr, int nc, int64_t L, int n_off, const int* offs, const double* diag,
                          const double* tail, int tail_start, const double* d, const double* p, const double* q,

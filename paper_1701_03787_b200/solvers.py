@@ -207,16 +207,6 @@ def solve_many(jobs):
 
 MIRROR_PAIRS = _env_int("SHEN_PAIRS", 1)  # solve mirror-paired systems together (biharmonic stream)
 PAIRS_MIN = _env_int("SHEN_PAIRS_MIN", 8192)  # below: one system per thread (c1: 40 vs 33 us; c3 pairs: 0.097 vs 0.120 ms)
-# Helmholtz, complex RHS on mirror pairs: chunk-split kernel (RHS re-read from L2, csrc/shen_solve_split.cu)
-HELM_SPLIT = _env_int("SHEN_HELM_SPLIT", 0)
-
-
-def helm_split_ok(n_modes: int, R: int) -> bool:
-    """Shapes the chunk-split kernel takes: 8-row checkpoints, 2..4 segments
-    in each of the 16 chunks of a parity column (n_x <= 1024)."""
-    nseg0 = -(-((n_modes + 1) // 2) // 8)
-    return R == 8 and 2 <= nseg0 and -(-nseg0 // 16) <= 4
-
 
 def mirror_pairs(z2):
     """Pairs of systems with bitwise-identical z2 rows (the channel grid's
@@ -352,7 +342,6 @@ class HelmholtzLU:
         self.chunk_rows = int(chunk_rows)
         self._ckpt = ckpt
         self.method = method
-        self._pairs = None  # device (2, P) int64 mirror pairs (build_helmholtz), or None
         self._stored = stored  # list of 8 device tensors (exact factors) or None
         self._host = None
 
@@ -434,14 +423,6 @@ class HelmholtzLU:
             check(h.shen_helm_solve_stored(nd, B, ptrs, rhs_dev.data_ptr(), out_dev.data_ptr(),
                                            int(is_complex), sh), "shen_helm_solve_stored")
             del keep
-        elif (HELM_SPLIT and is_complex and self._pairs is not None and j0 == 0 and j1 in (-1, B)
-              and helm_split_ok(nd, self.chunk_rows) and rhs_dev.data_ptr() % 16 == 0 and out_dev.data_ptr() % 16 == 0):
-            sd, st, md = self._tab
-            ck = self._ckpt.data_ptr() if self._ckpt is not None else None
-            check(h.shen_helm_solve_split_pairs(nd, self.ca, self._cb.data_ptr(), B, sd.data_ptr(), st.data_ptr(),
-                                                md.data_ptr(), self.chunk_rows, ck, rhs_dev.data_ptr(),
-                                                out_dev.data_ptr(), self._pairs.data_ptr(), int(self._pairs.shape[1]),
-                                                max_ctas, sh), "shen_helm_solve_split_pairs")
         else:
             sd, st, md = self._tab
             ck = self._ckpt.data_ptr() if self._ckpt is not None else None
@@ -501,12 +482,7 @@ def build_helmholtz(mats: MatrixSet, nu: float, dt: float, z2, method: str = "st
         del keep
     if B > 0:
         _raise_pivot(pivot.cpu().numpy(), "Helmholtz")
-    lu = HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
-    if method == "stream" and MIRROR_PAIRS:
-        pr = mirror_pairs(z2)
-        if pr is not None and pr.shape[1] >= PAIRS_MIN:
-            lu._pairs = torch.from_numpy(np.ascontiguousarray(pr)).to(dev)
-    return lu
+    return HelmholtzLU(mats.n_x, mats.family, np.shape(z2), ca, cb_dev, tabs, R, ckpt, method, stored)
 
 
 # ------------------------------------------------------------------ biharmonic
