@@ -296,6 +296,20 @@ int shen_scale_lines(int64_t rows, int64_t L, const void* x, const double* c_re,
                      void* stream);
 int shen_cross(int64_t n, const double* fields, double* h, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Periodic (y, z) plane transforms of the 3-D transforms (reference
+ * transforms.py:181-205, numpy rfft2 / irfft2 over axes (1, 2)), one
+ * thread-block cluster per plane, one HBM pass each way.
+ * shen_plane_rfft2:  x  (n_planes, n_y, n_z) float64 -> X (n_planes, n_y, n_z/2+1) complex128
+ * shen_plane_irfft2: X -> x, times `scale` (1/(n_y n_z) = numpy's "backward"
+ *   norm; 1 = "forward"); imaginary parts of the z = 0 and z = n_z/2 columns
+ *   are ignored, as numpy's irfft does.
+ * Sizes: shen_plane_fft_supported(n_y, n_z) (256 x 256); others -> SHEN_ERR_ARG.
+ * ------------------------------------------------------------------- */
+int shen_plane_fft_supported(int n_y, int n_z);
+int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* X, void* stream);
+int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -340,6 +340,22 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream) {
   return cuda_check(shen::launch_cross(n, fields, h, S(stream)), "shen_cross");
 }
 
+int shen_plane_fft_supported(int n_y, int n_z) { return shen::plane_fft_supported(n_y, n_z) ? 1 : 0; }
+
+int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* X, void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z))
+    return fail(SHEN_ERR_ARG, "shen_plane_rfft2: bad args");
+  return cuda_check(shen::launch_plane_rfft2(n_planes, n_y, n_z, x, X, S(stream)), "shen_plane_rfft2");
+}
+
+int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z))
+    return fail(SHEN_ERR_ARG, "shen_plane_irfft2: bad args");
+  return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, S(stream)), "shen_plane_irfft2");
+}
+
 int shen_recover_velocity(const shen_recover_args* r, void* stream) {
   if (!r) return fail(SHEN_ERR_ARG, "shen_recover_velocity: NULL args");
   if (r->L == 0 || r->n_dir == 0) return SHEN_OK;

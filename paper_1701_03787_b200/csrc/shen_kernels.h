@@ -173,6 +173,12 @@ cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const dou
                                cudaStream_t st);
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
 
+// periodic (y, z) plane FFTs (shen_plane_fft.cu): one 8-CTA cluster per plane
+bool plane_fft_supported(int n_y, int n_z);
+cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, cudaStream_t st);
+cudaError_t launch_plane_irfft2(int64_t planes, int n_y, int n_z, const void* X, double* x, double scale,
+                                cudaStream_t st);
+
 // fused wall-normal transforms (shen_wall.cu); tables built on the host (wall.py)
 struct WallPlan {
   int direction;   // 0 forward (points -> coefficients), 1 inverse

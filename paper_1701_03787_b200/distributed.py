@@ -26,6 +26,7 @@ Plane split: balanced contiguous (sizes differ by at most one).
 from __future__ import annotations
 
 from .shard import kx_rows_folded
+from .transforms import plane_irfft2, plane_rfft2
 
 __all__ = ["plane_slab", "kx_rows", "planes_to_kx", "kx_to_planes", "forward_transform_slab", "inverse_transform_slab"]
 
@@ -132,7 +133,7 @@ def forward_transform_slab(u_planes, mesh, space, group=None, solve_mass: bool =
     from .transforms import wall_forward
 
     N = mesh.n_x + 1
-    fourier = torch.fft.rfft2(u_planes.to(torch.float64), dim=(1, 2)).contiguous()
+    fourier = plane_rfft2(u_planes.to(torch.float64))
     cols = planes_to_kx(fourier, N, group, rows_of)
     m, K = cols.shape[1], cols.shape[2]
     out = wall_forward(cols.reshape(N, m * K), mesh.n_x, family_code(mesh.family), space_code(space), solve_mass)
@@ -151,4 +152,4 @@ def inverse_transform_slab(c_slab, mesh, space, group=None, rows_of=None):
     lines, norm = wall_inverse(c_slab.to(torch.complex128).reshape(n, m * K).contiguous(), mesh.n_x,
                                family_code(mesh.family), space_code(space), mesh.n_y * mesh.n_z)
     planes = kx_to_planes(lines.reshape(mesh.n_x + 1, m, K), mesh.n_y, group, rows_of)
-    return torch.fft.irfft2(planes, s=(mesh.n_y, mesh.n_z), dim=(1, 2), norm=norm)
+    return plane_irfft2(planes, mesh.n_y, mesh.n_z, norm)

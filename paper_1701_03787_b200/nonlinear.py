@@ -31,6 +31,7 @@ import numpy as np
 from . import _lib
 from ._device import device, is_torch, stream_handle
 from .mesh import family_code
+from .transforms import plane_irfft2, plane_rfft2
 
 __all__ = ["NonlinearTerm", "compute_nonlinear"]
 
@@ -110,14 +111,13 @@ class NonlinearTerm:
         self._wall(self._inv_ddx, self._deriv(w_hat.view(w_hat.shape[0], L)), spec[5])
         self._scale(spec[0], self._cm, spec[6])  # du/dy lines
         self._scale(spec[0], self._cn, spec[7])  # du/dz lines
-        phys = torch.fft.irfft2(spec.view(8, N, self.n_y, self.nzh), s=(self.n_y, self.n_z), dim=(2, 3),
-                                norm="forward").contiguous()
+        phys = plane_irfft2(spec.view(8, N, self.n_y, self.nzh), self.n_y, self.n_z, "forward")
         del spec
         npt = N * self.n_y * self.n_z
         h = torch.empty((3, N, self.n_y, self.n_z), dtype=torch.float64, device=self.dev)
         _lib.check(_lib.lib().shen_cross(npt, phys.data_ptr(), h.data_ptr(), stream_handle()), "shen_cross")
         del phys
-        hf = torch.fft.rfft2(h, dim=(2, 3)).contiguous().view(3, N, L)
+        hf = plane_rfft2(h).view(3, N, L)
         del h
         n_dir = self.n_x - 1
         out = []

@@ -36,6 +36,7 @@ without the library or a GPU every call raises ``ShenBackendError``.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from functools import lru_cache
 
@@ -167,8 +168,6 @@ def _fam(family) -> int:
 
 def _wall_run(plan, x, rows_out):
     """shen_wall_transform of (rows_in, L) complex128 lines -> (rows_out, L)."""
-    import ctypes
-
     import torch
 
     L = x.shape[1]
@@ -414,6 +413,40 @@ def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
 
 # ---------------------------------------------------------------- 3-D transforms
 
+def plane_rfft2(u):
+    """numpy ``rfft2`` over the last two axes of a contiguous float64 CUDA
+    tensor (..., n_y, n_z).  256 x 256 planes run on the cluster kernel of
+    ``csrc/shen_plane_fft.cu`` (one HBM pass); other sizes on cuFFT."""
+    import torch
+
+    n_y, n_z = u.shape[-2], u.shape[-1]
+    if not _lib.lib().shen_plane_fft_supported(n_y, n_z):
+        return torch.fft.rfft2(u, dim=(-2, -1)).contiguous()
+    u = u.contiguous()
+    out = torch.empty(u.shape[:-1] + (n_z // 2 + 1,), dtype=torch.complex128, device=u.device)
+    planes = u.numel() // (n_y * n_z)
+    _lib.check(_lib.lib().shen_plane_rfft2(planes, n_y, n_z, u.data_ptr(), out.data_ptr(), stream_handle()),
+               "shen_plane_rfft2")
+    return out
+
+
+def plane_irfft2(X, n_y: int, n_z: int, norm: str = "backward"):
+    """numpy ``irfft2(X, s=(n_y, n_z), norm=norm)`` over the last two axes of
+    a contiguous complex128 CUDA tensor (..., n_y, n_z/2 + 1); cluster kernel
+    for 256 x 256 planes, cuFFT otherwise."""
+    import torch
+
+    if not _lib.lib().shen_plane_fft_supported(n_y, n_z) or X.shape[-1] != n_z // 2 + 1 or X.shape[-2] != n_y:
+        return torch.fft.irfft2(X, s=(n_y, n_z), dim=(-2, -1), norm=norm)
+    X = X.contiguous()
+    out = torch.empty(X.shape[:-1] + (n_z,), dtype=torch.float64, device=X.device)
+    planes = X.numel() // (n_y * (n_z // 2 + 1))
+    scale = {"backward": 1.0 / (n_y * n_z), "forward": 1.0, "ortho": 1.0 / np.sqrt(n_y * n_z)}[norm]
+    _lib.check(_lib.lib().shen_plane_irfft2(planes, n_y, n_z, X.data_ptr(), out.data_ptr(), ctypes.c_double(scale),
+                                            stream_handle()), "shen_plane_irfft2")
+    return out
+
+
 def _physical_to_device(field: PhysicalField):
     import torch
 
@@ -433,7 +466,7 @@ def _forward(field: PhysicalField, space, solve_mass: bool):
     sp = space_code(space)
     fam = _fam(mesh.family)
     u, from_numpy = _physical_to_device(field)
-    fourier = torch.fft.rfft2(u, dim=(1, 2)).contiguous()
+    fourier = plane_rfft2(u)
     del u
     N = fourier.shape[0]
     yz = tuple(fourier.shape[1:])
@@ -477,7 +510,7 @@ def inverse_transform(coeffs: SpectralField) -> PhysicalField:
     _check_expand_rows(n, sp, mesh.n_x)
     lines, norm = wall_inverse(t.reshape(n, -1), mesh.n_x, fam, sp, mesh.n_y * mesh.n_z)
     del t
-    data = torch.fft.irfft2(lines.reshape((mesh.n_x + 1,) + yz), s=(mesh.n_y, mesh.n_z), dim=(1, 2), norm=norm)
+    data = plane_irfft2(lines.reshape((mesh.n_x + 1,) + yz), mesh.n_y, mesh.n_z, norm)
     if from_numpy:
         data = data.cpu().numpy()
     return PhysicalField(data, mesh)

@@ -32,7 +32,7 @@ def test_nonlinear_vs_reference_golden(golden, fi):
         _close(out[i], g[f"{k}_nl{i}"])
 
 
-@pytest.mark.parametrize("n_x,n_y,n_z", [(64, 16, 12), (128, 32, 32)])
+@pytest.mark.parametrize("n_x,n_y,n_z", [(64, 16, 12), (128, 32, 32), (16, 256, 256)])
 @pytest.mark.parametrize("fi", [0, 1])
 def test_nonlinear_vs_oracle_larger(n_x, n_y, n_z, fi):
     import torch

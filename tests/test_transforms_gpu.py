@@ -228,3 +228,31 @@ def test_large_nx_routes_vs_oracle(n_x, fi, L):
         _close(c, want, 1e-10 if sc == 2 else TOL)
         back, _ = T.wall_inverse(torch.from_numpy(want).cuda(), n_x, fi, sc, 1)
         _close(back.cpu().numpy(), O.chebyshev_evaluate(O.shen_expand(want, sc, n_x), fi == 1))
+
+
+@pytest.mark.parametrize("lead", [(1,), (3,), (2, 5)])
+def test_plane_fft_vs_numpy(lead):
+    """256 x 256 (y, z) planes on the cluster kernel (csrc/shen_plane_fft.cu):
+    rfft2 / irfft2 as numpy's (reference transforms.py:181-205), every norm;
+    irfft2 ignores the imaginary parts of the z = 0 and z = n_z/2 columns as
+    numpy does."""
+    import torch
+
+    from paper_1701_03787_b200 import _lib
+    from paper_1701_03787_b200.transforms import plane_irfft2, plane_rfft2
+
+    assert _lib.lib().shen_plane_fft_supported(256, 256) == 1
+    rng = np.random.default_rng(len(lead))
+    x = rng.uniform(-1, 1, lead + (256, 256))
+    X = plane_rfft2(torch.from_numpy(x).cuda())
+    want = np.fft.rfft2(x)
+    assert X.shape == want.shape and X.dtype == torch.complex128
+    assert np.abs(X.cpu().numpy() - want).max() <= 1e-14 * np.abs(want).max()
+    Y = rng.standard_normal(want.shape) + 1j * rng.standard_normal(want.shape)
+    for norm in ("backward", "forward", "ortho"):
+        back = plane_irfft2(torch.from_numpy(Y).cuda(), 256, 256, norm).cpu().numpy()
+        wantb = np.fft.irfft2(Y, s=(256, 256), norm=norm)
+        assert back.shape == wantb.shape
+        assert np.abs(back - wantb).max() <= 1e-14 * np.abs(wantb).max(), norm
+    rt = plane_irfft2(X, 256, 256).cpu().numpy()
+    assert np.abs(rt - x).max() <= 1e-14
