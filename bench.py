@@ -565,7 +565,7 @@ def run_c3(args):
         "stages_ms": stages,
         "wall_normal_stages": wall["stages"],
         "roofline": wall["roofline"],
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": 10 * args.steps,  # per step: 2 x (plane rfft2, wall forward, solve, wall inverse, plane irfft2)
         "solved_unknowns_per_s": unk * args.steps / (total_ms / 1e3),
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }))
@@ -605,7 +605,24 @@ def c3_wall_stages(mesh, u, B):
             ms = e0.elapsed_time(e1) / 10
             byts = rows * L * 16
             res[f"{kind}_{name}"] = {"ms": ms, "bytes": byts, "GBps_alg": byts / (ms * 1e6), "frac": byts / (ms * 1e6) / peak}
-    dom = max(res, key=lambda k: res[k]["ms"])
+    # the periodic plane FFTs (csrc/shen_plane_fft.cu): 257 planes, real 256 x 256 <-> 256 x 129 complex
+    planes = mesh.n_x + 1
+    pbytes = planes * mesh.n_y * (mesh.n_z * 8 + (mesh.n_z // 2 + 1) * 16)
+    spec = T.plane_rfft2(u)
+    for kind, fn in (("plane_rfft2", lambda: T.plane_rfft2(u)),
+                     ("plane_irfft2", lambda: T.plane_irfft2(spec, mesh.n_y, mesh.n_z, "forward"))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        res[kind] = {"ms": ms, "bytes": pbytes, "GBps_alg": pbytes / (ms * 1e6), "frac": pbytes / (ms * 1e6) / peak}
+    dom = max((k for k in res if not k.startswith("plane")), key=lambda k: res[k]["ms"])
     # DRAM bytes per launch of that kernel from the committed ncu launch list
     # (profiles/r02/c3_launches_summary.json, cold-cache serialised launches)
     traffic, tsrc = None, None

@@ -13,3 +13,10 @@ ncu --set full --import-source on --clock-control none -k regex:'wall_' -s 12 -c
     python bench.py --config c3 --steps 1 --warmup 3 > gpurun_out/c3_ncu_full.log 2>&1
 ncu -i /tmp/c3_wall_full.ncu-rep --page raw --csv > gpurun_out/c3_wall_full_raw.csv
 ncu -i /tmp/c3_wall_full.ncu-rep --page details --csv > gpurun_out/c3_wall_full_details.csv
+# 4. one ncu --set full capture of each plane FFT kernel at the c3 size (257 planes)
+for k in rfft2 irfft2; do
+  ncu --set full --import-source on --clock-control none --kernel-name-base function -k regex:"^${k}_256_kernel" \
+      -s 3 -c 1 -o /tmp/c3_plane_$k -f python tools/plane_fft_check.py > gpurun_out/c3_plane_$k.log 2>&1
+  ncu -i /tmp/c3_plane_$k.ncu-rep --page details --csv > gpurun_out/c3_plane_${k}_details.csv
+  ncu -i /tmp/c3_plane_$k.ncu-rep --page raw --csv > gpurun_out/c3_plane_${k}_raw.csv
+done
