@@ -344,15 +344,17 @@ int shen_plane_fft_supported(int n_y, int n_z) { return shen::plane_fft_supporte
 
 int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* X, void* stream) {
   if (n_planes == 0) return SHEN_OK;
-  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z))
-    return fail(SHEN_ERR_ARG, "shen_plane_rfft2: bad args");
+  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
+      (reinterpret_cast<uintptr_t>(X) & 15))
+    return fail(SHEN_ERR_ARG, "shen_plane_rfft2: bad args (sizes: shen_plane_fft_supported; x 8-B, X 16-B aligned)");
   return cuda_check(shen::launch_plane_rfft2(n_planes, n_y, n_z, x, X, S(stream)), "shen_plane_rfft2");
 }
 
 int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream) {
   if (n_planes == 0) return SHEN_OK;
-  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z))
-    return fail(SHEN_ERR_ARG, "shen_plane_irfft2: bad args");
+  if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
+      (reinterpret_cast<uintptr_t>(X) & 15))
+    return fail(SHEN_ERR_ARG, "shen_plane_irfft2: bad args (sizes: shen_plane_fft_supported; x 8-B, X 16-B aligned)");
   return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, S(stream)), "shen_plane_irfft2");
 }
 

@@ -84,11 +84,14 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_scale_lines": (2, 2, None, None, None, None, None),
         "shen_cross": (8, None, None, None),
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
+        "shen_plane_rfft2": (1, 128, 256, 16, 16, None),  # unsupported plane size
+        "shen_plane_irfft2": (1, 256, 256, 24, 8, ctypes.c_double(1.0), None),  # X not 16-B aligned
     }
     for name, args in cases.items():
         st = getattr(h, name)(*args)
         assert st == 1, name
         assert name.encode() in h.shen_last_error() or b"bad args" in h.shen_last_error(), name
+    assert h.shen_plane_fft_supported(256, 256) == 1 and h.shen_plane_fft_supported(64, 32) == 0
     for name, cls in (("shen_rhs_g", _lib.ShenRhsGArgs), ("shen_rhs_u", _lib.ShenRhsUArgs),
                       ("shen_recover_velocity", _lib.ShenRecoverArgs)):
         a = cls()
