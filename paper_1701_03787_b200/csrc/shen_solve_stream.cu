@@ -1084,8 +1084,12 @@ static size_t bih_pair_smem(const BihChunkArgs& a) {
 template <typename V, int R, int SG>
 static cudaError_t bih_pair_launch(const BihChunkArgs& a, void* scratch, cudaStream_t st) {
   constexpr int kT = 64 * SG;
-  const size_t smem = bih_pair_smem<V, R, SG>(a);
+  size_t smem = bih_pair_smem<V, R, SG>(a);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  // the 8-warp CTA allocates all 512 TMEM columns: request enough shared
+  // memory that a second CTA can never be resident on the SM (it would spin
+  // in tcgen05.alloc until the first one exits)
+  if (SG == 4 && SHEN_PAIR_TMEM_SEGS > 0) smem = std::max(smem, (size_t)116 * 1024);
   auto kern = bih_pair_kernel<V, R, SG>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
