@@ -533,61 +533,61 @@ __device__ __forceinline__ void fwd_dft_post(const WallPlan& p, cd* T, cd* side,
   }
 }
 
-// Stencil + U^T y = s + U x = y for the (line, parity) system t < 2 TL of
-// the tile (the mass-solve block of the forward kernel, see below).
+// Stencil + U^T y = s + U x = y for the (line, parity, re | im) chain
+// t < 4 TL of the tile (the mass-solve block of the forward kernel, see below).
+// The factors are real, so the real and imaginary parts of a line are
+// independent chains: they run on different warps (t >> (TLs + 1) = 0 | 1),
+// which halves the fp64 issue per warp and row step.
 __device__ __forceinline__ void fwd_mass_system(const WallPlan& p, cd* T, const double* mf, int TLs, int t) {
   const int TL = 1 << TLs, n = p.n_out, sp = p.space;
-  {
-      const int l = t & (TL - 1), par = t >> TLs;
-      const int m = (n - par + 1) / 2;
-      const double2* F = reinterpret_cast<const double2*>(mf) + (size_t)par * (p.mmax + 1) * 4;  // [m][4] double2
-      cd* col = T + (par << TLs) + l;  // row par + 2 i at col[i << (TLs + 1)]
-      const int rs = 1 << (TLs + 1);
-      // w rows i, i+1, i+2 (w_k, w_{k+2}, w_{k+4}) in a register queue; row
-      // i+3 is loaded one iteration before its use (issued before the store
-      // of row i, so it need not wait behind it), as are the next row's
-      // coefficients
-      cd q0 = col[0], q1 = col[rs], q2 = col[2 * rs];
-      cd y1 = make_double2(0.0, 0.0), y2 = y1;
-      double2 F0 = F[0], F1 = F[1], F2 = F[2];
-#pragma unroll 2
-      for (int i = 0; i < m; ++i) {
-        const cd q3 = col[min(i + 3, m + 1) * rs];  // (rows past i + 2 = m + 1 are never used)
-        const double2 G0 = F[4 * (i + 1)], G1 = F[4 * (i + 1) + 1], G2 = F[4 * (i + 1) + 2];  // next row
-        const cd wc = sp == 2 ? q2 : make_double2(0.0, 0.0);
-        // t = a0 w_k - a2 w_{k+2} + a4 w_{k+4} - f2 y_{i-2};  y = t - f1 y_{i-1}
-        cd t = make_double2(fma(F0.x, q0.x, fma(-F0.y, q1.x, fma(F1.x, wc.x, -F2.x * y2.x))),
-                            fma(F0.x, q0.y, fma(-F0.y, q1.y, fma(F1.x, wc.y, -F2.x * y2.y))));
-        const cd y = make_double2(fma(-F1.y, y1.x, t.x), fma(-F1.y, y1.y, t.y));
-        col[i * rs] = y;
-        y2 = y1;
-        y1 = y;
-        q0 = q1;
-        q1 = q2;
-        q2 = q3;
-        F0 = G0;
-        F1 = G1;
-        F2 = G2;
-      }
-      cd x1 = make_double2(0.0, 0.0), x2 = x1;
-      const int il = m > 0 ? m - 1 : 0;
-      cd yn = col[il * rs];
-      double2 Fa = F[4 * il], Fc = F[4 * il + 2], Fd = F[4 * il + 3];
-#pragma unroll 2
-      for (int i = m - 1; i >= 0; --i) {
-        const cd yk = yn;
-        const int ip = i > 0 ? i - 1 : 0;  // next (upper) row, loaded one iteration ahead
-        yn = col[ip * rs];
-        const double2 Ha = F[4 * ip], Hc = F[4 * ip + 2], Hd = F[4 * ip + 3];  // a0 | f2 g1 | g2 -
-        const cd t = make_double2(fma(Fa.x, yk.x, -Fd.x * x2.x), fma(Fa.x, yk.y, -Fd.x * x2.y));
-        const cd x = make_double2(fma(-Fc.y, x1.x, t.x), fma(-Fc.y, x1.y, t.y));
-        col[i * rs] = x;
-        x2 = x1;
-        x1 = x;
-        Fa = Ha;
-        Fc = Hc;
-        Fd = Hd;
-      }
+  const int l = t & (TL - 1), par = (t >> TLs) & 1, comp = t >> (TLs + 1);
+  const int m = (n - par + 1) / 2;
+  const double2* F = reinterpret_cast<const double2*>(mf) + (size_t)par * (p.mmax + 1) * 4;  // [m][4] double2
+  double* col = reinterpret_cast<double*>(T + (par << TLs) + l) + comp;  // row par + 2 i at col[i * rs]
+  const int rs = 2 << (TLs + 1);
+  // w rows i, i+1, i+2 (w_k, w_{k+2}, w_{k+4}) in a register queue; row
+  // i+3 is loaded one iteration before its use (issued before the store
+  // of row i, so it need not wait behind it), as are the next row's
+  // coefficients
+  double q0 = col[0], q1 = col[rs], q2 = col[2 * rs];
+  double y1 = 0.0, y2 = 0.0;
+  double2 F0 = F[0], F1 = F[1], F2 = F[2];
+#pragma unroll 4
+  for (int i = 0; i < m; ++i) {
+    const double q3 = col[min(i + 3, m + 1) * rs];  // (rows past i + 2 = m + 1 are never used)
+    const double2 G0 = F[4 * (i + 1)], G1 = F[4 * (i + 1) + 1], G2 = F[4 * (i + 1) + 2];  // next row
+    const double wc = sp == 2 ? q2 : 0.0;
+    // t = a0 w_k - a2 w_{k+2} + a4 w_{k+4} - f2 y_{i-2};  y = t - f1 y_{i-1}
+    const double tt = fma(F0.x, q0, fma(-F0.y, q1, fma(F1.x, wc, -F2.x * y2)));
+    const double y = fma(-F1.y, y1, tt);
+    col[i * rs] = y;
+    y2 = y1;
+    y1 = y;
+    q0 = q1;
+    q1 = q2;
+    q2 = q3;
+    F0 = G0;
+    F1 = G1;
+    F2 = G2;
+  }
+  double x1 = 0.0, x2 = 0.0;
+  const int il = m > 0 ? m - 1 : 0;
+  double yn = col[il * rs];
+  double2 Fa = F[4 * il], Fc = F[4 * il + 2], Fd = F[4 * il + 3];
+#pragma unroll 4
+  for (int i = m - 1; i >= 0; --i) {
+    const double yk = yn;
+    const int ip = i > 0 ? i - 1 : 0;  // next (upper) row, loaded one iteration ahead
+    yn = col[ip * rs];
+    const double2 Ha = F[4 * ip], Hc = F[4 * ip + 2], Hd = F[4 * ip + 3];  // a0 | f2 g1 | g2 -
+    const double tt = fma(Fa.x, yk, -Fd.x * x2);
+    const double x = fma(-Fc.y, x1, tt);
+    col[i * rs] = x;
+    x2 = x1;
+    x1 = x;
+    Fa = Ha;
+    Fc = Hc;
+    Fd = Hd;
   }
 }
 
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
     // the stencil rides the forward sweep: s_k needs w_k, w_{k+2}, w_{k+4}
     // of the same parity, all at or ahead of the sweep, so y overwrites w in
     // place.  U^T y = s then U x = y (the reference's zpbtrs, transforms.py:
-    // 173) in LAPACK's row order, one thread per (line, parity) -- a chunked
+    // 173) in LAPACK's row order, one thread per (line, parity, re | im) -- a chunked
     // (scan) split measured less accurate on the biharmonic mass matrix,
     // whose recurrence is only marginally stable (roots near -0.98).  The
     // host folds the stencil and the reciprocal pivots into per-row
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kWallThreads, 2) wall_forward_kernel(const Wal
     // g2 = U_{i,i+2}/U_ii): one FMA per row on the dependency chain, the
     // w window slides in registers and the next row's coefficients are
     // loaded one row ahead.
-    if (tid < 2 * TL) fwd_mass_system(p, T, mf, TLs, tid);
+    if (tid < 4 * TL) fwd_mass_system(p, T, mf, TLs, tid);
   } else if (sp != 3) {
     // stencil alone, in place: chunks of R rows per thread walked upwards in
     // k, the 4 rows past the chunk read before anyone writes
