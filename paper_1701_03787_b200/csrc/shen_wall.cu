@@ -545,49 +545,78 @@ __device__ __forceinline__ void fwd_mass_system(const WallPlan& p, cd* T, const 
   const double2* F = reinterpret_cast<const double2*>(mf) + (size_t)par * (p.mmax + 1) * 4;  // [m][4] double2
   double* col = reinterpret_cast<double*>(T + (par << TLs) + l) + comp;  // row par + 2 i at col[i * rs]
   const int rs = 2 << (TLs + 1);
-  // w rows i, i+1, i+2 (w_k, w_{k+2}, w_{k+4}) in a register queue; row
-  // i+3 is loaded one iteration before its use (issued before the store
-  // of row i, so it need not wait behind it), as are the next row's
-  // coefficients
-  double q0 = col[0], q1 = col[rs], q2 = col[2 * rs];
+  // Blocks of KB rows.  A block's w rows and coefficients are loaded while the
+  // previous block's chain runs (before its stores: later rows, never
+  // overwritten by them), the stencil parts t0 = a0 w_k - a2 w_{k+2} + a4 w_{k+4}
+  // of a block are independent FMAs, and only y_i = (t0_i - f2 y_{i-2}) - f1 y_{i-1}
+  // is serial: one FMA per row behind y_{i-1}.  (A row-at-a-time loop stalls
+  // the warp on each row's own load -> FMA chain: ~55 cycles per row.)
+  constexpr int KB = 4;
+  const bool bih = sp == 2;
   double y1 = 0.0, y2 = 0.0;
-  double2 F0 = F[0], F1 = F[1], F2 = F[2];
-#pragma unroll 4
-  for (int i = 0; i < m; ++i) {
-    const double q3 = col[min(i + 3, m + 1) * rs];  // (rows past i + 2 = m + 1 are never used)
-    const double2 G0 = F[4 * (i + 1)], G1 = F[4 * (i + 1) + 1], G2 = F[4 * (i + 1) + 2];  // next row
-    const double wc = sp == 2 ? q2 : 0.0;
-    // t = a0 w_k - a2 w_{k+2} + a4 w_{k+4} - f2 y_{i-2};  y = t - f1 y_{i-1}
-    const double tt = fma(F0.x, q0, fma(-F0.y, q1, fma(F1.x, wc, -F2.x * y2)));
-    const double y = fma(-F1.y, y1, tt);
-    col[i * rs] = y;
-    y2 = y1;
-    y1 = y;
-    q0 = q1;
-    q1 = q2;
-    q2 = q3;
-    F0 = G0;
-    F1 = G1;
-    F2 = G2;
+  double q[KB + 2];
+  double2 c0[KB], c1[KB], c2[KB];
+  auto load_fwd = [&](int i0, double (&qq)[KB + 2], double2 (&a)[KB], double2 (&bb)[KB], double2 (&cc)[KB]) {
+#pragma unroll
+    for (int j = 0; j < KB + 2; ++j) qq[j] = col[min(i0 + j, m + 1) * rs];  // rows past m + 1 are never used
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const int i = min(i0 + j, m);  // the table has mmax + 1 >= m + 1 rows
+      a[j] = F[4 * i];
+      bb[j] = F[4 * i + 1];
+      cc[j] = F[4 * i + 2];
+    }
+  };
+  load_fwd(0, q, c0, c1, c2);
+  for (int i0 = 0; i0 < m; i0 += KB) {
+    double t0[KB], f1[KB], f2[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const double wc = bih ? q[j + 2] : 0.0;
+      t0[j] = fma(c0[j].x, q[j], fma(-c0[j].y, q[j + 1], c1[j].x * wc));
+      f1[j] = c1[j].y;
+      f2[j] = c2[j].x;
+    }
+    load_fwd(i0 + KB, q, c0, c1, c2);  // next block (clamped past the end)
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const double y = fma(-f1[j], y1, fma(-f2[j], y2, t0[j]));
+      if (i0 + j < m) col[(i0 + j) * rs] = y;
+      y2 = y1;
+      y1 = y;
+    }
   }
+  // U x = y bottom-up: x_i = (a0 y_i - g2 x_{i+2}) - g1 x_{i+1}
   double x1 = 0.0, x2 = 0.0;
-  const int il = m > 0 ? m - 1 : 0;
-  double yn = col[il * rs];
-  double2 Fa = F[4 * il], Fc = F[4 * il + 2], Fd = F[4 * il + 3];
-#pragma unroll 4
-  for (int i = m - 1; i >= 0; --i) {
-    const double yk = yn;
-    const int ip = i > 0 ? i - 1 : 0;  // next (upper) row, loaded one iteration ahead
-    yn = col[ip * rs];
-    const double2 Ha = F[4 * ip], Hc = F[4 * ip + 2], Hd = F[4 * ip + 3];  // a0 | f2 g1 | g2 -
-    const double tt = fma(Fa.x, yk, -Fd.x * x2);
-    const double x = fma(-Fc.y, x1, tt);
-    col[i * rs] = x;
-    x2 = x1;
-    x1 = x;
-    Fa = Ha;
-    Fc = Hc;
-    Fd = Hd;
+  double yy[KB];
+  double2 d0[KB], d2[KB], d3[KB];
+  auto load_bwd = [&](int i1, double (&v)[KB], double2 (&a)[KB], double2 (&cc)[KB], double2 (&dd)[KB]) {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const int i = max(i1 - j, 0);  // rows i1, i1 - 1, ...
+      v[j] = col[i * rs];
+      a[j] = F[4 * i];
+      cc[j] = F[4 * i + 2];
+      dd[j] = F[4 * i + 3];
+    }
+  };
+  load_bwd(m - 1, yy, d0, d2, d3);
+  for (int i1 = m - 1; i1 >= 0; i1 -= KB) {
+    double s0[KB], g1[KB], g2[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      s0[j] = d0[j].x * yy[j];
+      g1[j] = d2[j].y;
+      g2[j] = d3[j].x;
+    }
+    load_bwd(i1 - KB, yy, d0, d2, d3);  // next block: rows above, not written yet
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const double x = fma(-g1[j], x1, fma(-g2[j], x2, s0[j]));
+      if (i1 - j >= 0) col[(i1 - j) * rs] = x;
+      x2 = x1;
+      x1 = x;
+    }
   }
 }
 
@@ -841,7 +870,10 @@ static cudaError_t launch_wall_k(const WallPlan& p, int64_t L, const void* in, v
   if (!encode_tiled_2d(&tin, in, 2 * (uint64_t)L, rows_in, (uint64_t)L * sizeof(double2), 2 * TL, bi) ||
       !encode_tiled_2d(&tout, out, 2 * (uint64_t)L, rows_out, (uint64_t)L * sizeof(double2), 2 * TL, bo))
     return cudaErrorNotSupported;
-  const size_t smem = wall_smem_bytes(p);
+  size_t smem = wall_smem_bytes(p);
+#ifdef SHEN_WALL_ONE_CTA  // probe builds: one resident CTA per SM (phase times without the co-resident CTA)
+  smem = smem > (size_t)120 * 1024 ? smem : (size_t)120 * 1024;
+#endif
   auto kern = p.direction == 0 ? wall_forward_kernel<KMAX, SH> : wall_inverse_kernel<KMAX, SH>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;

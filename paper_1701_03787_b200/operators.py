@@ -22,7 +22,30 @@ import numpy as np
 from . import _lib
 from ._device import device, is_torch, stream_handle
 
-__all__ = ["apply", "DeviceOperator"]
+__all__ = ["apply", "DeviceOperator", "operator_tables"]
+
+
+def operator_tables(M):
+    """Host tables of one structured matrix, read through the attributes the
+    reference's classes and this package's share (``matrices.py:46-152``):
+    ``(2, (diag, p, q, r, s))`` for a rank-2 tail, else ``(kind, (offsets,
+    band table [n_off][rows], tail | None, tail_start))`` with kind 1 for a
+    constant tail and 0 for a plain banded matrix."""
+    if hasattr(M, "p") and hasattr(M, "q"):  # rank-2 tail
+        return 2, tuple(np.ascontiguousarray(v, dtype=np.float64) for v in (M.diag, M.p, M.q, M.r, M.s))
+    banded = M.banded if hasattr(M, "banded") else M
+    kind = 1 if hasattr(M, "tail") else 0
+    nr, nc = banded.shape
+    offs = tuple(int(d) for d in banded.offsets)
+    if len(offs) > 6:
+        raise ValueError("at most 6 diagonals")
+    tab = np.zeros((max(len(offs), 1), nr))
+    for i, (d, diag) in enumerate(zip(offs, banded.diagonals)):
+        a, b = max(0, -d), min(nr, nc - d)
+        tab[i, a:b] = diag
+    if kind == 1:
+        return 1, (offs, tab, np.ascontiguousarray(M.tail, dtype=np.float64), int(M.tail_start))
+    return 0, (offs, tab, None, 0)
 
 
 class DeviceOperator:
@@ -33,27 +56,17 @@ class DeviceOperator:
 
         dev = device()
         self.shape = tuple(M.shape)
-        if hasattr(M, "p") and hasattr(M, "q"):  # rank-2 tail
-            self.kind = 2
-            self._vecs = [torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(dev)
-                          for v in (M.diag, M.p, M.q, M.r, M.s)]
+        self.kind, tabs = operator_tables(M)
+        if self.kind == 2:
+            self._vecs = [torch.from_numpy(v).to(dev) for v in tabs]
             return
-        banded = M.banded if hasattr(M, "banded") else M
-        self.kind = 1 if hasattr(M, "tail") else 0
-        nr, nc = banded.shape
-        offs = tuple(int(d) for d in banded.offsets)
-        if len(offs) > 6:
-            raise ValueError("at most 6 diagonals")
-        tab = np.zeros((max(len(offs), 1), nr))
-        for i, (d, diag) in enumerate(zip(offs, banded.diagonals)):
-            a, b = max(0, -d), min(nr, nc - d)
-            tab[i, a:b] = diag
+        offs, tab, tail, tail_start = tabs
         self._offs = (ctypes.c_int * max(len(offs), 1))(*offs) if offs else None
         self._n_off = len(offs)
         self._tab = torch.from_numpy(tab).to(dev)
         if self.kind == 1:
-            self._tail = torch.from_numpy(np.ascontiguousarray(M.tail, dtype=np.float64)).to(dev)
-            self._tail_start = int(M.tail_start)
+            self._tail = torch.from_numpy(tail).to(dev)
+            self._tail_start = tail_start
 
     def __call__(self, x):
         """y = M x along axis 0; numpy or torch CUDA input."""
