@@ -142,41 +142,16 @@ __global__ void rhs_u_kernel(RhsUArgs a) {
 }
 
 
-// ---------------------------------------------------------------- fast path
-#ifndef SHEN_RHS_PF
-#define SHEN_RHS_PF 0  // extra prefetch rows of the rhs_u windows (measured: none is best)
-#endif
-#ifndef SHEN_RHS_UNROLL
-#define SHEN_RHS_UNROLL 1  // rows per loop trip (measured: unrolling 2-4 is slower)
-#endif
-constexpr int kRhsUnroll = SHEN_RHS_UNROLL;
-#ifndef SHEN_RHS_UPAR_PF
-#define SHEN_RHS_UPAR_PF 0  // measured: 1-3 rows of register prefetch do not help
-#endif
+// ---------------------------------------------------------------- fixed-structure path
 #ifndef SHEN_RHS_UPAR_MINB
-#define SHEN_RHS_UPAR_MINB 3
-#endif
-#ifndef SHEN_RHS_U_MINB
-#define SHEN_RHS_U_MINB 3  // resident 128-thread blocks per SM the register budget targets
+#define SHEN_RHS_UPAR_MINB 3  // resident 128-thread blocks per SM the register budget targets
 #endif
 // The reference's matrices have fixed structure: mass_dir / stiff_bih
 // offsets (-2, 0, 2), stiff_dir banded part (0) + tail from k+2, mass_bih
 // (-4, -2, 0, 2, 4), mixed_mass (-2, 0, 2, 4), deriv_dir_to_bih (-1, 1, 3).
-// For that structure each input row is loaded ONCE into a register window
-// that slides down with k (the generic kernel above re-reads neighbours and
-// recombines AB2 per use).  Same operations in the same order -> same bits.
-template <int LO, int HI>
-struct Win {  // values at rows k+LO .. k+HI
-  C2 v[HI - LO + 1];
-  __device__ __forceinline__ C2 at(int d) const { return v[d - LO]; }
-  // k -> k-1: everything moves one slot up, row (k-1)+LO enters at the bottom
-  __device__ __forceinline__ void shift(C2 fresh) {
-#pragma unroll
-    for (int i = HI - LO; i > 0; --i) v[i] = v[i - 1];
-    v[0] = fresh;
-  }
-};
-
+// For that structure each input row is loaded ONCE into a window that slides
+// down with k (the generic kernel above re-reads neighbours and recombines
+// AB2 per use).  Same operations in the same order -> same bits.
 __device__ __forceinline__ C2 term(const RhsBand& m, int q, int k, C2 x) {
   return rmul(__ldg(m.diag + (int64_t)q * m.nr + k), x);
 }
@@ -210,117 +185,12 @@ struct PWin {
   }
 };
 
-__global__ void __launch_bounds__(128) rhs_g_fast_kernel(RhsGArgs a) {
-  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= a.L) return;
-  const int64_t L = a.L;
-  const int n = a.n_dir;
-  auto ldr = [&](const void* base, int j) -> C2 {
-    return (j >= 0 && j < n) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
-  };
-  const C2 im_m = {__ldg(a.im_m_re + l), __ldg(a.im_m_im + l)}, im_n = {__ldg(a.im_n_re + l), __ldg(a.im_n_im + l)};
-  auto src_row = [&](int j) -> C2 {
-    if (j < 0 || j >= n) return {0.0, 0.0};
-    const C2 hy = sub(rmul(1.5, ldr(a.hcy, j)), rmul(0.5, ldr(a.hpy, j)));
-    const C2 hz = sub(rmul(1.5, ldr(a.hcz, j)), rmul(0.5, ldr(a.hpz, j)));
-    return sub(cmul(im_m, hz), cmul(im_n, hy));
-  };
-  const double cg = __ldg(a.cg + l);
-  Win<-2, 2> G, R;  // g and src at rows k-2 .. k+2
-#pragma unroll
-  for (int d = -2; d <= 2; ++d) {
-    G.v[d + 2] = ldr(a.g, n - 1 + d);
-    R.v[d + 2] = src_row(n - 1 + d);
-  }
-  C2 S[2] = {{0.0, 0.0}, {0.0, 0.0}};
-  bool have[2] = {false, false};
-  double2* out = static_cast<double2*>(a.out) + l;
-#pragma unroll kRhsUnroll
-  for (int k = n - 1; k >= 0; --k) {
-    C2 st = band_win<0>(a.stiff, k, G);
-    const int j = k + 2;  // tail_start == 2 (checked on the host side)
-    if (j < n) {
-      const int pj = j & 1;
-      S[pj] = have[pj] ? add(G.at(2), S[pj]) : G.at(2);
-      have[pj] = true;
-      st = add(st, rmul(__ldg(a.tail + k), S[pj]));
-    }
-    C2 r = rmul(a.c_stiff, st);
-    r = add(r, rmul(cg, band_win<-2, 0, 2>(a.mass, k, G)));
-    r = add(r, rmul(a.dt, band_win<-2, 0, 2>(a.mass, k, R)));
-    out[(int64_t)k * L] = make_double2(r.re, r.im);
-    G.shift(ldr(a.g, k - 3));
-    R.shift(src_row(k - 3));
-  }
-}
 
-__global__ void __launch_bounds__(128, SHEN_RHS_U_MINB) rhs_u_fast_kernel(RhsUArgs a) {
-  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= a.L) return;
-  const int64_t L = a.L;
-  const int n = a.n_bih, nd = a.mixed.nc;
-  auto ldr = [&](const void* base, int j, int rows) -> C2 {
-    return (j >= 0 && j < rows) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
-  };
-  auto hrow = [&](const void* c, const void* p, int j) -> C2 {
-    if (j < 0 || j >= nd) return {0.0, 0.0};
-    return sub(rmul(1.5, ldr(c, j, nd)), rmul(0.5, ldr(p, j, nd)));
-  };
-  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
-  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
-  // windows extended PF rows below what the bands use: those slots are a
-  // prefetch FIFO, so a row's loads are issued PF+1 iterations before use
-  constexpr int PF = SHEN_RHS_PF;
-  Win<-4 - PF, 4> U;   // u rows k-4 .. k+4 (+ prefetch)
-  Win<-2 - PF, 4> HX;  // h_x rows k-2 .. k+4
-  Win<-1 - PF, 3> HY, HZ;
-  const int k = n - 1;
-#pragma unroll
-  for (int d = -4 - PF; d <= 4; ++d) U.v[d + 4 + PF] = ldr(a.u, k + d, n);
-#pragma unroll
-  for (int d = -2 - PF; d <= 4; ++d) HX.v[d + 2 + PF] = hrow(a.hcx, a.hpx, k + d);
-#pragma unroll
-  for (int d = -1 - PF; d <= 3; ++d) {
-    HY.v[d + 1 + PF] = hrow(a.hcy, a.hpy, k + d);
-    HZ.v[d + 1 + PF] = hrow(a.hcz, a.hpz, k + d);
-  }
-  C2 sq[2] = {{0.0, 0.0}, {0.0, 0.0}}, ss[2] = {{0.0, 0.0}, {0.0, 0.0}};
-  bool have[2] = {false, false};
-  double2* out = static_cast<double2*>(a.out) + l;
-#pragma unroll kRhsUnroll
-  for (int k = n - 1; k >= 0; --k) {
-    const int j = k + 2;
-    if (j < n) {
-      const C2 uj = U.at(2);
-      const C2 qx = rmul(__ldg(a.q + j), uj), sx = rmul(__ldg(a.s + j), uj);
-      const int pj = j & 1;
-      sq[pj] = have[pj] ? add(qx, sq[pj]) : qx;
-      ss[pj] = have[pj] ? add(sx, ss[pj]) : sx;
-      have[pj] = true;
-    }
-    C2 f = rmul(__ldg(a.d + k), U.at(0));
-    if (k < n - 2) {
-      f = add(f, rmul(__ldg(a.p + k), sq[k & 1]));
-      f = add(f, rmul(__ldg(a.r + k), ss[k & 1]));
-    }
-    C2 r = rmul(a.c_fourth, f);
-    r = sub(r, rmul(cs, band_win<-2, 0, 2>(a.stiff, k, U)));
-    r = add(r, rmul(cm, band_win<-4, -2, 0, 2, 4>(a.mass, k, U)));
-    r = sub(r, rmul(cx, band_win<-2, 0, 2, 4>(a.mixed, k, HX)));
-    r = sub(r, cmul(cy, band_win<-1, 1, 3>(a.deriv, k, HY)));
-    r = sub(r, cmul(cz, band_win<-1, 1, 3>(a.deriv, k, HZ)));
-    out[(int64_t)k * L] = make_double2(r.re, r.im);
-    U.shift(ldr(a.u, k - 5 - PF, n));
-    HX.shift(hrow(a.hcx, a.hpx, k - 3 - PF));
-    HY.shift(hrow(a.hcy, a.hpy, k - 2 - PF));
-    HZ.shift(hrow(a.hcz, a.hpz, k - 2 - PF));
-  }
-}
 
 // ---------------------------------------------------------------- one thread per (line, parity)
 // The operators never mix parities except through odd offsets (read-only), and
 // the tails' suffix sums run within a parity: a thread can own one parity of
-// a line.  Twice the threads of the fast path above, each with half the
+// a line: twice the threads of a one-thread-per-line walk, each with half the
 // window registers -- more parallelism for the same (single) pass over HBM.
 __global__ void __launch_bounds__(128) rhs_g_par_kernel(RhsGArgs a) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -367,72 +237,8 @@ __global__ void __launch_bounds__(128) rhs_g_par_kernel(RhsGArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(128, SHEN_RHS_UPAR_MINB) rhs_u_par_kernel(RhsUArgs a) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 2 * a.L) return;
-  const int par = t >= a.L ? 1 : 0;
-  const int64_t l = t - (int64_t)par * a.L;
-  const int64_t L = a.L;
-  const int n = a.n_bih, nd = a.mixed.nc;
-  auto ldr = [&](const void* base, int j, int rows) -> C2 {
-    return (j >= 0 && j < rows) ? ld(static_cast<const double2*>(base) + (int64_t)j * L + l) : C2{0.0, 0.0};
-  };
-  auto hrow = [&](const void* c, const void* p, int j) -> C2 {
-    if (j < 0 || j >= nd) return {0.0, 0.0};
-    return sub(rmul(1.5, ldr(c, j, nd)), rmul(0.5, ldr(p, j, nd)));
-  };
-  const double cs = __ldg(a.c_stiff + l), cm = __ldg(a.c_mass + l), cx = __ldg(a.c_mixed + l);
-  const C2 cy = {__ldg(a.c_dy_re + l), __ldg(a.c_dy_im + l)}, cz = {__ldg(a.c_dz_re + l), __ldg(a.c_dz_im + l)};
-  const int m = (n - par + 1) / 2;
-  const int ktop = par + 2 * (m - 1);
-  // windows extended by PF rows (of this parity step) below what the bands
-  // use: those slots are a prefetch FIFO, a row's loads are issued PF + 1
-  // iterations before the bands read it (ncu: the unextended kernel stalls
-  // on long scoreboard ~6 cycles per issue)
-  constexpr int PF = SHEN_RHS_UPAR_PF;
-  PWin<-4 - 2 * PF, 4> U;    // u rows k-4 .. k+4 (this parity)
-  PWin<-2 - 2 * PF, 4> HX;   // h_x rows k-2 .. k+4 (this parity)
-  PWin<-1 - 2 * PF, 3> HY, HZ;  // h_y, h_z rows k-1, k+1, k+3 (other parity)
-#pragma unroll
-  for (int d = -4 - 2 * PF; d <= 4; d += 2) U.v[(d + 4 + 2 * PF) / 2] = ldr(a.u, ktop + d, n);
-#pragma unroll
-  for (int d = -2 - 2 * PF; d <= 4; d += 2) HX.v[(d + 2 + 2 * PF) / 2] = hrow(a.hcx, a.hpx, ktop + d);
-#pragma unroll
-  for (int d = -1 - 2 * PF; d <= 3; d += 2) {
-    HY.v[(d + 1 + 2 * PF) / 2] = hrow(a.hcy, a.hpy, ktop + d);
-    HZ.v[(d + 1 + 2 * PF) / 2] = hrow(a.hcz, a.hpz, ktop + d);
-  }
-  C2 sq = {0.0, 0.0}, ss = {0.0, 0.0};
-  bool have = false;
-  double2* out = static_cast<double2*>(a.out) + l;
-  for (int k = ktop; k >= 0; k -= 2) {
-    if (k + 2 < n) {  // fold row k + 2 of this parity into the rank-2 tail sums
-      const C2 uj = U.at(2);
-      const C2 qx = rmul(__ldg(a.q + k + 2), uj), sx = rmul(__ldg(a.s + k + 2), uj);
-      sq = have ? add(qx, sq) : qx;
-      ss = have ? add(sx, ss) : sx;
-      have = true;
-    }
-    C2 f = rmul(__ldg(a.d + k), U.at(0));
-    if (k < n - 2) {
-      f = add(f, rmul(__ldg(a.p + k), sq));
-      f = add(f, rmul(__ldg(a.r + k), ss));
-    }
-    C2 r = rmul(a.c_fourth, f);
-    r = sub(r, rmul(cs, band_win<-2, 0, 2>(a.stiff, k, U)));
-    r = add(r, rmul(cm, band_win<-4, -2, 0, 2, 4>(a.mass, k, U)));
-    r = sub(r, rmul(cx, band_win<-2, 0, 2, 4>(a.mixed, k, HX)));
-    r = sub(r, cmul(cy, band_win<-1, 1, 3>(a.deriv, k, HY)));
-    r = sub(r, cmul(cz, band_win<-1, 1, 3>(a.deriv, k, HZ)));
-    out[(int64_t)k * L] = make_double2(r.re, r.im);
-    U.shift(ldr(a.u, k - 6 - 2 * PF, n));
-    HX.shift(hrow(a.hcx, a.hpx, k - 4 - 2 * PF));
-    HY.shift(hrow(a.hcy, a.hpy, k - 3 - 2 * PF));
-    HZ.shift(hrow(a.hcz, a.hpz, k - 3 - 2 * PF));
-  }
-}
 
-// Same walk as rhs_u_par_kernel, but everything a row step reads arrives
+// One thread per (line, parity) as rhs_g_par_kernel, but everything a row step reads arrives
 // through a cp.async ring in shared memory, issued SHEN_RHS_RING - 1 steps
 // ahead: the seven input rows (per thread) and the row's 20 operator entries
 // (per warp: lanes 0..19 copy one each, all lanes read them as broadcasts).
@@ -608,11 +414,8 @@ static bool offs_are(const RhsBand& m, std::initializer_list<int> o) {
 cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_dir <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
-  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 2;
-  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant >= 2)
+  if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}))
     rhs_g_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
-  else if (offs_are(a.stiff, {0}) && a.tail_start == 2 && offs_are(a.mass, {-2, 0, 2}) && variant == 1)
-    rhs_g_fast_kernel<<<blocks, 128, 0, st>>>(a);
   else
     rhs_g_kernel<<<blocks, 128, 0, st>>>(a);
   return cudaGetLastError();
@@ -621,10 +424,9 @@ cudaError_t launch_rhs_g(const RhsGArgs& a, cudaStream_t st) {
 cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st) {
   if (a.L <= 0 || a.n_bih <= 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((a.L + 127) / 128);
-  static const int variant = getenv("SHEN_RHS_VARIANT") ? atoi(getenv("SHEN_RHS_VARIANT")) : 3;
   const bool fixed = offs_are(a.stiff, {-2, 0, 2}) && offs_are(a.mass, {-4, -2, 0, 2, 4}) &&
                      offs_are(a.mixed, {-2, 0, 2, 4}) && offs_are(a.deriv, {-1, 1, 3});
-  if (fixed && variant == 3) {
+  if (fixed) {
     constexpr int smem = kRhsRing * 7 * kRhsRingThreads * (int)sizeof(double2) +
                          kRhsRing * (kRhsRingThreads / 32) * kRhsTab * (int)sizeof(double);
     static const cudaError_t attr =
@@ -633,13 +435,9 @@ cudaError_t launch_rhs_u(const RhsUArgs& a, cudaStream_t st) {
     const int64_t Lp = (a.L + 31) / 32 * 32;  // single-parity warps
     rhs_u_ring_kernel<<<(unsigned)((2 * Lp + kRhsRingThreads - 1) / kRhsRingThreads), kRhsRingThreads, smem, st>>>(
         a, Lp);
-  }
-  else if (fixed && variant == 2)
-    rhs_u_par_kernel<<<(unsigned)((2 * a.L + 127) / 128), 128, 0, st>>>(a);
-  else if (fixed && variant == 1)
-    rhs_u_fast_kernel<<<blocks, 128, 0, st>>>(a);
-  else
+  } else {
     rhs_u_kernel<<<blocks, 128, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 

@@ -1042,11 +1042,6 @@ static cudaError_t helm_stream_R(const HelmChunkArgs& a, void* scratch, int ctas
   // deepest ring that fits next to the row table (bytes in flight per SM)
   const int n0 = (a.n_dir + 1) / 2;
   const size_t tabb = (size_t)2 * (((n0 + R - 1) / R) * R) * sizeof(double4);
-  static const int ring_env = getenv("SHEN_HELM_RING") ? atoi(getenv("SHEN_HELM_RING")) : 0;
-  if (ring_env == 6 && (size_t)6 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
-    return helm_stream_RR<V, R, SG, 6>(a, scratch, ctas_per_sm, st);
-  if (ring_env == 4 && (size_t)4 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
-    return helm_stream_RR<V, R, SG, 4>(a, scratch, ctas_per_sm, st);
   if ((size_t)3 * R * 64 * SG * sizeof(V) + tabb <= 220 * 1024)
     return helm_stream_RR<V, R, SG, 3>(a, scratch, ctas_per_sm, st);
   return helm_stream_RR<V, R, SG, 2>(a, scratch, ctas_per_sm, st);
@@ -1109,8 +1104,6 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
     // the pair kernel needs two RHS rings plus the one-parity table in shared
     // memory; past n_x ~ 1150 it does not fit and the one-system kernel
     // solves every system (the pair table lists each exactly once)
-    static const int pw = getenv("SHEN_PAIR_WARPS") ? atoi(getenv("SHEN_PAIR_WARPS")) : 8;
-    if (pw == 6 && bih_pair_smem<V, R, 3>(a) <= 227 * 1024) return bih_pair_launch<V, R, 3>(a, scratch, st);
     if (bih_pair_smem<V, R, 4>(a) <= 227 * 1024) return bih_pair_launch<V, R, 4>(a, scratch, st);
     // larger n_x (the one-parity table alone is ~115 KB at n_x = 2048): a
     // 4-warp pair CTA still fits (SHEN_PAIR_SMALL=0 falls through to the
@@ -1147,8 +1140,6 @@ static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w,
   switch (a.chunk_rows) {
     case 4: return small ? helm_stream_R<V, 4, 4>(a, sc, 1, st) : helm_stream_R<V, 4, 6>(a, sc, 1, st);
     case 8:
-      if (w == 4) return helm_stream_R<V, 8, 2>(a, sc, 1, st);
-      if (w == 6) return helm_stream_R<V, 8, 3>(a, sc, 1, st);
       return small ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
     case 16: return helm_stream_R<V, 16, 4>(a, sc, 1, st);
     default: return cudaErrorInvalidValue;
