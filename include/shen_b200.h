@@ -310,6 +310,34 @@ int shen_plane_fft_supported(int n_y, int n_z);
 int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* X, void* stream);
 int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream);
 
+/* ---------------------------------------------------------------------
+ * The same transforms with the slab decomposition's kx-row exchange fused in
+ * (several GPUs of one box; the reference is single-process, so this has no
+ * reference counterpart -- SURVEY.md 8(e), the paper's slab transpose).  A
+ * rank holds physical x-planes [plane0, plane0 + n_planes) and the kx rows
+ * {y : owner[y] == rank} of every plane.  Row y of global plane x lives in
+ * rank owner[y]'s buffer bases[owner[y]], a C-contiguous complex128 array
+ * (n_planes_total, rows[owner[y]], n_z/2+1), at [x][local_row[y]][:].
+ * bases[q] are pointers valid on THIS device (peer memory opened by CUDA IPC
+ * or the rank's own buffer); owner / local_row have n_y entries (host).
+ * shen_plane_rfft2_scatter: rfft2 of the rank's planes, each spectrum row
+ *   stored straight into its owner's buffer (no pack pass, no all-to-all).
+ * shen_plane_irfft2_gather: irfft2 of the rank's planes, each spectrum row
+ *   read from its owner's buffer.
+ * Ordering is the caller's: every rank's scatter must have completed (stream
+ * synchronised + a barrier across ranks) before any rank reads its buffer,
+ * and a buffer must not be rewritten while a peer may still gather from it.
+ * shen_enable_peer_access(d): cudaDeviceEnablePeerAccess to device d from
+ *   the current one (no-op when d is the current device or already enabled).
+ * ------------------------------------------------------------------- */
+int shen_plane_rfft2_scatter(int64_t n_planes, int n_y, int n_z, const double* x, int world, void* const* bases,
+                             const int64_t* rows, const int* owner, const int* local_row, int64_t plane0,
+                             int64_t n_planes_total, void* stream);
+int shen_plane_irfft2_gather(int64_t n_planes, int n_y, int n_z, int world, void* const* bases, const int64_t* rows,
+                             const int* owner, const int* local_row, int64_t plane0, int64_t n_planes_total,
+                             double* x, double scale, void* stream);
+int shen_enable_peer_access(int peer_device);
+
 #ifdef __cplusplus
 }
 #endif

@@ -358,6 +358,67 @@ int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double*
   return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, S(stream)), "shen_plane_irfft2");
 }
 
+// kx-row exchange descriptor from the caller's plain arrays (validated here:
+// the kernels index with it unchecked)
+static int make_xch(shen::PlaneXch* xc, int n_y, int world, void* const* bases, const int64_t* rows,
+                    const int* owner, const int* local_row, int64_t plane0, int64_t n_planes_total,
+                    int64_t n_planes) {
+  if (world < 1 || world > 8 || !bases || !rows || !owner || !local_row || n_y > 256 || plane0 < 0 ||
+      plane0 + n_planes > n_planes_total)
+    return 0;
+  for (int q = 0; q < 8; ++q) {
+    xc->base[q] = q < world ? bases[q] : nullptr;
+    xc->rows[q] = q < world ? rows[q] : 0;
+    if (q < world && (!bases[q] || (reinterpret_cast<uintptr_t>(bases[q]) & 15) || rows[q] < 0)) return 0;
+  }
+  for (int y = 0; y < 256; ++y) {
+    const int q = y < n_y ? owner[y] : 0, lr = y < n_y ? local_row[y] : 0;
+    if (q < 0 || q >= world || lr < 0 || (y < n_y && lr >= rows[q])) return 0;
+    xc->owner[y] = (unsigned char)q;
+    xc->local_row[y] = (short)lr;
+  }
+  xc->plane0 = plane0;
+  return 1;
+}
+
+int shen_plane_rfft2_scatter(int64_t n_planes, int n_y, int n_z, const double* x, int world, void* const* bases,
+                             const int64_t* rows, const int* owner, const int* local_row, int64_t plane0,
+                             int64_t n_planes_total, void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  shen::PlaneXch xc;
+  if (n_planes < 0 || !x || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
+      !make_xch(&xc, n_y, world, bases, rows, owner, local_row, plane0, n_planes_total, n_planes))
+    return fail(SHEN_ERR_ARG, "shen_plane_rfft2_scatter: bad args");
+  return cuda_check(shen::launch_plane_rfft2_scatter(n_planes, n_y, n_z, x, xc, S(stream)), "shen_plane_rfft2_scatter");
+}
+
+int shen_plane_irfft2_gather(int64_t n_planes, int n_y, int n_z, int world, void* const* bases, const int64_t* rows,
+                             const int* owner, const int* local_row, int64_t plane0, int64_t n_planes_total,
+                             double* x, double scale, void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  shen::PlaneXch xc;
+  if (n_planes < 0 || !x || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
+      !make_xch(&xc, n_y, world, bases, rows, owner, local_row, plane0, n_planes_total, n_planes))
+    return fail(SHEN_ERR_ARG, "shen_plane_irfft2_gather: bad args");
+  return cuda_check(shen::launch_plane_irfft2_gather(n_planes, n_y, n_z, xc, x, scale, S(stream)),
+                    "shen_plane_irfft2_gather");
+}
+
+int shen_enable_peer_access(int peer_device) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(SHEN_ERR_CUDA, "shen_enable_peer_access: no device");
+  if (peer_device == dev) return SHEN_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer_device) != cudaSuccess || !can)
+    return fail(SHEN_ERR_CUDA, "shen_enable_peer_access: no peer access between the devices");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return SHEN_OK;
+  }
+  return cuda_check(e, "shen_enable_peer_access");
+}
+
 int shen_recover_velocity(const shen_recover_args* r, void* stream) {
   if (!r) return fail(SHEN_ERR_ARG, "shen_recover_velocity: NULL args");
   if (r->L == 0 || r->n_dir == 0) return SHEN_OK;

@@ -174,7 +174,22 @@ cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const dou
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
 
 // periodic (y, z) plane FFTs (shen_plane_fft.cu): one 8-CTA cluster per plane
+// kx-row exchange fused into the plane FFTs (slab transforms over several
+// GPUs): spectrum row y of global plane x lives on rank owner[y], in its
+// (n_planes_total, rows[owner], n_z/2+1) complex128 buffer base[owner] at
+// [x][local_row[y]][:].  Up to 8 ranks, 256 rows (the supported plane size).
+struct PlaneXch {
+  void* base[8];
+  int64_t rows[8];
+  int64_t plane0;  // global index of this launch's first plane
+  unsigned char owner[256];
+  short local_row[256];
+};
 bool plane_fft_supported(int n_y, int n_z);
+cudaError_t launch_plane_rfft2_scatter(int64_t planes, int n_y, int n_z, const double* x, const PlaneXch& xc,
+                                       cudaStream_t st);
+cudaError_t launch_plane_irfft2_gather(int64_t planes, int n_y, int n_z, const PlaneXch& xc, double* x, double scale,
+                                       cudaStream_t st);
 cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, cudaStream_t st);
 cudaError_t launch_plane_irfft2(int64_t planes, int n_y, int n_z, const void* X, double* x, double scale,
                                 cudaStream_t st);

@@ -188,8 +188,12 @@ __device__ __forceinline__ void load_tw(double2* tw) {
   for (int j = threadIdx.x; j < 256; j += blockDim.x) tw[j] = g_tw[j];
 }
 
+// XCH: the spectrum rows do not go to `out` but straight into the kx-row
+// buffers of the ranks that own them (PlaneXch, peer memory over NVLink): the
+// slab transform's all-to-all fused into the FFT's store.
+template <bool XCH>
 __global__ void __launch_bounds__(kThreads, 4)
-    rfft2_256_kernel(const double* __restrict__ in, double2* __restrict__ out) {
+    rfft2_256_kernel(const double* __restrict__ in, double2* __restrict__ out, const __grid_constant__ PlaneXch xc) {
   extern __shared__ __align__(16) double sm[];
   double2* tw = reinterpret_cast<double2*>(sm);
   double* A = sm + 2 * 256;
@@ -268,17 +272,31 @@ __global__ void __launch_bounds__(kThreads, 4)
   PF_TS(4);
   if (z < kNZH) {
     dft16<false>(v);
-    double2* o = out + plane * (kNY * kNZH) + (int64_t)c * kNZH + z;
+    if (XCH) {
 #pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) st_cs2(o + (int64_t)(16 * k2) * kNZH, v[k2]);
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const int y = c + 16 * k2, q = xc.owner[y];
+        double2* o = static_cast<double2*>(xc.base[q]) +
+                     ((xc.plane0 + plane) * xc.rows[q] + xc.local_row[y]) * (int64_t)kNZH + z;
+        *o = v[k2];  // the consumer reads it soon (and possibly over NVLink): no streaming hint
+      }
+    } else {
+      double2* o = out + plane * (kNY * kNZH) + (int64_t)c * kNZH + z;
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) st_cs2(o + (int64_t)(16 * k2) * kNZH, v[k2]);
+    }
   }
   PF_TS(5);
   cl_wait();
   PF_TS(6);
 }
 
+// XCH: the spectrum rows are read from the kx-row buffers of their owners
+// (the inverse slab transform's all-to-all fused into the FFT's load).
+template <bool XCH>
 __global__ void __launch_bounds__(kThreads, 4)
-    irfft2_256_kernel(const double2* __restrict__ in, double* __restrict__ out, double scale) {
+    irfft2_256_kernel(const double2* __restrict__ in, double* __restrict__ out, double scale,
+                      const __grid_constant__ PlaneXch xc) {
   extern __shared__ __align__(16) double sm[];
   double2* tw = reinterpret_cast<double2*>(sm);
   double* A = sm + 2 * 256;
@@ -290,9 +308,19 @@ __global__ void __launch_bounds__(kThreads, 4)
   double2 v[16];
   // ---- y pass over k2 for k1 = c: rows c + 16 k2 of the spectrum
   if (z < kNZH) {
-    const double2* ip = in + plane * (kNY * kNZH) + (int64_t)c * kNZH + z;
+    if (XCH) {
 #pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) v[k2] = ld_nc2(ip + (int64_t)(16 * k2) * kNZH);
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const int y = c + 16 * k2, q = xc.owner[y];
+        const double2* ip = static_cast<const double2*>(xc.base[q]) +
+                            ((xc.plane0 + plane) * xc.rows[q] + xc.local_row[y]) * (int64_t)kNZH + z;
+        v[k2] = *ip;  // plain load: peer memory written by another GPU's kernel before the host barrier
+      }
+    } else {
+      const double2* ip = in + plane * (kNY * kNZH) + (int64_t)c * kNZH + z;
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) v[k2] = ld_nc2(ip + (int64_t)(16 * k2) * kNZH);
+    }
   }
   load_tw(tw);
   __syncthreads();
@@ -374,12 +402,17 @@ template <typename K, typename... Args>
 cudaError_t launch_cluster(K kernel, int64_t planes, cudaStream_t st, Args... args) {
   cudaError_t e = init_tw();
   if (e != cudaSuccess) return e;
-  static bool attr = false;
+  // per kernel, not per instantiation of this template: kernels of one
+  // signature (the <false> / <true> pairs) share K
+  static const void* ready[8] = {};
+  bool attr = false;
+  int slot = 0;
+  for (; slot < 8 && ready[slot] != nullptr; ++slot) attr = attr || ready[slot] == (const void*)kernel;
   if (!attr) {
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (slot < 8) ready[slot] = (const void*)kernel;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(planes * kC), 1, 1);
@@ -403,14 +436,28 @@ bool plane_fft_supported(int n_y, int n_z) { return n_y == kNY && n_z == kNZ; }
 cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(rfft2_256_kernel, planes, st, x, static_cast<double2*>(X));
+  return launch_cluster(rfft2_256_kernel<false>, planes, st, x, static_cast<double2*>(X), PlaneXch{});
+}
+
+cudaError_t launch_plane_rfft2_scatter(int64_t planes, int n_y, int n_z, const double* x, const PlaneXch& xc,
+                                       cudaStream_t st) {
+  if (planes <= 0) return cudaSuccess;
+  if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
+  return launch_cluster(rfft2_256_kernel<true>, planes, st, x, static_cast<double2*>(nullptr), xc);
+}
+
+cudaError_t launch_plane_irfft2_gather(int64_t planes, int n_y, int n_z, const PlaneXch& xc, double* x, double scale,
+                                       cudaStream_t st) {
+  if (planes <= 0) return cudaSuccess;
+  if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
+  return launch_cluster(irfft2_256_kernel<true>, planes, st, static_cast<const double2*>(nullptr), x, scale, xc);
 }
 
 cudaError_t launch_plane_irfft2(int64_t planes, int n_y, int n_z, const void* X, double* x, double scale,
                                 cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(irfft2_256_kernel, planes, st, static_cast<const double2*>(X), x, scale);
+  return launch_cluster(irfft2_256_kernel<false>, planes, st, static_cast<const double2*>(X), x, scale, PlaneXch{});
 }
 
 }  // namespace shen

@@ -166,12 +166,16 @@ def _fam(family) -> int:
     return family_code(family)  # 0 = Gauss, 1 = Gauss-Lobatto
 
 
-def _wall_run(plan, x, rows_out):
-    """shen_wall_transform of (rows_in, L) complex128 lines -> (rows_out, L)."""
+def _wall_run(plan, x, rows_out, out=None):
+    """shen_wall_transform of (rows_in, L) complex128 lines -> (rows_out, L)
+    (into ``out`` when given: a contiguous complex128 device buffer of that shape)."""
     import torch
 
     L = x.shape[1]
-    out = torch.empty((rows_out, L), dtype=torch.complex128, device=x.device)
+    if out is None:
+        out = torch.empty((rows_out, L), dtype=torch.complex128, device=x.device)
+    elif not (out.is_cuda and out.dtype == torch.complex128 and out.is_contiguous() and out.numel() == rows_out * L):
+        raise ValueError("out must be a contiguous complex128 device buffer of rows_out x L elements")
     _lib.check(_lib.lib().shen_wall_transform(ctypes.byref(plan.struct), L, x.data_ptr(), out.data_ptr(),
                                               stream_handle()), "shen_wall_transform")
     return out
@@ -398,17 +402,23 @@ def wall_forward(lines, n_x: int, fam: int, sp: int, solve_mass: bool = True):
     return scal
 
 
-def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1):
+def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1, out=None):
     """(n, L) coefficients -> (N, L) values on the Chebyshev points, and the
     ``norm`` for the following ``irfft2`` (the wall kernel folds the
-    1/(n_y n_z) of the inverse FFT into its output scale)."""
+    1/(n_y n_z) of the inverse FFT into its output scale).  ``out``: write the
+    values into this (N, L) complex128 device buffer (the slab transforms'
+    exchange buffer)."""
     if XFORM_METHOD == "wall" and n_x >= 2:
         from .wall import wall_plan
 
         plan = wall_plan(n_x, fam, sp, 1, False, 1.0 / yz_points)
         if plan is not None and plan.struct.n_in == coef.shape[0] and not (fam == 0 and plan.struct.log2_lines == 0):
-            return _wall_run(plan, coef.contiguous(), n_x + 1), "forward"
-    return _expand_pass(coef, sp, n_x, fam), "backward"
+            return _wall_run(plan, coef.contiguous(), n_x + 1, out), "forward"
+    vals = _expand_pass(coef, sp, n_x, fam)
+    if out is not None:
+        out.view(vals.shape).copy_(vals)
+        vals = out.view(vals.shape)
+    return vals, "backward"
 
 
 # ---------------------------------------------------------------- 3-D transforms

@@ -86,12 +86,26 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
         "shen_plane_rfft2": (1, 128, 256, 16, 16, None),  # unsupported plane size
         "shen_plane_irfft2": (1, 256, 256, 24, 8, ctypes.c_double(1.0), None),  # X not 16-B aligned
+        # exchange-fused plane FFTs: no rank tables / 9 ranks
+        "shen_plane_rfft2_scatter": (1, 256, 256, 16, 2, None, None, None, None, 0, 1, None),
+        "shen_plane_irfft2_gather": (1, 256, 256, 9, None, None, None, None, 0, 1, 16, ctypes.c_double(1.0), None),
     }
     for name, args in cases.items():
         st = getattr(h, name)(*args)
         assert st == 1, name
         assert name.encode() in h.shen_last_error() or b"bad args" in h.shen_last_error(), name
     assert h.shen_plane_fft_supported(256, 256) == 1 and h.shen_plane_fft_supported(64, 32) == 0
+    # a row table that points outside its owner's buffer, or planes past the total, are rejected
+    bases = (ctypes.c_void_p * 2)(4096, 8192)
+    rows = (ctypes.c_int64 * 2)(128, 128)
+    owner = (ctypes.c_int * 256)(*([0] * 128 + [1] * 128))
+    local = (ctypes.c_int * 256)(*(list(range(128)) * 2))
+    local_bad = (ctypes.c_int * 256)(*([128] + list(range(1, 128)) + list(range(128))))
+    owner_bad = (ctypes.c_int * 256)(*([2] + [0] * 127 + [1] * 128))
+    for ow, lo, plane0, total in ((owner, local_bad, 0, 4), (owner_bad, local, 0, 4), (owner, local, 3, 4)):
+        assert h.shen_plane_rfft2_scatter(2, 256, 256, 16, 2, bases, rows, ow, lo, plane0, total, None) == 1
+        assert h.shen_plane_irfft2_gather(2, 256, 256, 2, bases, rows, ow, lo, plane0, total, 16,
+                                          ctypes.c_double(1.0), None) == 1
     for name, cls in (("shen_rhs_g", _lib.ShenRhsGArgs), ("shen_rhs_u", _lib.ShenRhsUArgs),
                       ("shen_recover_velocity", _lib.ShenRecoverArgs)):
         a = cls()
