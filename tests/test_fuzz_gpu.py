@@ -7,6 +7,8 @@ sides, both point families).  Same gates as the reference's own tests
 relative difference <= 1e-10 for the solves, 1e-10 per line for the transforms
 (1e-12 in the Dirichlet space)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -18,13 +20,16 @@ from paper_1701_03787_b200.mesh import PointFamily, Space, build_mesh, channel_z
 
 pytestmark = pytest.mark.gpu
 
+# SHEN_FUZZ_SEEDS=n widens both sweeps (a soak run; the default keeps the suite short)
+_N = int(os.environ.get("SHEN_FUZZ_SEEDS", "0"))
+
 FAMS = [PointFamily.GAUSS, PointFamily.GAUSS_LOBATTO]
 SPACES = [Space.CHEBYSHEV, Space.DIRICHLET, Space.BIHARMONIC]
 
 
 def _solve_case(seed):
     rng = np.random.default_rng(1000 + seed)
-    n_x = int(rng.choice([rng.integers(6, 40), rng.integers(40, 200), rng.integers(200, 700)]))
+    n_x = int(rng.choice([rng.integers(8, 40), rng.integers(40, 200), rng.integers(200, 700)]))  # assemble: n_x >= 8
     fam = int(rng.integers(0, 2))
     kind = int(rng.integers(0, 3))
     if kind == 0:  # a channel plane: mirror pairs, self-paired rows
@@ -40,7 +45,7 @@ def _solve_case(seed):
     return rng, n_x, fam, z2, nu, dt, cplx
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(_N or 24))
 def test_random_solves_vs_oracle(seed):
     rng, n_x, fam, z2, nu, dt, cplx = _solve_case(seed)
     mats = assemble(n_x, fam)
@@ -59,7 +64,7 @@ def test_random_solves_vs_oracle(seed):
         assert err <= 1e-10, (seed, n_x, fam, z2.shape, cplx, build.__name__, err)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(_N // 2 or 12))
 def test_random_transforms_vs_oracle(seed):
     rng = np.random.default_rng(2000 + seed)
     n_x = 2 * int(rng.choice([rng.integers(4, 33), rng.integers(33, 130), rng.integers(130, 330)]))  # build_mesh: even
