@@ -85,3 +85,47 @@ def test_random_transforms_vs_oracle(seed):
         back = T.inverse_transform(T.SpectralField(want, c.grid, mesh)).data
         wb = O.inverse_transform(want, sc, fi == 1, n_x, mesh.n_y, mesh.n_z)
         assert np.abs(back - wb).max() <= 1e-12 * np.abs(wb).max(), (seed, n_x, fi, sc, "inverse")
+
+
+# ---------------------------------------------------------------- the stepper's callers
+APPLY_NAMES = ("mass_dir", "mass_bih", "mixed_mass", "stiff_dir", "stiff_bih", "fourth_bih", "deriv_dir_to_bih",
+               "deriv_bih_to_dir", "deriv_dir_to_cheb")
+
+
+@pytest.mark.parametrize("seed", range(_N // 4 or 8))
+def test_random_rhs_recover_apply_vs_oracle(seed):
+    """RHS assembly and structured apply bit-identical, velocity recovery to
+    1e-12, on random meshes (n_x even as build_mesh asks, line counts on both
+    sides of the kernels' 4096-line switch)."""
+    from paper_1701_03787_b200 import operators as P, recover as R, rhs as H
+    from paper_1701_03787_b200.mesh import wavenumber_grid
+
+    rng = np.random.default_rng(3000 + seed)
+    n_x = 2 * int(rng.choice([rng.integers(4, 20), rng.integers(20, 100), rng.integers(100, 300)]))
+    fi = int(rng.integers(0, 2))
+    n_y, n_z = 2 * int(rng.integers(1, 40)), 2 * int(rng.integers(1, 60))
+    mesh = build_mesh(n_x, n_y, n_z, float(rng.uniform(2, 14)), float(rng.uniform(1, 7)), FAMS[fi])
+    grid = wavenumber_grid(mesh, Space.DIRICHLET)
+    m, n, z2 = grid.m_scaled[:, None], grid.n_scaled[None, :], grid.z2()
+    mats = assemble(n_x, fi)
+    nu, dt = float(10 ** rng.uniform(-4, -2)), float(10 ** rng.uniform(-5, -2))
+    shp_d, shp_b = (mats.n_dir,) + z2.shape, (mats.n_bih,) + z2.shape
+
+    def c(shp):
+        return rng.standard_normal(shp) + 1j * rng.standard_normal(shp)
+
+    u, g = c(shp_b), c(shp_d)
+    hc, hp = [c(shp_d) for _ in range(3)], [c(shp_d) for _ in range(3)]
+    hab = O.ab2(hc, hp)
+    asm = H.RhsAssembler(mats, nu, dt, z2, m, n)
+    tag = (seed, n_x, fi, n_y, n_z)
+    assert np.array_equal(asm.rhs_u(u, hc, hp), O.assemble_rhs_u(mats, nu, dt, z2, m, n, u, hab)), tag
+    assert np.array_equal(asm.rhs_g(g, hc, hp), O.assemble_rhs_g(mats, nu, dt, z2, m, n, g, hab)), tag
+    want_v, want_w = O.recover_velocity(mats, z2, m, n, u, g)
+    v, w = R.VelocityRecovery(mats, z2, m, n)(u, g)
+    assert np.abs(v - want_v).max() <= 1e-12 * np.abs(want_v).max(), tag
+    assert np.abs(w - want_w).max() <= 1e-12 * np.abs(want_w).max(), tag
+    name = APPLY_NAMES[seed % len(APPLY_NAMES)]
+    M = getattr(mats, name)
+    x = c((M.shape[1],) + z2.shape) if seed % 2 else rng.standard_normal((M.shape[1],) + z2.shape)
+    assert np.array_equal(P.apply(M, x), M.apply(x)), tag + (name,)
