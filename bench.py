@@ -12,6 +12,10 @@ reported separately).  Multi-GPU: one process per GPU, kx slabs, no
 collectives on the data path (weak scaling of the wavenumber plane would be
 'strong' here: the plane is fixed and split -- see "scaling").
 
+--config c3 is BASELINE config 3 (transforms + solves on a 257 x 256 x 256
+field); with --gpus N > 1 it runs on x-plane / kx-row slabs with the exchange
+fused into the plane FFT kernels over peer memory (run_c3_slab).
+
 The reference arm (--impl reference) times the oracle port of the reference
 CPU algorithm (numpy, identical arithmetic) on all host cores over kx slabs.
 """
@@ -495,7 +499,7 @@ def run_c3(args):
     (n_x = 256, Gauss points); one step = forward Dirichlet transform ->
     Helmholtz solve per wavenumber -> inverse, then forward biharmonic
     transform -> biharmonic solve -> inverse, all on device-resident data.
-    Single GPU (the transforms do not shard without a transpose)."""
+    One rank: this function; several ranks: run_c3_slab (slab transforms)."""
     import torch
 
     from paper_1701_03787_b200 import solvers as S
@@ -504,8 +508,8 @@ def run_c3(args):
     from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
 
     rank, world, local = dist_env()
-    if rank != 0:
-        return
+    if world > 1:
+        return run_c3_slab(args)
     torch.cuda.set_device(local)
     nu, dt = 1e-3, 1e-3
     mesh = build_mesh(256, 256, 256, 2 * np.pi, np.pi)
@@ -569,6 +573,90 @@ def run_c3(args):
         "solved_unknowns_per_s": unk * args.steps / (total_ms / 1e3),
         "cpu_baseline": cpu, "clocks": clk.summary(),
     }))
+
+
+def run_c3_slab(args):
+    """Config 3 on several ranks: every rank holds its x-planes of the field
+    and its folded kx rows of the spectra.  One step =
+    the same six stages as run_c3 through distributed.forward_transform_slab /
+    inverse_transform_slab, with the kx-row exchange fused into the plane FFT
+    kernels over peer memory (distributed.PeerExchange), and the solves of
+    the rank's rows.  Strong scaling: the field is fixed, max over ranks.
+    SHEN_BENCH_BACKEND=gloo lets several ranks share one GPU (the launcher's
+    test; NCCL refuses that) -- not a bench number."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_03787_b200 import distributed as D
+    from paper_1701_03787_b200 import solvers as S
+    from paper_1701_03787_b200.matrices import assemble
+    from paper_1701_03787_b200.mesh import Space, build_mesh, wavenumber_grid
+
+    rank, world, local = dist_env()
+    backend = os.environ.get("SHEN_BENCH_BACKEND", "nccl")
+    shared_gpu = backend == "gloo"
+    dev = 0 if shared_gpu else local
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
+    nu, dt = 1e-3, 1e-3
+    n_x = int(os.environ.get("SHEN_BENCH_C3_NX", "256"))  # the launcher's test uses a thin mesh
+    mesh = build_mesh(n_x, 256, 256, 2 * np.pi, np.pi)
+    N = n_x + 1
+    mats = assemble(n_x, 0)
+    rows = D.kx_rows(mesh.n_y, rank, world)
+    z2 = wavenumber_grid(mesh, Space.DIRICHLET).z2()[rows]
+    hlu = S.build_helmholtz(mats, nu, dt, z2)
+    blu = S.build_biharmonic(mats, nu, dt, z2)
+    lo, hi = D.plane_slab(N, rank, world)
+    g = torch.Generator(device="cuda").manual_seed(33)
+    u = (torch.rand(mesh.shape, generator=g, device="cuda", dtype=torch.float64) * 2 - 1)[lo:hi].contiguous()
+    ex = D.PeerExchange(N, mesh.n_y, mesh.n_z)
+    out = {}
+
+    def step():
+        cd = D.forward_transform_slab(u, mesh, Space.DIRICHLET, exchange=ex)
+        xh = hlu.solve(cd)
+        out["ud"] = D.inverse_transform_slab(xh, mesh, Space.DIRICHLET, exchange=ex)
+        cb = D.forward_transform_slab(u, mesh, Space.BIHARMONIC, exchange=ex)
+        xb = blu.solve(cb)
+        out["ub"] = D.inverse_transform_slab(xb, mesh, Space.BIHARMONIC, exchange=ex)
+
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(dev) as clk:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            step()
+        t1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    if rank == 0:
+        B = mesh.n_y * (mesh.n_z // 2 + 1)
+        print(json.dumps({
+            "metric": "config-3 steps/s (fwd transform + solve + inverse, Dirichlet/Helmholtz and biharmonic)",
+            "value": args.steps / (total_ms / 1e3), "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": warm, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 (real field, complex128 spectra)",
+            "data": "synthetic: real U(-1,1) field, torch Philox seed 33",
+            "config": {"workload": f"config3: physical {N}x256x256 (n_x={n_x} Gauss, n_y=n_z=256), nu=dt=1e-3",
+                       "parallelism": f"x-plane slabs / folded kx-row slabs x{world}, exchange fused into the plane "
+                                      "FFT kernels (peer memory)" + (", ranks share one GPU (gloo)" if shared_gpu else ""),
+                       "l2_policy": "each stage streams arrays larger than L2 at n_x = 256"},
+            "solved_unknowns_per_s": (mats.n_dir + mats.n_bih) * B * args.steps / (total_ms / 1e3),
+            "gpu_launches": 10 * args.steps, "e2e": None, "clocks": clk.summary()}))
+    dist.barrier()
+    del ex
+    dist.destroy_process_group()
 
 
 def c3_wall_stages(mesh, u, B):
