@@ -309,6 +309,15 @@ int shen_cross(int64_t n, const double* fields, double* h, void* stream);
 int shen_plane_fft_supported(int n_y, int n_z);
 int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* X, void* stream);
 int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream);
+/* The same with a factor per (ky, kz) Fourier line, (n_y, n_z/2+1) float64 arrays on the device, applied to every
+ * plane: shen_plane_rfft2_fac multiplies the spectrum by the real `fac` at the store (the dealiasing mask of
+ * apply_mask, reference stepper.py:142-144, which commutes with the per-line wall-normal transform that follows);
+ * shen_plane_irfft2_fac multiplies the spectrum by fac_re + i fac_im at the load (i m, i n: the y / z derivatives of
+ * compute_nonlinear, stepper.py:171-172), so neither needs its own pass over the field. */
+int shen_plane_rfft2_fac(int64_t n_planes, int n_y, int n_z, const double* x, void* X, const double* fac,
+                         void* stream);
+int shen_plane_irfft2_fac(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale,
+                          const double* fac_re, const double* fac_im, void* stream);
 
 /* ---------------------------------------------------------------------
  * The same transforms with the slab decomposition's kx-row exchange fused in

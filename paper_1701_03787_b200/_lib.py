@@ -112,6 +112,9 @@ _SIGS = {
     "shen_plane_fft_supported": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "shen_plane_rfft2": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "shen_plane_irfft2": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_double, _vp]),
+    "shen_plane_rfft2_fac": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "shen_plane_irfft2_fac": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_double, _vp, _vp,
+                                             _vp]),
     "shen_plane_rfft2_scatter": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp, _vp, _vp,
                                                 _vp, _c_int64, _c_int64, _vp]),
     "shen_plane_irfft2_gather": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp,

@@ -347,7 +347,17 @@ int shen_plane_rfft2(int64_t n_planes, int n_y, int n_z, const double* x, void* 
   if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
       (reinterpret_cast<uintptr_t>(X) & 15))
     return fail(SHEN_ERR_ARG, "shen_plane_rfft2: bad args (sizes: shen_plane_fft_supported; x 8-B, X 16-B aligned)");
-  return cuda_check(shen::launch_plane_rfft2(n_planes, n_y, n_z, x, X, S(stream)), "shen_plane_rfft2");
+  return cuda_check(shen::launch_plane_rfft2(n_planes, n_y, n_z, x, X, nullptr, S(stream)), "shen_plane_rfft2");
+}
+
+int shen_plane_rfft2_fac(int64_t n_planes, int n_y, int n_z, const double* x, void* X, const double* fac,
+                         void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  if (n_planes < 0 || !x || !X || !fac || !shen::plane_fft_supported(n_y, n_z) ||
+      (reinterpret_cast<uintptr_t>(x) & 7) || (reinterpret_cast<uintptr_t>(X) & 15) ||
+      (reinterpret_cast<uintptr_t>(fac) & 7))
+    return fail(SHEN_ERR_ARG, "shen_plane_rfft2_fac: bad args (sizes: shen_plane_fft_supported; x, fac 8-B, X 16-B aligned)");
+  return cuda_check(shen::launch_plane_rfft2(n_planes, n_y, n_z, x, X, fac, S(stream)), "shen_plane_rfft2_fac");
 }
 
 int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale, void* stream) {
@@ -355,7 +365,19 @@ int shen_plane_irfft2(int64_t n_planes, int n_y, int n_z, const void* X, double*
   if (n_planes < 0 || !x || !X || !shen::plane_fft_supported(n_y, n_z) || (reinterpret_cast<uintptr_t>(x) & 7) ||
       (reinterpret_cast<uintptr_t>(X) & 15))
     return fail(SHEN_ERR_ARG, "shen_plane_irfft2: bad args (sizes: shen_plane_fft_supported; x 8-B, X 16-B aligned)");
-  return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, S(stream)), "shen_plane_irfft2");
+  return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, nullptr, nullptr, S(stream)),
+                    "shen_plane_irfft2");
+}
+
+int shen_plane_irfft2_fac(int64_t n_planes, int n_y, int n_z, const void* X, double* x, double scale,
+                          const double* fac_re, const double* fac_im, void* stream) {
+  if (n_planes == 0) return SHEN_OK;
+  if (n_planes < 0 || !x || !X || !fac_re || !fac_im || !shen::plane_fft_supported(n_y, n_z) ||
+      (reinterpret_cast<uintptr_t>(x) & 7) || (reinterpret_cast<uintptr_t>(X) & 15) ||
+      ((reinterpret_cast<uintptr_t>(fac_re) | reinterpret_cast<uintptr_t>(fac_im)) & 7))
+    return fail(SHEN_ERR_ARG, "shen_plane_irfft2_fac: bad args (sizes: shen_plane_fft_supported; x, fac 8-B, X 16-B aligned)");
+  return cuda_check(shen::launch_plane_irfft2(n_planes, n_y, n_z, X, x, scale, fac_re, fac_im, S(stream)),
+                    "shen_plane_irfft2_fac");
 }
 
 // kx-row exchange descriptor from the caller's plain arrays (validated here:

@@ -190,9 +190,10 @@ cudaError_t launch_plane_rfft2_scatter(int64_t planes, int n_y, int n_z, const d
                                        cudaStream_t st);
 cudaError_t launch_plane_irfft2_gather(int64_t planes, int n_y, int n_z, const PlaneXch& xc, double* x, double scale,
                                        cudaStream_t st);
-cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, cudaStream_t st);
+cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, const double* fac,
+                               cudaStream_t st);
 cudaError_t launch_plane_irfft2(int64_t planes, int n_y, int n_z, const void* X, double* x, double scale,
-                                cudaStream_t st);
+                                const double* fac_re, const double* fac_im, cudaStream_t st);
 
 // fused wall-normal transforms (shen_wall.cu); tables built on the host (wall.py)
 struct WallPlan {

@@ -193,7 +193,8 @@ __device__ __forceinline__ void load_tw(double2* tw) {
 // slab transform's all-to-all fused into the FFT's store.
 template <bool XCH>
 __global__ void __launch_bounds__(kThreads, 4)
-    rfft2_256_kernel(const double* __restrict__ in, double2* __restrict__ out, const __grid_constant__ PlaneXch xc) {
+    rfft2_256_kernel(const double* __restrict__ in, double2* __restrict__ out, const __grid_constant__ PlaneXch xc,
+                     const double* __restrict__ fac) {
   extern __shared__ __align__(16) double sm[];
   double2* tw = reinterpret_cast<double2*>(sm);
   double* A = sm + 2 * 256;
@@ -272,6 +273,13 @@ __global__ void __launch_bounds__(kThreads, 4)
   PF_TS(4);
   if (z < kNZH) {
     dft16<false>(v);
+    if (fac != nullptr) {  // a real factor per (ky, kz) line, e.g. the dealiasing mask
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const double f = __ldg(fac + (c + 16 * k2) * kNZH + z);
+        v[k2] = make_double2(v[k2].x * f, v[k2].y * f);
+      }
+    }
     if (XCH) {
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) {
@@ -296,7 +304,8 @@ __global__ void __launch_bounds__(kThreads, 4)
 template <bool XCH>
 __global__ void __launch_bounds__(kThreads, 4)
     irfft2_256_kernel(const double2* __restrict__ in, double* __restrict__ out, double scale,
-                      const __grid_constant__ PlaneXch xc) {
+                      const __grid_constant__ PlaneXch xc, const double* __restrict__ fac_re,
+                      const double* __restrict__ fac_im) {
   extern __shared__ __align__(16) double sm[];
   double2* tw = reinterpret_cast<double2*>(sm);
   double* A = sm + 2 * 256;
@@ -320,6 +329,15 @@ __global__ void __launch_bounds__(kThreads, 4)
       const double2* ip = in + plane * (kNY * kNZH) + (int64_t)c * kNZH + z;
 #pragma unroll
       for (int k2 = 0; k2 < 16; ++k2) v[k2] = ld_nc2(ip + (int64_t)(16 * k2) * kNZH);
+    }
+    if (fac_re != nullptr) {  // a complex factor per (ky, kz) line (i m, i n: the y / z derivatives)
+#pragma unroll
+      for (int k2 = 0; k2 < 16; ++k2) {
+        const int e = (c + 16 * k2) * kNZH + z;
+        const double fr = __ldg(fac_re + e), fi = __ldg(fac_im + e);
+        // (a + i b)(fr + i fi) as shen_scale_lines forms it
+        v[k2] = make_double2(v[k2].x * fr - v[k2].y * fi, v[k2].x * fi + v[k2].y * fr);
+      }
     }
   }
   load_tw(tw);
@@ -433,31 +451,35 @@ cudaError_t launch_cluster(K kernel, int64_t planes, cudaStream_t st, Args... ar
 
 bool plane_fft_supported(int n_y, int n_z) { return n_y == kNY && n_z == kNZ; }
 
-cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, cudaStream_t st) {
+cudaError_t launch_plane_rfft2(int64_t planes, int n_y, int n_z, const double* x, void* X, const double* fac,
+                               cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(rfft2_256_kernel<false>, planes, st, x, static_cast<double2*>(X), PlaneXch{});
+  return launch_cluster(rfft2_256_kernel<false>, planes, st, x, static_cast<double2*>(X), PlaneXch{}, fac);
 }
 
 cudaError_t launch_plane_rfft2_scatter(int64_t planes, int n_y, int n_z, const double* x, const PlaneXch& xc,
                                        cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(rfft2_256_kernel<true>, planes, st, x, static_cast<double2*>(nullptr), xc);
+  return launch_cluster(rfft2_256_kernel<true>, planes, st, x, static_cast<double2*>(nullptr), xc,
+                        static_cast<const double*>(nullptr));
 }
 
 cudaError_t launch_plane_irfft2_gather(int64_t planes, int n_y, int n_z, const PlaneXch& xc, double* x, double scale,
                                        cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(irfft2_256_kernel<true>, planes, st, static_cast<const double2*>(nullptr), x, scale, xc);
+  return launch_cluster(irfft2_256_kernel<true>, planes, st, static_cast<const double2*>(nullptr), x, scale, xc,
+                        static_cast<const double*>(nullptr), static_cast<const double*>(nullptr));
 }
 
 cudaError_t launch_plane_irfft2(int64_t planes, int n_y, int n_z, const void* X, double* x, double scale,
-                                cudaStream_t st) {
+                                const double* fac_re, const double* fac_im, cudaStream_t st) {
   if (planes <= 0) return cudaSuccess;
   if (!plane_fft_supported(n_y, n_z) || planes * kC > 0x7fffffffLL) return cudaErrorInvalidValue;
-  return launch_cluster(irfft2_256_kernel<false>, planes, st, static_cast<const double2*>(X), x, scale, PlaneXch{});
+  return launch_cluster(irfft2_256_kernel<false>, planes, st, static_cast<const double2*>(X), x, scale, PlaneXch{},
+                        fac_re, fac_im);
 }
 
 }  // namespace shen

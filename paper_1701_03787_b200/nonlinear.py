@@ -12,12 +12,15 @@ transforms):
   reference's structured apply) gives the Chebyshev coefficients, the inverse
   Chebyshev-space plan scales them by 1/mass_cheb in its gather (the
   reference's ``c *= mass_inv``, same product) and evaluates them;
-* du/dy, du/dz: the 1j m / 1j n factors act per Fourier line, so they scale
-  u's evaluated lines (``shen_scale_lines``);
-* one batched cuFFT irfft2 for the 8 fields (periodic directions),
-  ``shen_cross`` for om_y, om_z and the three components of H (one pass), one
-  batched rfft2, three forward Dirichlet plans (DCT + stencil + mass solve) and
-  the dealiasing mask (``shen_scale_lines``).
+* du/dy, du/dz: the 1j m / 1j n factors act per Fourier line, so the plane
+  irfft2 kernel applies them to u's evaluated lines while it loads them
+  (``shen_plane_irfft2_fac``): no pass or array of their own;
+* the periodic irfft2 of the 8 fields (``csrc/shen_plane_fft.cu`` for 256 x
+  256 planes), ``shen_cross`` for om_y, om_z and the three components of H
+  (one pass), one batched rfft2 with the dealiasing mask applied at its store
+  (``shen_plane_rfft2_fac``; the 0 / 1 factor per line commutes with the
+  per-line stage that follows), three forward Dirichlet plans (DCT + stencil
+  + mass solve).
 
 No GEMM: the wall-normal work is the O(N log N) on-chip DCTs.  Rounding
 differs from the reference's pocketfft/LAPACK chain at the 1e-15 level
@@ -82,10 +85,6 @@ class NonlinearTerm:
         _lib.check(_lib.lib().shen_wall_transform(ctypes.byref(plan.struct), self.L, x.data_ptr(), out.data_ptr(),
                                                   stream_handle()), "shen_wall_transform")
 
-    def _scale(self, x, c, y):
-        _lib.check(_lib.lib().shen_scale_lines(x.shape[0], self.L, x.data_ptr(), c[0].data_ptr(), c[1].data_ptr(),
-                                               y.data_ptr(), stream_handle()), "shen_scale_lines")
-
     def __call__(self, u_hat, v_hat, w_hat, g_hat):
         """Three (n_dir, n_y, n_z/2+1) complex128 arrays: masked Dirichlet
         coefficients of H = u x omega (numpy in -> numpy out)."""
@@ -102,29 +101,34 @@ class NonlinearTerm:
         L, N = self.L, self.n_x + 1
         # point values (wall-normal) of the 8 fields on the Fourier lines, in shen_cross order:
         # u, v, w, om_x, dv/dx, dw/dx, du/dy, du/dz (stepper.py:165-174)
-        spec = torch.empty((8, N, L), dtype=torch.complex128, device=self.dev)
+        # The y / z derivatives of u (fields 6, 7) are its lines times i m / i n: the plane kernel
+        # applies the factor while it loads the lines, so they need no pass (or array) of their own.
+        spec = torch.empty((6, N, L), dtype=torch.complex128, device=self.dev)
         self._wall(self._inv[2], u_hat, spec[0])
         self._wall(self._inv[1], v_hat, spec[1])
         self._wall(self._inv[1], w_hat, spec[2])
         self._wall(self._inv[1], g_hat, spec[3])
         self._wall(self._inv_ddx, self._deriv(v_hat.view(v_hat.shape[0], L)), spec[4])
         self._wall(self._inv_ddx, self._deriv(w_hat.view(w_hat.shape[0], L)), spec[5])
-        self._scale(spec[0], self._cm, spec[6])  # du/dy lines
-        self._scale(spec[0], self._cn, spec[7])  # du/dz lines
-        phys = plane_irfft2(spec.view(8, N, self.n_y, self.nzh), self.n_y, self.n_z, "forward")
+        phys = torch.empty((8, N, self.n_y, self.n_z), dtype=torch.float64, device=self.dev)
+        plane_irfft2(spec.view(6, N, self.n_y, self.nzh), self.n_y, self.n_z, "forward", out=phys[:6])
+        u_lines = spec[0].view(N, self.n_y, self.nzh)
+        plane_irfft2(u_lines, self.n_y, self.n_z, "forward", fac=self._cm, out=phys[6])  # du/dy
+        plane_irfft2(u_lines, self.n_y, self.n_z, "forward", fac=self._cn, out=phys[7])  # du/dz
         del spec
         npt = N * self.n_y * self.n_z
         h = torch.empty((3, N, self.n_y, self.n_z), dtype=torch.float64, device=self.dev)
         _lib.check(_lib.lib().shen_cross(npt, phys.data_ptr(), h.data_ptr(), stream_handle()), "shen_cross")
         del phys
-        hf = plane_rfft2(h).view(3, N, L)
+        # dealiasing mask (apply_mask, stepper.py:142-144) at the plane kernel's store: a 0 / 1 factor
+        # per Fourier line commutes with the per-line wall-normal transform that follows
+        hf = plane_rfft2(h, fac=self._mask[0]).view(3, N, L)
         del h
         n_dir = self.n_x - 1
         out = []
         for i in range(3):
             o = torch.empty((n_dir, L), dtype=torch.complex128, device=self.dev)
             self._wall(self._fwd, hf[i], o)
-            self._scale(o, self._mask, o)  # dealiasing mask (apply_mask, stepper.py:142-144)
             o = o.view(n_dir, self.n_y, self.nzh)
             out.append(o.cpu().numpy() if from_numpy else o)
         return tuple(out)

@@ -423,37 +423,76 @@ def wall_inverse(coef, n_x: int, fam: int, sp: int, yz_points: int = 1, out=None
 
 # ---------------------------------------------------------------- 3-D transforms
 
-def plane_rfft2(u):
+def plane_rfft2(u, fac=None):
     """numpy ``rfft2`` over the last two axes of a contiguous float64 CUDA
     tensor (..., n_y, n_z).  256 x 256 planes run on the cluster kernel of
-    ``csrc/shen_plane_fft.cu`` (one HBM pass); other sizes on cuFFT."""
+    ``csrc/shen_plane_fft.cu`` (one HBM pass); other sizes on cuFFT.
+    ``fac``: a real float64 device tensor of n_y (n_z/2+1) elements that
+    multiplies every plane's spectrum (applied at the kernel's store)."""
     import torch
 
     n_y, n_z = u.shape[-2], u.shape[-1]
     if not _lib.lib().shen_plane_fft_supported(n_y, n_z):
-        return torch.fft.rfft2(u, dim=(-2, -1)).contiguous()
+        X = torch.fft.rfft2(u, dim=(-2, -1))
+        if fac is not None:
+            X = X * fac.view(n_y, n_z // 2 + 1)
+        return X.contiguous()
     u = u.contiguous()
     out = torch.empty(u.shape[:-1] + (n_z // 2 + 1,), dtype=torch.complex128, device=u.device)
     planes = u.numel() // (n_y * n_z)
-    _lib.check(_lib.lib().shen_plane_rfft2(planes, n_y, n_z, u.data_ptr(), out.data_ptr(), stream_handle()),
-               "shen_plane_rfft2")
+    if fac is None:
+        _lib.check(_lib.lib().shen_plane_rfft2(planes, n_y, n_z, u.data_ptr(), out.data_ptr(), stream_handle()),
+                   "shen_plane_rfft2")
+    else:
+        _check_fac(fac, n_y, n_z, u.device)
+        _lib.check(_lib.lib().shen_plane_rfft2_fac(planes, n_y, n_z, u.data_ptr(), out.data_ptr(), fac.data_ptr(),
+                                                   stream_handle()), "shen_plane_rfft2_fac")
     return out
 
 
-def plane_irfft2(X, n_y: int, n_z: int, norm: str = "backward"):
-    """numpy ``irfft2(X, s=(n_y, n_z), norm=norm)`` over the last two axes of
-    a contiguous complex128 CUDA tensor (..., n_y, n_z/2 + 1); cluster kernel
-    for 256 x 256 planes, cuFFT otherwise."""
+def _check_fac(f, n_y, n_z, dev):
     import torch
 
+    if not (is_torch(f) and f.device == dev and f.dtype == torch.float64 and f.is_contiguous()
+            and f.numel() == n_y * (n_z // 2 + 1)):
+        raise ValueError("line factors must be contiguous float64 device tensors of n_y (n_z/2+1) elements")
+
+
+def plane_irfft2(X, n_y: int, n_z: int, norm: str = "backward", fac=None, out=None):
+    """numpy ``irfft2(X, s=(n_y, n_z), norm=norm)`` over the last two axes of
+    a contiguous complex128 CUDA tensor (..., n_y, n_z/2 + 1); cluster kernel
+    for 256 x 256 planes, cuFFT otherwise.  ``fac = (re, im)``: float64 device
+    tensors of n_y (n_z/2+1) elements; every plane's spectrum is multiplied by
+    re + i im first (at the kernel's load).  ``out``: a contiguous float64
+    device tensor of the result's shape to write into."""
+    import torch
+
+    shape = X.shape[:-2] + (n_y, n_z)
+    if out is not None and not (out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()
+                                and tuple(out.shape) == tuple(shape)):
+        raise ValueError(f"out must be a contiguous float64 device tensor of shape {tuple(shape)}")
     if not _lib.lib().shen_plane_fft_supported(n_y, n_z) or X.shape[-1] != n_z // 2 + 1 or X.shape[-2] != n_y:
-        return torch.fft.irfft2(X, s=(n_y, n_z), dim=(-2, -1), norm=norm)
+        if fac is not None:
+            X = X * torch.complex(fac[0], fac[1]).view(n_y, n_z // 2 + 1)
+        r = torch.fft.irfft2(X, s=(n_y, n_z), dim=(-2, -1), norm=norm)
+        if out is None:
+            return r
+        out.copy_(r)
+        return out
     X = X.contiguous()
-    out = torch.empty(X.shape[:-1] + (n_z,), dtype=torch.float64, device=X.device)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64, device=X.device)
     planes = X.numel() // (n_y * (n_z // 2 + 1))
     scale = {"backward": 1.0 / (n_y * n_z), "forward": 1.0, "ortho": 1.0 / np.sqrt(n_y * n_z)}[norm]
-    _lib.check(_lib.lib().shen_plane_irfft2(planes, n_y, n_z, X.data_ptr(), out.data_ptr(), ctypes.c_double(scale),
-                                            stream_handle()), "shen_plane_irfft2")
+    if fac is None:
+        _lib.check(_lib.lib().shen_plane_irfft2(planes, n_y, n_z, X.data_ptr(), out.data_ptr(), ctypes.c_double(scale),
+                                                stream_handle()), "shen_plane_irfft2")
+    else:
+        _check_fac(fac[0], n_y, n_z, X.device)
+        _check_fac(fac[1], n_y, n_z, X.device)
+        _lib.check(_lib.lib().shen_plane_irfft2_fac(planes, n_y, n_z, X.data_ptr(), out.data_ptr(),
+                                                    ctypes.c_double(scale), fac[0].data_ptr(), fac[1].data_ptr(),
+                                                    stream_handle()), "shen_plane_irfft2_fac")
     return out
 
 
