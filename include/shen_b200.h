@@ -75,7 +75,9 @@ int shen_pivot_reset(int* pivot_dev, void* stream);
  *     pivot_dev  = int[2]; atomic-min of the first row (within parity) whose
  *                  pivot has |d| < 1e-300 (reset it first).
  * shen_helm_solve_stream: fused factor+solve from the checkpoints (ckpt made
- *   with exact == 0, chunk_rows in {4, 8, 16}); one thread per (system,
+ *   with exact == 0, chunk_rows = 8: the spacing the solve kernels are
+ *   built for -- 4 doubles the checkpoint memory, 16 spills registers); one
+ *   thread per (system,
  *   parity) with coalesced row access; y is
  *   checkpointed at segment ends in `scratch` (shen_stream_scratch_bytes
  *   bytes) and recomputed in the backward sweep; warps_per_sm selects the

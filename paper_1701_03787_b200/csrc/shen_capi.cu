@@ -115,7 +115,7 @@ int shen_helm_solve_stream(int n_dir, double ca, const double* cb, int64_t batch
   if (n_dir < 2 || batch < 0 || !cb || !sd || !st || !md || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: bad args");
   const int rows0 = (n_dir + 1) / 2;
-  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: chunk_rows");
+  if (chunk_rows != 8) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: chunk_rows (8)");
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: rhs must not alias out");
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_helm_solve_stream: scratch required");
@@ -168,7 +168,7 @@ int shen_bih_solve_stream(int n_bih, double xi0, const double* xi1, const double
   if (n_bih < 2 || batch < 0 || !xi1 || !xi2 || !tab || !rhs || !out)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: bad args");
   const int rows0 = (n_bih + 1) / 2;
-  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: chunk_rows");
+  if (chunk_rows != 8) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: chunk_rows (8)");
   if (rows0 > chunk_rows && !ckpt) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: ckpt required");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: rhs must not alias out");
   if (rows0 > chunk_rows && !scratch) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream: scratch required");
@@ -188,8 +188,7 @@ int shen_bih_solve_stream_pairs(int n_bih, double xi0, const double* xi1, const 
   if (n_bih < 2 || batch < 0 || n_pairs < 0 || n_pairs > batch || !xi1 || !xi2 || !tab || !rhs || !out || !pairs)
     return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: bad args");
   const int rows0 = (n_bih + 1) / 2;
-  if (chunk_rows != 4 && chunk_rows != 8 && chunk_rows != 16)
-    return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: chunk_rows");
+  if (chunk_rows != 8) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: chunk_rows (8)");
   if (rows0 > chunk_rows && (!ckpt || !scratch)) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: ckpt/scratch");
   if (rhs == out) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: rhs must not alias out");
   if (max_ctas < 0) return fail(SHEN_ERR_ARG, "shen_bih_solve_stream_pairs: max_ctas");

@@ -1136,25 +1136,14 @@ static cudaError_t bih_stream_R(const BihChunkArgs& a, void* scratch, int ctas_p
 // can afford to prefetch the segment checkpoints into registers).
 template <typename V>
 static cudaError_t helm_stream_dispatch(const HelmChunkArgs& a, void* sc, int w, cudaStream_t st) {
-  const bool small = (w == 8);
-  switch (a.chunk_rows) {
-    case 4: return small ? helm_stream_R<V, 4, 4>(a, sc, 1, st) : helm_stream_R<V, 4, 6>(a, sc, 1, st);
-    case 8:
-      return small ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
-    case 16: return helm_stream_R<V, 16, 4>(a, sc, 1, st);
-    default: return cudaErrorInvalidValue;
-  }
+  if (a.chunk_rows != 8) return cudaErrorInvalidValue;  // the checkpoint spacing the kernels are built for
+  return w == 8 ? helm_stream_R<V, 8, 4>(a, sc, 1, st) : helm_stream_R<V, 8, 6>(a, sc, 1, st);
 }
 
 template <typename V>
 static cudaError_t bih_stream_dispatch(const BihChunkArgs& a, void* sc, int w, cudaStream_t st) {
-  const bool small = (w != 12);
-  switch (a.chunk_rows) {
-    case 4: return small ? bih_stream_R<V, 4, 4>(a, sc, 1, st) : bih_stream_R<V, 4, 6>(a, sc, 1, st);
-    case 8: return small ? bih_stream_R<V, 8, 4>(a, sc, 1, st) : bih_stream_R<V, 8, 6>(a, sc, 1, st);
-    case 16: return bih_stream_R<V, 16, 4>(a, sc, 1, st);
-    default: return cudaErrorInvalidValue;
-  }
+  if (a.chunk_rows != 8) return cudaErrorInvalidValue;
+  return w != 12 ? bih_stream_R<V, 8, 4>(a, sc, 1, st) : bih_stream_R<V, 8, 6>(a, sc, 1, st);
 }
 
 // per-CTA y-checkpoint scratch: grid is at most (#SMs x 8) CTAs

@@ -62,8 +62,8 @@ def _env_int(name, default):
     return int(os.environ.get(name, default))
 
 
-STREAM_ROWS_H = _env_int("SHEN_STREAM_ROWS_H", 8)  # checkpoint spacing of the streaming solve
-STREAM_ROWS_B = _env_int("SHEN_STREAM_ROWS_B", 8)
+STREAM_ROWS_H = 8  # checkpoint spacing (rows) the streaming solve kernels are built for
+STREAM_ROWS_B = 8
 
 
 def stream_warps() -> int:
