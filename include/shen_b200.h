@@ -284,18 +284,14 @@ typedef struct shen_recover_args {
 int shen_recover_velocity(const shen_recover_args* args, void* stream);
 
 /* ---------------------------------------------------------------------
- * Nonlinear term H = u x omega (reference stepper.py:148-185), pointwise
- * pieces; the transforms around them are shen_wall_transform + cuFFT.
- * shen_scale_lines: y[r][l] = c_l x[r][l] for rows x L complex128
- *   ((c.re x.re - c.im x.im, c.re x.im + c.im x.re), every product rounded);
- *   c = c_re + i c_im per line (1j m, 1j n, mask: exact either way).
+ * Nonlinear term H = u x omega (reference stepper.py:148-185), the pointwise
+ * piece; the transforms around it are shen_wall_transform and the plane FFTs
+ * below, whose _fac variants apply the per-line factors (1j m, 1j n, mask).
  * shen_cross: fields = 8 real planes-stacked arrays of n points
  *   [u, v, w, om_x, dv_dx, dw_dx, du_dy, du_dz] -> h = 3 arrays
  *   (v om_z - w om_y, w om_x - u om_z, u om_y - v om_x) with
  *   om_y = du_dz - dw_dx, om_z = dv_dx - du_dy.
  * ------------------------------------------------------------------- */
-int shen_scale_lines(int64_t rows, int64_t L, const void* x, const double* c_re, const double* c_im, void* y,
-                     void* stream);
 int shen_cross(int64_t n, const double* fields, double* h, void* stream);
 
 /* ---------------------------------------------------------------------

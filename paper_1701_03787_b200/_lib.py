@@ -107,7 +107,6 @@ _SIGS = {
     "shen_rhs_g": (ctypes.c_int, [ctypes.POINTER(ShenRhsGArgs), _vp]),
     "shen_rhs_u": (ctypes.c_int, [ctypes.POINTER(ShenRhsUArgs), _vp]),
     "shen_recover_velocity": (ctypes.c_int, [ctypes.POINTER(ShenRecoverArgs), _vp]),
-    "shen_scale_lines": (ctypes.c_int, [_c_int64, _c_int64, _vp, _vp, _vp, _vp, _vp]),
     "shen_cross": (ctypes.c_int, [_c_int64, _vp, _vp, _vp]),
     "shen_plane_fft_supported": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "shen_plane_rfft2": (ctypes.c_int, [_c_int64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),

@@ -326,13 +326,6 @@ int shen_rhs_u(const shen_rhs_u_args* u, void* stream) {
   return cuda_check(shen::launch_rhs_u(a, S(stream)), "shen_rhs_u");
 }
 
-int shen_scale_lines(int64_t rows, int64_t L, const void* x, const double* c_re, const double* c_im, void* y,
-                     void* stream) {
-  if (rows == 0 || L == 0) return SHEN_OK;
-  if (rows < 0 || L < 0 || !x || !c_re || !c_im || !y) return fail(SHEN_ERR_ARG, "shen_scale_lines: bad args");
-  return cuda_check(shen::launch_scale_lines(rows, L, x, c_re, c_im, y, S(stream)), "shen_scale_lines");
-}
-
 int shen_cross(int64_t n, const double* fields, double* h, void* stream) {
   if (n == 0) return SHEN_OK;
   if (n < 0 || !fields || !h) return fail(SHEN_ERR_ARG, "shen_cross: bad args");

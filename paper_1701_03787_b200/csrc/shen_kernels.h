@@ -169,8 +169,6 @@ struct RecoverArgs {
 cudaError_t launch_recover(const RecoverArgs& a, cudaStream_t st);
 
 // nonlinear-term pointwise kernels (shen_nonlinear.cu)
-cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const double* cre, const double* cim, void* y,
-                               cudaStream_t st);
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st);
 
 // periodic (y, z) plane FFTs (shen_plane_fft.cu): one 8-CTA cluster per plane

@@ -1,10 +1,9 @@
-// Pointwise pieces of the nonlinear term H = u x omega (reference
-// stepper.py:148-185), SURVEY.md 8(f) rank 3.  The transforms around them are
-// the fused wall-normal kernels (shen_wall.cu) and cuFFT (nonlinear.py).
+// Pointwise piece of the nonlinear term H = u x omega (reference
+// stepper.py:148-185), SURVEY.md 8(f) rank 3.  The transforms around it are
+// the fused wall-normal kernels (shen_wall.cu) and the plane FFT kernels
+// (shen_plane_fft.cu), which also apply the per-line factors (1j m, 1j n, the
+// dealiasing mask).
 //
-//   shen_scale_lines: y[r, l] = c_l * x[r, l] (complex, products rounded separately):
-//                     the 1j m / 1j n derivative factors and the dealiasing
-//                     mask, one per Fourier line;
 //   shen_cross:       om_y = du_dz - dw_dx, om_z = dv_dx - du_dy and
 //                     h = (v om_z - w om_y, w om_x - u om_z, u om_y - v om_x)
 //                     on the physical grid, in the reference's operation order
@@ -16,19 +15,6 @@
 
 namespace shen {
 namespace {
-
-__global__ void scale_lines_kernel(int64_t rows, int64_t L, const double2* x,
-                                   const double* __restrict__ cre, const double* __restrict__ cim,
-                                   double2* y) {  // x may alias y
-  const int64_t n = rows * L;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = i % L;
-    const double ar = __ldg(cre + l), ai = __ldg(cim + l);
-    const double2 b = x[i];
-    y[i] = make_double2(__dsub_rn(__dmul_rn(ar, b.x), __dmul_rn(ai, b.y)),
-                        __dadd_rn(__dmul_rn(ar, b.y), __dmul_rn(ai, b.x)));
-  }
-}
 
 // fields: [u, v, w, om_x, dv_dx, dw_dx, du_dy, du_dz], each n points apart
 __global__ void cross_kernel(int64_t n, const double* __restrict__ f, double* __restrict__ h) {
@@ -53,14 +39,6 @@ unsigned grid_for(int64_t n) {
 }
 
 }  // namespace
-
-cudaError_t launch_scale_lines(int64_t rows, int64_t L, const void* x, const double* cre, const double* cim, void* y,
-                               cudaStream_t st) {
-  if (rows <= 0 || L <= 0) return cudaSuccess;
-  scale_lines_kernel<<<grid_for(rows * L), 256, 0, st>>>(rows, L, static_cast<const double2*>(x), cre, cim,
-                                                         static_cast<double2*>(y));
-  return cudaGetLastError();
-}
 
 cudaError_t launch_cross(int64_t n, const double* fields, double* h, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -335,7 +335,6 @@ __global__ void __launch_bounds__(kThreads, 4)
       for (int k2 = 0; k2 < 16; ++k2) {
         const int e = (c + 16 * k2) * kNZH + z;
         const double fr = __ldg(fac_re + e), fi = __ldg(fac_im + e);
-        // (a + i b)(fr + i fi) as shen_scale_lines forms it
         v[k2] = make_double2(v[k2].x * fr - v[k2].y * fi, v[k2].x * fi + v[k2].y * fr);
       }
     }

@@ -81,11 +81,12 @@ def test_every_compute_entry_point_validates_arguments():
         "shen_apply_banded": (4, 4, 1, 9, None, None, None, None, 1, None),
         "shen_apply_const_tail": (4, 4, 1, 1, None, None, None, 2, None, None, 1, None),
         "shen_apply_rank2_tail": (4, 1, None, None, None, None, None, None, None, 1, None),
-        "shen_scale_lines": (2, 2, None, None, None, None, None),
         "shen_cross": (8, None, None, None),
         "shen_memcpy2d_async": (None, 16, None, 16, 16, 1, 0, None),
         "shen_plane_rfft2": (1, 128, 256, 16, 16, None),  # unsupported plane size
         "shen_plane_irfft2": (1, 256, 256, 24, 8, ctypes.c_double(1.0), None),  # X not 16-B aligned
+        "shen_plane_rfft2_fac": (1, 256, 256, 16, 16, None, None),  # no factor table
+        "shen_plane_irfft2_fac": (1, 256, 256, 16, 8, ctypes.c_double(1.0), 8, None, None),  # no imaginary table
         # exchange-fused plane FFTs: no rank tables / 9 ranks
         "shen_plane_rfft2_scatter": (1, 256, 256, 16, 2, None, None, None, None, 0, 1, None),
         "shen_plane_irfft2_gather": (1, 256, 256, 9, None, None, None, None, 0, 1, 16, ctypes.c_double(1.0), None),

@@ -256,3 +256,38 @@ def test_plane_fft_vs_numpy(lead):
         assert np.abs(back - wantb).max() <= 1e-14 * np.abs(wantb).max(), norm
     rt = plane_irfft2(X, 256, 256).cpu().numpy()
     assert np.abs(rt - x).max() <= 1e-14
+
+
+@pytest.mark.parametrize("n", [256, 64])
+def test_plane_fft_line_factors(n):
+    """The per-line factors of the nonlinear term inside the plane transforms:
+    rfft2 times a real mask (apply_mask, reference stepper.py:142-144) and
+    irfft2 of the spectrum times 1j m (stepper.py:171-172), on the cluster
+    kernel (256 x 256) and on the cuFFT fallback (64 x 64); ``out=`` writes
+    into a slice of a larger array."""
+    import torch
+
+    from paper_1701_03787_b200.transforms import plane_irfft2, plane_rfft2
+
+    rng = np.random.default_rng(n)
+    K = n // 2 + 1
+    x = rng.uniform(-1, 1, (3, n, n))
+    mask = (rng.uniform(0, 1, (n, K)) < 0.6).astype(np.float64)
+    X = plane_rfft2(torch.from_numpy(x).cuda(), fac=torch.from_numpy(mask.reshape(-1)).cuda()).cpu().numpy()
+    want = np.fft.rfft2(x) * mask
+    assert np.abs(X - want).max() <= 1e-14 * np.abs(want).max()
+    assert np.all(X[:, mask == 0] == 0)
+    Y = rng.standard_normal((3, n, K)) + 1j * rng.standard_normal((3, n, K))
+    m = 1j * (2 * np.pi * np.fft.fftfreq(n, 1.0 / n) / 7.0)[:, None] * np.ones((1, K))
+    fac = (torch.from_numpy(np.ascontiguousarray(m.real).reshape(-1)).cuda(),
+           torch.from_numpy(np.ascontiguousarray(m.imag).reshape(-1)).cuda())
+    big = torch.full((2, 3, n, n), 7.0, dtype=torch.float64, device="cuda")
+    got = plane_irfft2(torch.from_numpy(Y).cuda(), n, n, "forward", fac=fac, out=big[1])
+    assert got.data_ptr() == big[1].data_ptr() and bool((big[0] == 7.0).all())
+    wantb = np.fft.irfft2(Y * m, s=(n, n), norm="forward")
+    assert np.abs(big[1].cpu().numpy() - wantb).max() <= 1e-14 * np.abs(wantb).max()
+    with pytest.raises(ValueError):
+        plane_irfft2(torch.from_numpy(Y).cuda(), n, n, out=big)  # wrong shape
+    if n == 256:
+        with pytest.raises(ValueError):
+            plane_rfft2(torch.from_numpy(x).cuda(), fac=torch.from_numpy(mask.reshape(-1)[:-1].copy()).cuda())
