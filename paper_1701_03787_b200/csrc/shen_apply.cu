@@ -160,6 +160,10 @@ __global__ void apply_kernel(ApplyArgs a, const V* __restrict__ x, V* __restrict
 // the operations of apply_walk in the same order (banded terms in offset
 // order onto zero, then the tail with its parity's suffix sum folded
 // bottom-up), so the results stay bit-identical.
+#ifndef SHEN_APPLY_PF
+#define SHEN_APPLY_PF 6
+#endif
+constexpr int kApplyPf = SHEN_APPLY_PF;
 template <typename V>
 __global__ void __launch_bounds__(128) apply_par_kernel(ApplyArgs a, const V* __restrict__ x, V* __restrict__ y) {
   using O = A<V>;
@@ -200,7 +204,17 @@ __global__ void __launch_bounds__(128) apply_par_kernel(ApplyArgs a, const V* __
     next_j = a.nc - 1;
     if ((next_j & 1) != ((par + a.tail_start) & 1)) --next_j;
   }
+  // With ~450 threads per SM on the config-3 lines the walk is bound by load
+  // latency x loads in flight: the lowest x row a later step needs (the only
+  // new one, the others were read by earlier steps) is prefetched kApplyPf
+  // steps ahead.
+  int dmin = a.kind == 1 ? a.tail_start : 0;
+  for (int q = 0; q < a.n_off; ++q) dmin = min(dmin, a.off[q]);
   for (; k >= 0; k -= 2) {
+    {
+      const int r = k - 2 * kApplyPf + dmin;
+      if (r >= 0 && r < a.nc) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + (int64_t)r * L + l));
+    }
     V v = O::zero();
 #pragma unroll
     for (int q = 0; q < kMaxOff; ++q) {
